@@ -1,0 +1,143 @@
+/*
+ * oracle/heat3d_oracle.c -- CPU ORACLE (TEST INFRASTRUCTURE ONLY).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+ * reference leg may load this file's library.  The product path
+ * (paper_2211_15716_b200/, include/, csrc/) never includes, links or calls it,
+ * and this file includes nothing from the product.
+ *
+ * What it computes: the plain, single-process, single-array definition of the
+ * paper's 3-D heat-diffusion solver on the WHOLE global grid (no halos, no
+ * decomposition, no overlap):
+ *
+ *   PAPER.md:45-51 (Fig. 1, listing lines 6-12)
+ *     @inn(T2) = @inn(T) + dt*( lam*@inn(Ci)*(@d2_xi(T)/dx^2 +
+ *                                            @d2_yi(T)/dy^2 +
+ *                                            @d2_zi(T)/dz^2 ) )
+ *   PAPER.md:74-80 (listing 35-41): for it = 1:nt ... T, T2 = T2, T
+ *   PAPER.md:68-70 (listing 29-31): T2 = copy(T)
+ *
+ * Readings:
+ *   - @d2_xi(T)  = (T[i+1]-T[i]) - (T[i]-T[i-1])                (reading 6)
+ *   - dx^2 = dx*dx; Julia evaluates a*b*c as (a*b)*c and a+b+c as (a+b)+c,
+ *     so the literal form is
+ *       T + dt*((lam*Ci)*(((d2x/(dx*dx)) + (d2y/(dy*dy))) + (d2z/(dz*dz))))
+ *                                                                (reading 7)
+ *   - "canonical" mode replaces /(d*d) by *r_d with r_d = 1.0/(d*d) computed
+ *     once (reading 9); every other operation and its order is unchanged.
+ *   - Non-periodic axes: only cells 1..N-2 are updated; the two outer layers
+ *     keep their initial value (Dirichlet by initialisation, reading 10).
+ *   - Periodic axes: every cell 0..N-1 is updated with neighbours mod N
+ *     (reading 11 / SPEC.md:98).
+ *   - IEEE binary64, round to nearest even, compiled with -ffp-contract=off
+ *     (no FMA contraction) and without -ffast-math (reading 8).
+ *
+ * Layout: x fastest: index(x,y,z) = (z*Ny + y)*Nx + x.
+ * OpenMP (if compiled with -fopenmp) splits the z loop only; it never changes
+ * a cell's arithmetic.
+ */
+#include <stddef.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define IDX(x, y, z, Nx, Ny) ((((size_t)(z)) * (size_t)(Ny) + (size_t)(y)) * (size_t)(Nx) + (size_t)(x))
+
+/* neighbour index along one axis; periodic wraps mod N */
+static long nb(long i, long d, long N, int periodic)
+{
+    long j = i + d;
+    if (periodic) {
+        if (j < 0) j += N;
+        if (j >= N) j -= N;
+    }
+    return j;
+}
+
+/*
+ * One explicit Euler step of Fig. 1 on the global grid.
+ * Writes T2 at every updatable cell; leaves all other cells of T2 untouched.
+ * mode 0 = paper-literal division by dx^2; mode 1 = canonical reciprocal.
+ */
+void oracle_heat_step(double *T2, const double *T, const double *Ci,
+                      long Nx, long Ny, long Nz,
+                      int px, int py, int pz,
+                      double lam, double dt, double dx, double dy, double dz,
+                      int mode)
+{
+    const long xa = px ? 0 : 1, xb = px ? Nx : Nx - 1;
+    const long ya = py ? 0 : 1, yb = py ? Ny : Ny - 1;
+    const long za = pz ? 0 : 1, zb = pz ? Nz : Nz - 1;
+    const double dx2 = dx * dx, dy2 = dy * dy, dz2 = dz * dz;
+    const double rdx2 = 1.0 / dx2, rdy2 = 1.0 / dy2, rdz2 = 1.0 / dz2;
+    long z;
+#pragma omp parallel for schedule(static)
+    for (z = za; z < zb; ++z) {
+        for (long y = ya; y < yb; ++y) {
+            for (long x = xa; x < xb; ++x) {
+                const double c  = T[IDX(x, y, z, Nx, Ny)];
+                const double xm = T[IDX(nb(x, -1, Nx, px), y, z, Nx, Ny)];
+                const double xp = T[IDX(nb(x, +1, Nx, px), y, z, Nx, Ny)];
+                const double ym = T[IDX(x, nb(y, -1, Ny, py), z, Nx, Ny)];
+                const double yp = T[IDX(x, nb(y, +1, Ny, py), z, Nx, Ny)];
+                const double zm = T[IDX(x, y, nb(z, -1, Nz, pz), Nx, Ny)];
+                const double zp = T[IDX(x, y, nb(z, +1, Nz, pz), Nx, Ny)];
+                /* @d2_xi, @d2_yi, @d2_zi */
+                const double d2x = (xp - c) - (c - xm);
+                const double d2y = (yp - c) - (c - ym);
+                const double d2z = (zp - c) - (c - zm);
+                double lap;
+                if (mode == 0)
+                    lap = ((d2x / dx2) + (d2y / dy2)) + (d2z / dz2);
+                else
+                    lap = ((d2x * rdx2) + (d2y * rdy2)) + (d2z * rdz2);
+                const double ci = Ci[IDX(x, y, z, Nx, Ny)];
+                T2[IDX(x, y, z, Nx, Ny)] = c + dt * ((lam * ci) * lap);
+            }
+        }
+    }
+}
+
+/*
+ * The time loop of Fig. 1: T2 = copy(T); nt times
+ * { step!(T2, T, ...); T, T2 = T2, T }.  T (in) is the initial field and on
+ * return holds the final T.  Returns 0 on success, -1 on allocation failure.
+ */
+int oracle_heat_run(double *T, const double *Ci,
+                    long Nx, long Ny, long Nz,
+                    int px, int py, int pz,
+                    double lam, double dt, double dx, double dy, double dz,
+                    int nt, int mode)
+{
+    const size_t n = (size_t)Nx * (size_t)Ny * (size_t)Nz;
+    double *T2 = (double *)malloc(n * sizeof(double));
+    if (!T2) return -1;
+    memcpy(T2, T, n * sizeof(double)); /* T2 = copy(T) */
+    double *a = T, *b = T2;
+    for (int it = 0; it < nt; ++it) {
+        oracle_heat_step(b, a, Ci, Nx, Ny, Nz, px, py, pz, lam, dt, dx, dy, dz, mode);
+        double *t = a; a = b; b = t; /* T, T2 = T2, T */
+    }
+    if (a != T) memcpy(T, a, n * sizeof(double));
+    free(T2);
+    return 0;
+}
+
+/* maximum(Ci) of PAPER.md:73 over the whole global field */
+double oracle_max(const double *A, long n)
+{
+    double m = A[0];
+    for (long i = 1; i < n; ++i)
+        if (A[i] > m) m = A[i];
+    return m;
+}
+
+/* thread count the OpenMP runtime will use (1 without OpenMP) */
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    extern int omp_get_max_threads(void);
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
