@@ -1,0 +1,342 @@
+#!/usr/bin/env python3
+"""bench.py -- T_eff of the distributed Fig. 1 heat step on B200 (BASELINE.json).
+
+A "step" is one pass of the whole hot path: one
+@hide_communication (16,2,2) { step!(T2,T,Ci,...); update_halo!(T2) } time
+step of the paper's 512^3-per-GPU Float64 workload
+ followed by the pointer swap.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W]       # our CUDA path
+  python bench.py --impl reference ...                        # the CPU oracle
+  torchrun --nproc-per-node N ... bench.py --gpus N ...       # weak scaling, dims 2x1x1/2x2x1/2x2x2
+
+value = T_eff summed over all GPUs = N * 24 B * 512^3 / t_step (B:5), t_step =
+max over ranks of the CUDA-event time of K steps / K.  Inputs are 3 x 1 GiB
+per GPU (> the 126 MB L2), so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "T_eff GB/s per GPU and weak-scaling efficiency at 1/2/4/8 B200"
+BYTES_PER_CELL = 24          # T read + Ci read + T2 write, 8 B each (B:5)
+DIMS = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}   # B:9
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=512)
+    ap.add_argument("--bw", default="16,2,2")
+    ap.add_argument("--path", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--init", choices=["paper", "random"], default="paper")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic region kernel (ablation)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-exposed", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dram_traffic_per_launch():
+    """ncu dram__bytes_read+write per launch of the dominant kernel, from the
+    committed summary of this round's `ncu --set full` capture, else None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_oracle_baseline(n: int, target_s: float = 12.0):
+    """The oracle as it stands (plain C, OpenMP) on this host: full n^3 paper
+    workload, as many single steps as fit in ~target_s (at least 2)."""
+    import numpy as np
+    from oracle import heat3d as OH
+    OH.build()
+    T = np.full((n, n, n), 1.7)
+    T2 = T.copy()
+    Ci = np.full((n, n, n), 0.5)
+    d = 1.0 / (n - 1)
+    dt = OH.stable_dt(d, d, d, 1.0, Ci)
+    times = []
+    t_end = time.perf_counter() + target_s
+    while len(times) < 2 or (time.perf_counter() < t_end and len(times) < 50):
+        t0 = time.perf_counter()
+        OH.heat_step(T, Ci, T2, (0, 0, 0), 1.0, dt, d, d, d, OH.LITERAL)
+        times.append(time.perf_counter() - t0)
+        T, T2 = T2, T
+    t = statistics.median(times)
+    return {"value": BYTES_PER_CELL * n ** 3 / t / 1e9, "unit": "GB/s", "cores": OH.num_threads(),
+            "kind": "oracle",
+            "sample": f"{len(times)} oracle steps (paper-literal, full {n}^3 grid, T=1.7 Ci=0.5), median "
+                      f"{t:.3f} s/step, T_eff = 24 B x {n}^3 / t"}
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle timed as it stands on the host cores.
+    Each step = one oracle step on a bounded sample of the workload: the
+    full-x/y 512x512 plane extent with 66 z-planes (64 updated planes)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import heat3d as OH
+    OH.build()
+    n = a.n
+    nz = min(n, 66)
+    T = np.full((nz, n, n), 1.7)
+    T2 = T.copy()
+    Ci = np.full((nz, n, n), 0.5)
+    d = 1.0 / (n - 1)
+    dt = OH.stable_dt(d, d, d, 1.0, Ci)
+    for _ in range(a.warmup):
+        OH.heat_step(T, Ci, T2, (0, 0, 0), 1.0, dt, d, d, d, OH.LITERAL)
+        T, T2 = T2, T
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        OH.heat_step(T, Ci, T2, (0, 0, 0), 1.0, dt, d, d, d, OH.LITERAL)
+        T, T2 = T2, T
+    el = time.perf_counter() - t0
+    cells = nz * n * n
+    val = BYTES_PER_CELL * cells * a.steps / el / 1e9
+    sample = f"oracle step on a {n}x{n}x{nz} slab of the {n}^3 workload per step (paper-literal C, OpenMP)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"heat3d Float64 {n}^3 local, nt-step sample, CPU oracle", "bw": a.bw,
+                   "sample_cells": cells},
+        "cpu_baseline": {"value": val, "unit": "GB/s", "cores": OH.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2211_15716_b200 as P
+    from paper_2211_15716_b200 import heat3d as app
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dims = DIMS.get(world) or P.dims_create(world)
+    bw = tuple(int(x) for x in a.bw.split(","))
+    n = a.n
+    g = P.init_global_grid(n, n, n, dims=dims, path=a.path, device=local)
+    if a.kernel:
+        g.set_option(P.OPT_STENCIL_KERNEL, a.kernel)
+    T, T2, Ci = app.alloc_fields(g)
+    (app.init_paper if a.init == "paper" else app.init_random)(g, T, T2, Ci)
+    d = app.spacing(g)
+    dt = app.stable_dt(g, Ci, *d)
+    stream = torch.cuda.current_stream()
+
+    def steps(k):
+        nonlocal T, T2
+        for _ in range(k):
+            g.heat_step(T2, T, Ci, app.LAM, dt, *d, bw=bw)
+            T, T2 = T2, T
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    steps(max(a.warmup, 3))
+    barrier()
+
+    # ---------------- timed region: K steps, CUDA events on the launching stream
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.4)
+    g.set_option(P.OPT_PROFILE, 1)
+    g.profile_stencil()
+    l0 = g.kernel_launches()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps(a.steps)
+    e1.record(stream)
+    barrier()
+    launches = g.kernel_launches() - l0
+    ms = e0.elapsed_time(e1) / a.steps
+    ms = max_over_ranks(ms)
+    k_ms, k_n, k_cells = g.profile_stencil()
+    g.set_option(P.OPT_PROFILE, 0)
+    clk = clocks.stop() if clocks else None
+    g.check()
+
+    per_gpu = BYTES_PER_CELL * n ** 3 / (ms * 1e-3) / 1e9
+    value = per_gpu * world
+
+    # ---------------- exposed halo time: same schedule with the exchange skipped (timing only)
+    exposed = None
+    if world > 1 and not a.no_exposed:
+        g.set_option(P.OPT_SKIP_COMM, 1)
+        steps(3)
+        barrier()
+        e0.record(stream)
+        steps(a.steps)
+        e1.record(stream)
+        barrier()
+        ms_nc = max_over_ranks(e0.elapsed_time(e1) / a.steps)
+        g.set_option(P.OPT_SKIP_COMM, 0)
+        exposed = {"ms_per_step": ms - ms_nc, "ms_no_comm": ms_nc}
+        (app.init_paper if a.init == "paper" else app.init_random)(g, T, T2, Ci)   # results were invalid
+
+    # ---------------- roofline of the dominant kernel (the full-region / inner-box stencil)
+    peak, peak_src = measured_peak()
+    k_avg_ms = k_ms / max(k_n, 1)
+    k_bytes = BYTES_PER_CELL * k_cells / max(k_n, 1)
+    achieved = k_bytes / (k_avg_ms * 1e-3) / 1e9 if k_n else None
+    tr = dram_traffic_per_launch()
+    traffic = None
+    if tr and tr.get("n") == n and tr.get("dims") == list(dims):
+        traffic = tr.get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
+                "kernel": "heat_box_kernel (inner box)" if world > 1 else "heat_box_kernel (full region)",
+                "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_avg_ms, "launches": k_n,
+                "peak_source": peak_src, "share_of_step": k_avg_ms * (k_n / a.steps) / ms if k_n else None}
+
+    # ---------------- end to end through the C ABI from pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        nt = 100
+        cells = n ** 3
+        Th = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+        Ch = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+        Th.copy_(T[0].cpu() if a.init == "random" else torch.full((1,), 1.7, dtype=torch.float64).expand(n, n, n))
+        Ch.copy_(Ci[0].cpu())
+        del T, T2   # make room for the library's e2e scratch
+        torch.cuda.empty_cache()
+        T0h = Th.clone()
+        reps = 2
+        g.heat_run_host(Th, Ch, app.LAM, dt, *d, 2, bw=bw)     # warm the pool
+        barrier()
+        tt = []
+        for _ in range(reps):
+            Th.copy_(T0h)
+            barrier()
+            e0.record(stream)
+            g.heat_run_host(Th, Ch, app.LAM, dt, *d, nt, bw=bw)
+            e1.record(stream)
+            barrier()
+            tt.append(max_over_ranks(e0.elapsed_time(e1)))
+        t_call = statistics.median(tt)
+        h2d = 2 * cells * 8
+        d2h = cells * 8
+        e2e = {"value": world * BYTES_PER_CELL * cells * nt / (t_call * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": h2d / nt, "d2h_bytes_per_step": d2h / nt,
+               "call": "igg_heat_run_host: H2D T,Ci from pinned host + T2=copy(T) + nt=100 heat steps + D2H T",
+               "nt_per_call": nt, "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h,
+               "ms_per_call": t_call}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_oracle_baseline(n)
+
+    g.finalize()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"3-D heat diffusion Float64, local {n}^3 per GPU, dims "
+                                   f"{dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw} (paper Fig. 1)",
+                       "n_local": n, "dims": list(dims), "bw": list(bw), "path": a.path, "init": a.init,
+                       "t_eff_per_gpu_gbs": per_gpu, "cells_per_s": world * n ** 3 / (ms * 1e-3),
+                       "l2": "inputs 3 x 1 GiB per GPU > 126 MB L2; no flush needed",
+                       "frac_of_8TBs": per_gpu / 8000.0, "frac_of_measured_peak": per_gpu / peak},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk, "exposed_halo": exposed,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,241 @@
+/*
+ * igg.h -- C ABI of the B200-native implicit global grid library (libigg.so).
+ *
+ * The paper (arXiv 2211.15716, PAPER.md) states the problem as "as little as
+ * three functions": create the implicit global staggered grid, perform a halo
+ * update on it, finalize it (Fig. 1 listing lines 23, 38, 43 =
+ * PAPER.md:62, :77, :82), plus size queries nx_g()/ny_g()/nz_g()
+ * (PAPER.md:63-65), and hides communication behind the stencil step with
+ * @hide_communication (16,2,2).  This header is that API.
+ *
+ * Conventions (every entry point):
+ *   - returns igg_status; IGG_OK == 0.  On error igg_last_error() returns a
+ *     thread-local message naming the call and the reason.  C++ exceptions
+ *     never cross this boundary.
+ *   - arrays are Float64 ("@init_parallel_stencil(CUDA, Float64, 3)"),
+ *     x fastest: element (x,y,z) of a field of size (sx,sy,sz) is at
+ *     ptr[(z*sy + y)*sx + x], 0-based.
+ *   - field memory is OWNED BY THE CALLER (e.g. torch tensors) and BORROWED
+ *     for the duration of the enqueued work; the library owns its send/recv
+ *     buffer pool, streams, events, NCCL communicator and peer mappings and
+ *     frees them in igg_finalize_global_grid.
+ *   - update_halo / heat_step are stream-ordered and host-asynchronous: they
+ *     run after prior work on `stream` and later work on `stream` sees their
+ *     results.  init / finalize / global_max are synchronous collectives.
+ *   - collective calls: every rank calls them in the same order with the same
+ *     field list.
+ *   - "local ranks": one process normally hosts one rank on one GPU.  A
+ *     process may host `local_ranks` consecutive ranks on its one GPU
+ *     (virtual ranks, used to test topologies larger than the GPU count);
+ *     then every per-rank argument is an array of local_ranks entries,
+ *     rank-major.  Virtual ranks on one GPU exchange by stream-ordered copies,
+ *     never by spinning kernels.
+ */
+#ifndef IGG_H
+#define IGG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct igg_grid igg_grid;   /* opaque, library-owned */
+typedef void *igg_stream_t;          /* a cudaStream_t (0 = legacy default stream) */
+
+typedef enum igg_status {
+    IGG_OK = 0,
+    IGG_E_ARG = 1,       /* bad argument: n_d <= o_d, odd/negative overlap, dims product != nprocs, bad axis, null pointer */
+    IGG_E_STATE = 2,     /* use after finalize, double finalize */
+    IGG_E_STAGGER = 3,   /* field size s_d outside [n_d-o_d, n_d+o_d] */
+    IGG_E_WIDTH = 4,     /* 0 < b_d < ol_d on an exchanged axis */
+    IGG_E_CUDA = 5,      /* a CUDA runtime call failed */
+    IGG_E_NCCL = 6,      /* an NCCL call failed */
+    IGG_E_TIMEOUT = 7,   /* a P2P receive flag did not arrive in time (analog of SPEC.md:273, :308) */
+    IGG_E_UNSUPPORTED = 8
+} igg_status;
+
+enum {
+    IGG_PATH_NCCL = 0,   /* halo faces cross GPUs with ncclSend/ncclRecv grouped per axis */
+    IGG_PATH_P2P = 1     /* pack kernels store faces straight into the peer's receive buffers over NVLink */
+};
+
+/* ------------------------------------------------------------------ errors */
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *igg_last_error(void);
+
+/* ------------------------------------------------------------------ host-only topology math
+ * No GPU needed.  Readings of the paper for these formulas: DESIGN.md.      */
+
+/* SPEC.md:37-46 (paper: topology "automatically defined"): the
+ * ordered factorisation of nprocs honouring non-zero entries of fixed[3] with
+ * minimal max-min, ties to the lexicographically largest.  IGG_E_ARG if none. */
+igg_status igg_dims_create(int nprocs, const int fixed[3], int dims_out[3]);
+
+/* Cartesian rank order, last axis fastest: rank = (cx*py + cy)*pz + cz. */
+igg_status igg_rank_of_coords(const int dims[3], const int coords[3], int *rank_out);
+igg_status igg_coords_of_rank(const int dims[3], int rank, int coords_out[3]);
+
+/* Global size of one axis, PAPER.md:63-65 nx_g(): p(n-o)+o non-periodic,
+ * p(n-o) periodic.  IGG_E_ARG if n <= o or p < 1. */
+igg_status igg_global_size(int n, int o, int p, int periodic, long long *out);
+
+/* Halo geometry of a field of local size s on an axis with local size n and
+ * overlap o: ol = s-(n-o), h = ol/2; 0-based half-open layer
+ * ranges.  IGG_E_STAGGER if s < n-o or s > n+o. */
+typedef struct igg_halo_spec {
+    int ol, h;
+    int send_lower[2], recv_lower[2], send_upper[2], recv_upper[2];
+} igg_halo_spec;
+igg_status igg_halo_spec_of(int n, int o, long long s, igg_halo_spec *out);
+
+/* ------------------------------------------------------------------ lifecycle */
+typedef struct igg_init_args igg_init_args;
+
+/* The exchange plan of one update_halo call of THIS process (host only, no
+ * GPU): every face it packs (op 0) or unpacks (op 1), axis by axis in
+ * execution order.  Validates args like igg_init_global_grid
+ * and sizes like igg_update_halo.  sizes: nfields*3 (sx,sy,sz).  Writes at
+ * most `capacity` entries to out (out may be NULL to query) and the total to
+ * *count; IGG_E_ARG if capacity is too small. */
+typedef struct igg_plan_entry {
+    int axis;          /* 0 = x, 1 = y, 2 = z */
+    int op;            /* 0 = pack send layers toward `peer`, 1 = unpack receive layers from `peer` */
+    int local_rank;    /* hosted rank index (global rank = rank0 + local_rank) */
+    int field;         /* index in the call's field list */
+    int recv_side;     /* halo side of the RECEIVING rank: 0 = lower, 1 = upper */
+    int peer;          /* global rank at the other end */
+    int transport;     /* 0 = local copy, 1 = NCCL, 2 = P2P store */
+    int lo, h;         /* layers [lo, lo+h) of `axis` (0-based) */
+    long long count;   /* doubles in the face: h * (other two sizes) */
+    int order;         /* NCCL posting position among this axis' sends (op 0) or receives (op 1); -1 otherwise */
+} igg_plan_entry;
+igg_status igg_plan_update_halo(const igg_init_args *args, const long long *sizes, int nfields,
+                                igg_plan_entry *out, int capacity, int *count);
+
+struct igg_init_args {
+    int nx, ny, nz;          /* local size of a canonical (non-staggered) field */
+    int dims[3];             /* process topology; 0 entries = automatic (igg_dims_create) */
+    int periods[3];          /* 0/1 per axis; Fig. 1 passes none -> non-periodic */
+    int overlaps[3];         /* even, >= 2; 0 = default 2 */
+    int nprocs;              /* total number of ranks of the grid */
+    int rank0;               /* first global rank hosted by this process */
+    int local_ranks;         /* ranks hosted by this process (>= 1), all on `device` */
+    int device;              /* CUDA device ordinal of this process */
+    int path;                /* IGG_PATH_NCCL or IGG_PATH_P2P */
+    int reserved;
+    unsigned char comm_id[128]; /* ncclUniqueId from igg_get_unique_id on process 0, broadcast by
+                                   the caller; unused when one process hosts every rank */
+};
+
+/* Fill out[128] with a fresh NCCL unique id (call on process 0 only). */
+igg_status igg_get_unique_id(unsigned char out[128]);
+
+/* init_global_grid (listing 23).  Collective over processes.
+ * Validates the arguments, builds the topology, sets the device, creates the
+ * priority streams, the NCCL communicator (when more than one
+ * process) and the P2P mappings.  Outputs (any may be NULL): me = rank0,
+ * coords of rank0, the dims used and the canonical global sizes n_g. */
+igg_status igg_init_global_grid(const igg_init_args *args, igg_grid **grid_out,
+                                int *me, int coords[3], int dims_out[3], long long n_g[3]);
+
+/* finalize_global_grid (listing 43).  Collective, synchronous.
+ * Frees everything the library owns.  The handle is invalid afterwards. */
+igg_status igg_finalize_global_grid(igg_grid *grid);
+
+/* ------------------------------------------------------------------ queries */
+/* Distinct global layers of a field of local size field_size on axis (0=x,1=y,2=z):
+ * non-periodic n_g + (s - n); periodic the period p(n-o).  field_size = 0
+ * means the canonical size n (then this is nx_g()/ny_g()/nz_g()). */
+igg_status igg_n_g(const igg_grid *grid, int axis, long long field_size, long long *out);
+
+/* Coordinates of a global rank in the grid's topology. */
+igg_status igg_coords(const igg_grid *grid, int rank, int coords_out[3]);
+
+/* 0-based local layer l of `rank` on axis -> 0-based global layer:
+ * g = c(n-o) + l; on a periodic axis (g - o/2) mod p(n-o) (reading 15). */
+igg_status igg_local_to_global(const igg_grid *grid, int rank, int axis, long long l, long long *g_out);
+
+/* Buffer-pool allocation counter: constant once every
+ * field shape has been exchanged once. */
+igg_status igg_buffer_allocs(const igg_grid *grid, long long *count_out);
+
+/* ------------------------------------------------------------------ halo update */
+typedef struct igg_field {
+    double *ptr;             /* device pointer, x fastest */
+    long long size[3];       /* (sx, sy, sz): n_d-o_d <= s_d <= n_d+o_d; staggered fields are n+1 */
+} igg_field;
+
+/* update_halo! (listing 38).  Collective.
+ * fields: local_ranks*nfields entries, rank-major ([r*nfields + f]).
+ * For axis x, then y, then z: the send layers of every field and side with a
+ * neighbour (full extent of the other axes, halos included) are packed,
+ * moved (locally, over NCCL, or by direct stores into the peer's receive
+ * buffer), and unpacked into the neighbour's receive layers.
+ * Runs on the library's high-priority comm stream, joined to `stream`.
+ * Errors: IGG_E_STAGGER, IGG_E_ARG (nfields < 1, null pointer). */
+igg_status igg_update_halo(igg_grid *grid, const igg_field *fields, int nfields, igg_stream_t stream);
+
+/* ------------------------------------------------------------------ the heat step */
+/* @hide_communication bw begin @parallel step!(T2,T,Ci,lam,dt,dx,dy,dz); update_halo!(T2) end
+ * (PAPER.md:45-51, :75-78).  T2, T, Ci: local_ranks device pointers each, all
+ * of the canonical size (nx,ny,nz).  Writes T2 at inner points 1..s-2 of
+ * every axis (PAPER.md:46 @inn), then refreshes T2's halos.  T2 must be a
+ * copy of T's boundary layers (PAPER.md:69 T2 = copy(T)); global-boundary
+ * layers are never written (Dirichlet by initialisation).
+ * Arithmetic per cell, binary64, no FMA contraction:
+ *   T2 = T + dt*((lam*Ci)*(((d2x*rdx2) + (d2y*rdy2)) + (d2z*rdz2))),
+ *   d2x = (T[x+1]-T[x]) - (T[x]-T[x-1]), rdx2 = 1.0/(dx*dx) (readings 6-9).
+ * bw: boundary widths per axis; {0,0,0} = sequential step then update.
+ * Otherwise the six boundary slabs run first on the high-priority stream,
+ * the halo exchange follows them there, and the inner box [b_d, s_d-b_d)
+ * runs concurrently on a low-priority stream.  An exchanged axis needs
+ * b_d >= ol_d (IGG_E_WIDTH); an empty inner box degenerates to sequential. */
+igg_status igg_heat_step(igg_grid *grid, double *const *T2, const double *const *T,
+                         const double *const *Ci, double lam, double dt,
+                         double dx, double dy, double dz, const int bw[3], igg_stream_t stream);
+
+/* Fig. 1 end to end from HOST memory: copies T (initial, local_ranks*nx*ny*nz
+ * doubles, rank-major) and Ci to the device, sets T2 = copy(T), runs nt heat
+ * steps with swap, and copies the final T back into T_host.
+ * Device scratch comes from the library pool (allocated once per size).
+ * Synchronous: returns after the result is in T_host.  Host buffers should be
+ * pinned for full copy bandwidth. */
+igg_status igg_heat_run_host(igg_grid *grid, double *T_host, const double *Ci_host,
+                             double lam, double dt, double dx, double dy, double dz,
+                             int nt, const int bw[3], igg_stream_t stream);
+
+/* ------------------------------------------------------------------ reductions */
+/* maximum over all ranks of `local` (PAPER.md:73 maximum(Ci), reading 12). */
+igg_status igg_global_max(igg_grid *grid, double local, double *out);
+
+/* maximum over all ranks and all elements of a field (local_ranks device
+ * pointers of `count` doubles each), computed by the library's reduction
+ * kernel and an NCCL max-allreduce.  Synchronous on `stream`. */
+igg_status igg_field_global_max(igg_grid *grid, const double *const *f, long long count,
+                                double *out, igg_stream_t stream);
+
+/* ------------------------------------------------------------------ control */
+enum {
+    IGG_OPT_SKIP_COMM = 1,       /* timing-only: skip pack/exchange/unpack (results INVALID) */
+    IGG_OPT_SPIN_TIMEOUT_MS = 2, /* P2P flag wait bound (default 20000) */
+    IGG_OPT_STENCIL_KERNEL = 3,  /* 0 = auto, 1 = generic region kernel only (ablation) */
+    IGG_OPT_PROFILE = 4          /* 1 = bracket every main stencil launch (the full-region or
+                                    inner-box kernel) with CUDA events on its own stream */
+};
+igg_status igg_set_option(igg_grid *grid, int key, long long value);
+
+/* Blocks until all work of the grid's streams is done, then reports a P2P
+ * wait timeout (IGG_E_TIMEOUT) or an NCCL asynchronous error. */
+igg_status igg_check(igg_grid *grid);
+
+/* With IGG_OPT_PROFILE on: synchronizes the device, returns the summed
+ * CUDA-event duration (ms) of the main stencil launches recorded since the
+ * last call, their number and the cells they updated, and resets the record. */
+igg_status igg_profile_stencil(igg_grid *grid, double *ms_total, long long *launches, long long *cells);
+
+/* Number of kernels the library has launched since init (launch accounting). */
+igg_status igg_kernel_launches(const igg_grid *grid, long long *count_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGG_H */

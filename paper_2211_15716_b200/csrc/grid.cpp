@@ -1,0 +1,668 @@
+// grid.cpp -- lifecycle, buffer pool, update_halo orchestration, the
+// hide_communication heat step and reductions of libigg (host side).
+//
+// init_global_grid / update_halo! / finalize_global_grid: PAPER.md:36, :62,
+// :77, :82.  "Low level management of memory, CUDA streams ... permits to
+// efficiently reuse send and receive buffers and streams ... all data
+// transfers are performed on non-blocking high-priority streams"  PAPER.md:94.
+// @hide_communication (16,2,2): PAPER.md:75.
+#include <algorithm>
+#include <cstring>
+
+#include "igg_internal.h"
+
+namespace igg {
+
+int proc_of(const igg_grid *g, int r) { return r / g->nlocal; }
+int local_index(const igg_grid *g, int r) { return proc_of(g, r) == g->proc ? r - g->rank0 : -1; }
+
+void check_live(const igg_grid *g, const char *what) {
+    if (!g) fail(IGG_E_ARG, std::string(what) + ": grid is NULL");
+    if (g->finalized) fail(IGG_E_STATE, std::string(what) + ": grid already finalized");
+}
+
+static void *dev_alloc(igg_grid *g, size_t bytes) {
+    void *p = nullptr;
+    IGG_CUDA(cudaMalloc(&p, bytes));
+    g->allocs++;
+    return p;
+}
+
+// all-gather of a small host blob over the NCCL communicator (init-time only)
+static std::vector<char> allgather_bytes(igg_grid *g, const void *mine, size_t bytes) {
+    std::vector<char> out(bytes * g->nproc_procs);
+    char *d = nullptr;
+    IGG_CUDA(cudaMalloc(&d, out.size()));
+    IGG_CUDA(cudaMemcpy(d + bytes * g->proc, mine, bytes, cudaMemcpyHostToDevice));
+    IGG_NCCL(ncclAllGather(d + bytes * g->proc, d, bytes, ncclChar, g->comm, g->s_comm));
+    IGG_CUDA(cudaStreamSynchronize(g->s_comm));
+    IGG_CUDA(cudaMemcpy(out.data(), d, out.size(), cudaMemcpyDeviceToHost));
+    IGG_CUDA(cudaFree(d));
+    return out;
+}
+
+static void process_barrier(igg_grid *g) {
+    IGG_CUDA(cudaDeviceSynchronize());
+    if (g->nproc_procs > 1) {
+        char x = 0;
+        allgather_bytes(g, &x, 1);
+    }
+}
+
+static void unmap_peers(igg_grid *g, std::vector<char *> &peers) {
+    for (int p = 0; p < (int)peers.size(); ++p)
+        if (peers[p] && p != g->proc) cudaIpcCloseMemHandle(peers[p]);
+    peers.assign(g->nproc_procs, nullptr);
+}
+
+// Buffer pool: one receive arena with two parity halves
+// (P2P ping-pong) and one send arena (NCCL).
+// Every rank computes the same sizes from the same field list, so growth is a
+// consistent collective; once every field list has been seen it never grows.
+void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap) {
+    const bool grow_recv = recv_half > g->recv_half;
+    const bool grow_send = send_cap > g->send_cap;
+    if (!grow_recv && !grow_send) return;
+    process_barrier(g);   // nobody may still be writing into the old arenas
+    if (grow_send) {
+        if (g->send_arena) IGG_CUDA(cudaFree(g->send_arena));
+        g->send_arena = (char *)dev_alloc(g, send_cap);
+        g->send_cap = send_cap;
+    }
+    if (grow_recv) {
+        if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) unmap_peers(g, g->peer_recv);
+        if (g->recv_arena) IGG_CUDA(cudaFree(g->recv_arena));
+        g->recv_arena = (char *)dev_alloc(g, 2 * recv_half);
+        IGG_CUDA(cudaMemset(g->recv_arena, 0, 2 * recv_half));
+        g->recv_half = recv_half;
+        if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
+            cudaIpcMemHandle_t h;
+            IGG_CUDA(cudaIpcGetMemHandle(&h, g->recv_arena));
+            std::vector<char> all = allgather_bytes(g, &h, sizeof h);
+            g->peer_recv.assign(g->nproc_procs, nullptr);
+            for (int p = 0; p < g->nproc_procs; ++p) {
+                if (p == g->proc) {
+                    g->peer_recv[p] = g->recv_arena;
+                    continue;
+                }
+                cudaIpcMemHandle_t ph;
+                std::memcpy(&ph, all.data() + p * sizeof ph, sizeof ph);
+                void *ptr = nullptr;
+                IGG_CUDA(cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess));
+                g->peer_recv[p] = (char *)ptr;
+            }
+        }
+    }
+    process_barrier(g);
+}
+
+// ------------------------------------------------------------------ update_halo
+// Executes the plan of plan.cpp: per axis one pack launch (faces into the
+// receiver's arena slot: local, peer-mapped over NVLink, or the NCCL send
+// arena), the grouped NCCL send/recv of that axis, one unpack launch.
+void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
+    if (nf < 1 || !fields) fail(IGG_E_ARG, "update_halo: need at least one field");
+    const int L = g->nlocal;
+    std::vector<long long> sizes(nf * 3);
+    for (int f = 0; f < nf; ++f)
+        for (int a = 0; a < 3; ++a) sizes[f * 3 + a] = fields[f].size[a];
+    for (int r = 0; r < L; ++r)
+        for (int f = 0; f < nf; ++f) {
+            const igg_field &F = fields[r * nf + f];
+            if (!F.ptr) fail(IGG_E_ARG, "update_halo: NULL field pointer");
+            for (int a = 0; a < 3; ++a)
+                if (F.size[a] != sizes[f * 3 + a]) fail(IGG_E_ARG, "update_halo: local ranks disagree on a field size");
+        }
+    const Plan plan = build_plan(*g, sizes.data(), nf);
+    const size_t half = (size_t)L * plan.block * sizeof(double);
+    ensure_arena(g, half, plan.any_nccl ? half : 0);
+
+    g->epoch++;
+    if (g->skip_comm) return;
+    const int parity = (int)(g->epoch & 1);
+    double *recv = reinterpret_cast<double *>(g->recv_arena + parity * g->recv_half);
+    double *sendb = reinterpret_cast<double *>(g->send_arena);
+
+    for (int a = 0; a < 3; ++a) {   // x -> y -> z, each axis complete before the next
+        if (plan.msgs[a].empty()) continue;
+        CopyList P{}, U{};
+        P.ticket = g->tickets + a;
+        P.epoch = U.epoch = g->epoch;
+        U.err = P.err = g->d_err;
+        U.timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
+        std::vector<const PlanMsg *> sends, recvs;
+        for (const PlanMsg &m : plan.msgs[a]) {
+            CopyList &C = m.op == 0 ? P : U;
+            if (C.n >= kMaxCopy) fail(IGG_E_UNSUPPORTED, "update_halo: too many faces per axis");
+            CopyDesc d{};
+            const igg_field &F = fields[m.lr * nf + m.field];
+            d.field = F.ptr;
+            d.sx = F.size[0];
+            d.sy = F.size[1];
+            d.sz = F.size[2];
+            d.count = m.count;
+            d.axis = a;
+            d.lo = m.lo;
+            d.h = m.h;
+            d.flag_slot = -1;
+            if (m.op == 0) {
+                if (m.transport == kLocal) {
+                    d.buf = recv + m.slot;
+                } else if (m.transport == kP2P) {
+                    d.buf = reinterpret_cast<double *>(g->peer_recv[m.peer_proc] + parity * g->recv_half) + m.slot;
+                    unsigned long long *fl = g->peer_flags[m.peer_proc] + (m.peer_lr * 3 + a) * 2 + m.recv_side;
+                    bool have = false;
+                    for (int s = 0; s < P.nsignal; ++s) have |= P.signal[s] == fl;
+                    if (!have) {
+                        if (P.nsignal >= kMaxSignal) fail(IGG_E_UNSUPPORTED, "update_halo: too many peers");
+                        P.signal[P.nsignal++] = fl;
+                    }
+                } else {
+                    d.buf = sendb + m.sbuf;
+                    sends.push_back(&m);
+                }
+            } else {
+                d.buf = recv + m.slot;
+                if (m.transport == kP2P) {
+                    const unsigned long long *fl = g->flags + (m.lr * 3 + a) * 2 + m.recv_side;
+                    int w = -1;
+                    for (int s = 0; s < U.nsignal; ++s)
+                        if (U.wait[s] == fl) w = s;
+                    if (w < 0) {
+                        if (U.nsignal >= kMaxSignal) fail(IGG_E_UNSUPPORTED, "update_halo: too many peers");
+                        w = U.nsignal;
+                        U.wait[U.nsignal++] = fl;
+                    }
+                    d.flag_slot = w;
+                } else if (m.transport == kNccl) {
+                    recvs.push_back(&m);
+                }
+            }
+            C.d[C.n++] = d;
+        }
+        launch_pack(P, st);
+        g->launches++;
+        if (!sends.empty() || !recvs.empty()) {
+            auto by_order = [](const PlanMsg *x, const PlanMsg *y) { return x->order < y->order; };
+            std::sort(sends.begin(), sends.end(), by_order);
+            std::sort(recvs.begin(), recvs.end(), by_order);
+            IGG_NCCL(ncclGroupStart());
+            for (const PlanMsg *m : sends)
+                IGG_NCCL(ncclSend(sendb + m->sbuf, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
+            for (const PlanMsg *m : recvs)
+                IGG_NCCL(ncclRecv(recv + m->slot, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
+            IGG_NCCL(ncclGroupEnd());
+        }
+        launch_unpack(U, st);
+        g->launches++;
+    }
+}
+
+// ------------------------------------------------------------------ profiling
+void prof_begin(igg_grid *g, cudaStream_t s) {
+    if (!g->profile) return;
+    while (g->prof_ev.size() < g->prof_used + 2) {
+        cudaEvent_t e;
+        IGG_CUDA(cudaEventCreate(&e));
+        g->prof_ev.push_back(e);
+    }
+    IGG_CUDA(cudaEventRecord(g->prof_ev[g->prof_used], s));
+}
+
+void prof_end(igg_grid *g, cudaStream_t s, long long cells) {
+    if (!g->profile) return;
+    IGG_CUDA(cudaEventRecord(g->prof_ev[g->prof_used + 1], s));
+    g->prof_used += 2;
+    g->prof_cells += cells;
+}
+
+// ------------------------------------------------------------------ the heat step
+static void launch_full(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
+                        const HeatCoef &k, cudaStream_t s) {
+    HeatRegionList RL{};
+    RL.k = k;
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        HeatRegion R{};
+        R.T = T[lr];
+        R.Ci = Ci[lr];
+        R.T2 = T2[lr];
+        R.sx = g->n[0];
+        R.sy = g->n[1];
+        R.sz = g->n[2];
+        R.x0 = R.y0 = R.z0 = 1;
+        R.wx = g->n[0] - 2;
+        R.wy = g->n[1] - 2;
+        R.wz = g->n[2] - 2;
+        if (g->stencil_kernel != 1 && heat_box_vectorizable(R)) {
+            prof_begin(g, s);
+            launch_heat_box(R, k, s);
+            prof_end(g, s, (long long)R.wx * R.wy * R.wz);
+            g->launches++;
+        } else {
+            RL.r[RL.n++] = R;
+            if (RL.n == kMaxRegions) {
+                launch_heat_regions(RL, s);
+                g->launches++;
+                RL.n = 0;
+            }
+        }
+    }
+    if (RL.n) {
+        launch_heat_regions(RL, s);
+        g->launches++;
+    }
+}
+
+void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, double lam,
+               double dt, double dx, double dy, double dz, const int bw[3], cudaStream_t s) {
+    for (int lr = 0; lr < g->nlocal; ++lr)
+        if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "heat_step: NULL field pointer");
+    for (int a = 0; a < 3; ++a)
+        if (g->n[a] < 3) fail(IGG_E_ARG, "heat_step: every axis needs at least 3 cells");
+    // reciprocals computed once on the host (reading 9, canonical form)
+    const HeatCoef k{lam, dt, 1.0 / (dx * dx), 1.0 / (dy * dy), 1.0 / (dz * dz)};
+    bool exch[3] = {false, false, false};
+    bool any = false;
+    for (int a = 0; a < 3; ++a)
+        for (int lr = 0; lr < g->nlocal; ++lr)
+            if (g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0) exch[a] = any = true;
+    if (!any) {   // nothing to exchange or hide: one full-region launch
+        launch_full(g, T2, T, Ci, k, s);
+        return;
+    }
+    const int zero[3] = {0, 0, 0};
+    if (!bw) bw = zero;
+    const bool sequential_req = bw[0] == 0 && bw[1] == 0 && bw[2] == 0;
+    int lo[3], hi[3];
+    bool degenerate = false;
+    for (int a = 0; a < 3; ++a) {
+        if (bw[a] < 0) fail(IGG_E_ARG, "heat_step: negative boundary width");
+        // the send layers must be final before any face leaves
+        if (!sequential_req && exch[a] && bw[a] < g->o[a])
+            fail(IGG_E_WIDTH, "heat_step: boundary width " + std::to_string(bw[a]) + " on axis " +
+                                  std::to_string(a) + " is below the field overlap " + std::to_string(g->o[a]));
+        lo[a] = std::max(1, bw[a]);
+        hi[a] = std::min(g->n[a] - 1, g->n[a] - bw[a]);
+        if (hi[a] <= lo[a]) degenerate = true;   // empty inner box
+    }
+    std::vector<igg_field> f(g->nlocal);
+    for (int lr = 0; lr < g->nlocal; ++lr) f[lr] = igg_field{T2[lr], {g->n[0], g->n[1], g->n[2]}};
+
+    IGG_CUDA(cudaEventRecord(g->ev_start, s));
+    IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
+    if (sequential_req || degenerate) {
+        launch_full(g, T2, T, Ci, k, g->s_comm);
+        exchange(g, f.data(), 1, g->s_comm);
+        IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+        IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+        return;
+    }
+    IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
+    // (1) the six boundary slabs, x-lo, x-hi, y-lo, y-hi, z-lo, z-hi, high priority
+    HeatRegionList RL{};
+    RL.k = k;
+    const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
+    auto add = [&](int lr, int x0, int x1, int y0, int y1, int z0, int z1) {
+        if (x1 <= x0 || y1 <= y0 || z1 <= z0) return;
+        if (RL.n == kMaxRegions) {
+            launch_heat_regions(RL, g->s_comm);
+            g->launches++;
+            RL.n = 0;
+        }
+        HeatRegion R{};
+        R.T = T[lr];
+        R.Ci = Ci[lr];
+        R.T2 = T2[lr];
+        R.sx = n0;
+        R.sy = n1;
+        R.sz = n2;
+        R.x0 = x0;
+        R.y0 = y0;
+        R.z0 = z0;
+        R.wx = x1 - x0;
+        R.wy = y1 - y0;
+        R.wz = z1 - z0;
+        RL.r[RL.n++] = R;
+    };
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        add(lr, 1, lo[0], 1, n1 - 1, 1, n2 - 1);
+        add(lr, hi[0], n0 - 1, 1, n1 - 1, 1, n2 - 1);
+        add(lr, lo[0], hi[0], 1, lo[1], 1, n2 - 1);
+        add(lr, lo[0], hi[0], hi[1], n1 - 1, 1, n2 - 1);
+        add(lr, lo[0], hi[0], lo[1], hi[1], 1, lo[2]);
+        add(lr, lo[0], hi[0], lo[1], hi[1], hi[2], n2 - 1);
+    }
+    if (RL.n) {
+        launch_heat_regions(RL, g->s_comm);
+        g->launches++;
+    }
+    // (2) the inner box on the low-priority stream, concurrently
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        HeatRegion R{};
+        R.T = T[lr];
+        R.Ci = Ci[lr];
+        R.T2 = T2[lr];
+        R.sx = n0;
+        R.sy = n1;
+        R.sz = n2;
+        R.x0 = lo[0];
+        R.y0 = lo[1];
+        R.z0 = lo[2];
+        R.wx = hi[0] - lo[0];
+        R.wy = hi[1] - lo[1];
+        R.wz = hi[2] - lo[2];
+        prof_begin(g, g->s_inner);
+        if (g->stencil_kernel != 1 && heat_box_vectorizable(R)) {
+            launch_heat_box(R, k, g->s_inner);
+        } else {
+            HeatRegionList one{};
+            one.k = k;
+            one.r[0] = R;
+            one.n = 1;
+            launch_heat_regions(one, g->s_inner);
+        }
+        prof_end(g, g->s_inner, (long long)R.wx * R.wy * R.wz);
+        g->launches++;
+    }
+    // (3) update_halo!(T2) behind the boundary, on the high-priority stream
+    exchange(g, f.data(), 1, g->s_comm);
+    IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+    IGG_CUDA(cudaEventRecord(g->ev_inner, g->s_inner));
+    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
+}
+
+}  // namespace igg
+
+// ============================================================== C ABI
+using igg::fail;
+
+IGG_API igg_status igg_get_unique_id(unsigned char out[128]) {
+    IGG_TRY
+    if (!out) fail(IGG_E_ARG, "igg_get_unique_id: out is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    IGG_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, 128);
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_out, int *me, int coords[3],
+                                        int dims_out[3], long long n_g[3]) {
+    igg_grid *g = nullptr;
+    try {
+        if (!A || !grid_out) fail(IGG_E_ARG, "igg_init_global_grid: NULL argument");
+        igg::Geom geo = igg::make_geom(A);
+        g = new igg_grid();
+        static_cast<igg::Geom &>(*g) = geo;
+        IGG_CUDA(cudaSetDevice(g->device));
+        IGG_CUDA(cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, g->device));
+        int khz = 0;
+        if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->device) == cudaSuccess && khz > 0)
+            g->clock_khz = khz;
+        int least = 0, greatest = 0;
+        IGG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        IGG_CUDA(cudaStreamCreateWithPriority(&g->s_comm, cudaStreamNonBlocking, greatest));
+        IGG_CUDA(cudaStreamCreateWithPriority(&g->s_inner, cudaStreamNonBlocking, least));
+        IGG_CUDA(cudaEventCreateWithFlags(&g->ev_start, cudaEventDisableTiming));
+        IGG_CUDA(cudaEventCreateWithFlags(&g->ev_comm, cudaEventDisableTiming));
+        IGG_CUDA(cudaEventCreateWithFlags(&g->ev_inner, cudaEventDisableTiming));
+        if (g->nproc_procs > 1) {
+            ncclUniqueId id;
+            std::memcpy(&id, A->comm_id, sizeof id);
+            IGG_NCCL(ncclCommInitRank(&g->comm, g->nproc_procs, id, g->proc));
+        }
+        // receive flags (P2P), last-block tickets, error word, reduction scratch
+        g->flags = (unsigned long long *)igg::dev_alloc(g, sizeof(unsigned long long) * g->nlocal * 6);
+        IGG_CUDA(cudaMemset(g->flags, 0, sizeof(unsigned long long) * g->nlocal * 6));
+        g->tickets = (unsigned int *)igg::dev_alloc(g, sizeof(unsigned int) * 4);
+        IGG_CUDA(cudaMemset(g->tickets, 0, sizeof(unsigned int) * 4));
+        g->d_err = (int *)igg::dev_alloc(g, sizeof(int) * 2);
+        IGG_CUDA(cudaMemset(g->d_err, 0, sizeof(int) * 2));
+        g->d_scratch = (double *)igg::dev_alloc(g, sizeof(double) * (igg::field_max_scratch_len() + 2));
+        IGG_CUDA(cudaMallocHost(&g->d_pinned_out, sizeof(double)));
+        g->peer_recv.assign(g->nproc_procs, nullptr);
+        g->peer_flags.assign(g->nproc_procs, nullptr);
+        g->peer_flags[g->proc] = g->flags;
+        if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
+            cudaIpcMemHandle_t h;
+            IGG_CUDA(cudaIpcGetMemHandle(&h, g->flags));
+            std::vector<char> all = igg::allgather_bytes(g, &h, sizeof h);
+            for (int p = 0; p < g->nproc_procs; ++p) {
+                if (p == g->proc) continue;
+                cudaIpcMemHandle_t ph;
+                std::memcpy(&ph, all.data() + p * sizeof ph, sizeof ph);
+                void *ptr = nullptr;
+                IGG_CUDA(cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess));
+                g->peer_flags[p] = (unsigned long long *)ptr;
+            }
+        }
+        IGG_CUDA(cudaDeviceSynchronize());
+        if (me) *me = g->rank0;
+        if (coords)
+            for (int a = 0; a < 3; ++a) coords[a] = g->coords[0][a];
+        if (dims_out) std::memcpy(dims_out, g->dims, sizeof g->dims);
+        if (n_g)
+            for (int a = 0; a < 3; ++a) n_g[a] = g->ng[a];
+        *grid_out = g;
+        return IGG_OK;
+    } catch (const igg::IggException &e) {
+        delete g;   // partial init: resources of a failed init are leaked to the process (rare)
+        return e.code;
+    } catch (const std::exception &e) {
+        delete g;
+        igg::set_error(std::string("internal error: ") + e.what());
+        return IGG_E_ARG;
+    }
+}
+
+IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
+    IGG_TRY
+    igg::check_live(g, "igg_finalize_global_grid");
+    g->finalized = true;
+    igg::process_barrier(g);
+    if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
+        igg::unmap_peers(g, g->peer_recv);
+        for (int p = 0; p < g->nproc_procs; ++p)
+            if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
+    }
+    igg::process_barrier(g);
+    for (void *p : {(void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+                    (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
+        if (p) cudaFree(p);
+    if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
+    if (g->comm) ncclCommDestroy(g->comm);
+    for (cudaEvent_t e : g->prof_ev) cudaEventDestroy(e);
+    cudaEventDestroy(g->ev_start);
+    cudaEventDestroy(g->ev_comm);
+    cudaEventDestroy(g->ev_inner);
+    cudaStreamDestroy(g->s_comm);
+    cudaStreamDestroy(g->s_inner);
+    delete g;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_n_g(const igg_grid *g, int axis, long long field_size, long long *out) {
+    IGG_TRY
+    igg::check_live(g, "igg_n_g");
+    if (axis < 0 || axis > 2 || !out) fail(IGG_E_ARG, "igg_n_g: bad axis or NULL out");
+    const long long s = field_size == 0 ? g->n[axis] : field_size;
+    igg::HaloSpec hs;
+    if (!igg::halo_spec(g->n[axis], g->o[axis], s, &hs)) fail(IGG_E_STAGGER, "igg_n_g: field size out of range");
+    *out = g->periods[axis] ? g->ng[axis] : g->ng[axis] + (s - g->n[axis]);
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_coords(const igg_grid *g, int rank, int coords_out[3]) {
+    IGG_TRY
+    igg::check_live(g, "igg_coords");
+    if (rank < 0 || rank >= g->nprocs || !coords_out) fail(IGG_E_ARG, "igg_coords: bad rank or NULL out");
+    igg::coords_of_rank(g->dims, rank, coords_out);
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_local_to_global(const igg_grid *g, int rank, int axis, long long l, long long *g_out) {
+    IGG_TRY
+    igg::check_live(g, "igg_local_to_global");
+    if (rank < 0 || rank >= g->nprocs || axis < 0 || axis > 2 || !g_out)
+        fail(IGG_E_ARG, "igg_local_to_global: bad argument");
+    int c[3];
+    igg::coords_of_rank(g->dims, rank, c);
+    long long v = (long long)c[axis] * (g->n[axis] - g->o[axis]) + l;
+    if (g->periods[axis]) {
+        const long long P = (long long)g->dims[axis] * (g->n[axis] - g->o[axis]);
+        v = ((v - g->o[axis] / 2) % P + P) % P;
+    }
+    *g_out = v;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_buffer_allocs(const igg_grid *g, long long *count_out) {
+    IGG_TRY
+    igg::check_live(g, "igg_buffer_allocs");
+    if (!count_out) fail(IGG_E_ARG, "igg_buffer_allocs: NULL out");
+    *count_out = g->allocs;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_kernel_launches(const igg_grid *g, long long *count_out) {
+    IGG_TRY
+    igg::check_live(g, "igg_kernel_launches");
+    if (!count_out) fail(IGG_E_ARG, "igg_kernel_launches: NULL out");
+    *count_out = g->launches;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_update_halo(igg_grid *g, const igg_field *fields, int nfields, igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_update_halo");
+    cudaStream_t s = (cudaStream_t)stream;
+    IGG_CUDA(cudaEventRecord(g->ev_start, s));
+    IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
+    igg::exchange(g, fields, nfields, g->s_comm);
+    IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
+                                 double lam, double dt, double dx, double dy, double dz, const int bw[3],
+                                 igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_heat_step");
+    if (!T2 || !T || !Ci) fail(IGG_E_ARG, "igg_heat_step: NULL pointer array");
+    igg::heat_step(g, T2, T, Ci, lam, dt, dx, dy, dz, bw, (cudaStream_t)stream);
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *Ci_host, double lam, double dt,
+                                     double dx, double dy, double dz, int nt, const int bw[3], igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_heat_run_host");
+    if (!T_host || !Ci_host || nt < 0) fail(IGG_E_ARG, "igg_heat_run_host: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t cells = (size_t)g->n[0] * g->n[1] * g->n[2];
+    const size_t bytes = cells * g->nlocal * sizeof(double);
+    if (bytes > g->run_bytes) {
+        for (double *p : {g->run_T, g->run_T2, g->run_Ci})
+            if (p) IGG_CUDA(cudaFree(p));
+        g->run_T = (double *)igg::dev_alloc(g, bytes);
+        g->run_T2 = (double *)igg::dev_alloc(g, bytes);
+        g->run_Ci = (double *)igg::dev_alloc(g, bytes);
+        g->run_bytes = bytes;
+    }
+    IGG_CUDA(cudaMemcpyAsync(g->run_T, T_host, bytes, cudaMemcpyHostToDevice, s));
+    IGG_CUDA(cudaMemcpyAsync(g->run_Ci, Ci_host, bytes, cudaMemcpyHostToDevice, s));
+    IGG_CUDA(cudaMemcpyAsync(g->run_T2, g->run_T, bytes, cudaMemcpyDeviceToDevice, s));   // T2 = copy(T)
+    std::vector<double *> a(g->nlocal), b(g->nlocal);
+    std::vector<const double *> c(g->nlocal);
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        a[lr] = g->run_T + lr * cells;
+        b[lr] = g->run_T2 + lr * cells;
+        c[lr] = g->run_Ci + lr * cells;
+    }
+    for (int it = 0; it < nt; ++it) {
+        std::vector<const double *> ac(a.begin(), a.end());
+        igg::heat_step(g, b.data(), ac.data(), c.data(), lam, dt, dx, dy, dz, bw, s);
+        std::swap(a, b);   // T, T2 = T2, T
+    }
+    for (int lr = 0; lr < g->nlocal; ++lr)
+        IGG_CUDA(cudaMemcpyAsync(T_host + lr * cells, a[lr], cells * sizeof(double), cudaMemcpyDeviceToHost, s));
+    IGG_CUDA(cudaStreamSynchronize(s));
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_global_max(igg_grid *g, double local, double *out) {
+    IGG_TRY
+    igg::check_live(g, "igg_global_max");
+    if (!out) fail(IGG_E_ARG, "igg_global_max: NULL out");
+    double *d = g->d_scratch + igg::field_max_scratch_len();
+    IGG_CUDA(cudaMemcpyAsync(d, &local, sizeof(double), cudaMemcpyHostToDevice, g->s_comm));
+    if (g->nproc_procs > 1) IGG_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, g->comm, g->s_comm));
+    IGG_CUDA(cudaMemcpyAsync(g->d_pinned_out, d, sizeof(double), cudaMemcpyDeviceToHost, g->s_comm));
+    IGG_CUDA(cudaStreamSynchronize(g->s_comm));
+    *out = *g->d_pinned_out;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_field_global_max(igg_grid *g, const double *const *f, long long count, double *out,
+                                        igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_field_global_max");
+    if (!f || !out || count < 1) fail(IGG_E_ARG, "igg_field_global_max: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    double *d = g->d_scratch + igg::field_max_scratch_len();
+    igg::launch_field_max(f, g->nlocal, count, g->d_scratch, igg::field_max_scratch_len(), d, s);
+    g->launches += 2;
+    if (g->nproc_procs > 1) IGG_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, g->comm, s));
+    IGG_CUDA(cudaMemcpyAsync(g->d_pinned_out, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+    IGG_CUDA(cudaStreamSynchronize(s));
+    *out = *g->d_pinned_out;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
+    IGG_TRY
+    igg::check_live(g, "igg_set_option");
+    switch (key) {
+        case IGG_OPT_SKIP_COMM: g->skip_comm = value != 0; break;
+        case IGG_OPT_SPIN_TIMEOUT_MS: g->spin_timeout_ms = value; break;
+        case IGG_OPT_STENCIL_KERNEL: g->stencil_kernel = (int)value; break;
+        case IGG_OPT_PROFILE: g->profile = value != 0; break;
+        default: fail(IGG_E_ARG, "igg_set_option: unknown key " + std::to_string(key));
+    }
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_profile_stencil(igg_grid *g, double *ms_total, long long *launches, long long *cells) {
+    IGG_TRY
+    igg::check_live(g, "igg_profile_stencil");
+    IGG_CUDA(cudaDeviceSynchronize());
+    double tot = 0.0;
+    for (size_t i = 0; i + 1 < g->prof_used; i += 2) {
+        float ms = 0.f;
+        IGG_CUDA(cudaEventElapsedTime(&ms, g->prof_ev[i], g->prof_ev[i + 1]));
+        tot += ms;
+    }
+    if (ms_total) *ms_total = tot;
+    if (launches) *launches = (long long)(g->prof_used / 2);
+    if (cells) *cells = g->prof_cells;
+    g->prof_used = 0;
+    g->prof_cells = 0;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_check(igg_grid *g) {
+    IGG_TRY
+    igg::check_live(g, "igg_check");
+    IGG_CUDA(cudaDeviceSynchronize());
+    int err = 0;
+    IGG_CUDA(cudaMemcpy(&err, g->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) fail(IGG_E_TIMEOUT, "igg_check: a P2P receive flag wait timed out");
+    if (g->comm) {
+        ncclResult_t r = ncclSuccess;
+        IGG_NCCL(ncclCommGetAsyncError(g->comm, &r));
+        if (r != ncclSuccess) fail(IGG_E_NCCL, std::string("igg_check: NCCL async error: ") + ncclGetErrorString(r));
+    }
+    IGG_CATCH
+}

@@ -1,0 +1,217 @@
+// igg_internal.h -- internal types shared by the libigg translation units.
+// Nothing here crosses the C ABI (include/igg.h is the boundary).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/igg.h"
+
+namespace igg {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    igg_status code;
+    std::string msg;
+};
+struct IggException {
+    igg_status code;
+};
+void set_error(const std::string &msg);
+[[noreturn]] void fail(igg_status code, const std::string &msg);
+
+#define IGG_CUDA(call)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            ::igg::fail(IGG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+#define IGG_NCCL(call)                                                                      \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            ::igg::fail(IGG_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));    \
+    } while (0)
+
+#define IGG_API extern "C" __attribute__((visibility("default")))
+#define IGG_TRY try {
+#define IGG_CATCH                                                       \
+    }                                                                   \
+    catch (const ::igg::IggException &e) { return e.code; }             \
+    catch (const std::exception &e) {                                   \
+        ::igg::set_error(std::string("internal error: ") + e.what());   \
+        return IGG_E_ARG;                                               \
+    }                                                                   \
+    return IGG_OK;
+
+// ---------------------------------------------------------------- host topology math
+int dims_create(int nprocs, const int fixed[3], int out[3]);          // 0 ok, -1 none
+int rank_of_coords(const int dims[3], const int c[3]);
+void coords_of_rank(const int dims[3], int rank, int c[3]);
+long long global_size(int n, int o, int p, int periodic);
+struct HaloSpec {
+    int ol, h;
+    int send_lo[2], recv_lo[2], send_up[2], recv_up[2];   // 0-based [a,b)
+};
+bool halo_spec(int n, int o, long long s, HaloSpec *out);             // false: bad stagger
+
+// ---------------------------------------------------------------- device-side descriptors
+// one face copy: the slab [lo, lo+h) of `axis` of a field <-> a contiguous buffer,
+// buffer layout x fastest, then y, then z, restricted to the slab
+struct CopyDesc {
+    double *field;
+    double *buf;
+    long long sx, sy, sz;
+    long long count;                 // h * (other two sizes)
+    int axis, lo, h;
+    int flag_slot;                   // unpack: index into WaitList flags (-1 = no wait)
+};
+
+constexpr int kMaxCopy = 48;
+constexpr int kMaxSignal = 16;
+struct CopyList {
+    CopyDesc d[kMaxCopy];
+    int n;
+    int blocks_per_desc;
+    // pack: after every block stored its part (to peers), the last block
+    // publishes `epoch` to these remote flags (st.release.sys)
+    unsigned long long *signal[kMaxSignal];
+    int nsignal;
+    unsigned int *ticket;            // device counter for the last-block election
+    // unpack: wait until *wait[flag_slot] >= epoch (ld.acquire.sys) before reading
+    const unsigned long long *wait[kMaxSignal];
+    unsigned long long epoch;
+    long long timeout_cycles;
+    int *err;                        // set to 1 on timeout
+};
+
+// one stencil region [x0,x0+wx) x [y0,y0+wy) x [z0,z0+wz) of one rank's field
+struct HeatRegion {
+    const double *T;
+    const double *Ci;
+    double *T2;
+    int sx, sy, sz;
+    int x0, y0, z0;
+    int wx, wy, wz;
+    int zchunks;
+    int col_blocks;
+    int block_begin;
+};
+constexpr int kMaxRegions = 16;
+struct HeatCoef {
+    double lam, dt, rdx2, rdy2, rdz2;
+};
+struct HeatRegionList {
+    HeatRegion r[kMaxRegions];
+    int n;
+    int total_blocks;
+    HeatCoef k;
+};
+
+// ---------------------------------------------------------------- kernel launchers (kernels.cu)
+void launch_pack(const CopyList &L, cudaStream_t s);
+void launch_unpack(const CopyList &L, cudaStream_t s);
+// generic region kernel: any region list
+void launch_heat_regions(HeatRegionList &L, cudaStream_t s);
+// vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field
+bool heat_box_vectorizable(const HeatRegion &r);
+void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s);
+// max over `count` doubles of each of n pointers -> partials -> *out_dev (one double)
+void launch_field_max(const double *const *ptrs, int n, long long count, double *scratch,
+                      int scratch_len, double *out_dev, cudaStream_t s);
+int field_max_scratch_len();
+
+// ---------------------------------------------------------------- geometry and exchange plan (plan.cpp)
+// Validated grid geometry of one process (host only, no CUDA).
+struct Geom {
+    int n[3], o[3], dims[3], periods[3];
+    long long ng[3];
+    int nprocs, rank0, nlocal, nproc_procs, proc, device, path;
+    std::vector<std::array<int, 3>> coords;              // per local rank
+    std::vector<std::array<std::array<int, 2>, 3>> nbr;   // per local rank: [axis][0=lower,1=upper], -1 none
+};
+Geom make_geom(const igg_init_args *A);   // validates (IGG_E_ARG), fills topology
+
+enum Transport { kLocal = 0, kNccl = 1, kP2P = 2 };
+// one face of one update_halo call: op 0 packs a rank's send layers toward a
+// receiver, op 1 unpacks a rank's receive layers
+struct PlanMsg {
+    int op, lr, field, recv_side, peer, peer_proc, peer_lr, transport;
+    int lo, h;
+    long long count;
+    long long slot;    // element offset in the receive-arena half of the RECEIVING process
+    long long sbuf;    // op 0, NCCL: element offset in the send arena
+    int order;         // NCCL: posting position among this axis' sends (op 0) / recvs (op 1); else -1
+};
+struct Plan {
+    long long block = 0;                                   // doubles per rank in the receive arena half
+    std::vector<std::array<long long, 3>> sz;
+    std::vector<PlanMsg> msgs[3];                          // per axis: all packs, then all unpacks
+    bool any_nccl = false;
+};
+Plan build_plan(const Geom &G, const long long *sizes /* nf*3, (sx,sy,sz) */, int nf);
+
+}  // namespace igg
+
+// ---------------------------------------------------------------- the grid object
+struct igg_grid : igg::Geom {
+    bool finalized = false;
+
+    // streams and events (transfers on non-blocking high-priority streams)
+    cudaStream_t s_comm = nullptr, s_inner = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_comm = nullptr, ev_inner = nullptr;
+
+    // communicator
+    ncclComm_t comm = nullptr;
+
+    // buffer pool: receive arena (two parity halves), send arena (NCCL path)
+    char *recv_arena = nullptr;
+    size_t recv_half = 0;                                // bytes per parity half
+    char *send_arena = nullptr;
+    size_t send_cap = 0;
+    std::vector<char *> peer_recv;                       // per process: mapped recv arena (P2P)
+    unsigned long long *flags = nullptr;                 // [nlocal][3][2] receive flags
+    std::vector<unsigned long long *> peer_flags;        // per process: mapped flags (P2P)
+    unsigned int *tickets = nullptr;                     // [3] pack last-block election
+    int *d_err = nullptr;
+    double *d_scratch = nullptr;                         // reductions
+    double *d_pinned_out = nullptr;                      // host-pinned scalar
+    unsigned long long epoch = 0;
+    long long allocs = 0;
+    long long launches = 0;
+
+    // e2e scratch (igg_heat_run_host)
+    double *run_T = nullptr, *run_T2 = nullptr, *run_Ci = nullptr;
+    size_t run_bytes = 0;
+
+    // profiling of the main stencil launches (IGG_OPT_PROFILE)
+    bool profile = false;
+    std::vector<cudaEvent_t> prof_ev;
+    size_t prof_used = 0;
+    long long prof_cells = 0;
+
+    // options
+    bool skip_comm = false;
+    long long spin_timeout_ms = 20000;
+    int stencil_kernel = 0;
+    int sm_count = 148;
+    double clock_khz = 1.9e6;
+};
+
+namespace igg {
+void exchange(igg_grid *g, const igg_field *fields, int nfields, cudaStream_t st);
+void check_live(const igg_grid *g, const char *what);
+void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
+               double lam, double dt, double dx, double dy, double dz, const int bw[3],
+               cudaStream_t s);
+void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap);
+int local_index(const igg_grid *g, int global_rank);   // -1 if not hosted here
+void prof_begin(igg_grid *g, cudaStream_t s);
+void prof_end(igg_grid *g, cudaStream_t s, long long cells);
+int proc_of(const igg_grid *g, int global_rank);
+}  // namespace igg

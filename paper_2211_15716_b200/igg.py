@@ -1,0 +1,299 @@
+"""Python binding of libigg (include/igg.h): same names, argument marshalling only.
+
+Every step of the hot path (stencil, pack/unpack, exchange, scheduling) runs
+in libigg's CUDA kernels and C++ host code.  PyTorch supplies device memory
+(tensors), the caller's stream and the process group used to broadcast the
+NCCL unique id.
+
+The three functions of the paper: ``init_global_grid`` (listing
+23), ``Grid.update_halo`` (listing 38) and
+``Grid.finalize_global_grid`` (listing 43), plus ``nx_g()``
+``ny_g()`` ``nz_g()`` and the fused hide_communication heat
+step.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Sequence
+
+from . import _lib as L
+
+PATH_NCCL = 0
+PATH_P2P = 1
+_PATHS = {"nccl": PATH_NCCL, "p2p": PATH_P2P}
+
+OPT_SKIP_COMM = 1
+OPT_SPIN_TIMEOUT_MS = 2
+OPT_STENCIL_KERNEL = 3
+OPT_PROFILE = 4
+
+STATUS = {0: "IGG_OK", 1: "IGG_E_ARG", 2: "IGG_E_STATE", 3: "IGG_E_STAGGER", 4: "IGG_E_WIDTH",
+          5: "IGG_E_CUDA", 6: "IGG_E_NCCL", 7: "IGG_E_TIMEOUT", 8: "IGG_E_UNSUPPORTED"}
+
+
+class IggError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+def _ok(rc: int) -> None:
+    if rc != 0:
+        raise IggError(rc, L.lib().igg_last_error().decode(errors="replace"))
+
+
+def _i3(v) -> ctypes.Array:
+    return (ctypes.c_int * 3)(*[int(x) for x in v])
+
+
+# ------------------------------------------------------------------ host-only topology math
+def dims_create(nprocs: int, fixed=(0, 0, 0)) -> tuple:
+    out = (ctypes.c_int * 3)()
+    _ok(L.lib().igg_dims_create(nprocs, _i3(fixed), out))
+    return tuple(out)
+
+
+def rank_of_coords(dims, coords) -> int:
+    r = ctypes.c_int()
+    _ok(L.lib().igg_rank_of_coords(_i3(dims), _i3(coords), ctypes.byref(r)))
+    return r.value
+
+
+def coords_of_rank(dims, rank: int) -> tuple:
+    out = (ctypes.c_int * 3)()
+    _ok(L.lib().igg_coords_of_rank(_i3(dims), rank, out))
+    return tuple(out)
+
+
+def global_size(n: int, o: int, p: int, periodic: bool) -> int:
+    out = ctypes.c_longlong()
+    _ok(L.lib().igg_global_size(n, o, p, int(bool(periodic)), ctypes.byref(out)))
+    return out.value
+
+
+def halo_spec(n: int, o: int, s: int) -> dict:
+    hs = L.igg_halo_spec()
+    _ok(L.lib().igg_halo_spec_of(n, o, s, ctypes.byref(hs)))
+    return dict(ol=hs.ol, h=hs.h, send_lower=tuple(hs.send_lower), recv_lower=tuple(hs.recv_lower),
+                send_upper=tuple(hs.send_upper), recv_upper=tuple(hs.recv_upper))
+
+
+def _init_args(nx, ny, nz, dims, periods, overlaps, nprocs, rank0, local_ranks, device, path):
+    a = L.igg_init_args()
+    a.nx, a.ny, a.nz = nx, ny, nz
+    for i in range(3):
+        a.dims[i], a.periods[i], a.overlaps[i] = int(dims[i]), int(bool(periods[i])), int(overlaps[i])
+    a.nprocs, a.rank0, a.local_ranks, a.device = nprocs, rank0, local_ranks, device
+    a.path = _PATHS[path] if isinstance(path, str) else int(path)
+    return a
+
+
+TRANSPORTS = {0: "local", 1: "nccl", 2: "p2p"}
+
+
+def plan_update_halo(n, dims, periods, overlaps, nprocs: int, rank0: int, local_ranks: int, path, sizes) -> list:
+    """Host-only exchange plan of one update_halo call of a process (igg_plan_update_halo).
+    sizes: list of (sx, sy, sz) per field.  Returns a list of dicts in execution order."""
+    a = _init_args(*n, dims, periods, overlaps, nprocs, rank0, local_ranks, 0, path)
+    sz = (ctypes.c_longlong * (3 * len(sizes)))(*[int(v) for s in sizes for v in s])
+    cnt = ctypes.c_int()
+    _ok(L.lib().igg_plan_update_halo(ctypes.byref(a), sz, len(sizes), None, 0, ctypes.byref(cnt)))
+    out = (L.igg_plan_entry * max(cnt.value, 1))()
+    _ok(L.lib().igg_plan_update_halo(ctypes.byref(a), sz, len(sizes), out, cnt.value, ctypes.byref(cnt)))
+    keys = [k for k, _ in L.igg_plan_entry._fields_]
+    res = [{k: getattr(out[i], k) for k in keys} for i in range(cnt.value)]
+    for e in res:
+        e["transport"] = TRANSPORTS[e["transport"]]
+    return res
+
+
+def get_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _ok(L.lib().igg_get_unique_id(buf))
+    return bytes(buf)
+
+
+# ------------------------------------------------------------------ tensors
+def _as_list(x, n: int) -> list:
+    lst = list(x) if isinstance(x, (list, tuple)) else [x]
+    if len(lst) != n:
+        raise ValueError(f"expected {n} per-rank tensors, got {len(lst)}")
+    return lst
+
+
+def _dev_ptr(t) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError("fields must be torch tensors")
+    if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.dim() != 3:
+        raise ValueError("fields must be contiguous 3-D float64 CUDA tensors of shape (sz, sy, sx)")
+    return t.data_ptr()
+
+
+def _ptr_array(ts) -> ctypes.Array:
+    return (ctypes.c_void_p * len(ts))(*[_dev_ptr(t) for t in ts])
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+# ------------------------------------------------------------------ the grid
+class Grid:
+    """A live implicit global grid (one process, `local_ranks` ranks on one GPU)."""
+
+    def __init__(self, handle, me, coords, dims, n_g, n, overlaps, periods, nprocs, rank0, local_ranks, path):
+        self._h = handle
+        self.me, self.coords, self.dims, self.n_g = me, coords, dims, n_g
+        self.n, self.overlaps, self.periods = n, overlaps, periods
+        self.nprocs, self.rank0, self.local_ranks, self.path = nprocs, rank0, local_ranks, path
+
+    # -- queries
+    def _handle(self):
+        if self._h is None:
+            raise IggError(2, "grid already finalized")
+        return self._h
+
+    def n_global(self, axis: int, field_size: int = 0) -> int:
+        out = ctypes.c_longlong()
+        _ok(L.lib().igg_n_g(self._handle(), axis, field_size, ctypes.byref(out)))
+        return out.value
+
+    def nx_g(self, field_size: int = 0) -> int:
+        return self.n_global(0, field_size)
+
+    def ny_g(self, field_size: int = 0) -> int:
+        return self.n_global(1, field_size)
+
+    def nz_g(self, field_size: int = 0) -> int:
+        return self.n_global(2, field_size)
+
+    def coords_of(self, rank: int) -> tuple:
+        out = (ctypes.c_int * 3)()
+        _ok(L.lib().igg_coords(self._handle(), rank, out))
+        return tuple(out)
+
+    def local_to_global(self, rank: int, axis: int, l: int) -> int:
+        out = ctypes.c_longlong()
+        _ok(L.lib().igg_local_to_global(self._handle(), rank, axis, l, ctypes.byref(out)))
+        return out.value
+
+    def global_indices(self, rank: int, axis: int, size: int):
+        import numpy as np
+        return np.array([self.local_to_global(rank, axis, l) for l in range(size)], dtype=np.int64)
+
+    def buffer_allocs(self) -> int:
+        out = ctypes.c_longlong()
+        _ok(L.lib().igg_buffer_allocs(self._handle(), ctypes.byref(out)))
+        return out.value
+
+    def kernel_launches(self) -> int:
+        out = ctypes.c_longlong()
+        _ok(L.lib().igg_kernel_launches(self._handle(), ctypes.byref(out)))
+        return out.value
+
+    # -- update_halo!
+    def update_halo(self, *fields, stream=None) -> None:
+        """Each field: a tensor (one local rank) or a list of local_ranks tensors."""
+        per = [_as_list(f, self.local_ranks) for f in fields]
+        nf = len(per)
+        arr = (L.igg_field * (nf * self.local_ranks))()
+        for r in range(self.local_ranks):
+            for f in range(nf):
+                t = per[f][r]
+                e = arr[r * nf + f]
+                e.ptr = _dev_ptr(t)
+                sz, sy, sx = t.shape
+                e.size[0], e.size[1], e.size[2] = sx, sy, sz
+        _ok(L.lib().igg_update_halo(self._handle(), arr, nf, _stream(stream)))
+
+    # -- @hide_communication bw begin step!; update_halo!(T2) end
+    def heat_step(self, T2, T, Ci, lam: float, dt: float, dx: float, dy: float, dz: float,
+                  bw=(16, 2, 2), stream=None) -> None:
+        n = self.local_ranks
+        t2, t, c = (_as_list(x, n) for x in (T2, T, Ci))
+        for x in t2 + t + c:
+            if tuple(x.shape) != (self.n[2], self.n[1], self.n[0]):
+                raise ValueError("heat_step fields must have the canonical local shape (nz, ny, nx)")
+        _ok(L.lib().igg_heat_step(self._handle(), _ptr_array(t2), _ptr_array(t), _ptr_array(c),
+                                  lam, dt, dx, dy, dz, _i3(bw), _stream(stream)))
+
+    def heat_run_host(self, T_host, Ci_host, lam, dt, dx, dy, dz, nt: int, bw=(16, 2, 2), stream=None) -> None:
+        """Fig. 1 end to end from host memory (numpy arrays or CPU tensors, ideally pinned);
+        T_host is overwritten with the final T."""
+        def hp(a):
+            if hasattr(a, "data_ptr"):
+                assert not a.is_cuda and a.is_contiguous() and str(a.dtype) == "torch.float64"
+                return a.data_ptr()
+            assert a.dtype.name == "float64" and a.flags.c_contiguous
+            return a.ctypes.data
+        _ok(L.lib().igg_heat_run_host(self._handle(), hp(T_host), hp(Ci_host), lam, dt, dx, dy, dz, nt,
+                                      _i3(bw), _stream(stream)))
+
+    # -- reductions
+    def global_max(self, local: float) -> float:
+        out = ctypes.c_double()
+        _ok(L.lib().igg_global_max(self._handle(), float(local), ctypes.byref(out)))
+        return out.value
+
+    def field_global_max(self, f, stream=None) -> float:
+        ts = _as_list(f, self.local_ranks)
+        out = ctypes.c_double()
+        _ok(L.lib().igg_field_global_max(self._handle(), _ptr_array(ts), ts[0].numel(), ctypes.byref(out),
+                                         _stream(stream)))
+        return out.value
+
+    # -- control
+    def set_option(self, key: int, value: int) -> None:
+        _ok(L.lib().igg_set_option(self._handle(), key, int(value)))
+
+    def profile_stencil(self) -> tuple:
+        """(ms_total, launches, cells) of the profiled main stencil launches; resets."""
+        ms, n, c = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
+        _ok(L.lib().igg_profile_stencil(self._handle(), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(c)))
+        return ms.value, n.value, c.value
+
+    def check(self) -> None:
+        _ok(L.lib().igg_check(self._handle()))
+
+    # -- finalize_global_grid
+    def finalize_global_grid(self) -> None:
+        _ok(L.lib().igg_finalize_global_grid(self._handle()))
+        self._h = None
+
+    finalize = finalize_global_grid
+
+
+def init_global_grid(nx: int, ny: int, nz: int, dims=(0, 0, 0), periods=(0, 0, 0), overlaps=(2, 2, 2),
+                     path: str = "nccl", local_ranks: int = 1, device: int | None = None,
+                     process_group=None) -> Grid:
+    """init_global_grid.  With torch.distributed initialised and
+    world size > 1 this is collective: process 0's NCCL unique id is broadcast
+    over the process group (gloo or nccl)."""
+    import torch
+    world, prank = 1, 0
+    dist = torch.distributed
+    if dist.is_available() and dist.is_initialized():
+        world = dist.get_world_size(process_group)
+        prank = dist.get_rank(process_group)
+    if device is None:
+        device = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device() if torch.cuda.is_available() else 0))
+    a = _init_args(nx, ny, nz, dims, periods, overlaps, world * local_ranks, prank * local_ranks, local_ranks,
+                   device, path)
+    if world > 1:
+        obj = [get_unique_id() if prank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=process_group)
+        ctypes.memmove(a.comm_id, obj[0], 128)
+    h = ctypes.c_void_p()
+    me = ctypes.c_int()
+    c = (ctypes.c_int * 3)()
+    d = (ctypes.c_int * 3)()
+    ng = (ctypes.c_longlong * 3)()
+    _ok(L.lib().igg_init_global_grid(ctypes.byref(a), ctypes.byref(h), ctypes.byref(me), c, d, ng))
+    return Grid(h, me.value, tuple(c), tuple(d), tuple(ng), (nx, ny, nz), tuple(int(x) for x in overlaps),
+                tuple(int(bool(p)) for p in periods), a.nprocs, a.rank0, local_ranks, a.path)

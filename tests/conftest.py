@@ -10,3 +10,13 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run through gpurun)")
     config.addinivalue_line("markers", "slow: long-running (full-size) case")
+
+
+def pytest_sessionstart(session):
+    # test infrastructure: make sure the in-tree library and the C oracle are
+    # built (the product itself never builds or falls back; it raises)
+    from paper_2211_15716_b200 import build as B
+    if B.needs_build():
+        B.build()
+    from oracle import heat3d as OH
+    OH.build()

@@ -1,0 +1,114 @@
+"""Multi-GPU parity worker (launched by tests/test_gpu_multi.py with torchrun,
+one process per GPU).  Every check compares the CUDA path (NCCL or P2P
+transport) with the CPU oracle bit-exactly; exits non-zero on any failure."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import paper_2211_15716_b200 as P
+from paper_2211_15716_b200 import heat3d as app
+from oracle import grid as OG
+from oracle import halo as OHL
+from oracle import heat3d as OH
+import synthetic_inputs as SI
+
+DIMS = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+
+
+def log(*a):
+    print(f"[rank {dist.get_rank()}]", *a, flush=True)
+
+
+def heat_case(path, n, dims, per, local, bw, nt=8):
+    world = dist.get_world_size()
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
+                           device=int(os.environ["LOCAL_RANK"]))
+    try:
+        T, T2, Ci = app.alloc_fields(g)
+        app.init_random(g, T, T2, Ci)
+        d = app.spacing(g)
+        dt = app.stable_dt(g, Ci, *d)
+        T, T2 = app.run(g, T, T2, Ci, nt, dt, d, bw=bw)
+        torch.cuda.synchronize()
+        g.check()
+        N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+        T0g, Cig = SI.global_heat_fields(*N)
+        dref = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+        dtr = OH.stable_dt(*dref, 1.0, Cig)
+        assert dt == dtr, (dt, dtr)
+        ref = OH.heat_run(T0g, Cig, nt, per, 1.0, dtr, *dref, OH.CANONICAL)
+        for lr in range(local):
+            c = OG.coords_of_rank(g.rank0 + lr, dims)
+            W = OG.window(ref, c, dims, n, (2, 2, 2), per, n)
+            got = T[lr].cpu().numpy()
+            if not np.array_equal(got, W):
+                raise AssertionError(f"heat {path} {dims} per={per} rank {g.rank0 + lr}: "
+                                     f"{int((got != W).sum())} cells differ")
+    finally:
+        g.finalize()
+    log("heat OK", path, dims, per, "local", local, "world", world)
+
+
+def halo_case(path, n, dims, per, local, sizes, seed, repeat=2):
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
+                           device=int(os.environ["LOCAL_RANK"]))
+    try:
+        nprocs = g.nprocs
+        mine = {g.rank0 + lr: [SI.random_field(s[::-1], seed * 1000 + 10 * (g.rank0 + lr) + f)
+                               for f, s in enumerate(sizes)] for lr in range(local)}
+        allp = [None] * dist.get_world_size()
+        dist.all_gather_object(allp, mine)
+        ref = {}
+        for x in allp:
+            ref.update(x)
+        for _ in range(repeat):
+            OHL.update_halo(ref, dims, per, n, (2, 2, 2))
+        dev = [[torch.from_numpy(mine[g.rank0 + lr][f]).cuda() for lr in range(local)] for f in range(len(sizes))]
+        for _ in range(repeat):
+            g.update_halo(*dev)
+        torch.cuda.synchronize()
+        g.check()
+        for f in range(len(sizes)):
+            for lr in range(local):
+                got = dev[f][lr].cpu().numpy()
+                if not np.array_equal(got, ref[g.rank0 + lr][f]):
+                    raise AssertionError(f"halo {path} {dims} per={per} rank {g.rank0 + lr} field {f}")
+    finally:
+        g.finalize()
+    log("halo OK", path, dims, per, "local", local)
+
+
+def main():
+    local_rank = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    world = dist.get_world_size()
+    paths = sys.argv[1].split(",") if len(sys.argv) > 1 else ["nccl", "p2p"]
+    dims = DIMS[world]
+    n = (40, 36, 34)
+    sizes = [n, (41, 36, 34), (40, 37, 34), (40, 36, 35)]
+    for path in paths:
+        heat_case(path, n, dims, (0, 0, 0), 1, (16, 2, 2))
+        heat_case(path, n, dims, (1, 0, 1), 1, (4, 2, 2))
+        halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
+        halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
+        # 8 ranks as virtual ranks over the processes (2x2x2 correctness on fewer GPUs)
+        if 8 % world == 0 and world < 8:
+            heat_case(path, (24, 20, 18), (2, 2, 2), (0, 0, 0), 8 // world, (4, 2, 2))
+            halo_case(path, (24, 20, 18), (2, 2, 2), (1, 0, 1), 8 // world,
+                      [(24, 20, 18), (25, 20, 18), (24, 21, 18), (24, 20, 19)], seed=3)
+    dist.barrier()
+    if dist.get_rank() == 0:
+        print("MULTI-GPU PARITY OK", world, paths, flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

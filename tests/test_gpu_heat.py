@@ -1,0 +1,156 @@
+"""GPU parity of the heat step (CUDA path through the C ABI) against the CPU
+oracle on the global grid.  Gates (north star):
+bit-exact vs the canonical oracle, max relative error <= 1e-12 vs the
+paper-literal oracle, halos included; distributed == single-GPU bit-exact."""
+import numpy as np
+import pytest
+
+import paper_2211_15716_b200 as P
+from paper_2211_15716_b200 import heat3d as app
+from oracle import grid as OG
+from oracle import heat3d as OH
+
+from _heat_cases import assert_windows, gpu_run, oracle_global
+
+pytestmark = pytest.mark.gpu
+
+
+def _N(n, dims, per, o):
+    return tuple(OG.global_size(n[i], o[i], dims[i], bool(per[i])) for i in range(3))
+
+
+@pytest.mark.parametrize("n", [(40, 33, 30), (37, 33, 30), (130, 20, 66)])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_single_rank_vs_oracle(n, kernel):
+    dims, per, o = (1, 1, 1), (0, 0, 0), (2, 2, 2)
+    out, dt, _, _ = gpu_run(P, app, n, dims, per, o, 10, (16, 2, 2), options={P.OPT_STENCIL_KERNEL: kernel})
+    can, dtr = oracle_global(n, per, 10)
+    assert dt == dtr
+    assert_windows(out, can, dims, n, o, per)
+    lit, _ = oracle_global(n, per, 10, mode=OH.LITERAL)
+    assert_windows(out, lit, dims, n, o, per, exact=False)
+
+
+@pytest.mark.parametrize("bw", [(0, 0, 0), (16, 2, 2), (4, 2, 2)])
+@pytest.mark.parametrize("n", [(32, 32, 32), (17, 32, 32)])
+def test_config_b7_emulated_2x1x1(n, bw):
+    """B:7: local 32^3 nt=10 (reading i) and global 32^3 split in two 17x32x32 (reading ii)."""
+    dims, per, o = (2, 1, 1), (0, 0, 0), (2, 2, 2)
+    out, dt, _, _ = gpu_run(P, app, n, dims, per, o, 10, bw)
+    N = _N(n, dims, per, o)
+    can, dtr = oracle_global(N, per, 10)
+    assert dt == dtr
+    assert_windows(out, can, dims, n, o, per)
+    lit, _ = oracle_global(N, per, 10, mode=OH.LITERAL)
+    assert_windows(out, lit, dims, n, o, per, exact=False)
+
+
+def test_config_b7_periodic_x():
+    dims, per, o, n = (2, 1, 1), (1, 0, 0), (2, 2, 2), (32, 32, 32)
+    out, _, _, _ = gpu_run(P, app, n, dims, per, o, 10, (4, 2, 2))
+    can, _ = oracle_global(_N(n, dims, per, o), per, 10)
+    assert_windows(out, can, dims, n, o, per)
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=(24, 20, 18), dims=(2, 2, 2), per=(0, 0, 0), o=(2, 2, 2), bw=(16, 2, 2)),
+    dict(n=(24, 20, 18), dims=(2, 2, 2), per=(0, 0, 0), o=(2, 2, 2), bw=(4, 3, 2)),
+    dict(n=(26, 20, 18), dims=(2, 2, 1), per=(1, 0, 1), o=(2, 2, 2), bw=(4, 2, 2)),
+    dict(n=(22, 21, 19), dims=(3, 1, 2), per=(0, 1, 0), o=(4, 2, 2), bw=(4, 2, 2)),
+    dict(n=(20, 18, 16), dims=(1, 1, 1), per=(1, 1, 1), o=(2, 2, 2), bw=(4, 2, 2)),   # self-wrap
+    dict(n=(34, 18, 16), dims=(4, 1, 1), per=(0, 0, 0), o=(2, 2, 2), bw=(2, 2, 2)),
+])
+def test_virtual_topologies_bit_exact(case):
+    n, dims, per, o, bw = case["n"], case["dims"], case["per"], case["o"], case["bw"]
+    out, dt, _, _ = gpu_run(P, app, n, dims, per, o, 6, bw)
+    can, dtr = oracle_global(_N(n, dims, per, o), per, 6)
+    assert dt == dtr
+    assert_windows(out, can, dims, n, o, per)
+
+
+def test_overlap_schedule_equals_sequential():
+    n, dims, per, o = (40, 24, 20), (2, 2, 1), (0, 0, 0), (2, 2, 2)
+    a, _, _, _ = gpu_run(P, app, n, dims, per, o, 8, (0, 0, 0))
+    b, _, _, _ = gpu_run(P, app, n, dims, per, o, 8, (16, 2, 2))
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_width_precondition():
+    import torch
+    g = P.init_global_grid(32, 16, 16, dims=(2, 1, 1), local_ranks=2, device=0)
+    try:
+        T, T2, Ci = app.alloc_fields(g)
+        app.init_paper(g, T, T2, Ci)
+        with pytest.raises(P.IggError) as e:
+            g.heat_step(T2, T, Ci, 1.0, 1e-3, 0.1, 0.1, 0.1, bw=(1, 2, 2))
+        assert e.value.name == "IGG_E_WIDTH"
+        g.heat_step(T2, T, Ci, 1.0, 1e-3, 0.1, 0.1, 0.1, bw=(2, 0, 0))   # y, z have no neighbours
+        torch.cuda.synchronize()
+    finally:
+        g.finalize()
+
+
+def test_fixed_point_and_buffer_reuse():
+    n, dims, per, o = (34, 18, 16), (2, 1, 1), (0, 0, 0), (2, 2, 2)
+    out, _, allocs, _ = gpu_run(P, app, n, dims, per, o, 100, (16, 2, 2), init="paper")
+    for A in out:
+        assert np.all(A == 1.7)
+    assert allocs[0] == allocs[-1]
+
+
+def test_state_errors():
+    g = P.init_global_grid(8, 8, 8, dims=(1, 1, 1), device=0)
+    g.finalize()
+    with pytest.raises(P.IggError) as e:
+        g.nx_g()
+    assert e.value.name == "IGG_E_STATE"
+
+
+def test_field_global_max_and_dt():
+    import torch
+    g = P.init_global_grid(20, 18, 16, dims=(2, 1, 1), local_ranks=2, device=0)
+    try:
+        T, T2, Ci = app.alloc_fields(g)
+        app.init_random(g, T, T2, Ci)
+        ref = max(float(c.max()) for c in Ci)
+        assert g.field_global_max(Ci) == ref
+        assert g.global_max(0.25) == 0.25
+        torch.cuda.synchronize()
+    finally:
+        g.finalize()
+
+
+def test_heat_run_host_equals_device_loop():
+    import torch
+    n = (40, 24, 20)
+    g = P.init_global_grid(*n, dims=(2, 1, 1), local_ranks=2, device=0)
+    try:
+        T, T2, Ci = app.alloc_fields(g)
+        app.init_random(g, T, T2, Ci)
+        d = app.spacing(g)
+        dt = app.stable_dt(g, Ci, *d)
+        Th = torch.stack([t.cpu() for t in T]).contiguous().pin_memory()
+        Ch = torch.stack([c.cpu() for c in Ci]).contiguous().pin_memory()
+        g.heat_run_host(Th, Ch, 1.0, dt, *d, 7, bw=(16, 2, 2))
+        T, T2 = app.run(g, T, T2, Ci, 7, dt, d)
+        torch.cuda.synchronize()
+        for r in range(2):
+            assert torch.equal(Th[r], T[r].cpu())
+    finally:
+        g.finalize()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("init", ["random", "paper"])
+def test_full_size_512_nt100_vs_oracle(init):
+    """B:8 at full size in the bench's launch configuration (1 GPU, 512^3,
+    nt=100, hide_communication (16,2,2)), every cell compared."""
+    n, dims, per, o = (512, 512, 512), (1, 1, 1), (0, 0, 0), (2, 2, 2)
+    out, dt, _, _ = gpu_run(P, app, n, dims, per, o, 100, (16, 2, 2), init=init)
+    can, dtr = oracle_global(n, per, 100, init=init)
+    assert dt == dtr
+    assert np.array_equal(out[0], can)
+    if init == "random":
+        lit, _ = oracle_global(n, per, 100, init=init, mode=OH.LITERAL)
+        assert np.max(np.abs(out[0] - lit) / np.abs(lit)) <= 1e-12
