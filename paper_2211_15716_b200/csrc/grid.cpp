@@ -126,14 +126,13 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
     for (int a = 0; a < 3; ++a) {   // x -> y -> z, each axis complete before the next
         if (plan.msgs[a].empty()) continue;
         CopyList P{}, U{};
+        std::vector<CopyDesc> pd, ud;
         P.ticket = g->tickets + a;
         P.epoch = U.epoch = g->epoch;
         U.err = P.err = g->d_err;
         U.timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
         std::vector<const PlanMsg *> sends, recvs;
         for (const PlanMsg &m : plan.msgs[a]) {
-            CopyList &C = m.op == 0 ? P : U;
-            if (C.n >= kMaxCopy) fail(IGG_E_UNSUPPORTED, "update_halo: too many faces per axis");
             CopyDesc d{};
             const igg_field &F = fields[m.lr * nf + m.field];
             d.field = F.ptr;
@@ -178,10 +177,9 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
                     recvs.push_back(&m);
                 }
             }
-            C.d[C.n++] = d;
+            (m.op == 0 ? pd : ud).push_back(d);
         }
-        launch_pack(P, st);
-        g->launches++;
+        g->launches += launch_copies(0, pd, P, st);
         if (!sends.empty() || !recvs.empty()) {
             auto by_order = [](const PlanMsg *x, const PlanMsg *y) { return x->order < y->order; };
             std::sort(sends.begin(), sends.end(), by_order);
@@ -193,8 +191,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
                 IGG_NCCL(ncclRecv(recv + m->slot, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
             IGG_NCCL(ncclGroupEnd());
         }
-        launch_unpack(U, st);
-        g->launches++;
+        g->launches += launch_copies(1, ud, U, st);
     }
 }
 

@@ -83,6 +83,7 @@ struct CopyList {
     unsigned long long *signal[kMaxSignal];
     int nsignal;
     unsigned int *ticket;            // device counter for the last-block election
+    unsigned int ticket_total;       // blocks over ALL chunks of this pack (the last one signals)
     // unpack: wait until *wait[flag_slot] >= epoch (ld.acquire.sys) before reading
     const unsigned long long *wait[kMaxSignal];
     unsigned long long epoch;
@@ -114,8 +115,9 @@ struct HeatRegionList {
 };
 
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
-void launch_pack(const CopyList &L, cudaStream_t s);
-void launch_unpack(const CopyList &L, cudaStream_t s);
+// pack (op 0) or unpack (op 1) of any number of faces: chunks of kMaxCopy
+// descriptors per launch; `proto` carries signals/waits/epoch; returns launches
+int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s);
 // generic region kernel: any region list
 void launch_heat_regions(HeatRegionList &L, cudaStream_t s);
 // vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field

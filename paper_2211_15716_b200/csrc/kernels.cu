@@ -5,6 +5,7 @@
 //
 // Fp64 throughout ("@init_parallel_stencil(CUDA, Float64, 3)").
 // No tensor cores: the 7-point stencil is not a contraction.
+#include <algorithm>
 #include <cstdio>
 
 #include "igg_internal.h"
@@ -204,9 +205,8 @@ __global__ void __launch_bounds__(kCopyThreads) pack_kernel(const __grid_constan
         __threadfence_system();
         __syncthreads();
         if (threadIdx.x == 0) {
-            const unsigned total = gridDim.x * gridDim.y;
             const unsigned t = atomicAdd(L.ticket, 1u);
-            if (t == total - 1) {
+            if (t == L.ticket_total - 1) {
                 __threadfence_system();
                 for (int s = 0; s < L.nsignal; ++s) st_release_sys(L.signal[s], L.epoch);
                 atomicExch(L.ticket, 0u);
@@ -239,27 +239,40 @@ __global__ void __launch_bounds__(kCopyThreads) unpack_kernel(const __grid_const
         d.field[face_index(d, i)] = __ldcg(d.buf + i);
 }
 
-static int copy_blocks(const CopyList &L) {
+static int copy_blocks(const CopyDesc *d, int n) {
     long long mx = 1;
-    for (int j = 0; j < L.n; ++j) mx = L.d[j].count > mx ? L.d[j].count : mx;
+    for (int j = 0; j < n; ++j) mx = d[j].count > mx ? d[j].count : mx;
     long long b = (mx + kCopyThreads * 4 - 1) / (kCopyThreads * 4);
     if (b < 1) b = 1;
     if (b > 1024) b = 1024;
     return (int)b;
 }
 
-void launch_pack(const CopyList &L, cudaStream_t s) {
-    if (L.n == 0) return;
-    dim3 grid(copy_blocks(L), L.n);
-    pack_kernel<<<grid, kCopyThreads, 0, s>>>(L);
-    IGG_CUDA(cudaGetLastError());
-}
-
-void launch_unpack(const CopyList &L, cudaStream_t s) {
-    if (L.n == 0) return;
-    dim3 grid(copy_blocks(L), L.n);
-    unpack_kernel<<<grid, kCopyThreads, 0, s>>>(L);
-    IGG_CUDA(cudaGetLastError());
+int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s) {
+    const int n = (int)descs.size();
+    if (n == 0) return 0;
+    // total blocks of all chunks: the pack block that draws the last ticket
+    // (necessarily in the last chunk, stream order) publishes the flags
+    unsigned total = 0;
+    for (int c = 0; c < n; c += kMaxCopy) {
+        const int m = std::min(kMaxCopy, n - c);
+        total += (unsigned)copy_blocks(descs.data() + c, m) * m;
+    }
+    int launches = 0;
+    for (int c = 0; c < n; c += kMaxCopy) {
+        CopyList L = proto;
+        L.n = std::min(kMaxCopy, n - c);
+        for (int j = 0; j < L.n; ++j) L.d[j] = descs[c + j];
+        L.ticket_total = total;
+        dim3 grid(copy_blocks(L.d, L.n), L.n);
+        if (op == 0)
+            pack_kernel<<<grid, kCopyThreads, 0, s>>>(L);
+        else
+            unpack_kernel<<<grid, kCopyThreads, 0, s>>>(L);
+        IGG_CUDA(cudaGetLastError());
+        ++launches;
+    }
+    return launches;
 }
 
 // ============================================================== max reduction
