@@ -232,7 +232,7 @@ static void launch_full(igg_grid *g, double *const *T2, const double *const *T, 
         R.wz = g->n[2] - 2;
         if (g->stencil_kernel != 1 && heat_box_vectorizable(R)) {
             prof_begin(g, s);
-            launch_heat_box(R, k, s);
+            launch_heat_box(R, k, s, g->stencil_kernel);
             prof_end(g, s, (long long)R.wx * R.wy * R.wz);
             g->launches++;
         } else {
@@ -350,7 +350,7 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
         R.wz = hi[2] - lo[2];
         prof_begin(g, g->s_inner);
         if (g->stencil_kernel != 1 && heat_box_vectorizable(R)) {
-            launch_heat_box(R, k, g->s_inner);
+            launch_heat_box(R, k, g->s_inner, g->stencil_kernel);
         } else {
             HeatRegionList one{};
             one.k = k;

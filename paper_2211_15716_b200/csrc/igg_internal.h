@@ -122,7 +122,7 @@ int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &pr
 void launch_heat_regions(HeatRegionList &L, cudaStream_t s);
 // vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field
 bool heat_box_vectorizable(const HeatRegion &r);
-void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s);
+void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant);
 // max over `count` doubles of each of n pointers -> partials -> *out_dev (one double)
 void launch_field_max(const double *const *ptrs, int n, long long count, double *scratch,
                       int scratch_len, double *out_dev, cudaStream_t s);

@@ -91,11 +91,15 @@ void launch_heat_regions(HeatRegionList &L, cudaStream_t s) {
 // rows of the adjacent warps (L1 hits; tile-edge rows from L2).  DRAM sees
 // T, Ci read once and T2 written once per cell plus tile-edge re-reads:
 // 24 B/cell algorithmic.
-constexpr int kBoxTY = 8;
-constexpr int kBoxThreads = 32 * kBoxTY;
-constexpr int kBoxKc = 32;
+__device__ __forceinline__ double2 ldg2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
 
-__global__ void __launch_bounds__(kBoxThreads)
+// TY rows per CTA (one warp per row), KC planes per z-sweep.  With PF the
+// loads of plane z+1 (T[z+2], T[z+1] rows y+-1, Ci[z+1]) are issued before
+// plane z is computed, so every thread keeps two planes of DRAM reads in
+// flight (the kernel is bound by HBM latency x bytes in flight, not by issue;
+// see profiles/).
+template <int TY, int KC, bool PF>
+__global__ void __launch_bounds__(32 * TY, (PF ? 1024 : 1280) / (32 * TY))
     heat_box_kernel(const double *__restrict__ T, const double *__restrict__ Ci, double *__restrict__ T2,
                     int sx, int sy, int x0, int y0, int z0, int wx, int wy, int wz, int ax0, int xtiles,
                     int ytiles, const HeatCoef k) {
@@ -106,27 +110,43 @@ __global__ void __launch_bounds__(kBoxThreads)
     b /= xtiles;
     const int ty = b % ytiles;
     const int tz = b / ytiles;
-    const int y = y0 + ty * kBoxTY + warp;
+    const int y = y0 + ty * TY + warp;
     if (y >= y0 + wy) return;                       // whole warp leaves together
     const int p = ax0 + tx * 64 + 2 * lane;          // first of my two cells
     const int xend = x0 + wx;
     const bool pair_in = p < sx;                     // sx even: p+1 < sx too
     const bool w0 = pair_in && p >= x0 && p < xend;
     const bool w1 = pair_in && p + 1 >= x0 && p + 1 < xend;
-    int z = z0 + tz * kBoxKc;
-    const int zend = min(z0 + wz, z + kBoxKc);
+    int z = z0 + tz * KC;
+    const int zend = min(z0 + wz, z + KC);
     const long long sxy = (long long)sx * sy;
     long long i = (long long)z * sxy + (long long)y * sx + p;   // even -> 16-B aligned
     const double2 zero2 = make_double2(0.0, 0.0);
-    double2 zm = pair_in ? __ldg(reinterpret_cast<const double2 *>(T + i - sxy)) : zero2;
-    double2 c = pair_in ? __ldg(reinterpret_cast<const double2 *>(T + i)) : zero2;
+    double2 zm = zero2, c = zero2, zp = zero2, ym = zero2, yp = zero2, ci = zero2;
+    if (pair_in) {
+        zm = ldg2(T + i - sxy);
+        c = ldg2(T + i);
+        if (PF) {
+            zp = ldg2(T + i + sxy);
+            ym = ldg2(T + i - sx);
+            yp = ldg2(T + i + sx);
+            ci = ldg2(Ci + i);
+        }
+    }
     for (; z < zend; ++z, i += sxy) {
-        double2 zp = zero2, ym = zero2, yp = zero2, ci = zero2;
-        if (pair_in) {
-            zp = __ldg(reinterpret_cast<const double2 *>(T + i + sxy));
-            ym = __ldg(reinterpret_cast<const double2 *>(T + i - sx));
-            yp = __ldg(reinterpret_cast<const double2 *>(T + i + sx));
-            ci = __ldg(reinterpret_cast<const double2 *>(Ci + i));
+        double2 zpn = zero2, ymn = zero2, ypn = zero2, cin = zero2;
+        if (PF) {   // prefetch plane z+1 (z+2 <= sz-1 always holds inside a region)
+            if (pair_in && z + 1 < zend) {
+                zpn = ldg2(T + i + 2 * sxy);
+                ymn = ldg2(T + i + sxy - sx);
+                ypn = ldg2(T + i + sxy + sx);
+                cin = ldg2(Ci + i + sxy);
+            }
+        } else if (pair_in) {
+            zp = ldg2(T + i + sxy);
+            ym = ldg2(T + i - sx);
+            yp = ldg2(T + i + sx);
+            ci = ldg2(Ci + i);
         }
         double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
         double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
@@ -142,7 +162,25 @@ __global__ void __launch_bounds__(kBoxThreads)
         }
         zm = c;
         c = zp;
+        if (PF) {
+            zp = zpn;
+            ym = ymn;
+            yp = ypn;
+            ci = cin;
+        }
     }
+}
+
+template <int TY, int KC, bool PF>
+static void launch_box_variant(const HeatRegion &r, const HeatCoef &k, cudaStream_t s) {
+    const int ax0 = r.x0 & ~1;
+    const int xtiles = (r.x0 + r.wx - ax0 + 63) / 64;
+    const int ytiles = (r.wy + TY - 1) / TY;
+    const int ztiles = (r.wz + KC - 1) / KC;
+    const long long blocks = (long long)xtiles * ytiles * ztiles;
+    heat_box_kernel<TY, KC, PF><<<(unsigned)blocks, 32 * TY, 0, s>>>(r.T, r.Ci, r.T2, r.sx, r.sy, r.x0, r.y0, r.z0,
+                                                                      r.wx, r.wy, r.wz, ax0, xtiles, ytiles, k);
+    IGG_CUDA(cudaGetLastError());
 }
 
 bool heat_box_vectorizable(const HeatRegion &r) {
@@ -150,16 +188,171 @@ bool heat_box_vectorizable(const HeatRegion &r) {
                                 reinterpret_cast<uintptr_t>(r.T2)) % 16 == 0);
 }
 
-void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s) {
-    if (r.wx <= 0 || r.wy <= 0 || r.wz <= 0) return;
+// ------------------------------------------------------------- cp.async z-pipeline
+// Same tile and arithmetic as heat_box_kernel, but the two DRAM streams of a
+// plane (T[z+1] of my row, Ci[z]) are fetched D planes ahead with cp.async
+// (LDGSTS, L1-bypassing) into a per-thread smem ring, so the bytes in flight
+// per SM are set by D and the smem ring, not by registers.  Rows y+-1 of
+// plane z were fetched by the neighbouring warps' pipelines and are L2 hits.
+// Grid: x-tiles fastest, then y-tiles, then z-chunks; the last z-range is cut
+// into short chunks (kc2) so the final wave's tail is short.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int TY, int D, bool ST>
+__global__ void __launch_bounds__(32 * TY)
+    heat_box_async_kernel(const double *__restrict__ T, const double *__restrict__ Ci, double *__restrict__ T2,
+                          int sx, int sy, int x0, int y0, int z0, int wx, int wy, int wz, int ax0, int xtiles,
+                          int ytiles, int kc1, int nbig, int kc2, const HeatCoef k) {
+    extern __shared__ double2 ring[];   // [D][blockDim] T rows, then [D][blockDim] Ci rows
+    const int tid = threadIdx.x, bd = blockDim.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int ntiles = xtiles * ytiles;
+    const int tile = blockIdx.x % ntiles;
+    const int chunk = blockIdx.x / ntiles;
+    int zs, ze;
+    if (chunk < nbig) {
+        zs = z0 + chunk * kc1;
+        ze = min(zs + kc1, z0 + wz);
+    } else {
+        zs = z0 + nbig * kc1 + (chunk - nbig) * kc2;
+        ze = min(zs + kc2, z0 + wz);
+    }
+    const int tx = tile % xtiles, ty = tile / xtiles;
+    const int y = y0 + ty * TY + warp;
+    if (y >= y0 + wy || zs >= ze) return;            // per-thread pipeline: no CTA barrier is used
+    const int p = ax0 + tx * 64 + 2 * lane;
+    const int xend = x0 + wx;
+    const bool pair_in = p < sx;
+    const bool w0 = pair_in && p >= x0 && p < xend;
+    const bool w1 = pair_in && p + 1 >= x0 && p + 1 < xend;
+    const long long sxy = (long long)sx * sy;
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+    double2 *sT = ring, *sC = ring + D * bd;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {                    // stage q: T[zs+q+1], Ci[zs+q]
+        if (pair_in && zs + q < ze) {
+            cp_async16(&sT[q * bd + tid], T + i + (q + 1) * sxy);
+            cp_async16(&sC[q * bd + tid], Ci + i + q * sxy);
+        }
+        cp_async_commit();
+    }
+    const double2 zero2 = make_double2(0.0, 0.0);
+    double2 zm = pair_in ? ldg2(T + i - sxy) : zero2;
+    double2 c = pair_in ? ldg2(T + i) : zero2;
+    int slot = 0;
+    for (int z = zs; z < ze; ++z, i += sxy) {
+        cp_async_wait<D - 1>();
+        double2 ym = zero2, yp = zero2;
+        if (pair_in) {
+            ym = ldg2(T + i - sx);
+            yp = ldg2(T + i + sx);
+        }
+        const double2 zp = sT[slot * bd + tid];
+        const double2 ci = sC[slot * bd + tid];
+        double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
+        double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0 && w0) xm = __ldg(T + i - 1);
+        if (lane == 31 && w1) xp = __ldg(T + i + 2);
+        const double r0 = heat_cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, k);
+        const double r1 = heat_cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, k);
+        if (w0 && w1) {
+            if (ST)   // streaming store: T2 is not re-read in this step, keep L2 for T rows
+                __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+            else
+                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+        } else {
+            if (w0) T2[i] = r0;
+            if (w1) T2[i + 1] = r1;
+        }
+        zm = c;
+        c = zp;
+        // refill this slot with plane z+D (its values were consumed above)
+        if (pair_in && z + D < ze) {
+            cp_async16(&sT[slot * bd + tid], T + i + (D + 1) * sxy);
+            cp_async16(&sC[slot * bd + tid], Ci + i + D * sxy);
+        }
+        cp_async_commit();
+        slot = slot + 1 == D ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
+}
+
+template <int TY, int D, bool ST = false>
+static void launch_box_async(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int kc1, int kc2) {
     const int ax0 = r.x0 & ~1;
     const int xtiles = (r.x0 + r.wx - ax0 + 63) / 64;
-    const int ytiles = (r.wy + kBoxTY - 1) / kBoxTY;
-    const int ztiles = (r.wz + kBoxKc - 1) / kBoxKc;
-    const long long blocks = (long long)xtiles * ytiles * ztiles;
-    heat_box_kernel<<<(unsigned)blocks, kBoxThreads, 0, s>>>(r.T, r.Ci, r.T2, r.sx, r.sy, r.x0, r.y0, r.z0,
-                                                             r.wx, r.wy, r.wz, ax0, xtiles, ytiles, k);
+    const int ytiles = (r.wy + TY - 1) / TY;
+    const int ntiles = xtiles * ytiles;
+    const size_t smem = 2 * D * 32 * TY * sizeof(double2);
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        if (smem > 48 * 1024)
+            IGG_CUDA(cudaFuncSetAttribute(heat_box_async_kernel<TY, D, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, heat_box_async_kernel<TY, D, ST>, 32 * TY, smem));
+        int dev = 0;
+        IGG_CUDA(cudaGetDevice(&dev));
+        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    // tail: about two waves' worth of tile-planes at the end go in short chunks
+    int small = 0;
+    if (kc2 > 0 && kc2 < kc1) {
+        const long long conc = (long long)occ * nsm;
+        small = (int)((2 * conc * kc2 + ntiles - 1) / ntiles);
+        small = ((small + kc2 - 1) / kc2) * kc2;
+        if (small > r.wz) small = r.wz;
+    }
+    const int big = r.wz - small;
+    const int nbig = (big + kc1 - 1) / kc1;
+    // a partial last big chunk would overlap the small range: shrink the big range to whole chunks
+    const int big_planes = nbig * kc1 > big ? (nbig - 1) * kc1 : big;
+    const int nbig2 = big_planes / kc1;
+    const int rest = r.wz - nbig2 * kc1;
+    const int nsmall = kc2 > 0 ? (rest + kc2 - 1) / kc2 : 0;
+    const long long blocks = (long long)ntiles * (nbig2 + nsmall);
+    heat_box_async_kernel<TY, D, ST><<<(unsigned)blocks, 32 * TY, smem, s>>>(
+        r.T, r.Ci, r.T2, r.sx, r.sy, r.x0, r.y0, r.z0, r.wx, r.wy, r.wz, ax0, xtiles, ytiles, kc1, nbig2,
+        kc2 > 0 ? kc2 : kc1, k);
     IGG_CUDA(cudaGetLastError());
+}
+
+// variant: 0 = default (cp.async pipeline, TY=4, D=3, streaming stores, z-chunks 64 with an
+// 8-plane tail); 2..24 = the ablation variants measured in profiles/ (IGG_OPT_STENCIL_KERNEL)
+void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant) {
+    if (r.wx <= 0 || r.wy <= 0 || r.wz <= 0) return;
+    switch (variant) {
+        case 2: launch_box_variant<8, 32, false>(r, k, s); break;
+        case 4: launch_box_variant<8, 64, true>(r, k, s); break;
+        case 5: launch_box_variant<16, 32, true>(r, k, s); break;
+        case 6: launch_box_variant<4, 32, true>(r, k, s); break;
+        case 7: launch_box_variant<8, 16, true>(r, k, s); break;
+        case 8: launch_box_variant<4, 64, false>(r, k, s); break;
+        case 9: launch_box_variant<16, 64, false>(r, k, s); break;
+        case 10: launch_box_async<8, 4>(r, k, s, 64, 8); break;
+        case 11: launch_box_async<8, 6>(r, k, s, 64, 8); break;
+        case 12: launch_box_async<4, 4>(r, k, s, 64, 8); break;
+        case 13: launch_box_async<8, 4>(r, k, s, 128, 16); break;
+        case 14: launch_box_async<8, 4>(r, k, s, 32, 32); break;
+        case 15: launch_box_async<8, 3>(r, k, s, 64, 8); break;
+        case 16: launch_box_variant<4, 64, false>(r, k, s); break;
+        case 17: launch_box_async<8, 3, true>(r, k, s, 64, 8); break;
+        case 18: launch_box_async<4, 3>(r, k, s, 64, 8); break;
+        case 19: launch_box_async<8, 2>(r, k, s, 64, 8); break;
+        case 20: launch_box_async<4, 3, true>(r, k, s, 64, 8); break;
+        case 21: launch_box_async<8, 3>(r, k, s, 96, 8); break;
+        case 22: launch_box_async<16, 3>(r, k, s, 64, 8); break;
+        case 23: launch_box_async<8, 3>(r, k, s, 64, 4); break;
+        case 24: launch_box_async<8, 3>(r, k, s, 48, 8); break;
+        case 3: launch_box_variant<8, 32, true>(r, k, s); break;
+        default: launch_box_async<4, 3, true>(r, k, s, 64, 8); break;   // 0 = 20: the measured best
+    }
 }
 
 // ============================================================== face pack / unpack

@@ -154,3 +154,17 @@ def test_full_size_512_nt100_vs_oracle(init):
     if init == "random":
         lit, _ = oracle_global(n, per, 100, init=init, mode=OH.LITERAL)
         assert np.max(np.abs(out[0] - lit) / np.abs(lit)) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", list(range(2, 25)))
+def test_box_kernel_variants_bit_exact(variant):
+    """Every tuning variant of the box kernel computes the same cells (ablations
+    must be valid): 2 virtual ranks, overlap schedule, vs the canonical oracle."""
+    n, dims, per, o = (130, 44, 70), (2, 1, 1), (0, 0, 0), (2, 2, 2)
+    out, _, _, _ = gpu_run(P, app, n, dims, per, o, 5, (16, 2, 2), options={P.OPT_STENCIL_KERNEL: variant})
+    can, _ = oracle_global(_N(n, dims, per, o), per, 5)
+    assert_windows(out, can, dims, n, o, per)
+    out1, _, _, _ = gpu_run(P, app, (130, 44, 70), (1, 1, 1), per, o, 5, (16, 2, 2),
+                            options={P.OPT_STENCIL_KERNEL: variant})
+    can1, _ = oracle_global((130, 44, 70), per, 5)
+    assert np.array_equal(out1[0], can1)
