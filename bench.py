@@ -46,6 +46,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exposed", action="store_true")
+    ap.add_argument("--schedule", type=int, default=0, help="0 concurrent, 1 boundary first (paper order)")
+    ap.add_argument("--timeline", action="store_true", help="record the overlap timeline (extra events)")
+    ap.add_argument("--xalign", type=int, default=64, help="x boundary-slab alignment in cells (1 = exact bw)")
+    ap.add_argument("--periodic", default="0,0,0", help="periodic axes (1-GPU self-wrap experiments)")
+    ap.add_argument("--skip-comm", action="store_true", help="timing experiment only: no exchange (INVALID results)")
     return ap.parse_args()
 
 
@@ -195,9 +200,14 @@ def main():
     dims = DIMS.get(world) or P.dims_create(world)
     bw = tuple(int(x) for x in a.bw.split(","))
     n = a.n
-    g = P.init_global_grid(n, n, n, dims=dims, path=a.path, device=local)
+    periods = tuple(int(x) for x in a.periodic.split(","))
+    g = P.init_global_grid(n, n, n, dims=dims, periods=periods, path=a.path, device=local)
     if a.kernel:
         g.set_option(P.OPT_STENCIL_KERNEL, a.kernel)
+    g.set_option(P.OPT_X_ALIGN, a.xalign)
+    g.set_option(P.OPT_SCHEDULE, a.schedule)
+    if a.skip_comm:
+        g.set_option(P.OPT_SKIP_COMM, 1)
     T, T2, Ci = app.alloc_fields(g)
     (app.init_paper if a.init == "paper" else app.init_random)(g, T, T2, Ci)
     d = app.spacing(g)
@@ -231,7 +241,7 @@ def main():
     if clocks:
         clocks.start()
         time.sleep(0.4)
-    g.set_option(P.OPT_PROFILE, 1)
+    g.set_option(P.OPT_PROFILE, 2 if a.timeline else 1)
     g.profile_stencil()
     l0 = g.kernel_launches()
     barrier()
@@ -244,6 +254,7 @@ def main():
     ms = e0.elapsed_time(e1) / a.steps
     ms = max_over_ranks(ms)
     k_ms, k_n, k_cells = g.profile_stencil()
+    timeline = g.profile_timeline() if a.timeline else None
     g.set_option(P.OPT_PROFILE, 0)
     clk = clocks.stop() if clocks else None
     g.check()
@@ -272,7 +283,7 @@ def main():
 
     # ---------------- exposed halo time: same schedule with the exchange skipped (timing only)
     exposed = None
-    if world > 1 and not a.no_exposed:
+    if (world > 1 or any(periods)) and not a.no_exposed and not a.skip_comm:
         g.set_option(P.OPT_SKIP_COMM, 1)
         steps(3)
         barrier()
@@ -346,6 +357,8 @@ def main():
             "config": {"workload": f"3-D heat diffusion Float64, local {n}^3 per GPU, dims "
                                    f"{dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw} (paper Fig. 1)",
                        "n_local": n, "dims": list(dims), "bw": list(bw), "path": a.path, "init": a.init,
+                       "x_align": a.xalign, "periods": list(periods), "schedule": a.schedule,
+                       "skip_comm_INVALID_RESULTS": bool(a.skip_comm),
                        "t_eff_per_gpu_gbs": per_gpu, "cells_per_s": world * n ** 3 / (ms * 1e-3),
                        "l2": "inputs 3 x 1 GiB per GPU > 126 MB L2; no flush needed",
                        "frac_of_8TBs": per_gpu / 8000.0, "frac_of_measured_peak": per_gpu / peak,
@@ -353,7 +366,7 @@ def main():
                        "frac_of_stream_2r1w": per_gpu / stream_ref if stream_ref else None,
                        "stencil_variant": a.kernel},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk, "exposed_halo": exposed,
+            "clocks": clk, "exposed_halo": exposed, "timeline_ms": timeline,
         }
         print(json.dumps(line))
     if world > 1:

@@ -218,8 +218,13 @@ enum {
     IGG_OPT_SKIP_COMM = 1,       /* timing-only: skip pack/exchange/unpack (results INVALID) */
     IGG_OPT_SPIN_TIMEOUT_MS = 2, /* P2P flag wait bound (default 20000) */
     IGG_OPT_STENCIL_KERNEL = 3,  /* 0 = auto, 1 = generic region kernel only (ablation) */
-    IGG_OPT_PROFILE = 4          /* 1 = bracket every main stencil launch (the full-region or
-                                    inner-box kernel) with CUDA events on its own stream */
+    IGG_OPT_PROFILE = 4,         /* 1 = bracket every main stencil launch (the full-region or
+                                    inner-box kernel) with CUDA events on its own stream;
+                                    2 = also record the overlap timeline (igg_profile_timeline) */
+    IGG_OPT_X_ALIGN = 5,         /* x boundary-slab edges rounded to this many cells (default 64 =
+                                    512-B row segments; 1 = the exact widths given) */
+    IGG_OPT_SCHEDULE = 6         /* 0 = inner box concurrent with the boundary slabs; 1 = inner box
+                                    after the boundary slabs (paper order), concurrent with the exchange */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 
@@ -231,6 +236,12 @@ igg_status igg_check(igg_grid *grid);
  * CUDA-event duration (ms) of the main stencil launches recorded since the
  * last call, their number and the cells they updated, and resets the record. */
 igg_status igg_profile_stencil(igg_grid *grid, double *ms_total, long long *launches, long long *cells);
+
+/* With IGG_OPT_PROFILE = 2: averages over the overlapped steps since the last
+ * call of the times (ms, CUDA events) from the step's start on the caller's
+ * stream to: [0] boundary slabs done, [1] inner box start, [2] inner box done,
+ * [3] halo exchange done; [4] = number of steps.  Synchronizes; resets. */
+igg_status igg_profile_timeline(igg_grid *grid, double out[5]);
 
 /* Number of kernels the library has launched since init (launch accounting). */
 igg_status igg_kernel_launches(const igg_grid *grid, long long *count_out);

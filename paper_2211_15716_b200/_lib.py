@@ -71,6 +71,7 @@ SIGNATURES = {
     "igg_set_option": [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong],
     "igg_check": [ctypes.c_void_p],
     "igg_profile_stencil": [ctypes.c_void_p, c_dbl_p, c_ll_p, c_ll_p],
+    "igg_profile_timeline": [ctypes.c_void_p, c_dbl_p],
 }
 
 _lib = None

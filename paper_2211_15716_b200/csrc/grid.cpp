@@ -213,41 +213,93 @@ void prof_end(igg_grid *g, cudaStream_t s, long long cells) {
     g->prof_cells += cells;
 }
 
+void tl_mark(igg_grid *g, cudaStream_t s, int k) {
+    if (g->profile < 2) return;
+    const size_t idx = g->tl_used + k;
+    while (g->tl_ev.size() <= idx) {
+        cudaEvent_t e;
+        IGG_CUDA(cudaEventCreate(&e));
+        g->tl_ev.push_back(e);
+    }
+    IGG_CUDA(cudaEventRecord(g->tl_ev[idx], s));
+    if (k == 4) g->tl_used += 5;
+}
+
 // ------------------------------------------------------------------ the heat step
-static void launch_full(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
-                        const HeatCoef &k, cudaStream_t s) {
-    HeatRegionList RL{};
-    RL.k = k;
-    for (int lr = 0; lr < g->nlocal; ++lr) {
-        HeatRegion R{};
-        R.T = T[lr];
-        R.Ci = Ci[lr];
-        R.T2 = T2[lr];
-        R.sx = g->n[0];
-        R.sy = g->n[1];
-        R.sz = g->n[2];
-        R.x0 = R.y0 = R.z0 = 1;
-        R.wx = g->n[0] - 2;
-        R.wy = g->n[1] - 2;
-        R.wz = g->n[2] - 2;
-        if (g->stencil_kernel != 1 && heat_box_vectorizable(R)) {
-            prof_begin(g, s);
-            launch_heat_box(R, k, s, g->stencil_kernel);
-            prof_end(g, s, (long long)R.wx * R.wy * R.wz);
+static HeatRegion make_region(igg_grid *g, int lr, double *const *T2, const double *const *T,
+                              const double *const *Ci, int x0, int x1, int y0, int y1, int z0, int z1) {
+    HeatRegion R{};
+    R.T = T[lr];
+    R.Ci = Ci[lr];
+    R.T2 = T2[lr];
+    R.sx = g->n[0];
+    R.sy = g->n[1];
+    R.sz = g->n[2];
+    R.x0 = x0;
+    R.y0 = y0;
+    R.z0 = z0;
+    R.wx = x1 - x0;
+    R.wy = y1 - y0;
+    R.wz = z1 - z0;
+    return R;
+}
+
+// Launch a list of regions with the kernel selected by IGG_OPT_STENCIL_KERNEL:
+// 0 = cp.async box-list kernel (production), 1 = generic scalar region kernel,
+// >= 2 = per-region box-kernel ablation variants (regions) / slab kernel (slabs).
+// `main` regions are the profiled ones (full region or inner boxes).
+static void launch_regions(igg_grid *g, const std::vector<HeatRegion> &regs, const HeatCoef &k, cudaStream_t s,
+                           bool main) {
+    std::vector<HeatRegion> rs;
+    long long cells = 0;
+    bool vec = true;
+    for (const HeatRegion &R : regs)
+        if (R.wx > 0 && R.wy > 0 && R.wz > 0) {
+            rs.push_back(R);
+            cells += (long long)R.wx * R.wy * R.wz;
+            vec = vec && heat_box_vectorizable(R);
+        }
+    if (rs.empty()) return;
+    if (main) prof_begin(g, s);
+    const int v = g->stencil_kernel;
+    if (((v >= 2 && v < 30) || v == 0) && vec && main) {   // 0: launch_heat_box's default (variant 20)
+        for (const HeatRegion &R : rs) {
+            launch_heat_box(R, k, s, v);
             g->launches++;
-        } else {
-            RL.r[RL.n++] = R;
-            if (RL.n == kMaxRegions) {
-                launch_heat_regions(RL, s);
+        }
+    } else {
+        // narrow regions (x-slabs up to 32 cells from their 16-B aligned start) go to the slab
+        // kernel, which reads only their own row segments; wide ones to the pipelined box kernel
+        std::vector<HeatRegion> narrow, wide;
+        for (const HeatRegion &R : rs) {
+            const bool is_narrow = (R.x0 + R.wx - (R.x0 & ~1)) <= 32;
+            (((v == 0 || v >= 30) && !is_narrow) ? wide : narrow).push_back(R);
+        }
+        for (int pass = 0; pass < 2; ++pass) {
+            const std::vector<HeatRegion> &part = pass == 0 ? wide : narrow;
+            for (size_t c = 0; c < part.size(); c += kMaxRegions) {
+                HeatRegionList L{};
+                L.k = k;
+                for (size_t j = c; j < part.size() && j < c + kMaxRegions; ++j) L.r[L.n++] = part[j];
+                if (v == 1 || !vec)
+                    launch_heat_regions(L, s);
+                else if (pass == 0)
+                    launch_heat_box_list(L, s, v);
+                else
+                    launch_heat_slabs(L, s);
                 g->launches++;
-                RL.n = 0;
             }
         }
     }
-    if (RL.n) {
-        launch_heat_regions(RL, s);
-        g->launches++;
-    }
+    if (main) prof_end(g, s, cells);
+}
+
+static void launch_full(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
+                        const HeatCoef &k, cudaStream_t s) {
+    std::vector<HeatRegion> rs;
+    for (int lr = 0; lr < g->nlocal; ++lr)
+        rs.push_back(make_region(g, lr, T2, T, Ci, 1, g->n[0] - 1, 1, g->n[1] - 1, 1, g->n[2] - 1));
+    launch_regions(g, rs, k, s, true);
 }
 
 void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, double lam,
@@ -278,8 +330,17 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
         if (!sequential_req && exch[a] && bw[a] < g->o[a])
             fail(IGG_E_WIDTH, "heat_step: boundary width " + std::to_string(bw[a]) + " on axis " +
                                   std::to_string(a) + " is below the field overlap " + std::to_string(g->o[a]));
-        lo[a] = std::max(1, bw[a]);
-        hi[a] = std::min(g->n[a] - 1, g->n[a] - bw[a]);
+        // an axis without an exchange has nothing to send early: no boundary slabs on it
+        const int b = exch[a] ? bw[a] : 0;
+        lo[a] = std::max(1, b);
+        hi[a] = std::min(g->n[a] - 1, g->n[a] - b);
+        if (a == 0 && exch[0] && g->x_align > 1) {
+            // B200: x-boundaries on 512-B row segments; the
+            // boundary phase grows to whole 64-cell tiles, results are unchanged
+            const int A = g->x_align;
+            lo[0] = ((lo[0] + A - 1) / A) * A;
+            hi[0] = (hi[0] / A) * A;
+        }
         if (hi[a] <= lo[a]) degenerate = true;   // empty inner box
     }
     std::vector<igg_field> f(g->nlocal);
@@ -294,75 +355,36 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
         IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
         return;
     }
-    IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
     // (1) the six boundary slabs, x-lo, x-hi, y-lo, y-hi, z-lo, z-hi, high priority
-    HeatRegionList RL{};
-    RL.k = k;
     const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
-    auto add = [&](int lr, int x0, int x1, int y0, int y1, int z0, int z1) {
-        if (x1 <= x0 || y1 <= y0 || z1 <= z0) return;
-        if (RL.n == kMaxRegions) {
-            launch_heat_regions(RL, g->s_comm);
-            g->launches++;
-            RL.n = 0;
-        }
-        HeatRegion R{};
-        R.T = T[lr];
-        R.Ci = Ci[lr];
-        R.T2 = T2[lr];
-        R.sx = n0;
-        R.sy = n1;
-        R.sz = n2;
-        R.x0 = x0;
-        R.y0 = y0;
-        R.z0 = z0;
-        R.wx = x1 - x0;
-        R.wy = y1 - y0;
-        R.wz = z1 - z0;
-        RL.r[RL.n++] = R;
-    };
+    std::vector<HeatRegion> slabs, inner;
     for (int lr = 0; lr < g->nlocal; ++lr) {
-        add(lr, 1, lo[0], 1, n1 - 1, 1, n2 - 1);
-        add(lr, hi[0], n0 - 1, 1, n1 - 1, 1, n2 - 1);
-        add(lr, lo[0], hi[0], 1, lo[1], 1, n2 - 1);
-        add(lr, lo[0], hi[0], hi[1], n1 - 1, 1, n2 - 1);
-        add(lr, lo[0], hi[0], lo[1], hi[1], 1, lo[2]);
-        add(lr, lo[0], hi[0], lo[1], hi[1], hi[2], n2 - 1);
+        slabs.push_back(make_region(g, lr, T2, T, Ci, 1, lo[0], 1, n1 - 1, 1, n2 - 1));
+        slabs.push_back(make_region(g, lr, T2, T, Ci, hi[0], n0 - 1, 1, n1 - 1, 1, n2 - 1));
+        slabs.push_back(make_region(g, lr, T2, T, Ci, lo[0], hi[0], 1, lo[1], 1, n2 - 1));
+        slabs.push_back(make_region(g, lr, T2, T, Ci, lo[0], hi[0], hi[1], n1 - 1, 1, n2 - 1));
+        slabs.push_back(make_region(g, lr, T2, T, Ci, lo[0], hi[0], lo[1], hi[1], 1, lo[2]));
+        slabs.push_back(make_region(g, lr, T2, T, Ci, lo[0], hi[0], lo[1], hi[1], hi[2], n2 - 1));
+        inner.push_back(make_region(g, lr, T2, T, Ci, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]));
     }
-    if (RL.n) {
-        launch_heat_regions(RL, g->s_comm);
-        g->launches++;
+    tl_mark(g, s, 0);
+    launch_regions(g, slabs, k, g->s_comm, false);
+    tl_mark(g, g->s_comm, 1);
+    // (2) the inner box on the low-priority stream.  schedule 0: starts with the boundary
+    // (they share the GPU); schedule 1 (the paper's order): starts when the
+    // boundary is done, so the inner box never shares SM slots with the latency-bound slabs
+    if (g->schedule == 1) {
+        IGG_CUDA(cudaEventRecord(g->ev_bnd, g->s_comm));
+        IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_bnd, 0));
+    } else {
+        IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
     }
-    // (2) the inner box on the low-priority stream, concurrently
-    for (int lr = 0; lr < g->nlocal; ++lr) {
-        HeatRegion R{};
-        R.T = T[lr];
-        R.Ci = Ci[lr];
-        R.T2 = T2[lr];
-        R.sx = n0;
-        R.sy = n1;
-        R.sz = n2;
-        R.x0 = lo[0];
-        R.y0 = lo[1];
-        R.z0 = lo[2];
-        R.wx = hi[0] - lo[0];
-        R.wy = hi[1] - lo[1];
-        R.wz = hi[2] - lo[2];
-        prof_begin(g, g->s_inner);
-        if (g->stencil_kernel != 1 && heat_box_vectorizable(R)) {
-            launch_heat_box(R, k, g->s_inner, g->stencil_kernel);
-        } else {
-            HeatRegionList one{};
-            one.k = k;
-            one.r[0] = R;
-            one.n = 1;
-            launch_heat_regions(one, g->s_inner);
-        }
-        prof_end(g, g->s_inner, (long long)R.wx * R.wy * R.wz);
-        g->launches++;
-    }
+    tl_mark(g, g->s_inner, 2);
+    launch_regions(g, inner, k, g->s_inner, true);
+    tl_mark(g, g->s_inner, 3);
     // (3) update_halo!(T2) behind the boundary, on the high-priority stream
     exchange(g, f.data(), 1, g->s_comm);
+    tl_mark(g, g->s_comm, 4);
     IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
     IGG_CUDA(cudaEventRecord(g->ev_inner, g->s_inner));
     IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
@@ -404,6 +426,7 @@ IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_start, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_comm, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_inner, cudaEventDisableTiming));
+        IGG_CUDA(cudaEventCreateWithFlags(&g->ev_bnd, cudaEventDisableTiming));
         if (g->nproc_procs > 1) {
             ncclUniqueId id;
             std::memcpy(&id, A->comm_id, sizeof id);
@@ -470,9 +493,11 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
     if (g->comm) ncclCommDestroy(g->comm);
     for (cudaEvent_t e : g->prof_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->tl_ev) cudaEventDestroy(e);
     cudaEventDestroy(g->ev_start);
     cudaEventDestroy(g->ev_comm);
     cudaEventDestroy(g->ev_inner);
+    cudaEventDestroy(g->ev_bnd);
     cudaStreamDestroy(g->s_comm);
     cudaStreamDestroy(g->s_inner);
     delete g;
@@ -625,7 +650,9 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_SKIP_COMM: g->skip_comm = value != 0; break;
         case IGG_OPT_SPIN_TIMEOUT_MS: g->spin_timeout_ms = value; break;
         case IGG_OPT_STENCIL_KERNEL: g->stencil_kernel = (int)value; break;
-        case IGG_OPT_PROFILE: g->profile = value != 0; break;
+        case IGG_OPT_PROFILE: g->profile = (int)value; break;
+        case IGG_OPT_X_ALIGN: g->x_align = (int)(value < 1 ? 1 : value); break;
+        case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
         default: fail(IGG_E_ARG, "igg_set_option: unknown key " + std::to_string(key));
     }
     IGG_CATCH
@@ -646,6 +673,25 @@ IGG_API igg_status igg_profile_stencil(igg_grid *g, double *ms_total, long long 
     if (cells) *cells = g->prof_cells;
     g->prof_used = 0;
     g->prof_cells = 0;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_profile_timeline(igg_grid *g, double out[5]) {
+    IGG_TRY
+    igg::check_live(g, "igg_profile_timeline");
+    if (!out) fail(IGG_E_ARG, "igg_profile_timeline: NULL out");
+    IGG_CUDA(cudaDeviceSynchronize());
+    double acc[4] = {0, 0, 0, 0};
+    const size_t nsteps = g->tl_used / 5;
+    for (size_t st = 0; st < nsteps; ++st)
+        for (int k = 1; k < 5; ++k) {
+            float ms = 0.f;
+            IGG_CUDA(cudaEventElapsedTime(&ms, g->tl_ev[st * 5], g->tl_ev[st * 5 + k]));
+            acc[k - 1] += ms;
+        }
+    for (int k = 0; k < 4; ++k) out[k] = nsteps ? acc[k] / nsteps : 0.0;
+    out[4] = (double)nsteps;
+    g->tl_used = 0;
     IGG_CATCH
 }
 

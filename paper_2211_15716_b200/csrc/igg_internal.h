@@ -102,6 +102,9 @@ struct HeatRegion {
     int zchunks;
     int col_blocks;
     int block_begin;
+    // vectorised tiling (slab / box-list kernels): lanes per row segment, z-chunk(s), tile counts
+    int lx, kc, xtiles, ytiles, ax0;
+    int nbig, kc2;   // box-list kernel: nbig chunks of kc planes, then chunks of kc2 planes
 };
 constexpr int kMaxRegions = 16;
 struct HeatCoef {
@@ -120,6 +123,11 @@ struct HeatRegionList {
 int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s);
 // generic region kernel: any region list
 void launch_heat_regions(HeatRegionList &L, cudaStream_t s);
+// vectorised region-list kernel for thin boundary slabs (falls back to the generic kernel)
+void launch_heat_slabs(HeatRegionList &L, cudaStream_t s);
+// the production stencil: cp.async-pipelined z-sweep over a list of box regions
+// (all local ranks' inner boxes, or the boundary slabs), one launch
+void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant);
 // vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field
 bool heat_box_vectorizable(const HeatRegion &r);
 void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant);
@@ -166,7 +174,7 @@ struct igg_grid : igg::Geom {
 
     // streams and events (transfers on non-blocking high-priority streams)
     cudaStream_t s_comm = nullptr, s_inner = nullptr;
-    cudaEvent_t ev_start = nullptr, ev_comm = nullptr, ev_inner = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_comm = nullptr, ev_inner = nullptr, ev_bnd = nullptr;
 
     // communicator
     ncclComm_t comm = nullptr;
@@ -192,15 +200,21 @@ struct igg_grid : igg::Geom {
     size_t run_bytes = 0;
 
     // profiling of the main stencil launches (IGG_OPT_PROFILE)
-    bool profile = false;
+    int profile = 0;
     std::vector<cudaEvent_t> prof_ev;
     size_t prof_used = 0;
     long long prof_cells = 0;
+    // timeline of the overlap schedule (IGG_OPT_PROFILE >= 2): per step 5 timing events
+    // t0 (caller stream), boundary end, inner start, inner end, exchange end
+    std::vector<cudaEvent_t> tl_ev;
+    size_t tl_used = 0;
 
     // options
     bool skip_comm = false;
     long long spin_timeout_ms = 20000;
     int stencil_kernel = 0;
+    int x_align = 64;
+    int schedule = 0;
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
@@ -215,5 +229,6 @@ void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap);
 int local_index(const igg_grid *g, int global_rank);   // -1 if not hosted here
 void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
+void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step
 int proc_of(const igg_grid *g, int global_rank);
 }  // namespace igg

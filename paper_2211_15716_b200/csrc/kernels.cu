@@ -82,6 +82,98 @@ void launch_heat_regions(HeatRegionList &L, cudaStream_t s) {
     IGG_CUDA(cudaGetLastError());
 }
 
+// ============================================================== vectorised slab kernel
+// Boundary slabs of hide_communication are thin (x-slabs 15 cells wide, y/z
+// slabs one layer): a warp is split into 32/lx row segments of lx lanes
+// (2 cells per lane, 16-B loads/stores), 4 warps per CTA, short z-chunks for
+// parallelism (the slabs are latency-bound, they sit on the comm critical path).
+constexpr int kSlabWarps = 4;
+
+__global__ void __launch_bounds__(32 * kSlabWarps) heat_slabs_kernel(const __grid_constant__ HeatRegionList L) {
+    const int b = blockIdx.x;
+    int ri = 0;
+    while (ri + 1 < L.n && b >= L.r[ri + 1].block_begin) ++ri;
+    const HeatRegion &R = L.r[ri];
+    const int local = b - R.block_begin;
+    const int tx = local % R.xtiles;
+    const int rest = local / R.xtiles;
+    const int ty = rest % R.ytiles, tz = rest / R.ytiles;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = R.lx, rpw = 32 / lx;
+    const int seg = lane / lx, l = lane % lx;
+    const int yw = R.y0 + (ty * kSlabWarps + warp) * rpw;
+    if (yw >= R.y0 + R.wy) return;                    // whole warp out
+    const int y = yw + seg;
+    const int p = R.ax0 + tx * 2 * lx + 2 * l;
+    const bool pair_in = y < R.y0 + R.wy && p < R.sx;
+    const bool w0 = pair_in && p >= R.x0 && p < R.x0 + R.wx;
+    const bool w1 = pair_in && p + 1 >= R.x0 && p + 1 < R.x0 + R.wx;
+    int z = R.z0 + tz * R.kc;
+    const int zend = min(R.z0 + R.wz, z + R.kc);
+    const long long sx = R.sx, sxy = (long long)R.sx * R.sy;
+    const double *__restrict__ T = R.T;
+    const double *__restrict__ Ci = R.Ci;
+    double *__restrict__ T2 = R.T2;
+    long long i = (long long)z * sxy + (long long)y * sx + p;
+    const double2 zero2 = make_double2(0.0, 0.0);
+    double2 zm = zero2, c = zero2;
+    if (pair_in) {
+        zm = __ldg(reinterpret_cast<const double2 *>(T + i - sxy));
+        c = __ldg(reinterpret_cast<const double2 *>(T + i));
+    }
+    for (; z < zend; ++z, i += sxy) {
+        double2 zp = zero2, ym = zero2, yp = zero2, ci = zero2;
+        if (pair_in) {
+            zp = __ldg(reinterpret_cast<const double2 *>(T + i + sxy));
+            ym = __ldg(reinterpret_cast<const double2 *>(T + i - sx));
+            yp = __ldg(reinterpret_cast<const double2 *>(T + i + sx));
+            ci = __ldg(reinterpret_cast<const double2 *>(Ci + i));
+        }
+        double xm = __shfl_up_sync(0xffffffffu, c.y, 1, lx);
+        double xp = __shfl_down_sync(0xffffffffu, c.x, 1, lx);
+        if (l == 0 && w0) xm = __ldg(T + i - 1);
+        if (l == lx - 1 && w1) xp = __ldg(T + i + 2);
+        const double r0 = heat_cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, L.k);
+        const double r1 = heat_cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, L.k);
+        if (w0 && w1) {
+            *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+        } else {
+            if (w0) T2[i] = r0;
+            if (w1) T2[i + 1] = r1;
+        }
+        zm = c;
+        c = zp;
+    }
+}
+
+void launch_heat_slabs(HeatRegionList &L, cudaStream_t s) {
+    bool vec = true;
+    for (int r = 0; r < L.n; ++r) vec = vec && heat_box_vectorizable(L.r[r]);
+    if (!vec) {
+        launch_heat_regions(L, s);
+        return;
+    }
+    int total = 0;
+    for (int r = 0; r < L.n; ++r) {
+        HeatRegion &R = L.r[r];
+        R.ax0 = R.x0 & ~1;
+        const int span = R.x0 + R.wx - R.ax0;   // cells from the aligned start
+        R.lx = 1;   // lanes per row segment: the smallest power of two covering the span
+        while (R.lx < 32 && 2 * R.lx < span) R.lx *= 2;
+        const int rows = kSlabWarps * (32 / R.lx);
+        R.kc = R.wz <= 2 ? R.wz : 4;
+        R.xtiles = (span + 2 * R.lx - 1) / (2 * R.lx);
+        R.ytiles = (R.wy + rows - 1) / rows;
+        R.zchunks = (R.wz + R.kc - 1) / R.kc;
+        R.block_begin = total;
+        total += R.xtiles * R.ytiles * R.zchunks;
+    }
+    L.total_blocks = total;
+    if (total == 0) return;
+    heat_slabs_kernel<<<total, 32 * kSlabWarps, 0, s>>>(L);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ============================================================== vectorised box kernel
 // Tile = 64 x-cells x kBoxTY rows; a warp owns one 64-cell row segment, each
 // lane two consecutive cells (one 16-B double2 load/store per field).  The
@@ -173,7 +265,7 @@ __global__ void __launch_bounds__(32 * TY, (PF ? 1024 : 1280) / (32 * TY))
 
 template <int TY, int KC, bool PF>
 static void launch_box_variant(const HeatRegion &r, const HeatCoef &k, cudaStream_t s) {
-    const int ax0 = r.x0 & ~1;
+    const int ax0 = r.x0 & ~63;   // 512-B aligned row segments (the region start is masked)
     const int xtiles = (r.x0 + r.wx - ax0 + 63) / 64;
     const int ytiles = (r.wy + TY - 1) / TY;
     const int ztiles = (r.wz + KC - 1) / KC;
@@ -286,7 +378,7 @@ __global__ void __launch_bounds__(32 * TY)
 
 template <int TY, int D, bool ST = false>
 static void launch_box_async(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int kc1, int kc2) {
-    const int ax0 = r.x0 & ~1;
+    const int ax0 = r.x0 & ~63;   // 512-B aligned row segments (the region start is masked)
     const int xtiles = (r.x0 + r.wx - ax0 + 63) / 64;
     const int ytiles = (r.wy + TY - 1) / TY;
     const int ntiles = xtiles * ytiles;
@@ -320,6 +412,149 @@ static void launch_box_async(const HeatRegion &r, const HeatCoef &k, cudaStream_
     heat_box_async_kernel<TY, D, ST><<<(unsigned)blocks, 32 * TY, smem, s>>>(
         r.T, r.Ci, r.T2, r.sx, r.sy, r.x0, r.y0, r.z0, r.wx, r.wy, r.wz, ax0, xtiles, ytiles, kc1, nbig2,
         kc2 > 0 ? kc2 : kc1, k);
+    IGG_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- the production kernel
+// heat_box_async_kernel's sweep over a LIST of box regions (one launch for all
+// local ranks, or for all six boundary slabs).  TY=4 rows per CTA, D=3 planes
+// in flight per thread, streaming stores: the configuration measured best in
+// profiles/r01_box_variant_sweep.log.
+constexpr int kListTY = 4;
+constexpr int kListD = 3;
+
+template <int MINB>
+__global__ void __launch_bounds__(32 * kListTY, MINB) heat_box_list_kernel(const __grid_constant__ HeatRegionList L) {
+    __shared__ double2 sT[kListD][32 * kListTY];
+    __shared__ double2 sC[kListD][32 * kListTY];
+    const int b = blockIdx.x;
+    int ri = 0;
+    while (ri + 1 < L.n && b >= L.r[ri + 1].block_begin) ++ri;
+    const HeatRegion &R = L.r[ri];
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int ntiles = R.xtiles * R.ytiles;
+    const int local = b - R.block_begin;
+    const int tile = local % ntiles, chunk = local / ntiles;
+    int zs, ze;
+    if (chunk < R.nbig) {
+        zs = R.z0 + chunk * R.kc;
+        ze = min(zs + R.kc, R.z0 + R.wz);
+    } else {
+        zs = R.z0 + R.nbig * R.kc + (chunk - R.nbig) * R.kc2;
+        ze = min(zs + R.kc2, R.z0 + R.wz);
+    }
+    const int tx = tile % R.xtiles, ty = tile / R.xtiles;
+    const int y = R.y0 + ty * kListTY + warp;
+    if (y >= R.y0 + R.wy || zs >= ze) return;
+    const int p = R.ax0 + tx * 64 + 2 * lane;
+    const bool pair_in = p < R.sx;
+    const bool w0 = pair_in && p >= R.x0 && p < R.x0 + R.wx;
+    const bool w1 = pair_in && p + 1 >= R.x0 && p + 1 < R.x0 + R.wx;
+    const long long sx = R.sx, sxy = (long long)R.sx * R.sy;
+    const double *__restrict__ T = R.T;
+    const double *__restrict__ Ci = R.Ci;
+    double *__restrict__ T2 = R.T2;
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+#pragma unroll
+    for (int q = 0; q < kListD; ++q) {
+        if (pair_in && zs + q < ze) {
+            cp_async16(&sT[q][tid], T + i + (q + 1) * sxy);
+            cp_async16(&sC[q][tid], Ci + i + q * sxy);
+        }
+        cp_async_commit();
+    }
+    const double2 zero2 = make_double2(0.0, 0.0);
+    double2 zm = pair_in ? ldg2(T + i - sxy) : zero2;
+    double2 c = pair_in ? ldg2(T + i) : zero2;
+    int slot = 0;
+    for (int z = zs; z < ze; ++z, i += sxy) {
+        cp_async_wait<kListD - 1>();
+        double2 ym = zero2, yp = zero2;
+        if (pair_in) {
+            ym = ldg2(T + i - sx);
+            yp = ldg2(T + i + sx);
+        }
+        const double2 zp = sT[slot][tid];
+        const double2 ci = sC[slot][tid];
+        double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
+        double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0 && w0) xm = __ldg(T + i - 1);
+        if (lane == 31 && w1) xp = __ldg(T + i + 2);
+        const double r0 = heat_cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, L.k);
+        const double r1 = heat_cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, L.k);
+        if (w0 && w1) {
+            __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+        } else {
+            if (w0) T2[i] = r0;
+            if (w1) T2[i + 1] = r1;
+        }
+        zm = c;
+        c = zp;
+        if (pair_in && z + kListD < ze) {
+            cp_async16(&sT[slot][tid], T + i + (kListD + 1) * sxy);
+            cp_async16(&sC[slot][tid], Ci + i + kListD * sxy);
+        }
+        cp_async_commit();
+        slot = slot + 1 == kListD ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
+}
+
+// variant (IGG_OPT_STENCIL_KERNEL >= 30, ablation): occupancy control by extra dynamic smem
+void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant) {
+    static int occs[64];
+    static bool init = false;
+    static int nsm = 0;
+    if (!init) {
+        for (int &o : occs) o = -1;
+        init = true;
+    }
+    const int vi = variant >= 30 && variant < 40 ? variant - 30 : 0;
+    const size_t extra = (size_t)vi * 4096;   // 0, 4 KB, 8 KB, ...
+    auto kern = heat_box_list_kernel<1>;
+    int &occ = occs[vi];
+    if (occ < 0) {
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kListTY, extra));
+        int dev = 0;
+        IGG_CUDA(cudaGetDevice(&dev));
+        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int kc1 = 64, kc2 = 8;
+    long long tiles_all = 0;
+    for (int r = 0; r < L.n; ++r) {
+        HeatRegion &R = L.r[r];
+        R.ax0 = R.x0 & ~63;   // 512-B aligned row segments (cells before x0 are read, not written)
+        R.xtiles = (R.x0 + R.wx - R.ax0 + 63) / 64;
+        R.ytiles = (R.wy + kListTY - 1) / kListTY;
+        tiles_all += (long long)R.xtiles * R.ytiles;
+    }
+    long long total = 0;
+    for (int r = 0; r < L.n; ++r) {
+        HeatRegion &R = L.r[r];
+        const long long ntiles = (long long)R.xtiles * R.ytiles;
+        if (R.wx <= 0 || R.wy <= 0 || R.wz <= 0) {
+            R.nbig = 0;
+            R.kc = kc1;
+            R.kc2 = kc2;
+            R.block_begin = (int)total;
+            continue;
+        }
+        // the last ~2 waves of tile-planes run as short chunks so the tail is short
+        const long long conc = (long long)occ * nsm;
+        int small = (int)((2 * conc * kc2 + tiles_all - 1) / tiles_all);
+        small = ((small + kc2 - 1) / kc2) * kc2;
+        if (small > R.wz) small = R.wz;
+        R.nbig = (R.wz - small) / kc1;
+        R.kc = kc1;
+        R.kc2 = kc2;
+        const int rest = R.wz - R.nbig * kc1;
+        R.block_begin = (int)total;
+        total += ntiles * (R.nbig + (rest + kc2 - 1) / kc2);
+    }
+    L.total_blocks = (int)total;
+    if (total == 0) return;
+    kern<<<(unsigned)total, 32 * kListTY, extra, s>>>(L);
     IGG_CUDA(cudaGetLastError());
 }
 
@@ -383,6 +618,33 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 
 constexpr int kCopyThreads = 256;
+constexpr int kCopyILP = 8;   // elements per thread, all loads issued before the stores
+
+// Copies of the faces run concurrently with the bandwidth-bound inner box: each
+// thread issues kCopyILP independent loads before storing, so a CTA finishes
+// in about one memory round trip and holds its SM slot as briefly as possible.
+template <bool PACK>
+__device__ __forceinline__ void copy_face(const CopyDesc &d) {
+    const long long chunk = (long long)kCopyThreads * kCopyILP;
+    for (long long base = (long long)blockIdx.x * chunk; base < d.count; base += (long long)gridDim.x * chunk) {
+        double v[kCopyILP];
+#pragma unroll
+        for (int u = 0; u < kCopyILP; ++u) {
+            const long long i = base + u * kCopyThreads + threadIdx.x;
+            if (i < d.count) v[u] = PACK ? __ldcg(d.field + face_index(d, i)) : __ldcg(d.buf + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kCopyILP; ++u) {
+            const long long i = base + u * kCopyThreads + threadIdx.x;
+            if (i < d.count) {
+                if (PACK)
+                    d.buf[i] = v[u];
+                else
+                    d.field[face_index(d, i)] = v[u];
+            }
+        }
+    }
+}
 
 // pack: field slab -> buffer (own send buffer, a local rank's receive slot, or a
 // peer GPU's receive slot over NVLink).  If the list carries signals, the last
@@ -391,9 +653,7 @@ constexpr int kCopyThreads = 256;
 // acquires through the ticket and release-stores each flag.
 __global__ void __launch_bounds__(kCopyThreads) pack_kernel(const __grid_constant__ CopyList L) {
     const CopyDesc &d = L.d[blockIdx.y];
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d.count; i += stride)
-        d.buf[i] = d.field[face_index(d, i)];
+    copy_face<true>(d);
     if (L.nsignal > 0) {
         __threadfence_system();
         __syncthreads();
@@ -427,15 +687,31 @@ __global__ void __launch_bounds__(kCopyThreads) unpack_kernel(const __grid_const
         }
         __syncthreads();
     }
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < d.count; i += stride)
-        d.field[face_index(d, i)] = __ldcg(d.buf + i);
+    copy_face<false>(d);
+}
+
+// one CTA waits for every peer flag of this axis (bounded spin), so the
+// unpack CTAs that follow never occupy SM slots while the peers are still
+// packing (they would starve the concurrent inner-box kernel)
+__global__ void flag_wait_kernel(const __grid_constant__ CopyList L) {
+    const int t = threadIdx.x;
+    if (t < L.nsignal) {
+        const unsigned long long *f = L.wait[t];
+        const long long t0 = clock64();
+        while (ld_acquire_sys(f) < L.epoch) {
+            if (clock64() - t0 > L.timeout_cycles) {
+                atomicExch(L.err, 1);
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
 }
 
 static int copy_blocks(const CopyDesc *d, int n) {
     long long mx = 1;
     for (int j = 0; j < n; ++j) mx = d[j].count > mx ? d[j].count : mx;
-    long long b = (mx + kCopyThreads * 4 - 1) / (kCopyThreads * 4);
+    long long b = (mx + kCopyThreads * kCopyILP - 1) / (kCopyThreads * kCopyILP);
     if (b < 1) b = 1;
     if (b > 1024) b = 1024;
     return (int)b;
@@ -452,10 +728,19 @@ int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &pr
         total += (unsigned)copy_blocks(descs.data() + c, m) * m;
     }
     int launches = 0;
+    const bool waits = op == 1 && proto.nsignal > 0;
+    if (waits) {
+        flag_wait_kernel<<<1, 32, 0, s>>>(proto);
+        IGG_CUDA(cudaGetLastError());
+        ++launches;
+    }
     for (int c = 0; c < n; c += kMaxCopy) {
         CopyList L = proto;
         L.n = std::min(kMaxCopy, n - c);
-        for (int j = 0; j < L.n; ++j) L.d[j] = descs[c + j];
+        for (int j = 0; j < L.n; ++j) {
+            L.d[j] = descs[c + j];
+            if (waits) L.d[j].flag_slot = -1;   // already waited above
+        }
         L.ticket_total = total;
         dim3 grid(copy_blocks(L.d, L.n), L.n);
         if (op == 0)

@@ -27,6 +27,8 @@ OPT_SKIP_COMM = 1
 OPT_SPIN_TIMEOUT_MS = 2
 OPT_STENCIL_KERNEL = 3
 OPT_PROFILE = 4
+OPT_X_ALIGN = 5
+OPT_SCHEDULE = 6
 
 STATUS = {0: "IGG_OK", 1: "IGG_E_ARG", 2: "IGG_E_STATE", 3: "IGG_E_STAGGER", 4: "IGG_E_WIDTH",
           5: "IGG_E_CUDA", 6: "IGG_E_NCCL", 7: "IGG_E_TIMEOUT", 8: "IGG_E_UNSUPPORTED"}
@@ -257,6 +259,13 @@ class Grid:
         ms, n, c = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
         _ok(L.lib().igg_profile_stencil(self._handle(), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(c)))
         return ms.value, n.value, c.value
+
+    def profile_timeline(self) -> dict:
+        """Average overlap timeline (ms from step start) recorded with OPT_PROFILE = 2; resets."""
+        out = (ctypes.c_double * 5)()
+        _ok(L.lib().igg_profile_timeline(self._handle(), out))
+        return dict(boundary_done=out[0], inner_start=out[1], inner_done=out[2], exchange_done=out[3],
+                    steps=int(out[4]))
 
     def check(self) -> None:
         _ok(L.lib().igg_check(self._handle()))

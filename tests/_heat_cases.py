@@ -18,13 +18,14 @@ def oracle_global(N, per, nt, init="random", mode=OH.CANONICAL, seeds=(SI.SEED_T
     return OH.heat_run(T0, Ci, nt, per, 1.0, dt, *d, mode), dt
 
 
-def gpu_run(P, app, n, dims, per, o, nt, bw, init="random", path="nccl", options=None, seeds=None):
+def gpu_run(P, app, n, dims, per, o, nt, bw, init="random", path="nccl", options=None, seeds=None, x_align=1):
     """Fig. 1 on R = prod(dims) virtual ranks of one process; returns
     (list of final local T arrays, dt, grid-allocation counts, launches)."""
     import torch
     nprocs = dims[0] * dims[1] * dims[2]
     g = P.init_global_grid(*n, dims=dims, periods=per, overlaps=o, local_ranks=nprocs, device=0, path=path)
     try:
+        g.set_option(P.OPT_X_ALIGN, x_align)    # 1: the exact widths, so small grids still split
         for k, v in (options or {}).items():
             g.set_option(k, v)
         T, T2, Ci = app.alloc_fields(g)

@@ -60,11 +60,29 @@ def test_config_b7_periodic_x():
     dict(n=(20, 18, 16), dims=(1, 1, 1), per=(1, 1, 1), o=(2, 2, 2), bw=(4, 2, 2)),   # self-wrap
     dict(n=(34, 18, 16), dims=(4, 1, 1), per=(0, 0, 0), o=(2, 2, 2), bw=(2, 2, 2)),
 ])
-def test_virtual_topologies_bit_exact(case):
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_virtual_topologies_bit_exact(case, kernel):
     n, dims, per, o, bw = case["n"], case["dims"], case["per"], case["o"], case["bw"]
-    out, dt, _, _ = gpu_run(P, app, n, dims, per, o, 6, bw)
+    out, dt, _, _ = gpu_run(P, app, n, dims, per, o, 6, bw, options={P.OPT_STENCIL_KERNEL: kernel})
     can, dtr = oracle_global(_N(n, dims, per, o), per, 6)
     assert dt == dtr
+    assert_windows(out, can, dims, n, o, per)
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=(260, 40, 36), dims=(2, 1, 1), per=(0, 0, 0)),
+    dict(n=(200, 24, 20), dims=(2, 2, 2), per=(0, 0, 0)),
+    dict(n=(136, 30, 26), dims=(2, 1, 2), per=(1, 0, 0)),
+])
+@pytest.mark.parametrize("kernel", [0, 1, 8])
+@pytest.mark.parametrize("schedule", [0, 1])
+@pytest.mark.parametrize("x_align", [1, 64])
+def test_schedules_bit_exact(case, kernel, schedule, x_align):
+    """Both schedules, exact and 512-B-rounded x boundaries, three kernels."""
+    n, dims, per, o = case["n"], case["dims"], case["per"], (2, 2, 2)
+    out, _, _, _ = gpu_run(P, app, n, dims, per, o, 5, (16, 2, 2), x_align=x_align,
+                           options={P.OPT_STENCIL_KERNEL: kernel, P.OPT_SCHEDULE: schedule})
+    can, _ = oracle_global(_N(n, dims, per, o), per, 5)
     assert_windows(out, can, dims, n, o, per)
 
 
