@@ -40,12 +40,13 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--bw", default="16,2,2")
-    ap.add_argument("--path", choices=["nccl", "p2p"], default="nccl")
+    ap.add_argument("--path", choices=["nccl", "p2p"], default="p2p")
     ap.add_argument("--init", choices=["paper", "random"], default="paper")
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic region kernel (ablation)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exposed", action="store_true")
+    ap.add_argument("--fused", type=int, default=0, help="1: fused stencil+P2P exchange kernel (p2p path)")
     ap.add_argument("--schedule", type=int, default=0, help="0 concurrent, 1 boundary first (paper order)")
     ap.add_argument("--timeline", action="store_true", help="record the overlap timeline (extra events)")
     ap.add_argument("--xalign", type=int, default=64, help="x boundary-slab alignment in cells (1 = exact bw)")
@@ -206,6 +207,7 @@ def main():
         g.set_option(P.OPT_STENCIL_KERNEL, a.kernel)
     g.set_option(P.OPT_X_ALIGN, a.xalign)
     g.set_option(P.OPT_SCHEDULE, a.schedule)
+    g.set_option(P.OPT_FUSED, a.fused)
     if a.skip_comm:
         g.set_option(P.OPT_SKIP_COMM, 1)
     T, T2, Ci = app.alloc_fields(g)
@@ -357,7 +359,7 @@ def main():
             "config": {"workload": f"3-D heat diffusion Float64, local {n}^3 per GPU, dims "
                                    f"{dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw} (paper Fig. 1)",
                        "n_local": n, "dims": list(dims), "bw": list(bw), "path": a.path, "init": a.init,
-                       "x_align": a.xalign, "periods": list(periods), "schedule": a.schedule,
+                       "x_align": a.xalign, "periods": list(periods), "schedule": a.schedule, "fused": a.fused,
                        "skip_comm_INVALID_RESULTS": bool(a.skip_comm),
                        "t_eff_per_gpu_gbs": per_gpu, "cells_per_s": world * n ** 3 / (ms * 1e-3),
                        "l2": "inputs 3 x 1 GiB per GPU > 126 MB L2; no flush needed",

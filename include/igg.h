@@ -223,8 +223,11 @@ enum {
                                     2 = also record the overlap timeline (igg_profile_timeline) */
     IGG_OPT_X_ALIGN = 5,         /* x boundary-slab edges rounded to this many cells (default 64 =
                                     512-B row segments; 1 = the exact widths given) */
-    IGG_OPT_SCHEDULE = 6         /* 0 = inner box concurrent with the boundary slabs; 1 = inner box
+    IGG_OPT_SCHEDULE = 6,        /* 0 = inner box concurrent with the boundary slabs; 1 = inner box
                                     after the boundary slabs (paper order), concurrent with the exchange */
+    IGG_OPT_FUSED = 7            /* 1 (default) = P2P path with one rank per GPU: one stencil kernel
+                                    that stores send layers into the peers' slots as it computes them;
+                                    0 = boundary/inner kernels + separate pack/exchange/unpack */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

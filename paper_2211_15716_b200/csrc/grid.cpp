@@ -315,7 +315,7 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
     for (int a = 0; a < 3; ++a)
         for (int lr = 0; lr < g->nlocal; ++lr)
             if (g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0) exch[a] = any = true;
-    if (!any) {   // nothing to exchange or hide: one full-region launch
+    if (!any && !(g->fused == 2 && g->nlocal == 1)) {   // nothing to exchange or hide: one full-region launch
         launch_full(g, T2, T, Ci, k, s);
         return;
     }
@@ -345,6 +345,13 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
     }
     std::vector<igg_field> f(g->nlocal);
     for (int lr = 0; lr < g->nlocal; ++lr) f[lr] = igg_field{T2[lr], {g->n[0], g->n[1], g->n[2]}};
+    if (!sequential_req && g->stencil_kernel == 0 && fused_eligible(g)) {
+        HeatRegion R = make_region(g, 0, T2, T, Ci, 1, g->n[0] - 1, 1, g->n[1] - 1, 1, g->n[2] - 1);
+        if (heat_box_vectorizable(R)) {   // one kernel: stencil + exchange in peer memory
+            fused_step(g, T2[0], T[0], Ci[0], k, s);
+            return;
+        }
+    }
 
     IGG_CUDA(cudaEventRecord(g->ev_start, s));
     IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
@@ -487,7 +494,7 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->fused_tiles, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
@@ -653,6 +660,7 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_PROFILE: g->profile = (int)value; break;
         case IGG_OPT_X_ALIGN: g->x_align = (int)(value < 1 ? 1 : value); break;
         case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
+        case IGG_OPT_FUSED: g->fused = (int)value; break;
         default: fail(IGG_E_ARG, "igg_set_option: unknown key " + std::to_string(key));
     }
     IGG_CATCH

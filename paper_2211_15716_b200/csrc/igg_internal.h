@@ -117,6 +117,34 @@ struct HeatRegionList {
     HeatCoef k;
 };
 
+// ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
+struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
+    double *dst;                     // receiver's slot (peer-mapped), this step's parity half
+    unsigned long long *flag;        // receiver's flag for (axis, side)
+    unsigned int *counter;           // my contribution counter for this face
+    unsigned int target;             // contributions that complete the face
+    int layer;                       // my send layer along the axis
+    int active;
+};
+struct FusedHalo {                   // one halo side I receive
+    const double *src;               // my slot, this step's parity half
+    const unsigned long long *flag;  // my flag
+    int layer;                       // halo layer (0 or s-1)
+    int active;
+};
+struct FusedParams {
+    const double *T;
+    const double *Ci;
+    double *T2;
+    int s[3];
+    FusedFace face[3][2];
+    FusedHalo halo[3][2];
+    unsigned long long epoch;
+    long long timeout_cycles;
+    int *err;
+    HeatCoef k;
+};
+
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
 // pack (op 0) or unpack (op 1) of any number of faces: chunks of kMaxCopy
 // descriptors per launch; `proto` carries signals/waits/epoch; returns launches
@@ -215,6 +243,12 @@ struct igg_grid : igg::Geom {
     int stencil_kernel = 0;
     int x_align = 64;
     int schedule = 0;
+    int fused = 1;                                       // IGG_OPT_FUSED
+    int4 *fused_tiles = nullptr;
+    int fused_ntiles = 0, fused_nedge = 0, fused_key = -1;
+    long long fused_rest_cells = 0;
+    int fused_tiles_per_face[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+    unsigned int *fused_ctr = nullptr;
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
@@ -227,6 +261,8 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
                cudaStream_t s);
 void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap);
 int local_index(const igg_grid *g, int global_rank);   // -1 if not hosted here
+bool fused_eligible(const igg_grid *g);
+void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s);
 void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
 void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step

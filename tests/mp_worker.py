@@ -26,11 +26,13 @@ def log(*a):
     print(f"[rank {dist.get_rank()}]", *a, flush=True)
 
 
-def heat_case(path, n, dims, per, local, bw, nt=8):
+def heat_case(path, n, dims, per, local, bw, nt=8, opts=None):
     world = dist.get_world_size()
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
                            device=int(os.environ["LOCAL_RANK"]))
     try:
+        for k, v in (opts or {}).items():
+            g.set_option(k, v)
         T, T2, Ci = app.alloc_fields(g)
         app.init_random(g, T, T2, Ci)
         d = app.spacing(g)
@@ -53,7 +55,7 @@ def heat_case(path, n, dims, per, local, bw, nt=8):
                                      f"{int((got != W).sum())} cells differ")
     finally:
         g.finalize()
-    log("heat OK", path, dims, per, "local", local, "world", world)
+    log("heat OK", path, dims, per, "local", local, "world", world, "opts", opts)
 
 
 def halo_case(path, n, dims, per, local, sizes, seed, repeat=2):
@@ -97,6 +99,13 @@ def main():
     for path in paths:
         heat_case(path, n, dims, (0, 0, 0), 1, (16, 2, 2))
         heat_case(path, n, dims, (1, 0, 1), 1, (4, 2, 2))
+        heat_case(path, (130, 36, 34), dims, (0, 0, 0), 1, (16, 2, 2))
+        if path == "p2p":   # the fused stencil+exchange kernel is the p2p default; also check the split path
+            for o in ({P.OPT_FUSED: 0}, {P.OPT_FUSED: 0, P.OPT_SCHEDULE: 1}):
+                heat_case(path, n, dims, (0, 0, 0), 1, (16, 2, 2), opts=o)
+                heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), opts=o)
+            heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=12)
+            heat_case(path, (66, 40, 36), dims, (0, 1, 0), 1, (16, 2, 2), nt=9)
         halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
         # 8 ranks as virtual ranks over the processes (2x2x2 correctness on fewer GPUs)
