@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exposed", action="store_true")
-    ap.add_argument("--fused", type=int, default=0, help="1: fused stencil+P2P exchange kernel (p2p path)")
+    ap.add_argument("--fused", type=int, default=1, help="1: fused stencil+P2P exchange kernel (p2p path)")
+    ap.add_argument("--fused-mode", type=int, default=2, help="ablation bits of the fused path")
     ap.add_argument("--schedule", type=int, default=0, help="0 concurrent, 1 boundary first (paper order)")
     ap.add_argument("--timeline", action="store_true", help="record the overlap timeline (extra events)")
     ap.add_argument("--xalign", type=int, default=64, help="x boundary-slab alignment in cells (1 = exact bw)")
@@ -208,6 +209,7 @@ def main():
     g.set_option(P.OPT_X_ALIGN, a.xalign)
     g.set_option(P.OPT_SCHEDULE, a.schedule)
     g.set_option(P.OPT_FUSED, a.fused)
+    g.set_option(8, a.fused_mode)
     if a.skip_comm:
         g.set_option(P.OPT_SKIP_COMM, 1)
     T, T2, Ci = app.alloc_fields(g)

@@ -1,20 +1,24 @@
 // fused.cu -- the fused hide_communication step: stencil + halo exchange in
-// peer memory (IGG_PATH_P2P, one rank per process, every neighbour on another GPU).
+// peer memory, pipelined by z-chunks (IGG_PATH_P2P, one rank per process,
+// every neighbour on another GPU).
 //
-// The paper hides update_halo! behind the inner-point computation by computing
-// boundary slabs first and exchanging while the inner box runs (PAPER.md:75,
-// :94).  On B200 the same overlap is done inside ONE stencil
-// kernel: its CTAs visit the tiles holding send layers first, and every cell
-// of a send layer is stored straight into the receiving GPU's receive slot
-// over NVLink as it is computed (the "pack" is fused into the stencil).  Each
-// contributing CTA counts itself on a per-face counter after a system-scope
-// fence; the CTA completing the count publishes the epoch to the receiver's
-// flag (st.release.sys).  Face cells that are not computed by the stencil come
-// from a small rim kernel (values that never survive or never change) or are
-// forwarded by the unpack of an earlier axis (the fresh edge/corner values the
-// dimension-sequential update_halo delivers).  The receiver
-// waits per axis (one spinning CTA, then the unpack), x -> y -> z.  The final
-// state is bit-identical to {step!; update_halo!(T2)} (tests/test_gpu_multi.py).
+// The paper hides update_halo! behind the inner-point computation (PAPER.md:75,
+// :94 "pipelining is applied on all stages of the data transfers").
+// On B200 one stencil kernel keeps the 1-GPU tile order (z-chunk, then y-tile,
+// then x-tile: whole 4-KB rows stream together, which the boundary/inner split
+// breaks) and stores every cell of a send layer straight into the receiving
+// GPU's receive slot over NVLink as it computes it (the pack is fused into the
+// stencil).  Faces are published chunk by chunk: each CTA that holds part of
+// face f in chunk c counts itself on counter (f, c) after a system fence; the
+// contribution completing (f, c) release-stores the epoch into the receiver's
+// flag (f, c).  The receiver's unpack CTAs (one per chunk and side, waiting with
+// ld.acquire.sys) run while the stencil is still going, so only the last small
+// chunk's unpack can be exposed.  Face cells the stencil does not compute come
+// from a rim kernel (values that never change or are overwritten later on the
+// receiver) or are forwarded by the unpack of an earlier axis (fresh
+// edge/corner values of the dimension-sequential update_halo, SPEC.md:211,
+// :236).  The final state is bit-identical to {step!; update_halo!(T2)}
+// (tests/test_gpu_multi.py).
 #include <algorithm>
 #include <array>
 #include <cstring>
@@ -54,58 +58,83 @@ __device__ __forceinline__ double cell(double c, double xm, double xp, double ym
 }
 
 // face index of a cell on a face normal to axis a.  y- and z-faces: x fastest
-// (z*sx + x, y*sx + x); the x-face is stored z fastest (y*sz + z) so
-// that a warp sweeping z writes its x-face cells as contiguous 256-B runs over
-// NVLink (sender and receiver of the fused path both use this layout)
+// (z*sx + x, y*sx + x).  The x-face is stored z fastest (y*sz + z)
+// so a tile's x-face cells of one chunk are contiguous runs (sender and
+// receiver of the fused path share this layout).
 __device__ __forceinline__ long long fidx(int a, int x, int y, int z, const int *s) {
     return a == 0 ? (long long)y * s[2] + z : (a == 1 ? (long long)z * s[0] + x : (long long)y * s[0] + x);
 }
-__device__ __forceinline__ int fast_axis(int a) { return a == 0 ? 2 : 0; }
-__device__ __forceinline__ int slow_axis(int a) { return a == 0 ? 1 : (a == 1 ? 2 : 1); }
 
-// publish one contribution to face (a, rs); the completing contribution releases the flag
-__device__ __forceinline__ void contribute(const FusedFace &f, unsigned long long epoch) {
-    const unsigned old = atomicAdd(f.counter, 1u);
-    if (old == f.target - 1) {
+__device__ __forceinline__ void contribute(const FusedParams &F, int a, int rs, int c) {
+    const int i = (a * 2 + rs) * kMaxChunks + c;
+    const unsigned old = atomicAdd(F.ctr + i, 1u);
+    if (old == F.tgt[i] - 1) {
         __threadfence_system();
-        st_rel_sys(f.flag, epoch);
-        atomicExch(f.counter, 0u);
+        st_rel_sys(F.face[a][rs].flag + c, F.epoch);
+        atomicExch(F.ctr + i, 0u);
     }
 }
 
-// the stores of one cell pair into every send face it belongs to
-__device__ __forceinline__ void face_store(const FusedParams &F, int p, int y, int z, bool w0, bool w1, double r0,
-                                        double r1) {
-    const int sx = F.s[0];
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        const FusedFace &fy = F.face[1][rs];
-        if (fy.active && y == fy.layer) {
-            if (w0) fy.dst[(long long)z * sx + p] = r0;
-            if (w1) fy.dst[(long long)z * sx + p + 1] = r1;
-        }
-        const FusedFace &fz = F.face[2][rs];
-        if (fz.active && z == fz.layer) {
-            if (w0) fz.dst[(long long)y * sx + p] = r0;
-            if (w1) fz.dst[(long long)y * sx + p + 1] = r1;
-        }
+// the earlier axis whose unpack writes this cell last in the dimension-sequential
+// exchange (-1: none) -- that unpack forwards the cell to face a
+__device__ __forceinline__ int forward_phase(const FusedParams &F, int a, const int *c) {
+    int fwd = -1;
+    for (int b = 0; b < a; ++b) {
+        if (c[b] == 0 && F.halo[b][0].active) fwd = b;
+        if (c[b] == F.s[b] - 1 && F.halo[b][1].active) fwd = b;
     }
+    return fwd;
 }
 
-constexpr int kFTY = 4;   // rows per CTA (one warp each)
-constexpr int kFD = 3;    // planes in flight per thread
+// chunk visited at order position oc: 0, cz, then the others ascending
+__device__ __forceinline__ int chunk_id(const FusedParams &F, int oc) {
+    if (F.cz <= 1 || oc == 0) return oc;
+    if (oc == 1) return F.cz;
+    return oc - 1 < F.cz ? oc - 1 : oc;
+}
+// z range [z0, z1) of the chunk at order position oc
+__device__ __forceinline__ int2 chunk_range(const FusedParams &F, int oc) {
+    const int j = chunk_id(F, oc);
+    const int zmax = F.s[2] - 1;
+    if (j < F.nbig) return make_int2(1 + F.kc1 * j, 1 + F.kc1 * (j + 1));
+    const int z0 = 1 + F.kc1 * F.nbig + F.kc2 * (j - F.nbig);
+    return make_int2(z0, min(z0 + F.kc2, zmax));
+}
+// z range a chunk covers on the x- and y-faces (the rim planes 0 and s-1 go with the end chunks)
+__device__ __forceinline__ int2 ext_range(const FusedParams &F, int c) {
+    int2 r = chunk_range(F, c);
+    if (r.x == 1) r.x = 0;
+    if (r.y == F.s[2] - 1) r.y = F.s[2];
+    return r;
+}
+
+constexpr int kFTY = 4;    // rows per CTA (one warp each)
+constexpr int kFD = 3;     // planes in flight per thread
+constexpr int kFKC = 64;   // longest z-chunk
 
 }  // namespace
 
-// EDGE = true: the tiles holding send layers (launched first, high priority, with the
-// fused pack and the per-face counting); EDGE = false: all other tiles, the plain
-// pipelined sweep (register budget of the 1-GPU kernel)
-template <bool EDGE>
-__global__ void __launch_bounds__(32 * kFTY, EDGE ? 8 : 10) heat_fused_kernel(const __grid_constant__ FusedParams F,
-                                                                              const int4 *__restrict__ tiles) {
+// One launch over all tiles, the 1-GPU loop unchanged.  A CTA whose tile holds
+// send-layer cells (x layer of its rows, a y layer row, or a z layer plane in
+// its chunk) re-reads them from T2 after its sweep (its own just-written, L2-hot
+// values) and stores them into the receivers' slots as contiguous runs, then
+// counts itself on the (face, chunk) counters.  Keeping the face work out of the
+// z loop keeps the loop's instruction stream identical to the 1-GPU kernel.
+template <bool XS>   // XS: capture the x send layer in smem during the sweep (else re-read T2)
+__global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
-    const int4 td = tiles[blockIdx.x];   // (x-tile, y-tile, z0, z1)
+    __shared__ double xs[XS ? kFTY : 1][XS ? kFKC : 1];   // my rows' x send-layer cells over the chunk
+    // tile from the block index alone (x-tiles fastest, then y-tiles, then chunks in visit order)
+    int4 td;
+    {
+        const int b = blockIdx.x;
+        td.x = b % F.xtiles;
+        const int r = b / F.xtiles;
+        td.y = r % F.ytiles;
+        td.z = r / F.ytiles;
+    }
+    const int2 zr = chunk_range(F, td.z);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sx = F.s[0], sy = F.s[1];
     const int y = 1 + td.y * kFTY + warp;
@@ -113,12 +142,31 @@ __global__ void __launch_bounds__(32 * kFTY, EDGE ? 8 : 10) heat_fused_kernel(co
     const bool pair_in = y < sy - 1 && p < sx;
     const bool w0 = pair_in && p >= 1 && p < sx - 1;
     const bool w1 = pair_in && p + 1 >= 1 && p + 1 < sx - 1;
-    const int zs = td.z, ze = td.w;
+    const int zs = zr.x, ze = zr.y;
     const long long sxy = (long long)sx * sy;
     const double *__restrict__ T = F.T;
     const double *__restrict__ Ci = F.Ci;
     double *__restrict__ T2 = F.T2;
+    bool face_tile = false;   // this tile holds send-layer cells
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        const int xl = F.face[0][rs].layer, yl = F.face[1][rs].layer;
+        face_tile |= F.face[0][rs].active && xl >= max(td.x * 64, 1) && xl < min(td.x * 64 + 64, sx - 1);
+        face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
+        face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
+    }
     long long i = (long long)zs * sxy + (long long)y * sx + p;
+    // the lane holding an x send-layer cell of my row (-1: none) and which of its two cells
+    int xlane = -1;
+    bool xodd = false;
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        const int L = F.face[0][rs].layer;
+        if (F.face[0][rs].active && pair_in && ((w0 && p == L) || (w1 && p + 1 == L))) {
+            xlane = lane;
+            xodd = p + 1 == L;
+        }
+    }
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
@@ -131,25 +179,6 @@ __global__ void __launch_bounds__(32 * kFTY, EDGE ? 8 : 10) heat_fused_kernel(co
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
     int slot = 0;
-    bool fstore = false;   // this thread holds a cell of a y send layer (EDGE only)
-    int zf0 = -1, zf1 = -1;
-    // x send layers: the lane holding the layer cell in this warp's row segment (-1: none);
-    // its per-plane values are parked one per lane and written as 32-plane runs
-    // (fused_eligible requires sx >= 66, so a 64-cell segment holds at most one x send layer)
-    int xrs = -1, xoff = 0;
-    double xstage = 0.0;
-    const int tile_x0 = td.x * 64;
-    const bool row_ok = y < sy - 1;
-#pragma unroll
-    for (int rs = 0; rs < 2 && EDGE; ++rs) {
-        const FusedFace &fx = F.face[0][rs], &fy = F.face[1][rs], &fz = F.face[2][rs];
-        if (fx.active && row_ok && fx.layer >= tile_x0 && fx.layer < tile_x0 + 64) {
-            xrs = rs;
-            xoff = fx.layer - tile_x0;   // cell offset in the 64-cell segment
-        }
-        if (fy.active && pair_in && y == fy.layer) fstore = true;
-        if (fz.active) (rs == 0 ? zf0 : zf1) = fz.layer;
-    }
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
         double2 ym = zero2, yp = zero2;
@@ -166,22 +195,15 @@ __global__ void __launch_bounds__(32 * kFTY, EDGE ? 8 : 10) heat_fused_kernel(co
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
         if (w0 && w1) {
-            __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+            if (face_tile)   // keep the face cells in L2 for the re-read below
+                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+            else
+                __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
         } else {
             if (w0) T2[i] = r0;
             if (w1) T2[i + 1] = r1;
         }
-        // fused pack: send-layer cells go straight into the receivers' slots
-        // (hoisted tests: only threads on an x/y send layer, or the planes of a z send layer)
-        if (EDGE && (fstore || z == zf0 || z == zf1)) face_store(F, p, y, z, w0, w1, r0, r1);
-        if (EDGE && xrs >= 0) {   // warp-uniform
-            const double v = __shfl_sync(0xffffffffu, (xoff & 1) ? r1 : r0, xoff >> 1);
-            const int k = (z - zs) & 31;
-            if (lane == k) xstage = v;
-            if (k == 31 || z == ze - 1) {   // flush a run of k+1 planes: dst[y*sz + zbase + lane]
-                if (lane <= k) F.face[0][xrs].dst[(long long)y * F.s[2] + (z - k) + lane] = xstage;
-            }
-        }
+        if (XS && lane == xlane) xs[warp][z - zs] = xodd ? r1 : r0;   // predicated, no branch
         zm = c;
         c = zp;
         if (pair_in && z + kFD < ze) {
@@ -192,41 +214,61 @@ __global__ void __launch_bounds__(32 * kFTY, EDGE ? 8 : 10) heat_fused_kernel(co
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
-    if (!EDGE) return;
-    // count this CTA on every face whose send layer its tile holds
-    unsigned mask = 0;
+    if (!face_tile) return;   // CTA-uniform
+    __syncthreads();          // the CTA's T2 stores are visible to the CTA
+    const int nz = ze - zs;
+    const int tx0 = td.x * 64, ty0 = 1 + td.y * kFTY;
+    const int xlo = max(tx0, 1), xhi = min(tx0 + 64, sx - 1);   // inner x of this tile
+    const int yhi = min(ty0 + kFTY, sy - 1);
+    bool did[6] = {false, false, false, false, false, false};
 #pragma unroll
     for (int rs = 0; rs < 2; ++rs) {
-        const int lx = F.face[0][rs].layer, ly = F.face[1][rs].layer, lz = F.face[2][rs].layer;
-        if (F.face[0][rs].active && lx >= td.x * 64 && lx < td.x * 64 + 64) mask |= 1u << rs;
-        if (F.face[1][rs].active && ly >= 1 + td.y * kFTY && ly < 1 + td.y * kFTY + kFTY) mask |= 1u << (2 + rs);
-        if (F.face[2][rs].active && lz >= zs && lz < ze) mask |= 1u << (4 + rs);
+        // x face: layer column of my rows over the chunk -> runs y*sz + z (z fastest)
+        const FusedFace &fx = F.face[0][rs];
+        if (fx.active && fx.layer >= xlo && fx.layer < xhi) {
+            for (int t = tid; t < kFTY * nz; t += blockDim.x) {
+                const int w = t / nz, zz = t - w * nz;
+                const int yy = ty0 + w;
+                if (yy < yhi)
+                    fx.dst[(long long)yy * F.s[2] + zs + zz] =
+                        XS ? xs[XS ? w : 0][XS ? zz : 0]
+                           : T2[(long long)(zs + zz) * sxy + (long long)yy * sx + fx.layer];
+            }
+            did[rs] = true;
+        }
+        // y face: the layer row over the chunk -> z*sx + x
+        const FusedFace &fy = F.face[1][rs];
+        if (fy.active && fy.layer >= ty0 && fy.layer < yhi) {
+            const int w = xhi - xlo;
+            for (int t = tid; t < w * nz; t += blockDim.x) {
+                const int zz = zs + t / w, xx = xlo + t % w;
+                fy.dst[(long long)zz * sx + xx] = T2[(long long)zz * sxy + (long long)fy.layer * sx + xx];
+            }
+            did[2 + rs] = true;
+        }
+        // z face: the layer plane's rows of this tile -> y*sx + x
+        const FusedFace &fz = F.face[2][rs];
+        if (fz.active && F.zchunk[rs] == td.z) {
+            const int w = xhi - xlo;
+            for (int t = tid; t < w * (yhi - ty0); t += blockDim.x) {
+                const int yy = ty0 + t / w, xx = xlo + t % w;
+                fz.dst[(long long)yy * sx + xx] = T2[(long long)fz.layer * sxy + (long long)yy * sx + xx];
+            }
+            did[4 + rs] = true;
+        }
     }
-    if (mask) {
-        // only the threads that stored into a peer's slot need their stores ordered
-        // before the count (a system fence drains all of a thread's outstanding stores)
-        if (fstore || xrs >= 0 || zf0 >= 0 || zf1 >= 0) __threadfence_system();
-        __syncthreads();
-        if (tid == 0)
-            for (int f = 0; f < 6; ++f)
-                if (mask & (1u << f)) contribute(F.face[f >> 1][f & 1], F.epoch);
-    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0)
+        for (int f = 0; f < 6; ++f)
+            if (did[f]) contribute(F, f >> 1, f & 1, f < 4 ? td.z : 0);
 }
 
-// Face cells the stencil does not compute: the send layer's cells on the other
-// axes' halo/boundary layers.  Those that an earlier axis' unpack will write
-// this step are forwarded by that unpack; all others keep a value that either
-// never changes (global boundary) or is overwritten on the receiver by a later
-// axis, so the current T2 value is sent.
-__device__ __forceinline__ int forward_phase(const FusedParams &F, int a, const int *c) {
-    int fwd = -1;
-    for (int b = 0; b < a; ++b) {
-        if (c[b] == 0 && F.halo[b][0].active) fwd = b;
-        if (c[b] == F.s[b] - 1 && F.halo[b][1].active) fwd = b;
-    }
-    return fwd;
-}
-
+// Face cells the stencil does not compute (on other axes' halo/boundary layers):
+// the ones an earlier axis' unpack writes this step are forwarded by it; all
+// others keep a value that never changes (global boundary) or that a later axis
+// overwrites on the receiver, so the current T2 value is sent.
+// One contribution to every (face, chunk) at the end (ticket).
 __global__ void fused_rim_kernel(const __grid_constant__ FusedParams F, unsigned int *ticket, unsigned total) {
     const int f = blockIdx.y, a = f >> 1, rs = f & 1;
     const FusedFace &fc = F.face[a][rs];
@@ -253,89 +295,156 @@ __global__ void fused_rim_kernel(const __grid_constant__ FusedParams F, unsigned
             const long long gi = ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0];
             fc.dst[fidx(a, c[0], c[1], c[2], F.s)] = F.T2[gi];
         }
+        __threadfence_system();
     }
-    if (fc.active) __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned t = atomicAdd(ticket, 1u);
         if (t == total - 1) {
             __threadfence_system();
-            for (int g = 0; g < 6; ++g)
-                if (F.face[g >> 1][g & 1].active) contribute(F.face[g >> 1][g & 1], F.epoch);
+            for (int g = 0; g < 6; ++g) {
+                const int ga = g >> 1, grs = g & 1;
+                if (!F.face[ga][grs].active) continue;
+                if (ga == 2)
+                    contribute(F, 2, grs, 0);
+                else
+                    for (int ch = 0; ch < F.nchunks; ++ch) contribute(F, ga, grs, ch);
+            }
             atomicExch(ticket, 0u);
         }
     }
 }
 
-// one CTA waits until both receive flags of axis b reached this epoch
-__global__ void fused_wait_kernel(const __grid_constant__ FusedParams F, int b) {
-    const int side = threadIdx.x;
-    if (side < 2 && F.halo[b][side].active) {
-        const unsigned long long *fl = F.halo[b][side].flag;
+__device__ __forceinline__ void wait_flag(const FusedParams &F, const unsigned long long *fl) {
+    if (threadIdx.x == 0) {
         const long long t0 = clock64();
         while (ld_acq_sys(fl) < F.epoch) {
             if (clock64() - t0 > F.timeout_cycles) {
                 atomicExch(F.err, 1);
                 break;
             }
-            __nanosleep(32);
+            __nanosleep(128);
+        }
+    }
+    __syncthreads();
+}
+
+// The receiver side: kCommCTAs persistent CTAs walk the chunks in kernel order.
+// Per chunk: x faces (wait both flags, unpack a 1/kCommCTAs share into T2's x
+// halo, forward the cells the y/z faces need), then y faces likewise; after the
+// chunks holding the z layers, the z planes.  Each CTA counts itself once per
+// (face, chunk) it forwarded into.  The peers' comm kernels progress the same
+// way, so a y flag (which needs the peer's x forward of that chunk) never waits
+// on anything behind it.
+constexpr int kCommCTAs = 32;
+constexpr int kUnpackILP = 2;
+
+__device__ __forceinline__ void unpack_share(const FusedParams &F, int b, int side, int2 zr, bool &fwd) {
+    const FusedHalo &h = F.halo[b][side];
+    const int nz = zr.y - zr.x;
+    const int U = b == 0 ? F.s[1] : F.s[0];   // cells (u, z): u = y (x faces) or x (y faces)
+    const long long n = (long long)U * nz;
+    const long long step = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += step * kUnpackILP) {
+        double v[kUnpackILP];
+        long long si[kUnpackILP];
+#pragma unroll
+        for (int k = 0; k < kUnpackILP; ++k) {
+            const long long t = base + k * step + threadIdx.x;
+            long long q = 0;
+            if (t < n) {
+                if (b == 0) {   // x-face slot layout y*sz + z (z fastest)
+                    const int u = (int)(t / nz);
+                    q = (long long)u * F.s[2] + zr.x + (t - (long long)u * nz);
+                } else {        // y-face slot layout z*sx + x
+                    const int zz = (int)(t / U);
+                    q = (long long)(zr.x + zz) * F.s[0] + (t - (long long)zz * U);
+                }
+            }
+            si[k] = q;
+            v[k] = t < n ? __ldcg(h.src + q) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kUnpackILP; ++k) {
+            const long long t = base + k * step + threadIdx.x;
+            if (t >= n) continue;
+            int c[3];
+            if (b == 0) {
+                c[1] = (int)(si[k] / F.s[2]);
+                c[2] = (int)(si[k] - (long long)c[1] * F.s[2]);
+                c[0] = h.layer;
+            } else {
+                c[2] = (int)(si[k] / F.s[0]);
+                c[0] = (int)(si[k] - (long long)c[2] * F.s[0]);
+                c[1] = h.layer;
+            }
+            F.T2[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v[k];
+            for (int a = b + 1; a < 3; ++a)
+                for (int rs = 0; rs < 2; ++rs) {
+                    const FusedFace &fc = F.face[a][rs];
+                    if (fc.active && c[a] == fc.layer && forward_phase(F, a, c) == b) {
+                        fc.dst[fidx(a, c[0], c[1], c[2], F.s)] = v[k];
+                        fwd = true;
+                    }
+                }
         }
     }
 }
 
-// unpack axis b into T2's halo layers and forward the cells later faces need;
-// kUnpackILP values per thread are loaded before any store (latency-bound
-// scattered stores: the x halo is one double per row)
-constexpr int kUnpackILP = 8;
-__global__ void __launch_bounds__(256) fused_unpack_kernel(const __grid_constant__ FusedParams F, int b,
-                                                           unsigned int *ticket, unsigned total) {
-    const int side = blockIdx.y;
-    const FusedHalo &h = F.halo[b][side];
-    if (h.active) {
-        const int b1 = fast_axis(b), b2 = slow_axis(b);   // slot index = c[b2]*S[b1] + c[b1]
-        const int S1 = F.s[b1];
-        const long long n = (long long)S1 * F.s[b2];
-        bool fwd_any = false;
-        for (int a = b + 1; a < 3; ++a) fwd_any |= F.face[a][0].active || F.face[a][1].active;
-        const long long chunk = (long long)blockDim.x * kUnpackILP;
-        for (long long base = (long long)blockIdx.x * chunk; base < n; base += (long long)gridDim.x * chunk) {
-            double v[kUnpackILP];
-#pragma unroll
-            for (int u = 0; u < kUnpackILP; ++u) {
-                const long long t = base + u * blockDim.x + threadIdx.x;
-                v[u] = t < n ? __ldcg(h.src + t) : 0.0;
+__global__ void __launch_bounds__(128, 12) fused_comm_kernel(const __grid_constant__ FusedParams F, int zafter) {
+    for (int ch = 0; ch < F.nchunks; ++ch) {
+        const int2 zr = ext_range(F, ch);
+        for (int b = 0; b < 2; ++b) {
+            if (!(F.halo[b][0].active || F.halo[b][1].active)) continue;
+            if (threadIdx.x < 2 && F.halo[b][threadIdx.x].active) {
+                const unsigned long long *fl = F.halo[b][threadIdx.x].flag + ch;
+                const long long t0 = clock64();
+                while (ld_acq_sys(fl) < F.epoch) {
+                    if (clock64() - t0 > F.timeout_cycles) {
+                        atomicExch(F.err, 1);
+                        break;
+                    }
+                    __nanosleep(128);
+                }
             }
-#pragma unroll
-            for (int u = 0; u < kUnpackILP; ++u) {
-                const long long t = base + u * blockDim.x + threadIdx.x;
-                if (t >= n) continue;
-                int c[3];
-                c[b] = h.layer;
-                c[b1] = (int)(t % S1);
-                c[b2] = (int)(t / S1);
-                F.T2[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v[u];
-                if (fwd_any)
-                    for (int a = b + 1; a < 3; ++a)
-                        for (int rs = 0; rs < 2; ++rs) {
-                            const FusedFace &fc = F.face[a][rs];
-                            if (fc.active && c[a] == fc.layer && forward_phase(F, a, c) == b)
-                                fc.dst[fidx(a, c[0], c[1], c[2], F.s)] = v[u];
-                        }
-            }
+            __syncthreads();
+            bool fwd = false;
+            for (int side = 0; side < 2; ++side)
+                if (F.halo[b][side].active && !F.dry) unpack_share(F, b, side, zr, fwd);
+            if (__syncthreads_or(fwd)) __threadfence_system();
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int a = b + 1; a < 3; ++a)
+                    for (int rs = 0; rs < 2; ++rs) {
+                        if (!F.face[a][rs].active) continue;
+                        if (a == 1)
+                            contribute(F, 1, rs, ch);
+                        else if (F.face[2][rs].layer >= zr.x && F.face[2][rs].layer < zr.y)
+                            contribute(F, 2, rs, 0);
+                    }
         }
-    }
-    bool fwd = false;   // forwarded values went to peers: order them before the count
-    for (int a = b + 1; a < 3; ++a) fwd |= F.face[a][0].active || F.face[a][1].active;
-    if (fwd && h.active) __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned t = atomicAdd(ticket, 1u);
-        if (t == total - 1) {
-            __threadfence_system();
-            for (int a = b + 1; a < 3; ++a)
-                for (int rs = 0; rs < 2; ++rs)
-                    if (F.face[a][rs].active) contribute(F.face[a][rs], F.epoch);
-            atomicExch(ticket, 0u);
+        if (ch == zafter) {   // both z send layers' chunks are done everywhere: the z planes
+            if (threadIdx.x < 2 && F.halo[2][threadIdx.x].active) {
+                const unsigned long long *fl = F.halo[2][threadIdx.x].flag;
+                const long long t0 = clock64();
+                while (ld_acq_sys(fl) < F.epoch) {
+                    if (clock64() - t0 > F.timeout_cycles) {
+                        atomicExch(F.err, 1);
+                        break;
+                    }
+                    __nanosleep(128);
+                }
+            }
+            __syncthreads();
+            const long long n = (long long)F.s[0] * F.s[1];
+            for (int side = 0; side < 2; ++side) {
+                const FusedHalo &h = F.halo[2][side];
+                if (!h.active) continue;
+                double *dst = F.T2 + (long long)h.layer * n;
+                for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+                     t += (long long)gridDim.x * blockDim.x)
+                    dst[t] = __ldcg(h.src + t);
+            }
         }
     }
 }
@@ -343,90 +452,100 @@ __global__ void __launch_bounds__(256) fused_unpack_kernel(const __grid_constant
 // ------------------------------------------------------------------ host side
 bool fused_eligible(const igg_grid *g) {
     if (g->fused == 2 && g->nlocal == 1) return true;   // ablation/profiling: force the fused kernel
+    // fused = 3/5: timing experiments on the same path (see fused_step)
     if (g->path != IGG_PATH_P2P || g->nlocal != 1 || g->nproc_procs < 2 || g->fused == 0) return false;
     for (int a = 0; a < 3; ++a)
         for (int k = 0; k < 2; ++k) {
             const int nb = g->nbr[0][a][k];
             if (nb >= 0 && proc_of(g, nb) == g->proc) return false;   // self-wrap: stream-ordered path
         }
-    for (int a = 0; a < 3; ++a)
-        if (g->n[a] < 5) return false;
-    if (g->n[0] < 66) return false;   // one x send layer per 64-cell segment
+    if (g->n[0] < 66 || g->n[1] < 6 || g->n[2] < 6) return false;   // one x send layer per 64-cell segment
     return true;
 }
 
-// tile list: the tiles holding send layers first (x, then y, then z), then the rest;
-// z-chunks of 64 planes with the last ~2 waves in 8-plane chunks (short tail)
-static void build_tiles(igg_grid *g, const int layer[3][2], const bool act[3][2]) {
+static int g_fused_occ = -1, g_fused_nsm = 0;
+
+// chunks: 64 planes, the last ~2 waves in 8-plane chunks; the chunk holding
+// plane n2-2 (the upper z send layer) is visited second, right after chunk 0
+// (holding plane 1).  The layout depends on the geometry only, so every rank
+// numbers chunks identically (flags are per chunk position).
+static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2]) {
     const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
     const int xtiles = (n0 - 1 + 63) / 64;
     const int ytiles = (n1 - 2 + kFTY - 1) / kFTY;
     const int wz = n2 - 2;
-    static int occ = -1, nsm = 0;
-    if (occ < 0) {
-        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, heat_fused_kernel<false>, 32 * kFTY, 0));
-        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+    if (g_fused_occ < 0) {
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false>, 32 * kFTY, 0));
+        IGG_CUDA(cudaDeviceGetAttribute(&g_fused_nsm, cudaDevAttrMultiProcessorCount, g->device));
     }
-    const int kc1 = 64, kc2 = 8;
+    const int kc1 = kFKC, kc2 = 8;
     const long long ntile = (long long)xtiles * ytiles;
-    int small = (int)((2LL * occ * nsm * kc2 + ntile - 1) / ntile);
+    int small = (int)((2LL * g_fused_occ * g_fused_nsm * kc2 + ntile - 1) / ntile);
     small = std::min(((small + kc2 - 1) / kc2) * kc2, wz);
     const int nbig = (wz - small) / kc1;
-    std::vector<std::array<int, 2>> chunks;
-    for (int c = 0; c < nbig; ++c) chunks.push_back({1 + c * kc1, 1 + (c + 1) * kc1});
-    for (int z = 1 + nbig * kc1; z < 1 + wz; z += kc2) chunks.push_back({z, std::min(z + kc2, 1 + wz)});
-    std::vector<int4> edge[3], rest;
-    for (const auto &ch : chunks)
-        for (int yt = 0; yt < ytiles; ++yt)
-            for (int xt = 0; xt < xtiles; ++xt) {
-                const int4 t = make_int4(xt, yt, ch[0], ch[1]);
-                int cls = -1;
-                for (int rs = 0; rs < 2 && cls < 0; ++rs)
-                    if (act[0][rs] && layer[0][rs] >= xt * 64 && layer[0][rs] < xt * 64 + 64) cls = 0;
-                for (int rs = 0; rs < 2 && cls < 0; ++rs)
-                    if (act[1][rs] && layer[1][rs] >= 1 + yt * kFTY && layer[1][rs] < 1 + yt * kFTY + kFTY) cls = 1;
-                for (int rs = 0; rs < 2 && cls < 0; ++rs)
-                    if (act[2][rs] && layer[2][rs] >= ch[0] && layer[2][rs] < ch[1]) cls = 2;
-                (cls >= 0 ? edge[cls] : rest).push_back(t);
-                if (cls < 0) {
-                    const long long cx = std::min(n0 - 1, xt * 64 + 64) - std::max(1, xt * 64);
-                    const long long cy = std::min(n1 - 1, 1 + yt * kFTY + kFTY) - (1 + yt * kFTY);
-                    g->fused_rest_cells += cx * cy * (ch[1] - ch[0]);
-                }
-                for (int a = 0; a < 3; ++a)
-                    for (int rs = 0; rs < 2; ++rs) {
-                        if (!act[a][rs]) continue;
-                        const int L = layer[a][rs];
-                        const bool in = a == 0 ? (L >= xt * 64 && L < xt * 64 + 64)
-                                                : (a == 1 ? (L >= 1 + yt * kFTY && L < 1 + yt * kFTY + kFTY)
-                                                          : (L >= ch[0] && L < ch[1]));
-                        if (in) g->fused_tiles_per_face[a][rs]++;
-                    }
-            }
-    std::vector<int4> all;
-    for (int a = 0; a < 3; ++a) all.insert(all.end(), edge[a].begin(), edge[a].end());
-    g->fused_nedge = (int)all.size();
-    all.insert(all.end(), rest.begin(), rest.end());
-    if (g->fused_tiles) cudaFree(g->fused_tiles);
-    IGG_CUDA(cudaMalloc(&g->fused_tiles, all.size() * sizeof(int4)));
-    g->allocs++;
-    IGG_CUDA(cudaMemcpy(g->fused_tiles, all.data(), all.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    g->fused_ntiles = (int)all.size();
+    std::vector<int2> zc;   // by chunk id
+    for (int c = 0; c < nbig; ++c) zc.push_back(make_int2(1 + c * kc1, 1 + (c + 1) * kc1));
+    for (int z = 1 + nbig * kc1; z < 1 + wz; z += kc2) zc.push_back(make_int2(z, std::min(z + kc2, 1 + wz)));
+    const int nch = (int)zc.size();
+    if (nch > kMaxChunks) fail(IGG_E_UNSUPPORTED, "fused step: too many z-chunks");
+    int cz = 0;
+    for (int c = 0; c < nch; ++c)
+        if (n2 - 2 >= zc[c].x && n2 - 2 < zc[c].y) cz = c;
+    // visit order position of each chunk id (mirror of chunk_id() on the device)
+    auto id_of = [&](int oc) { return (cz <= 1 || oc == 0) ? oc : (oc == 1 ? cz : (oc - 1 < cz ? oc - 1 : oc)); };
+    g->fused_zchunk[0] = g->fused_zchunk[1] = -1;
+    for (int oc = 0; oc < nch; ++oc) {
+        const int2 r = zc[id_of(oc)];
+        for (int rs = 0; rs < 2; ++rs)
+            if (act[2][rs] && layer[2][rs] >= r.x && layer[2][rs] < r.y) g->fused_zchunk[rs] = oc;
+    }
+    g->fused_zafter = 0;
+    for (int oc = 0; oc < nch; ++oc) {
+        const int2 r = zc[id_of(oc)];
+        if ((1 >= r.x && 1 < r.y) || (n2 - 2 >= r.x && n2 - 2 < r.y)) g->fused_zafter = std::max(g->fused_zafter, oc);
+    }
+    // targets: tiles holding (face, chunk) + 1 (rim) + forwarding comm CTAs
+    int xsides = 0, ysides = 0;
+    for (int sd = 0; sd < 2; ++sd) {
+        xsides += g->nbr[0][0][sd] >= 0 ? 1 : 0;
+        ysides += g->nbr[0][1][sd] >= 0 ? 1 : 0;
+    }
+    const unsigned xfw = xsides ? kCommCTAs : 0, yfw = ysides ? kCommCTAs : 0;
+    std::vector<unsigned> tgt(6 * kMaxChunks, 0u);
+    for (int rs = 0; rs < 2; ++rs) {
+        for (int c = 0; c < nch; ++c) {
+            if (act[0][rs]) tgt[(0 * 2 + rs) * kMaxChunks + c] = ytiles + 1;
+            if (act[1][rs]) tgt[(1 * 2 + rs) * kMaxChunks + c] = xtiles + 1 + xfw;
+        }
+        if (act[2][rs]) tgt[(2 * 2 + rs) * kMaxChunks] = xtiles * ytiles + 1 + xfw + yfw;
+    }
+    if (!g->fused_tgt) {
+        IGG_CUDA(cudaMalloc(&g->fused_tgt, tgt.size() * sizeof(unsigned)));
+        g->allocs++;
+    }
+    IGG_CUDA(cudaMemcpy(g->fused_tgt, tgt.data(), tgt.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+    g->fused_ntiles = (int)(ntile * nch);
+    g->fused_nchunks = nch;
+    g->fused_geo[0] = nbig;
+    g->fused_geo[1] = kc1;
+    g->fused_geo[2] = kc2;
+    g->fused_geo[3] = cz;
+    g->fused_geo[4] = xtiles;
+    g->fused_geo[5] = ytiles;
 }
 
 void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s) {
-    // buffer pool and slot layout of one canonical field (the same plan update_halo uses)
+    // buffer pool and slot layout of one canonical field (the plan update_halo uses)
     const long long sizes[3] = {g->n[0], g->n[1], g->n[2]};
     const Plan plan = build_plan(*g, sizes, 1);
     const size_t half = (size_t)plan.block * sizeof(double);
     ensure_arena(g, half, 0);
     if (!g->fused_ctr) {
-        IGG_CUDA(cudaMalloc(&g->fused_ctr, 16 * sizeof(unsigned int)));
-        IGG_CUDA(cudaMemset(g->fused_ctr, 0, 16 * sizeof(unsigned int)));
+        IGG_CUDA(cudaMalloc(&g->fused_ctr, (6 * kMaxChunks + 8) * sizeof(unsigned int)));
+        IGG_CUDA(cudaMemset(g->fused_ctr, 0, (6 * kMaxChunks + 8) * sizeof(unsigned int)));
         g->allocs++;
     }
-    // receive-slot offsets of (axis, side) within one rank's block (plan order: axis-major, side)
-    long long off[3][2];
+    long long off[3][2];   // slot of (axis, side) in a rank's block: plan order, h = 1
     {
         long long o = 0;
         for (int a = 0; a < 3; ++a) {
@@ -435,12 +554,13 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
                 if (b != a) other *= sizes[b];
             for (int sd = 0; sd < 2; ++sd) {
                 off[a][sd] = o;
-                o += other;   // h = 1 for a canonical field with overlap 2
+                o += other;
             }
         }
     }
     g->epoch++;
     const int parity = (int)(g->epoch & 1);
+    const bool comm = !g->skip_comm;
     FusedParams F{};
     F.T = T;
     F.Ci = Ci;
@@ -450,7 +570,7 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
     F.timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
     F.err = g->d_err;
     F.k = k;
-    const bool comm = !g->skip_comm;
+    F.ctr = g->fused_ctr;
     int layer[3][2];
     bool act[3][2];
     for (int a = 0; a < 3; ++a)
@@ -463,84 +583,75 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
             FusedFace &f = F.face[a][rs];
             f.layer = layer[a][rs];
             f.active = act[a][rs];
-            f.counter = g->fused_ctr + a * 2 + rs;
             if (f.active) {
                 const int pp = proc_of(g, nb);
                 f.dst = reinterpret_cast<double *>(g->peer_recv[pp] + parity * g->recv_half) + off[a][rs];
-                f.flag = g->peer_flags[pp] + a * 2 + rs;
+                f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
             }
-            const int hb = g->nbr[0][a][rs];   // my halo side rs is filled by neighbour on side rs
+            const int hb = g->nbr[0][a][rs];   // my halo side rs is filled by my neighbour on side rs
             FusedHalo &h = F.halo[a][rs];
             h.active = comm && hb >= 0;
             h.layer = rs == 0 ? 0 : g->n[a] - 1;
             h.src = reinterpret_cast<const double *>(g->recv_arena + parity * g->recv_half) + off[a][rs];
-            h.flag = g->flags + a * 2 + rs;
+            h.flag = g->flags + (a * 2 + rs) * kMaxChunks;
         }
-    // tiles (once per activity pattern)
     int key = 0;
     for (int a = 0; a < 3; ++a)
         for (int rs = 0; rs < 2; ++rs) key |= (act[a][rs] ? 1 : 0) << (a * 2 + rs);
-    if (!g->fused_tiles || g->fused_key != key) {
-        std::memset(g->fused_tiles_per_face, 0, sizeof g->fused_tiles_per_face);
-        g->fused_rest_cells = 0;
-        build_tiles(g, layer, act);
+    if (g->fused_key != key) {
+        build_layout(g, layer, act);
         g->fused_key = key;
     }
-    bool unpack_axis[3];
-    for (int b = 0; b < 3; ++b) unpack_axis[b] = F.halo[b][0].active || F.halo[b][1].active;
-    for (int a = 0; a < 3; ++a)
-        for (int rs = 0; rs < 2; ++rs) {
-            unsigned t = (unsigned)g->fused_tiles_per_face[a][rs] + 1;   // + the rim kernel
-            for (int b = 0; b < a; ++b) t += unpack_axis[b] ? 1 : 0;
-            F.face[a][rs].target = t;
-        }
+    F.nchunks = g->fused_nchunks;
+    F.nbig = g->fused_geo[0];
+    F.kc1 = g->fused_geo[1];
+    F.kc2 = g->fused_geo[2];
+    F.cz = g->fused_geo[3];
+    F.xtiles = g->fused_geo[4];
+    F.ytiles = g->fused_geo[5];
+    F.zchunk[0] = g->fused_zchunk[0];
+    F.zchunk[1] = g->fused_zchunk[1];
+    F.tgt = g->fused_tgt;
 
     IGG_CUDA(cudaEventRecord(g->ev_start, s));
     IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
-    IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
     tl_mark(g, s, 0);
-    // the edge tiles with the fused pack first, high priority; the other tiles concurrently,
-    // low priority (they fill the SM slots the edge CTAs leave)
-    const int nedge = g->fused_nedge, nrest = g->fused_ntiles - g->fused_nedge;
-    if (nedge > 0) {
-        heat_fused_kernel<true><<<nedge, 32 * kFTY, 0, g->s_comm>>>(F, g->fused_tiles);
-        IGG_CUDA(cudaGetLastError());
-        g->launches++;
-    }
-    tl_mark(g, g->s_comm, 1);   // timeline: my edge tiles (and their face stores) done
-    tl_mark(g, g->s_inner, 2);
-    prof_begin(g, g->s_inner);
-    if (nrest > 0) {
-        heat_fused_kernel<false><<<nrest, 32 * kFTY, 0, g->s_inner>>>(F, g->fused_tiles + nedge);
-        IGG_CUDA(cudaGetLastError());
-        g->launches++;
-    }
-    prof_end(g, g->s_inner, g->fused_rest_cells);
-    tl_mark(g, g->s_inner, 3);
     if (comm) {
+        // rim first (tiny), then the waiting unpack CTAs of every axis: they sit in the
+        // SM slots the register-limited stencil leaves free and unpack chunk by chunk
         const int rim_blocks = 8;
-        fused_rim_kernel<<<dim3(rim_blocks, 6), 256, 0, g->s_comm>>>(F, g->fused_ctr + 8, rim_blocks * 6);
+        fused_rim_kernel<<<dim3(rim_blocks, 6), 256, 0, g->s_comm>>>(F, g->fused_ctr + 6 * kMaxChunks,
+                                                                     rim_blocks * 6);
         IGG_CUDA(cudaGetLastError());
         g->launches++;
-        for (int b = 0; b < 3; ++b) {
-            if (!unpack_axis[b]) continue;
-            fused_wait_kernel<<<1, 32, 0, g->s_comm>>>(F, b);
-            IGG_CUDA(cudaGetLastError());
-
-            long long other = 1;
-            for (int c = 0; c < 3; ++c)
-                if (c != b) other *= g->n[c];
-            const int blocks = (int)std::min<long long>(std::max<long long>((other + 2047) / 2048, 1), 148);
-            fused_unpack_kernel<<<dim3(blocks, 2), 256, 0, g->s_comm>>>(F, b, g->fused_ctr + 9 + b, blocks * 2);
-            IGG_CUDA(cudaGetLastError());
-            g->launches += 2;
-        }
+    }
+    tl_mark(g, g->s_comm, 1);
+    // the stencil on the caller's stream (fused_mode bit 1: on the low-priority inner stream)
+    cudaStream_t ss = (g->fused_mode & 2) ? g->s_inner : s;
+    if (ss != s) IGG_CUDA(cudaStreamWaitEvent(ss, g->ev_start, 0));
+    tl_mark(g, ss, 2);
+    prof_begin(g, ss);
+    if (g->fused_mode & 1)
+        heat_fused_kernel<true><<<g->fused_ntiles, 32 * kFTY, 0, ss>>>(F);
+    else
+        heat_fused_kernel<false><<<g->fused_ntiles, 32 * kFTY, 0, ss>>>(F);
+    IGG_CUDA(cudaGetLastError());
+    g->launches++;
+    prof_end(g, ss, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2));
+    tl_mark(g, ss, 3);
+    if (ss != s) {
+        IGG_CUDA(cudaEventRecord(g->ev_inner, ss));
+        IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
+    }
+    if (comm && g->fused != 3) {   // fused == 3: timing experiment, no receive side (INVALID halos)
+        F.dry = g->fused == 5;        // fused == 5: timing experiment, wait only (INVALID halos)
+        fused_comm_kernel<<<kCommCTAs, 128, 0, g->s_comm>>>(F, g->fused_zafter);
+        IGG_CUDA(cudaGetLastError());
+        g->launches++;
     }
     tl_mark(g, g->s_comm, 4);
     IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
-    IGG_CUDA(cudaEventRecord(g->ev_inner, g->s_inner));
     IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
-    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
 }
 
 }  // namespace igg

@@ -149,7 +149,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
                     d.buf = recv + m.slot;
                 } else if (m.transport == kP2P) {
                     d.buf = reinterpret_cast<double *>(g->peer_recv[m.peer_proc] + parity * g->recv_half) + m.slot;
-                    unsigned long long *fl = g->peer_flags[m.peer_proc] + (m.peer_lr * 3 + a) * 2 + m.recv_side;
+                    unsigned long long *fl = g->peer_flags[m.peer_proc] + ((m.peer_lr * 3 + a) * 2 + m.recv_side) * kMaxChunks;
                     bool have = false;
                     for (int s = 0; s < P.nsignal; ++s) have |= P.signal[s] == fl;
                     if (!have) {
@@ -163,7 +163,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
             } else {
                 d.buf = recv + m.slot;
                 if (m.transport == kP2P) {
-                    const unsigned long long *fl = g->flags + (m.lr * 3 + a) * 2 + m.recv_side;
+                    const unsigned long long *fl = g->flags + ((m.lr * 3 + a) * 2 + m.recv_side) * kMaxChunks;
                     int w = -1;
                     for (int s = 0; s < U.nsignal; ++s)
                         if (U.wait[s] == fl) w = s;
@@ -440,8 +440,9 @@ IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_
             IGG_NCCL(ncclCommInitRank(&g->comm, g->nproc_procs, id, g->proc));
         }
         // receive flags (P2P), last-block tickets, error word, reduction scratch
-        g->flags = (unsigned long long *)igg::dev_alloc(g, sizeof(unsigned long long) * g->nlocal * 6);
-        IGG_CUDA(cudaMemset(g->flags, 0, sizeof(unsigned long long) * g->nlocal * 6));
+        const size_t flag_bytes = sizeof(unsigned long long) * g->nlocal * 6 * igg::kMaxChunks;
+        g->flags = (unsigned long long *)igg::dev_alloc(g, flag_bytes);
+        IGG_CUDA(cudaMemset(g->flags, 0, flag_bytes));
         g->tickets = (unsigned int *)igg::dev_alloc(g, sizeof(unsigned int) * 4);
         IGG_CUDA(cudaMemset(g->tickets, 0, sizeof(unsigned int) * 4));
         g->d_err = (int *)igg::dev_alloc(g, sizeof(int) * 2);
@@ -494,7 +495,7 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->fused_tiles, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->fused_tgt, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
@@ -661,6 +662,7 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_X_ALIGN: g->x_align = (int)(value < 1 ? 1 : value); break;
         case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
         case IGG_OPT_FUSED: g->fused = (int)value; break;
+        case IGG_OPT_FUSED_MODE: g->fused_mode = (int)value; break;
         default: fail(IGG_E_ARG, "igg_set_option: unknown key " + std::to_string(key));
     }
     IGG_CATCH

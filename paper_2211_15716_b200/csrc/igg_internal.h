@@ -118,17 +118,16 @@ struct HeatRegionList {
 };
 
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
+constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // receiver's slot (peer-mapped), this step's parity half
-    unsigned long long *flag;        // receiver's flag for (axis, side)
-    unsigned int *counter;           // my contribution counter for this face
-    unsigned int target;             // contributions that complete the face
+    unsigned long long *flag;        // receiver's flags of (axis, side): [kMaxChunks] (z faces: [0])
     int layer;                       // my send layer along the axis
     int active;
 };
 struct FusedHalo {                   // one halo side I receive
     const double *src;               // my slot, this step's parity half
-    const unsigned long long *flag;  // my flag
+    const unsigned long long *flag;  // my flags [kMaxChunks]
     int layer;                       // halo layer (0 or s-1)
     int active;
 };
@@ -139,6 +138,13 @@ struct FusedParams {
     int s[3];
     FusedFace face[3][2];
     FusedHalo halo[3][2];
+    int nchunks;                     // z-chunks; chunk ids 0..nbig-1 have kc1 planes, then kc2
+    int nbig, kc1, kc2, cz;          // cz: chunk id holding plane s_z-2, visited second
+    int xtiles, ytiles;
+    int dry;                         // timing experiment: waits without unpacking
+    int zchunk[2];                   // chunk holding z send layer of face (2, rs); -1 if none
+    unsigned int *ctr;               // [6][kMaxChunks] contribution counters (sender side)
+    const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk)
     unsigned long long epoch;
     long long timeout_cycles;
     int *err;
@@ -244,11 +250,12 @@ struct igg_grid : igg::Geom {
     int x_align = 64;
     int schedule = 0;
     int fused = 1;                                       // IGG_OPT_FUSED
-    int4 *fused_tiles = nullptr;
-    int fused_ntiles = 0, fused_nedge = 0, fused_key = -1;
-    long long fused_rest_cells = 0;
-    int fused_tiles_per_face[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-    unsigned int *fused_ctr = nullptr;
+    int fused_mode = 2;                                  // IGG_OPT_FUSED_MODE (ablation bits)
+    unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr;
+    int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
+    int fused_ntiles = 0, fused_nchunks = 0, fused_key = -1;
+    int fused_zchunk[2] = {-1, -1};
+    int fused_zafter = 1;
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
