@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exposed", action="store_true")
-    ap.add_argument("--fused", type=int, default=1, help="1: fused stencil+P2P exchange kernel (p2p path)")
+    ap.add_argument("--fused", type=int, default=-1, help="1 fused stencil+P2P put kernel, 0 split, -1 auto")
     ap.add_argument("--fused-mode", type=int, default=2, help="ablation bits of the fused path")
     ap.add_argument("--schedule", type=int, default=0, help="0 concurrent, 1 boundary first (paper order)")
     ap.add_argument("--timeline", action="store_true", help="record the overlap timeline (extra events)")

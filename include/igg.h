@@ -225,9 +225,10 @@ enum {
                                     512-B row segments; 1 = the exact widths given) */
     IGG_OPT_SCHEDULE = 6,        /* 0 = inner box concurrent with the boundary slabs; 1 = inner box
                                     after the boundary slabs (paper order), concurrent with the exchange */
-    IGG_OPT_FUSED = 7,           /* 1 (default) = P2P path with one rank per GPU: one stencil kernel
-                                    that stores send layers into the peers' slots as it computes them;
-                                    0 = boundary/inner kernels + separate pack/exchange/unpack */
+    IGG_OPT_FUSED = 7,           /* P2P path, one rank per GPU: 1 = one stencil kernel that stores its
+                                    send layers straight into the neighbours' halos over NVLink, chunk
+                                    by chunk; 0 = boundary/inner kernels + pack/exchange/unpack;
+                                    -1 (default) = fused when exactly one axis exchanges */
     IGG_OPT_FUSED_MODE = 8       /* ablation bits of the fused path: 1 = capture x send layer in smem,
                                     2 = stencil on the low-priority inner stream */
 };

@@ -1,24 +1,25 @@
-// fused.cu -- the fused hide_communication step: stencil + halo exchange in
-// peer memory, pipelined by z-chunks (IGG_PATH_P2P, one rank per process,
-// every neighbour on another GPU).
+// fused.cu -- the fused hide_communication step: stencil + halo exchange as
+// one-sided NVLink puts straight into the neighbours' arrays, pipelined by
+// z-chunks (IGG_PATH_P2P, one rank per process, every neighbour on another GPU).
 //
 // The paper hides update_halo! behind the inner-point computation (PAPER.md:75,
 // :94 "pipelining is applied on all stages of the data transfers").
 // On B200 one stencil kernel keeps the 1-GPU tile order (z-chunk, then y-tile,
-// then x-tile: whole 4-KB rows stream together, which the boundary/inner split
-// breaks) and stores every cell of a send layer straight into the receiving
-// GPU's receive slot over NVLink as it computes it (the pack is fused into the
-// stencil).  Faces are published chunk by chunk: each CTA that holds part of
-// face f in chunk c counts itself on counter (f, c) after a system fence; the
-// contribution completing (f, c) release-stores the epoch into the receiver's
-// flag (f, c).  The receiver's unpack CTAs (one per chunk and side, waiting with
-// ld.acquire.sys) run while the stencil is still going, so only the last small
-// chunk's unpack can be exposed.  Face cells the stencil does not compute come
-// from a rim kernel (values that never change or are overwritten later on the
-// receiver) or are forwarded by the unpack of an earlier axis (fresh
-// edge/corner values of the dimension-sequential update_halo, SPEC.md:211,
-// :236).  The final state is bit-identical to {step!; update_halo!(T2)}
-// (tests/test_gpu_multi.py).
+// then x-tile: whole 4-KB rows stream together) and, when a tile holding send
+// layers finishes its chunk, stores those cells directly into the receiving
+// rank's T2 halo layers over NVLink (pack, transfer and unpack fused into one
+// store; the receiver's SMs do no copy work).  Faces are published chunk by
+// chunk: each CTA that holds part of face f in chunk c counts itself on
+// counter (f, c) after a system fence; the contribution completing (f, c)
+// release-stores the epoch into the receiver's flag (f, c).  Face cells the
+// stencil does not compute come from a rim kernel (values that never change or
+// are overwritten later on the receiver) or are forwarded, after the flags of
+// an earlier axis arrived, by a tiny comm kernel (the fresh edge/corner values
+// of the dimension-sequential update_halo).  The receiver
+// waits for every flag before the step completes.  Hazard argument (DESIGN.md
+// §6): a peer writes my T2(t) halo only after it received my step t-1 faces,
+// i.e. after my step t-1 tiles that read those halo cells finished.  The final
+// state is bit-identical to {step!; update_halo!(T2)} (tests/test_gpu_multi.py).
 #include <algorithm>
 #include <array>
 #include <cstring>
@@ -223,36 +224,42 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     bool did[6] = {false, false, false, false, false, false};
 #pragma unroll
     for (int rs = 0; rs < 2; ++rs) {
-        // x face: layer column of my rows over the chunk -> runs y*sz + z (z fastest)
+        // rs = 0: the upper neighbour's lower halo layer 0; rs = 1: the lower neighbour's layer s-1
+        // x face: the layer column of my rows over the chunk -> peer T2 x halo
         const FusedFace &fx = F.face[0][rs];
         if (fx.active && fx.layer >= xlo && fx.layer < xhi) {
+            const int hx = rs == 0 ? 0 : sx - 1;
             for (int t = tid; t < kFTY * nz; t += blockDim.x) {
-                const int w = t / nz, zz = t - w * nz;
+                const int w = t / nz, zz = zs + (t - w * nz);
                 const int yy = ty0 + w;
-                if (yy < yhi)
-                    fx.dst[(long long)yy * F.s[2] + zs + zz] =
-                        XS ? xs[XS ? w : 0][XS ? zz : 0]
-                           : T2[(long long)(zs + zz) * sxy + (long long)yy * sx + fx.layer];
+                if (yy < yhi) {
+                    const long long row = (long long)zz * sxy + (long long)yy * sx;
+                    fx.dst[row + hx] = XS ? xs[XS ? w : 0][XS ? zz - zs : 0] : T2[row + fx.layer];
+                }
             }
             did[rs] = true;
         }
-        // y face: the layer row over the chunk -> z*sx + x
+        // y face: the layer row over the chunk -> peer T2 y halo row (512-B runs)
         const FusedFace &fy = F.face[1][rs];
         if (fy.active && fy.layer >= ty0 && fy.layer < yhi) {
+            const int hy = rs == 0 ? 0 : sy - 1;
             const int w = xhi - xlo;
             for (int t = tid; t < w * nz; t += blockDim.x) {
                 const int zz = zs + t / w, xx = xlo + t % w;
-                fy.dst[(long long)zz * sx + xx] = T2[(long long)zz * sxy + (long long)fy.layer * sx + xx];
+                fy.dst[(long long)zz * sxy + (long long)hy * sx + xx] =
+                    T2[(long long)zz * sxy + (long long)fy.layer * sx + xx];
             }
             did[2 + rs] = true;
         }
-        // z face: the layer plane's rows of this tile -> y*sx + x
+        // z face: the layer plane's rows of this tile -> peer T2 z halo plane
         const FusedFace &fz = F.face[2][rs];
         if (fz.active && F.zchunk[rs] == td.z) {
+            const int hz = rs == 0 ? 0 : F.s[2] - 1;
             const int w = xhi - xlo;
             for (int t = tid; t < w * (yhi - ty0); t += blockDim.x) {
                 const int yy = ty0 + t / w, xx = xlo + t % w;
-                fz.dst[(long long)yy * sx + xx] = T2[(long long)fz.layer * sxy + (long long)yy * sx + xx];
+                fz.dst[(long long)hz * sxy + (long long)yy * sx + xx] =
+                    T2[(long long)fz.layer * sxy + (long long)yy * sx + xx];
             }
             did[4 + rs] = true;
         }
@@ -293,7 +300,9 @@ __global__ void fused_rim_kernel(const __grid_constant__ FusedParams F, unsigned
             c[b2] = v;
             if (forward_phase(F, a, c) >= 0) continue;
             const long long gi = ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0];
-            fc.dst[fidx(a, c[0], c[1], c[2], F.s)] = F.T2[gi];
+            const double val = F.T2[gi];
+            c[a] = rs == 0 ? 0 : F.s[a] - 1;   // the receiver's halo layer
+            fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = val;
         }
         __threadfence_system();
     }
@@ -329,88 +338,63 @@ __device__ __forceinline__ void wait_flag(const FusedParams &F, const unsigned l
     __syncthreads();
 }
 
-// The receiver side: kCommCTAs persistent CTAs walk the chunks in kernel order.
-// Per chunk: x faces (wait both flags, unpack a 1/kCommCTAs share into T2's x
-// halo, forward the cells the y/z faces need), then y faces likewise; after the
-// chunks holding the z layers, the z planes.  Each CTA counts itself once per
-// (face, chunk) it forwarded into.  The peers' comm kernels progress the same
-// way, so a y flag (which needs the peer's x forward of that chunk) never waits
-// on anything behind it.
+// The receiver side: kCommCTAs persistent CTAs walk the chunks in kernel order
+// and wait for every face flag (the halos themselves were stored by the peers'
+// stencil CTAs).  After axis b's flags of a chunk arrived they forward the fresh
+// halo cells later faces need (the edge lines where my halo layer of b meets a
+// later send layer) into those receivers' halos, and count on those faces.
+// The x and the y/z pipelines run as two concurrent launches.
 constexpr int kCommCTAs = 32;
-constexpr int kUnpackILP = 2;
 
-__device__ __forceinline__ void unpack_share(const FusedParams &F, int b, int side, int2 zr, bool &fwd) {
-    const FusedHalo &h = F.halo[b][side];
-    const int nz = zr.y - zr.x;
-    const int U = b == 0 ? F.s[1] : F.s[0];   // cells (u, z): u = y (x faces) or x (y faces)
-    const long long n = (long long)U * nz;
-    const long long step = (long long)gridDim.x * blockDim.x;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += step * kUnpackILP) {
-        double v[kUnpackILP];
-        long long si[kUnpackILP];
-#pragma unroll
-        for (int k = 0; k < kUnpackILP; ++k) {
-            const long long t = base + k * step + threadIdx.x;
-            long long q = 0;
-            if (t < n) {
-                if (b == 0) {   // x-face slot layout y*sz + z (z fastest)
-                    const int u = (int)(t / nz);
-                    q = (long long)u * F.s[2] + zr.x + (t - (long long)u * nz);
-                } else {        // y-face slot layout z*sx + x
-                    const int zz = (int)(t / U);
-                    q = (long long)(zr.x + zz) * F.s[0] + (t - (long long)zz * U);
-                }
+__device__ __forceinline__ void wait_flags(const FusedParams &F, int b, int idx) {
+    if (threadIdx.x < 2 && F.halo[b][threadIdx.x].active) {
+        const unsigned long long *fl = F.halo[b][threadIdx.x].flag + idx;
+        const long long t0 = clock64();
+        while (ld_acq_sys(fl) < F.epoch) {
+            if (clock64() - t0 > F.timeout_cycles) {
+                atomicExch(F.err, 1);
+                break;
             }
-            si[k] = q;
-            v[k] = t < n ? __ldcg(h.src + q) : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < kUnpackILP; ++k) {
-            const long long t = base + k * step + threadIdx.x;
-            if (t >= n) continue;
-            int c[3];
-            if (b == 0) {
-                c[1] = (int)(si[k] / F.s[2]);
-                c[2] = (int)(si[k] - (long long)c[1] * F.s[2]);
-                c[0] = h.layer;
-            } else {
-                c[2] = (int)(si[k] / F.s[0]);
-                c[0] = (int)(si[k] - (long long)c[2] * F.s[0]);
-                c[1] = h.layer;
-            }
-            F.T2[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v[k];
-            for (int a = b + 1; a < 3; ++a)
-                for (int rs = 0; rs < 2; ++rs) {
-                    const FusedFace &fc = F.face[a][rs];
-                    if (fc.active && c[a] == fc.layer && forward_phase(F, a, c) == b) {
-                        fc.dst[fidx(a, c[0], c[1], c[2], F.s)] = v[k];
-                        fwd = true;
-                    }
-                }
+            __nanosleep(128);
         }
     }
+    __syncthreads();
 }
 
-__global__ void __launch_bounds__(128, 12) fused_comm_kernel(const __grid_constant__ FusedParams F, int zafter) {
+// forward my fresh halo line (axis b, side) x (face a, rs) over the third axis range [lo, hi)
+__device__ __forceinline__ bool forward_line(const FusedParams &F, int b, int side, int a, int rs, int lo, int hi) {
+    const FusedFace &fc = F.face[a][rs];
+    if (!fc.active || !F.halo[b][side].active) return false;
+    const int third = 3 - a - b;
+    bool any = false;
+    for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
+        int c[3];
+        c[b] = side == 0 ? 0 : F.s[b] - 1;
+        c[a] = fc.layer;
+        c[third] = t;
+        if (forward_phase(F, a, c) != b) continue;
+        const double v = __ldcg(F.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
+        c[a] = rs == 0 ? 0 : F.s[a] - 1;
+        fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v;
+        any = true;
+    }
+    return any;
+}
+
+__global__ void __launch_bounds__(128) fused_comm_kernel(const __grid_constant__ FusedParams F, int zafter,
+                                                         int axes) {
     for (int ch = 0; ch < F.nchunks; ++ch) {
         const int2 zr = ext_range(F, ch);
         for (int b = 0; b < 2; ++b) {
-            if (!(F.halo[b][0].active || F.halo[b][1].active)) continue;
-            if (threadIdx.x < 2 && F.halo[b][threadIdx.x].active) {
-                const unsigned long long *fl = F.halo[b][threadIdx.x].flag + ch;
-                const long long t0 = clock64();
-                while (ld_acq_sys(fl) < F.epoch) {
-                    if (clock64() - t0 > F.timeout_cycles) {
-                        atomicExch(F.err, 1);
-                        break;
-                    }
-                    __nanosleep(128);
-                }
-            }
-            __syncthreads();
+            if (!(axes & (1 << b)) || !(F.halo[b][0].active || F.halo[b][1].active)) continue;
+            wait_flags(F, b, ch);
             bool fwd = false;
             for (int side = 0; side < 2; ++side)
-                if (F.halo[b][side].active && !F.dry) unpack_share(F, b, side, zr, fwd);
+                for (int rs = 0; rs < 2; ++rs) {
+                    if (b == 0) fwd |= forward_line(F, 0, side, 1, rs, zr.x, zr.y);   // x halo -> y faces
+                    if (F.face[2][rs].layer >= zr.x && F.face[2][rs].layer < zr.y)   // -> z faces
+                        fwd |= forward_line(F, b, side, 2, rs, 0, F.s[b == 0 ? 1 : 0]);
+                }
             if (__syncthreads_or(fwd)) __threadfence_system();
             __syncthreads();
             if (threadIdx.x == 0)
@@ -423,29 +407,7 @@ __global__ void __launch_bounds__(128, 12) fused_comm_kernel(const __grid_consta
                             contribute(F, 2, rs, 0);
                     }
         }
-        if (ch == zafter) {   // both z send layers' chunks are done everywhere: the z planes
-            if (threadIdx.x < 2 && F.halo[2][threadIdx.x].active) {
-                const unsigned long long *fl = F.halo[2][threadIdx.x].flag;
-                const long long t0 = clock64();
-                while (ld_acq_sys(fl) < F.epoch) {
-                    if (clock64() - t0 > F.timeout_cycles) {
-                        atomicExch(F.err, 1);
-                        break;
-                    }
-                    __nanosleep(128);
-                }
-            }
-            __syncthreads();
-            const long long n = (long long)F.s[0] * F.s[1];
-            for (int side = 0; side < 2; ++side) {
-                const FusedHalo &h = F.halo[2][side];
-                if (!h.active) continue;
-                double *dst = F.T2 + (long long)h.layer * n;
-                for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-                     t += (long long)gridDim.x * blockDim.x)
-                    dst[t] = __ldcg(h.src + t);
-            }
-        }
+        if ((axes & 4) && ch == zafter && (F.halo[2][0].active || F.halo[2][1].active)) wait_flags(F, 2, 0);
     }
 }
 
@@ -454,6 +416,11 @@ bool fused_eligible(const igg_grid *g) {
     if (g->fused == 2 && g->nlocal == 1) return true;   // ablation/profiling: force the fused kernel
     // fused = 3/5: timing experiments on the same path (see fused_step)
     if (g->path != IGG_PATH_P2P || g->nlocal != 1 || g->nproc_procs < 2 || g->fused == 0) return false;
+    if (g->fused < 0) {   // auto (default): measured faster when exactly one axis exchanges
+        int axes = 0;
+        for (int a = 0; a < 3; ++a) axes += (g->nbr[0][a][0] >= 0 || g->nbr[0][a][1] >= 0) ? 1 : 0;
+        if (axes != 1) return false;
+    }
     for (int a = 0; a < 3; ++a)
         for (int k = 0; k < 2; ++k) {
             const int nb = g->nbr[0][a][k];
@@ -478,7 +445,7 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
         IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false>, 32 * kFTY, 0));
         IGG_CUDA(cudaDeviceGetAttribute(&g_fused_nsm, cudaDevAttrMultiProcessorCount, g->device));
     }
-    const int kc1 = kFKC, kc2 = 8;
+    const int kc1 = kFKC, kc2 = 16;
     const long long ntile = (long long)xtiles * ytiles;
     int small = (int)((2LL * g_fused_occ * g_fused_nsm * kc2 + ntile - 1) / ntile);
     small = std::min(((small + kc2 - 1) / kc2) * kc2, wz);
@@ -534,33 +501,67 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
     g->fused_geo[5] = ytiles;
 }
 
+// ------------------------------------------------------------------ peer arrays
+// The caller's T2 lives inside some cudaMalloc allocation (e.g. a torch caching-
+// allocator segment).  Its base is exported with cudaIpcGetMemHandle, every
+// process all-gathers (handle, offset) and opens its neighbours' handles once;
+// the result is cached per local T2 pointer (Fig. 1 alternates two arrays, so
+// two collective exchanges happen, on the first two steps, on every rank).
+typedef int (*MemGetAddressRangeFn)(unsigned long long *, size_t *, unsigned long long);
+
+static const std::vector<double *> &peer_arrays(igg_grid *g, double *T2) {
+    for (const auto &m : g->fused_peer_maps)
+        if (m.first == (const void *)T2) return m.second;
+    static MemGetAddressRangeFn range_fn = nullptr;
+    if (!range_fn) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        IGG_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) fail(IGG_E_CUDA, "cuMemGetAddressRange unavailable");
+        range_fn = (MemGetAddressRangeFn)fn;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range_fn(&base, &size, (unsigned long long)(uintptr_t)T2) != 0)
+        fail(IGG_E_CUDA, "cuMemGetAddressRange failed on the T2 array");
+    struct Entry {
+        cudaIpcMemHandle_t h;
+        unsigned long long off;
+    } mine;
+    IGG_CUDA(cudaIpcGetMemHandle(&mine.h, (void *)(uintptr_t)base));
+    mine.off = (unsigned long long)(uintptr_t)T2 - base;
+    std::vector<char> all = allgather_bytes_pub(g, &mine, sizeof mine);
+    std::vector<double *> peers(g->nproc_procs, nullptr);
+    for (int p = 0; p < g->nproc_procs; ++p) {
+        if (p == g->proc) {
+            peers[p] = T2;
+            continue;
+        }
+        Entry e;
+        std::memcpy(&e, all.data() + p * sizeof e, sizeof e);
+        const std::string key(reinterpret_cast<const char *>(&e.h), sizeof e.h);
+        void *opened = nullptr;
+        for (const auto &o : g->fused_opened)
+            if (o.first == key) opened = o.second;
+        if (!opened) {
+            IGG_CUDA(cudaIpcOpenMemHandle(&opened, e.h, cudaIpcMemLazyEnablePeerAccess));
+            g->fused_opened.push_back({key, opened});
+        }
+        peers[p] = reinterpret_cast<double *>(static_cast<char *>(opened) + e.off);
+    }
+    g->fused_peer_maps.push_back({(const void *)T2, peers});
+    return g->fused_peer_maps.back().second;
+}
+
 void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s) {
-    // buffer pool and slot layout of one canonical field (the plan update_halo uses)
-    const long long sizes[3] = {g->n[0], g->n[1], g->n[2]};
-    const Plan plan = build_plan(*g, sizes, 1);
-    const size_t half = (size_t)plan.block * sizeof(double);
-    ensure_arena(g, half, 0);
     if (!g->fused_ctr) {
         IGG_CUDA(cudaMalloc(&g->fused_ctr, (6 * kMaxChunks + 8) * sizeof(unsigned int)));
         IGG_CUDA(cudaMemset(g->fused_ctr, 0, (6 * kMaxChunks + 8) * sizeof(unsigned int)));
         g->allocs++;
     }
-    long long off[3][2];   // slot of (axis, side) in a rank's block: plan order, h = 1
-    {
-        long long o = 0;
-        for (int a = 0; a < 3; ++a) {
-            long long other = 1;
-            for (int b = 0; b < 3; ++b)
-                if (b != a) other *= sizes[b];
-            for (int sd = 0; sd < 2; ++sd) {
-                off[a][sd] = o;
-                o += other;
-            }
-        }
-    }
-    g->epoch++;
-    const int parity = (int)(g->epoch & 1);
     const bool comm = !g->skip_comm;
+    const std::vector<double *> &peer = comm ? peer_arrays(g, T2) : std::vector<double *>();
+    g->epoch++;
     FusedParams F{};
     F.T = T;
     F.Ci = Ci;
@@ -575,8 +576,8 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
     bool act[3][2];
     for (int a = 0; a < 3; ++a)
         for (int rs = 0; rs < 2; ++rs) {
-            // rs = receiver side: 0 <- my send_upper (layer n-2) to my upper neighbour,
-            //                     1 <- my send_lower (layer 1) to my lower neighbour
+            // rs = receiver side: 0 <- my send_upper (layer n-2) into my upper neighbour's layer 0,
+            //                     1 <- my send_lower (layer 1) into my lower neighbour's layer s-1
             const int nb = g->nbr[0][a][rs == 0 ? 1 : 0];
             layer[a][rs] = rs == 0 ? g->n[a] - 2 : 1;
             act[a][rs] = comm && nb >= 0;
@@ -585,14 +586,13 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
             f.active = act[a][rs];
             if (f.active) {
                 const int pp = proc_of(g, nb);
-                f.dst = reinterpret_cast<double *>(g->peer_recv[pp] + parity * g->recv_half) + off[a][rs];
+                f.dst = peer[pp];
                 f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
             }
             const int hb = g->nbr[0][a][rs];   // my halo side rs is filled by my neighbour on side rs
             FusedHalo &h = F.halo[a][rs];
             h.active = comm && hb >= 0;
             h.layer = rs == 0 ? 0 : g->n[a] - 1;
-            h.src = reinterpret_cast<const double *>(g->recv_arena + parity * g->recv_half) + off[a][rs];
             h.flag = g->flags + (a * 2 + rs) * kMaxChunks;
         }
     int key = 0;
@@ -643,11 +643,22 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
         IGG_CUDA(cudaEventRecord(g->ev_inner, ss));
         IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
     }
-    if (comm && g->fused != 3) {   // fused == 3: timing experiment, no receive side (INVALID halos)
-        F.dry = g->fused == 5;        // fused == 5: timing experiment, wait only (INVALID halos)
-        fused_comm_kernel<<<kCommCTAs, 128, 0, g->s_comm>>>(F, g->fused_zafter);
-        IGG_CUDA(cudaGetLastError());
-        g->launches++;
+    if (comm) {
+        const bool xa = F.halo[0][0].active || F.halo[0][1].active;
+        const bool yza = F.halo[1][0].active || F.halo[1][1].active || F.halo[2][0].active || F.halo[2][1].active;
+        if (xa) {
+            fused_comm_kernel<<<kCommCTAs, 128, 0, g->s_comm>>>(F, g->fused_zafter, 1);
+            IGG_CUDA(cudaGetLastError());
+            g->launches++;
+        }
+        if (yza) {
+            IGG_CUDA(cudaStreamWaitEvent(g->s_comm2, g->ev_start, 0));
+            fused_comm_kernel<<<kCommCTAs, 128, 0, g->s_comm2>>>(F, g->fused_zafter, 6);
+            IGG_CUDA(cudaGetLastError());
+            g->launches++;
+            IGG_CUDA(cudaEventRecord(g->ev_comm2, g->s_comm2));
+            IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_comm2, 0));
+        }
     }
     tl_mark(g, g->s_comm, 4);
     IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));

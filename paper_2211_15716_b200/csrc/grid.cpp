@@ -41,6 +41,10 @@ static std::vector<char> allgather_bytes(igg_grid *g, const void *mine, size_t b
     return out;
 }
 
+std::vector<char> allgather_bytes_pub(igg_grid *g, const void *mine, size_t bytes) {
+    return allgather_bytes(g, mine, bytes);
+}
+
 static void process_barrier(igg_grid *g) {
     IGG_CUDA(cudaDeviceSynchronize());
     if (g->nproc_procs > 1) {
@@ -430,10 +434,12 @@ IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_
         IGG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         IGG_CUDA(cudaStreamCreateWithPriority(&g->s_comm, cudaStreamNonBlocking, greatest));
         IGG_CUDA(cudaStreamCreateWithPriority(&g->s_inner, cudaStreamNonBlocking, least));
+        IGG_CUDA(cudaStreamCreateWithPriority(&g->s_comm2, cudaStreamNonBlocking, greatest));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_start, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_comm, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_inner, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_bnd, cudaEventDisableTiming));
+        IGG_CUDA(cudaEventCreateWithFlags(&g->ev_comm2, cudaEventDisableTiming));
         if (g->nproc_procs > 1) {
             ncclUniqueId id;
             std::memcpy(&id, A->comm_id, sizeof id);
@@ -489,6 +495,8 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
     igg::check_live(g, "igg_finalize_global_grid");
     g->finalized = true;
     igg::process_barrier(g);
+    for (auto &o : g->fused_opened) cudaIpcCloseMemHandle(o.second);
+    g->fused_opened.clear();
     if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
         igg::unmap_peers(g, g->peer_recv);
         for (int p = 0; p < g->nproc_procs; ++p)
@@ -506,8 +514,10 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
     cudaEventDestroy(g->ev_comm);
     cudaEventDestroy(g->ev_inner);
     cudaEventDestroy(g->ev_bnd);
+    cudaEventDestroy(g->ev_comm2);
     cudaStreamDestroy(g->s_comm);
     cudaStreamDestroy(g->s_inner);
+    cudaStreamDestroy(g->s_comm2);
     delete g;
     IGG_CATCH
 }

@@ -120,13 +120,12 @@ struct HeatRegionList {
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
-    double *dst;                     // receiver's slot (peer-mapped), this step's parity half
+    double *dst;                     // the receiver's T2 (peer-mapped); the face lands in its halo layer
     unsigned long long *flag;        // receiver's flags of (axis, side): [kMaxChunks] (z faces: [0])
     int layer;                       // my send layer along the axis
     int active;
 };
 struct FusedHalo {                   // one halo side I receive
-    const double *src;               // my slot, this step's parity half
     const unsigned long long *flag;  // my flags [kMaxChunks]
     int layer;                       // halo layer (0 or s-1)
     int active;
@@ -141,7 +140,6 @@ struct FusedParams {
     int nchunks;                     // z-chunks; chunk ids 0..nbig-1 have kc1 planes, then kc2
     int nbig, kc1, kc2, cz;          // cz: chunk id holding plane s_z-2, visited second
     int xtiles, ytiles;
-    int dry;                         // timing experiment: waits without unpacking
     int zchunk[2];                   // chunk holding z send layer of face (2, rs); -1 if none
     unsigned int *ctr;               // [6][kMaxChunks] contribution counters (sender side)
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk)
@@ -207,8 +205,8 @@ struct igg_grid : igg::Geom {
     bool finalized = false;
 
     // streams and events (transfers on non-blocking high-priority streams)
-    cudaStream_t s_comm = nullptr, s_inner = nullptr;
-    cudaEvent_t ev_start = nullptr, ev_comm = nullptr, ev_inner = nullptr, ev_bnd = nullptr;
+    cudaStream_t s_comm = nullptr, s_inner = nullptr, s_comm2 = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_comm = nullptr, ev_inner = nullptr, ev_bnd = nullptr, ev_comm2 = nullptr;
 
     // communicator
     ncclComm_t comm = nullptr;
@@ -249,10 +247,12 @@ struct igg_grid : igg::Geom {
     int stencil_kernel = 0;
     int x_align = 64;
     int schedule = 0;
-    int fused = 1;                                       // IGG_OPT_FUSED
+    int fused = -1;                                      // IGG_OPT_FUSED (-1 auto)
     int fused_mode = 2;                                  // IGG_OPT_FUSED_MODE (ablation bits)
     unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
+    std::vector<std::pair<const void *, std::vector<double *>>> fused_peer_maps;   // local T2 -> peers' T2
+    std::vector<std::pair<std::string, void *>> fused_opened;                     // IPC handle -> mapping
     int fused_ntiles = 0, fused_nchunks = 0, fused_key = -1;
     int fused_zchunk[2] = {-1, -1};
     int fused_zafter = 1;
@@ -268,6 +268,7 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
                cudaStream_t s);
 void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap);
 int local_index(const igg_grid *g, int global_rank);   // -1 if not hosted here
+std::vector<char> allgather_bytes_pub(igg_grid *g, const void *mine, size_t bytes);
 bool fused_eligible(const igg_grid *g);
 void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s);
 void prof_begin(igg_grid *g, cudaStream_t s);
