@@ -228,7 +228,7 @@ enum {
     IGG_OPT_FUSED = 7,           /* P2P path, one rank per GPU: 1 = one stencil kernel that stores its
                                     send layers straight into the neighbours' halos over NVLink, chunk
                                     by chunk; 0 = boundary/inner kernels + pack/exchange/unpack;
-                                    -1 (default) = fused when exactly one axis exchanges */
+                                    -1 (default) = fused whenever eligible */
     IGG_OPT_FUSED_MODE = 8       /* ablation bits of the fused path: 1 = capture x send layer in smem,
                                     2 = stencil on the low-priority inner stream */
 };

@@ -126,14 +126,22 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
     __shared__ double xs[XS ? kFTY : 1][XS ? kFKC : 1];   // my rows' x send-layer cells over the chunk
-    // tile from the block index alone (x-tiles fastest, then y-tiles, then chunks in visit order)
+    // tile from the block index (x-tiles fastest, then y-tiles, then chunks in visit order);
+    // the last chunks' tiles are re-ordered, face tiles first, from the parameter table
     int4 td;
     {
         const int b = blockIdx.x;
-        td.x = b % F.xtiles;
-        const int r = b / F.xtiles;
-        td.y = r % F.ytiles;
-        td.z = r / F.ytiles;
+        if (b < F.bmain) {
+            td.x = b % F.xtiles;
+            const int r = b / F.xtiles;
+            td.y = r % F.ytiles;
+            td.z = r / F.ytiles;
+        } else {
+            const unsigned e = F.tail[b - F.bmain];
+            td.x = e & 15u;
+            td.y = (e >> 4) & 1023u;
+            td.z = F.bmain / (F.xtiles * F.ytiles) + (int)(e >> 14);
+        }
     }
     const int2 zr = chunk_range(F, td.z);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -195,11 +203,8 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         if (lane == 31 && w1) xp = __ldg(T + i + 2);
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (w0 && w1) {
-            if (face_tile)   // keep the face cells in L2 for the re-read below
-                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
-            else
-                __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+        if (w0 && w1) {   // plain stores (streaming stores measured no faster; face cells stay in L2)
+            *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
         } else {
             if (w0) T2[i] = r0;
             if (w1) T2[i + 1] = r1;
@@ -223,7 +228,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const int yhi = min(ty0 + kFTY, sy - 1);
     bool did[6] = {false, false, false, false, false, false};
 #pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
+    for (int rs = 0; rs < 2 && !F.nostore; ++rs) {
         // rs = 0: the upper neighbour's lower halo layer 0; rs = 1: the lower neighbour's layer s-1
         // x face: the layer column of my rows over the chunk -> peer T2 x halo
         const FusedFace &fx = F.face[0][rs];
@@ -262,6 +267,13 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                     T2[(long long)fz.layer * sxy + (long long)yy * sx + xx];
             }
             did[4 + rs] = true;
+        }
+    }
+    if (F.nostore) {   // timing experiment: count without storing (INVALID halos)
+        for (int rs = 0; rs < 2; ++rs) {
+            did[rs] = F.face[0][rs].active && F.face[0][rs].layer >= xlo && F.face[0][rs].layer < xhi;
+            did[2 + rs] = F.face[1][rs].active && F.face[1][rs].layer >= ty0 && F.face[1][rs].layer < yhi;
+            did[4 + rs] = F.face[2][rs].active && F.zchunk[rs] == td.z;
         }
     }
     __threadfence_system();
@@ -416,11 +428,7 @@ bool fused_eligible(const igg_grid *g) {
     if (g->fused == 2 && g->nlocal == 1) return true;   // ablation/profiling: force the fused kernel
     // fused = 3/5: timing experiments on the same path (see fused_step)
     if (g->path != IGG_PATH_P2P || g->nlocal != 1 || g->nproc_procs < 2 || g->fused == 0) return false;
-    if (g->fused < 0) {   // auto (default): measured faster when exactly one axis exchanges
-        int axes = 0;
-        for (int a = 0; a < 3; ++a) axes += (g->nbr[0][a][0] >= 0 || g->nbr[0][a][1] >= 0) ? 1 : 0;
-        if (axes != 1) return false;
-    }
+
     for (int a = 0; a < 3; ++a)
         for (int k = 0; k < 2; ++k) {
             const int nb = g->nbr[0][a][k];
@@ -492,6 +500,35 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
     }
     IGG_CUDA(cudaMemcpy(g->fused_tgt, tgt.data(), tgt.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
     g->fused_ntiles = (int)(ntile * nch);
+    // tail: the last chunks' tiles (about 2-3 waves), face tiles first, so the last faces
+    // leave a couple of waves before the stencil ends and the forwarding chain is hidden
+    g->fused_tail.clear();
+    g->fused_bmain = g->fused_ntiles;
+    int ntail_ch = 0;
+    while (ntail_ch < std::min(4, nch - 1) && (long long)(ntail_ch + 1) * ntile <= kMaxTail) ++ntail_ch;
+    if (xtiles <= 16 && ytiles <= 1024 && ntail_ch > 0) {
+        const int c0 = nch - ntail_ch;
+        std::vector<unsigned short> face_t, rest_t;
+        for (int oc = c0; oc < nch; ++oc) {
+            const int2 r = zc[id_of(oc)];
+            for (int yt = 0; yt < ytiles; ++yt)
+                for (int xt = 0; xt < xtiles; ++xt) {
+                    bool face = false;
+                    const int xlo = std::max(xt * 64, 1), xhi = std::min(xt * 64 + 64, n0 - 1);
+                    const int ty0 = 1 + yt * kFTY, yhi = std::min(ty0 + kFTY, n1 - 1);
+                    for (int rs = 0; rs < 2; ++rs) {
+                        face |= act[0][rs] && layer[0][rs] >= xlo && layer[0][rs] < xhi;
+                        face |= act[1][rs] && layer[1][rs] >= ty0 && layer[1][rs] < yhi;
+                        face |= act[2][rs] && layer[2][rs] >= r.x && layer[2][rs] < r.y;
+                    }
+                    const unsigned short e = (unsigned short)(xt | (yt << 4) | ((oc - c0) << 14));
+                    (face ? face_t : rest_t).push_back(e);
+                }
+        }
+        g->fused_tail = face_t;
+        g->fused_tail.insert(g->fused_tail.end(), rest_t.begin(), rest_t.end());
+        g->fused_bmain = (int)(ntile * c0);
+    }
     g->fused_nchunks = nch;
     g->fused_geo[0] = nbig;
     g->fused_geo[1] = kc1;
@@ -560,7 +597,8 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
         g->allocs++;
     }
     const bool comm = !g->skip_comm;
-    const std::vector<double *> &peer = comm ? peer_arrays(g, T2) : std::vector<double *>();
+    static const std::vector<double *> none;
+    const std::vector<double *> &peer = (comm && g->nproc_procs > 1) ? peer_arrays(g, T2) : none;
     g->epoch++;
     FusedParams F{};
     F.T = T;
@@ -572,6 +610,7 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
     F.err = g->d_err;
     F.k = k;
     F.ctr = g->fused_ctr;
+    F.nostore = (g->fused_mode & 8) ? 1 : 0;
     int layer[3][2];
     bool act[3][2];
     for (int a = 0; a < 3; ++a)
@@ -609,6 +648,8 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
     F.cz = g->fused_geo[3];
     F.xtiles = g->fused_geo[4];
     F.ytiles = g->fused_geo[5];
+    F.bmain = g->fused_bmain;
+    std::copy(g->fused_tail.begin(), g->fused_tail.end(), F.tail);
     F.zchunk[0] = g->fused_zchunk[0];
     F.zchunk[1] = g->fused_zchunk[1];
     F.tgt = g->fused_tgt;
@@ -643,7 +684,7 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
         IGG_CUDA(cudaEventRecord(g->ev_inner, ss));
         IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
     }
-    if (comm) {
+    if (comm && !(g->fused_mode & 4)) {   // mode bit 4: timing experiment without receive side (INVALID)
         const bool xa = F.halo[0][0].active || F.halo[0][1].active;
         const bool yza = F.halo[1][0].active || F.halo[1][1].active || F.halo[2][0].active || F.halo[2][1].active;
         if (xa) {

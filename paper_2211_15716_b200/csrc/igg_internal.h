@@ -119,6 +119,7 @@ struct HeatRegionList {
 
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
+constexpr int kMaxTail = 6144;       // tiles of the last chunks, re-ordered face tiles first
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // the receiver's T2 (peer-mapped); the face lands in its halo layer
     unsigned long long *flag;        // receiver's flags of (axis, side): [kMaxChunks] (z faces: [0])
@@ -140,6 +141,9 @@ struct FusedParams {
     int nchunks;                     // z-chunks; chunk ids 0..nbig-1 have kc1 planes, then kc2
     int nbig, kc1, kc2, cz;          // cz: chunk id holding plane s_z-2, visited second
     int xtiles, ytiles;
+    int nostore;                     // timing experiment: face tiles count without storing
+    int bmain;                       // blocks in plain order; the rest decode tail[]
+    unsigned short tail[kMaxTail];   // (x-tile, y-tile, chunk - first tail chunk) of the tail blocks
     int zchunk[2];                   // chunk holding z send layer of face (2, rs); -1 if none
     unsigned int *ctr;               // [6][kMaxChunks] contribution counters (sender side)
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk)
@@ -252,6 +256,8 @@ struct igg_grid : igg::Geom {
     unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
     std::vector<std::pair<const void *, std::vector<double *>>> fused_peer_maps;   // local T2 -> peers' T2
+    std::vector<unsigned short> fused_tail;                                       // tail tile order
+    int fused_bmain = 0;
     std::vector<std::pair<std::string, void *>> fused_opened;                     // IPC handle -> mapping
     int fused_ntiles = 0, fused_nchunks = 0, fused_key = -1;
     int fused_zchunk[2] = {-1, -1};
