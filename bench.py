@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-exposed", action="store_true")
     ap.add_argument("--fused", type=int, default=-1, help="1 fused stencil+P2P put kernel, 0 split, -1 auto")
     ap.add_argument("--fused-mode", type=int, default=2, help="ablation bits of the fused path")
+    ap.add_argument("--kc2", type=int, default=0, help="fused path: tail z-chunk planes (0 auto)")
+    ap.add_argument("--ncomm", type=int, default=1, help="fused path: CTAs per receive/forward kernel")
     ap.add_argument("--schedule", type=int, default=0, help="0 concurrent, 1 boundary first (paper order)")
     ap.add_argument("--timeline", action="store_true", help="record the overlap timeline (extra events)")
     ap.add_argument("--xalign", type=int, default=64, help="x boundary-slab alignment in cells (1 = exact bw)")
@@ -210,6 +212,8 @@ def main():
     g.set_option(P.OPT_SCHEDULE, a.schedule)
     g.set_option(P.OPT_FUSED, a.fused)
     g.set_option(8, a.fused_mode)
+    g.set_option(9, a.kc2)
+    g.set_option(10, a.ncomm)
     if a.skip_comm:
         g.set_option(P.OPT_SKIP_COMM, 1)
     T, T2, Ci = app.alloc_fields(g)

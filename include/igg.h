@@ -229,8 +229,11 @@ enum {
                                     send layers straight into the neighbours' halos over NVLink, chunk
                                     by chunk; 0 = boundary/inner kernels + pack/exchange/unpack;
                                     -1 (default) = fused whenever eligible */
-    IGG_OPT_FUSED_MODE = 8       /* ablation bits of the fused path: 1 = capture x send layer in smem,
-                                    2 = stencil on the low-priority inner stream */
+    IGG_OPT_FUSED_MODE = 8,      /* ablation bits of the fused path: 1 = capture x send layer in smem,
+                                    2 = stencil on the low-priority inner stream (default) */
+    IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8 with one
+                                    exchanging axis, 16 with more) */
+    IGG_OPT_FUSED_COMM_CTAS = 10 /* CTAs of each fused receive/forward kernel (default 1) */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

@@ -110,6 +110,7 @@ __device__ __forceinline__ int2 ext_range(const FusedParams &F, int c) {
 }
 
 constexpr int kFTY = 4;    // rows per CTA (one warp each)
+constexpr unsigned g_poll_ns = 1000;   // flag polling period of the waiting CTAs
 constexpr int kFD = 3;     // planes in flight per thread
 constexpr int kFKC = 64;   // longest z-chunk
 
@@ -344,19 +345,18 @@ __device__ __forceinline__ void wait_flag(const FusedParams &F, const unsigned l
                 atomicExch(F.err, 1);
                 break;
             }
-            __nanosleep(128);
+            __nanosleep(g_poll_ns);
         }
     }
     __syncthreads();
 }
 
-// The receiver side: kCommCTAs persistent CTAs walk the chunks in kernel order
+// The receiver side: a few persistent CTAs (IGG_OPT_FUSED_COMM_CTAS) walk the chunks in kernel order
 // and wait for every face flag (the halos themselves were stored by the peers'
 // stencil CTAs).  After axis b's flags of a chunk arrived they forward the fresh
 // halo cells later faces need (the edge lines where my halo layer of b meets a
 // later send layer) into those receivers' halos, and count on those faces.
 // The x and the y/z pipelines run as two concurrent launches.
-constexpr int kCommCTAs = 32;
 
 __device__ __forceinline__ void wait_flags(const FusedParams &F, int b, int idx) {
     if (threadIdx.x < 2 && F.halo[b][threadIdx.x].active) {
@@ -367,7 +367,7 @@ __device__ __forceinline__ void wait_flags(const FusedParams &F, int b, int idx)
                 atomicExch(F.err, 1);
                 break;
             }
-            __nanosleep(128);
+            __nanosleep(g_poll_ns);
         }
     }
     __syncthreads();
@@ -453,7 +453,11 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
         IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false>, 32 * kFTY, 0));
         IGG_CUDA(cudaDeviceGetAttribute(&g_fused_nsm, cudaDevAttrMultiProcessorCount, g->device));
     }
-    const int kc1 = kFKC, kc2 = 16;
+    // tail chunk planes: short chunks shorten the last wave, but every chunk adds one hop to the
+    // per-chunk forwarding chain when several axes exchange (measured: 8 for one axis, 16 for more)
+    int naxes = 0;
+    for (int a = 0; a < 3; ++a) naxes += (act[a][0] || act[a][1]) ? 1 : 0;
+    const int kc1 = kFKC, kc2 = g->fused_kc2 > 0 ? g->fused_kc2 : (naxes <= 1 ? 8 : 16);
     const long long ntile = (long long)xtiles * ytiles;
     int small = (int)((2LL * g_fused_occ * g_fused_nsm * kc2 + ntile - 1) / ntile);
     small = std::min(((small + kc2 - 1) / kc2) * kc2, wz);
@@ -485,7 +489,7 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
         xsides += g->nbr[0][0][sd] >= 0 ? 1 : 0;
         ysides += g->nbr[0][1][sd] >= 0 ? 1 : 0;
     }
-    const unsigned xfw = xsides ? kCommCTAs : 0, yfw = ysides ? kCommCTAs : 0;
+    const unsigned xfw = xsides ? g->fused_ncomm : 0, yfw = ysides ? g->fused_ncomm : 0;   // forwarding CTAs
     std::vector<unsigned> tgt(6 * kMaxChunks, 0u);
     for (int rs = 0; rs < 2; ++rs) {
         for (int c = 0; c < nch; ++c) {
@@ -688,13 +692,13 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
         const bool xa = F.halo[0][0].active || F.halo[0][1].active;
         const bool yza = F.halo[1][0].active || F.halo[1][1].active || F.halo[2][0].active || F.halo[2][1].active;
         if (xa) {
-            fused_comm_kernel<<<kCommCTAs, 128, 0, g->s_comm>>>(F, g->fused_zafter, 1);
+            fused_comm_kernel<<<g->fused_ncomm, 128, 0, g->s_comm>>>(F, g->fused_zafter, 1);
             IGG_CUDA(cudaGetLastError());
             g->launches++;
         }
         if (yza) {
             IGG_CUDA(cudaStreamWaitEvent(g->s_comm2, g->ev_start, 0));
-            fused_comm_kernel<<<kCommCTAs, 128, 0, g->s_comm2>>>(F, g->fused_zafter, 6);
+            fused_comm_kernel<<<g->fused_ncomm, 128, 0, g->s_comm2>>>(F, g->fused_zafter, 6);
             IGG_CUDA(cudaGetLastError());
             g->launches++;
             IGG_CUDA(cudaEventRecord(g->ev_comm2, g->s_comm2));

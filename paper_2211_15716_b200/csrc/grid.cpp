@@ -673,6 +673,16 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
         case IGG_OPT_FUSED: g->fused = (int)value; break;
         case IGG_OPT_FUSED_MODE: g->fused_mode = (int)value; break;
+        case IGG_OPT_FUSED_COMM_CTAS:
+            if (value < 1 || value > 128) fail(IGG_E_ARG, "igg_set_option: FUSED_COMM_CTAS must be in [1, 128]");
+            g->fused_ncomm = (int)value;
+            g->fused_key = -1;
+            break;
+        case IGG_OPT_FUSED_KC2:
+            if (value < 0 || value > 64) fail(IGG_E_ARG, "igg_set_option: FUSED_KC2 must be in [0, 64]");
+            g->fused_kc2 = (int)value;
+            g->fused_key = -1;
+            break;
         default: fail(IGG_E_ARG, "igg_set_option: unknown key " + std::to_string(key));
     }
     IGG_CATCH

@@ -253,6 +253,8 @@ struct igg_grid : igg::Geom {
     int schedule = 0;
     int fused = -1;                                      // IGG_OPT_FUSED (-1 auto)
     int fused_mode = 2;                                  // IGG_OPT_FUSED_MODE (ablation bits)
+    int fused_kc2 = 0;                                   // IGG_OPT_FUSED_KC2: tail chunk planes (0 auto)
+    int fused_ncomm = 1;                                 // IGG_OPT_FUSED_COMM_CTAS
     unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
     std::vector<std::pair<const void *, std::vector<double *>>> fused_peer_maps;   // local T2 -> peers' T2

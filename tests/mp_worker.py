@@ -106,6 +106,11 @@ def main():
                 heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), opts=o)
             heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=12)
             heat_case(path, (66, 40, 36), dims, (0, 1, 0), 1, (16, 2, 2), nt=9)
+            # the fused put path on every split axis (z faces, corner forwarding x->y->z)
+            extra = {2: [(1, 2, 1), (1, 1, 2)], 4: [(2, 1, 2), (1, 2, 2), (4, 1, 1), (1, 1, 4)]}.get(world, [])
+            for d2 in extra:
+                heat_case(path, (130, 36, 34), d2, (0, 0, 0), 1, (16, 2, 2), nt=7)
+                heat_case(path, (130, 36, 34), d2, (1, 1, 1), 1, (16, 2, 2), nt=7)
         halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
         # 8 ranks as virtual ranks over the processes (2x2x2 correctness on fewer GPUs)
