@@ -125,6 +125,7 @@ def cpu_oracle_baseline(n: int, target_s: float = 12.0):
     import numpy as np
     from oracle import heat3d as OH
     OH.build()
+    OH.set_threads(len(os.sched_getaffinity(0)))   # all host cores (torchrun sets OMP_NUM_THREADS=1)
     T = np.full((n, n, n), 1.7)
     T2 = T.copy()
     Ci = np.full((n, n, n), 0.5)
@@ -154,6 +155,7 @@ def run_reference(a):
     import numpy as np
     from oracle import heat3d as OH
     OH.build()
+    OH.set_threads(len(os.sched_getaffinity(0)))   # all host cores (torchrun sets OMP_NUM_THREADS=1)
     n = a.n
     nz = min(n, 66)
     T = np.full((nz, n, n), 1.7)

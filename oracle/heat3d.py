@@ -57,6 +57,8 @@ def lib():
         L.oracle_heat_run.restype = ctypes.c_int
         L.oracle_max.argtypes = [dp, ctypes.c_long]
         L.oracle_max.restype = ctypes.c_double
+        L.oracle_set_threads.argtypes = [ctypes.c_int]
+        L.oracle_set_threads.restype = None
         L.oracle_num_threads.argtypes = []
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -70,6 +72,10 @@ def _ptr(a: np.ndarray):
 
 def num_threads() -> int:
     return lib().oracle_num_threads()
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
 
 
 def spacing(l: float, N: int, periodic: bool) -> float:

@@ -131,6 +131,17 @@ double oracle_max(const double *A, long n)
     return m;
 }
 
+/* set the OpenMP thread count (no-op without OpenMP) */
+void oracle_set_threads(int n)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* thread count the OpenMP runtime will use (1 without OpenMP) */
 int oracle_num_threads(void)
 {
