@@ -233,7 +233,11 @@ enum {
                                     2 = stencil on the low-priority inner stream (default) */
     IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8 with one
                                     exchanging axis, 16 with more) */
-    IGG_OPT_FUSED_COMM_CTAS = 10 /* CTAs of each fused receive/forward kernel (default 1) */
+    IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */
+    IGG_OPT_COOP_HALO = 11,      /* 1: update_halo without NCCL messages runs as one cooperative kernel
+                                    (grid barriers between axes); 0 (default, measured faster): per-axis launches */
+    IGG_OPT_HALO_STREAM = 12     /* 0 (default): update_halo runs on the library's high-priority comm
+                                    stream joined to the caller's; 1: directly on the caller's stream */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

@@ -104,7 +104,15 @@ void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap) {
 // Executes the plan of plan.cpp: per axis one pack launch (faces into the
 // receiver's arena slot: local, peer-mapped over NVLink, or the NCCL send
 // arena), the grouped NCCL send/recv of that axis, one unpack launch.
-void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
+// plans depend only on the field sizes: built once per field-list shape
+const Plan &cached_plan(igg_grid *g, const std::vector<long long> &sizes) {
+    for (const auto &e : g->plan_cache)
+        if (e.first == sizes) return e.second;
+    g->plan_cache.push_back({sizes, build_plan(*g, sizes.data(), (int)(sizes.size() / 3))});
+    return g->plan_cache.back().second;
+}
+
+void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, bool allow_coop) {
     if (nf < 1 || !fields) fail(IGG_E_ARG, "update_halo: need at least one field");
     const int L = g->nlocal;
     std::vector<long long> sizes(nf * 3);
@@ -117,7 +125,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
             for (int a = 0; a < 3; ++a)
                 if (F.size[a] != sizes[f * 3 + a]) fail(IGG_E_ARG, "update_halo: local ranks disagree on a field size");
         }
-    const Plan plan = build_plan(*g, sizes.data(), nf);
+    const Plan &plan = cached_plan(g, sizes);
     const size_t half = (size_t)L * plan.block * sizeof(double);
     ensure_arena(g, half, plan.any_nccl ? half : 0);
 
@@ -127,15 +135,16 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
     double *recv = reinterpret_cast<double *>(g->recv_arena + parity * g->recv_half);
     double *sendb = reinterpret_cast<double *>(g->send_arena);
 
+    // per axis: pack / unpack descriptors, peer signals and waits, NCCL messages
+    std::vector<CopyDesc> pd[3], ud[3];
+    CopyList P[3]{}, U[3]{};
+    std::vector<const PlanMsg *> sends[3], recvs[3];
+    bool any_nccl = false;
     for (int a = 0; a < 3; ++a) {   // x -> y -> z, each axis complete before the next
-        if (plan.msgs[a].empty()) continue;
-        CopyList P{}, U{};
-        std::vector<CopyDesc> pd, ud;
-        P.ticket = g->tickets + a;
-        P.epoch = U.epoch = g->epoch;
-        U.err = P.err = g->d_err;
-        U.timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
-        std::vector<const PlanMsg *> sends, recvs;
+        P[a].ticket = g->tickets + a;
+        P[a].epoch = U[a].epoch = g->epoch;
+        U[a].err = P[a].err = g->d_err;
+        U[a].timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
         for (const PlanMsg &m : plan.msgs[a]) {
             CopyDesc d{};
             const igg_field &F = fields[m.lr * nf + m.field];
@@ -153,49 +162,83 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st) {
                     d.buf = recv + m.slot;
                 } else if (m.transport == kP2P) {
                     d.buf = reinterpret_cast<double *>(g->peer_recv[m.peer_proc] + parity * g->recv_half) + m.slot;
-                    unsigned long long *fl = g->peer_flags[m.peer_proc] + ((m.peer_lr * 3 + a) * 2 + m.recv_side) * kMaxChunks;
+                    unsigned long long *fl =
+                        g->peer_flags[m.peer_proc] + ((m.peer_lr * 3 + a) * 2 + m.recv_side) * kMaxChunks;
                     bool have = false;
-                    for (int s = 0; s < P.nsignal; ++s) have |= P.signal[s] == fl;
+                    for (int q = 0; q < P[a].nsignal; ++q) have |= P[a].signal[q] == fl;
                     if (!have) {
-                        if (P.nsignal >= kMaxSignal) fail(IGG_E_UNSUPPORTED, "update_halo: too many peers");
-                        P.signal[P.nsignal++] = fl;
+                        if (P[a].nsignal >= kMaxSignal) fail(IGG_E_UNSUPPORTED, "update_halo: too many peers");
+                        P[a].signal[P[a].nsignal++] = fl;
                     }
                 } else {
                     d.buf = sendb + m.sbuf;
-                    sends.push_back(&m);
+                    sends[a].push_back(&m);
+                    any_nccl = true;
                 }
+                pd[a].push_back(d);
             } else {
                 d.buf = recv + m.slot;
                 if (m.transport == kP2P) {
                     const unsigned long long *fl = g->flags + ((m.lr * 3 + a) * 2 + m.recv_side) * kMaxChunks;
                     int w = -1;
-                    for (int s = 0; s < U.nsignal; ++s)
-                        if (U.wait[s] == fl) w = s;
+                    for (int q = 0; q < U[a].nsignal; ++q)
+                        if (U[a].wait[q] == fl) w = q;
                     if (w < 0) {
-                        if (U.nsignal >= kMaxSignal) fail(IGG_E_UNSUPPORTED, "update_halo: too many peers");
-                        w = U.nsignal;
-                        U.wait[U.nsignal++] = fl;
+                        if (U[a].nsignal >= kMaxSignal) fail(IGG_E_UNSUPPORTED, "update_halo: too many peers");
+                        w = U[a].nsignal;
+                        U[a].wait[U[a].nsignal++] = fl;
                     }
                     d.flag_slot = w;
                 } else if (m.transport == kNccl) {
-                    recvs.push_back(&m);
+                    recvs[a].push_back(&m);
+                    any_nccl = true;
                 }
+                ud[a].push_back(d);
             }
-            (m.op == 0 ? pd : ud).push_back(d);
         }
-        g->launches += launch_copies(0, pd, P, st);
-        if (!sends.empty() || !recvs.empty()) {
+    }
+    size_t ndesc = 0;
+    for (int a = 0; a < 3; ++a) ndesc += pd[a].size() + ud[a].size();
+    if (allow_coop && !any_nccl && ndesc <= (size_t)kCoopMax && g->coop) {
+        // one cooperative launch for the whole call
+        CoopPlan C{};
+        int j = 0;
+        for (int a = 0; a < 3; ++a) {
+            C.pk0[a] = j;
+            for (const CopyDesc &d : pd[a]) C.d[j++] = d;
+            C.pk1[a] = C.up0[a] = j;
+            for (CopyDesc d : ud[a]) {
+                d.flag_slot = -1;
+                C.d[j++] = d;
+            }
+            C.up1[a] = j;
+            C.nsignal[a] = P[a].nsignal;
+            for (int q = 0; q < P[a].nsignal; ++q) C.signal[a][q] = P[a].signal[q];
+            C.nwait[a] = U[a].nsignal;
+            for (int q = 0; q < U[a].nsignal; ++q) C.wait[a][q] = U[a].wait[q];
+        }
+        C.epoch = g->epoch;
+        C.timeout_cycles = U[0].timeout_cycles;
+        C.err = g->d_err;
+        launch_halo_coop(C, st);
+        g->launches++;
+        return;
+    }
+    for (int a = 0; a < 3; ++a) {
+        if (plan.msgs[a].empty()) continue;
+        g->launches += launch_copies(0, pd[a], P[a], st);
+        if (!sends[a].empty() || !recvs[a].empty()) {
             auto by_order = [](const PlanMsg *x, const PlanMsg *y) { return x->order < y->order; };
-            std::sort(sends.begin(), sends.end(), by_order);
-            std::sort(recvs.begin(), recvs.end(), by_order);
+            std::sort(sends[a].begin(), sends[a].end(), by_order);
+            std::sort(recvs[a].begin(), recvs[a].end(), by_order);
             IGG_NCCL(ncclGroupStart());
-            for (const PlanMsg *m : sends)
+            for (const PlanMsg *m : sends[a])
                 IGG_NCCL(ncclSend(sendb + m->sbuf, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
-            for (const PlanMsg *m : recvs)
+            for (const PlanMsg *m : recvs[a])
                 IGG_NCCL(ncclRecv(recv + m->slot, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
             IGG_NCCL(ncclGroupEnd());
         }
-        g->launches += launch_copies(1, ud, U, st);
+        g->launches += launch_copies(1, ud[a], U[a], st);
     }
 }
 
@@ -577,11 +620,15 @@ IGG_API igg_status igg_update_halo(igg_grid *g, const igg_field *fields, int nfi
     IGG_TRY
     igg::check_live(g, "igg_update_halo");
     cudaStream_t s = (cudaStream_t)stream;
-    IGG_CUDA(cudaEventRecord(g->ev_start, s));
-    IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
-    igg::exchange(g, fields, nfields, g->s_comm);
-    IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
-    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    if (g->halo_on_caller) {   // IGG_OPT_HALO_STREAM = 1: on the caller's stream (no cross-stream hops)
+        igg::exchange(g, fields, nfields, s, true);
+    } else {                   // default: the library's high-priority comm stream
+        IGG_CUDA(cudaEventRecord(g->ev_start, s));
+        IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
+        igg::exchange(g, fields, nfields, g->s_comm, true);   // standalone: nothing runs beside it
+        IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+        IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    }
     IGG_CATCH
 }
 
@@ -673,6 +720,8 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
         case IGG_OPT_FUSED: g->fused = (int)value; break;
         case IGG_OPT_FUSED_MODE: g->fused_mode = (int)value; break;
+        case IGG_OPT_COOP_HALO: g->coop = value != 0; break;
+        case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
         case IGG_OPT_FUSED_COMM_CTAS:
             if (value < 1 || value > 128) fail(IGG_E_ARG, "igg_set_option: FUSED_COMM_CTAS must be in [1, 128]");
             g->fused_ncomm = (int)value;

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <array>
+#include <list>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -74,8 +75,9 @@ struct CopyDesc {
 
 constexpr int kMaxCopy = 48;
 constexpr int kMaxSignal = 16;
-struct CopyList {
-    CopyDesc d[kMaxCopy];
+template <int N>
+struct CopyListT {
+    CopyDesc d[N];
     int n;
     int blocks_per_desc;
     // pack: after every block stored its part (to peers), the last block
@@ -90,6 +92,8 @@ struct CopyList {
     long long timeout_cycles;
     int *err;                        // set to 1 on timeout
 };
+using CopyList = CopyListT<kMaxCopy>;
+constexpr int kSmallCopy = 8;        // small calls launch with a ~1 KB parameter block
 
 // one stencil region [x0,x0+wx) x [y0,y0+wy) x [z0,z0+wz) of one rank's field
 struct HeatRegion {
@@ -154,6 +158,22 @@ struct FusedParams {
 };
 
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
+// the whole update_halo of a call in ONE cooperative launch (P2P / local transports):
+// per axis pack -> grid sync -> publish flags -> wait peers' flags -> unpack -> grid sync
+constexpr int kCoopMax = 96;
+struct CoopPlan {
+    CopyDesc d[kCoopMax];
+    int pk0[3], pk1[3], up0[3], up1[3];     // descriptor ranges of each axis
+    unsigned long long *signal[3][kMaxSignal];
+    int nsignal[3];
+    const unsigned long long *wait[3][kMaxSignal];
+    int nwait[3];
+    unsigned long long epoch;
+    long long timeout_cycles;
+    int *err;
+};
+void launch_halo_coop(const CoopPlan &C, cudaStream_t s);
+
 // pack (op 0) or unpack (op 1) of any number of faces: chunks of kMaxCopy
 // descriptors per launch; `proto` carries signals/waits/epoch; returns launches
 int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s);
@@ -255,6 +275,9 @@ struct igg_grid : igg::Geom {
     int fused_mode = 2;                                  // IGG_OPT_FUSED_MODE (ablation bits)
     int fused_kc2 = 0;                                   // IGG_OPT_FUSED_KC2: tail chunk planes (0 auto)
     int fused_ncomm = 1;                                 // IGG_OPT_FUSED_COMM_CTAS
+    bool coop = false;                                   // IGG_OPT_COOP_HALO
+    bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
+    std::list<std::pair<std::vector<long long>, igg::Plan>> plan_cache;   // field-list shape -> plan
     unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
     std::vector<std::pair<const void *, std::vector<double *>>> fused_peer_maps;   // local T2 -> peers' T2
@@ -269,7 +292,7 @@ struct igg_grid : igg::Geom {
 };
 
 namespace igg {
-void exchange(igg_grid *g, const igg_field *fields, int nfields, cudaStream_t st);
+void exchange(igg_grid *g, const igg_field *fields, int nfields, cudaStream_t st, bool allow_coop = false);
 void check_live(const igg_grid *g, const char *what);
 void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
                double lam, double dt, double dx, double dy, double dz, const int bw[3],
@@ -283,4 +306,5 @@ void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
 void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step
 int proc_of(const igg_grid *g, int global_rank);
+const Plan &cached_plan(igg_grid *g, const std::vector<long long> &sizes);
 }  // namespace igg

@@ -5,6 +5,8 @@
 //
 // Fp64 throughout ("@init_parallel_stencil(CUDA, Float64, 3)").
 // No tensor cores: the 7-point stencil is not a contraction.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdio>
 
@@ -415,6 +417,119 @@ static void launch_box_async(const HeatRegion &r, const HeatCoef &k, cudaStream_
     IGG_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------- row-staged pipeline (ablation)
+// Like heat_box_async_kernel, but the CTA stages whole planes of its tile --
+// T rows y0-1 .. y0+TY and Ci rows y0 .. y0+TY-1 -- with cp.async into a ring
+// of D+1 slots, so y neighbours and T[z+1] also come from shared memory (no
+// L2 round trip inside the loop).  One CTA barrier per plane.
+template <int TY, int D>
+__global__ void __launch_bounds__(32 * TY)
+    heat_box_rows_kernel(const double *__restrict__ T, const double *__restrict__ Ci, double *__restrict__ T2,
+                         int sx, int sy, int x0, int y0, int z0, int wx, int wy, int wz, int ax0, int xtiles,
+                         int ytiles, int kc1, int nbig, int kc2, const HeatCoef k) {
+    constexpr int S = D + 1;
+    constexpr int NT = 32 * TY;
+    __shared__ double2 sT[S][TY + 2][32];
+    __shared__ double2 sC[S][TY][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ntiles = xtiles * ytiles;
+    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    int zs, ze;
+    if (chunk < nbig) {
+        zs = z0 + chunk * kc1;
+        ze = min(zs + kc1, z0 + wz);
+    } else {
+        zs = z0 + nbig * kc1 + (chunk - nbig) * kc2;
+        ze = min(zs + kc2, z0 + wz);
+    }
+    const int tx = tile % xtiles, ty = tile / xtiles;
+    const int ybase = y0 + ty * TY;
+    const int y = ybase + warp;
+    const int p0 = ax0 + tx * 64;
+    const int p = p0 + 2 * lane;
+    const bool row_ok = y < y0 + wy;
+    const bool pair_in = row_ok && p < sx;
+    const int xend = x0 + wx;
+    const bool w0 = pair_in && p >= x0 && p < xend;
+    const bool w1 = pair_in && p + 1 >= x0 && p + 1 < xend;
+    const long long sxy = (long long)sx * sy;
+    auto issue = [&](int plane, int slot) {
+        const long long pb = (long long)plane * sxy;
+        for (int e = tid; e < (TY + 2) * 32; e += NT) {
+            const int r = e >> 5, l = e & 31;
+            const int yy = ybase - 1 + r, pp = p0 + 2 * l;
+            if (yy < sy && pp < sx) cp_async16(&sT[slot][r][l], T + pb + (long long)yy * sx + pp);
+        }
+        for (int e = tid; e < TY * 32; e += NT) {
+            const int r = e >> 5, l = e & 31;
+            const int yy = ybase + r, pp = p0 + 2 * l;
+            if (yy < sy && pp < sx) cp_async16(&sC[slot][r][l], Ci + pb + (long long)yy * sx + pp);
+        }
+    };
+    // prologue: stages zs .. zs+D-1 (stage q holds plane q)
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+        if (zs + q <= ze) issue(zs + q, q);
+        cp_async_commit();
+    }
+    const double2 zero2 = make_double2(0.0, 0.0);
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+    double2 zm = pair_in ? ldg2(T + i - sxy) : zero2;
+    cp_async_wait<D - 1>();   // stage zs landed (its own copies; the barrier publishes them)
+    __syncthreads();
+    double2 c = sT[0][warp + 1][lane];
+    for (int z = zs; z < ze; ++z, i += sxy) {
+        const int sl = (z - zs) % S, sn = (z + 1 - zs) % S;
+        cp_async_wait<D - 2>();   // stage z+1 landed
+        __syncthreads();          // ... for every thread; and everyone finished plane z-1
+        if (z + D <= ze) issue(z + D, (z + D - zs) % S);   // into the slot of plane z-1
+        cp_async_commit();
+        const double2 zp = sT[sn][warp + 1][lane];
+        const double2 ym = sT[sl][warp][lane];
+        const double2 yp = sT[sl][warp + 2][lane];
+        const double2 ci = sC[sl][warp][lane];
+        double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
+        double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0 && w0) xm = __ldg(T + i - 1);
+        if (lane == 31 && w1) xp = __ldg(T + i + 2);
+        const double r0 = heat_cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, k);
+        const double r1 = heat_cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, k);
+        if (w0 && w1) {
+            *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+        } else {
+            if (w0) T2[i] = r0;
+            if (w1) T2[i + 1] = r1;
+        }
+        zm = c;
+        c = zp;
+    }
+    cp_async_wait<0>();
+}
+
+template <int TY, int D>
+static void launch_box_rows(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int kc1, int kc2) {
+    const int ax0 = r.x0 & ~63;
+    const int xtiles = (r.x0 + r.wx - ax0 + 63) / 64;
+    const int ytiles = (r.wy + TY - 1) / TY;
+    const int ntiles = xtiles * ytiles;
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, heat_box_rows_kernel<TY, D>, 32 * TY, 0));
+        int dev = 0;
+        IGG_CUDA(cudaGetDevice(&dev));
+        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const long long conc = (long long)occ * nsm;
+    int small = (int)((2 * conc * kc2 + ntiles - 1) / ntiles);
+    small = std::min(((small + kc2 - 1) / kc2) * kc2, r.wz);
+    const int nbig = (r.wz - small) / kc1;
+    const int rest = r.wz - nbig * kc1;
+    const long long blocks = (long long)ntiles * (nbig + (rest + kc2 - 1) / kc2);
+    heat_box_rows_kernel<TY, D><<<(unsigned)blocks, 32 * TY, 0, s>>>(
+        r.T, r.Ci, r.T2, r.sx, r.sy, r.x0, r.y0, r.z0, r.wx, r.wy, r.wz, ax0, xtiles, ytiles, kc1, nbig, kc2, k);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------------- the production kernel
 // heat_box_async_kernel's sweep over a LIST of box regions (one launch for all
 // local ranks, or for all six boundary slabs).  TY=4 rows per CTA, D=3 planes
@@ -585,6 +700,11 @@ void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int
         case 22: launch_box_async<16, 3>(r, k, s, 64, 8); break;
         case 23: launch_box_async<8, 3>(r, k, s, 64, 4); break;
         case 24: launch_box_async<8, 3>(r, k, s, 48, 8); break;
+        case 25: launch_box_rows<4, 3>(r, k, s, 64, 8); break;
+        case 26: launch_box_rows<4, 4>(r, k, s, 64, 8); break;
+        case 27: launch_box_rows<8, 3>(r, k, s, 64, 8); break;
+        case 28: launch_box_rows<8, 4>(r, k, s, 64, 8); break;
+        case 29: launch_box_rows<4, 2>(r, k, s, 64, 8); break;
         case 3: launch_box_variant<8, 32, true>(r, k, s); break;
         default: launch_box_async<4, 3, true>(r, k, s, 64, 8); break;   // 0 = 20: the measured best
     }
@@ -651,7 +771,8 @@ __device__ __forceinline__ void copy_face(const CopyDesc &d) {
 // CTA to finish publishes the epoch to the peers' receive flags: every thread
 // fences its stores (system scope) before the CTA barrier, the elected CTA
 // acquires through the ticket and release-stores each flag.
-__global__ void __launch_bounds__(kCopyThreads) pack_kernel(const __grid_constant__ CopyList L) {
+template <int N>
+__global__ void __launch_bounds__(kCopyThreads) pack_kernel(const __grid_constant__ CopyListT<N> L) {
     const CopyDesc &d = L.d[blockIdx.y];
     copy_face<true>(d);
     if (L.nsignal > 0) {
@@ -671,7 +792,8 @@ __global__ void __launch_bounds__(kCopyThreads) pack_kernel(const __grid_constan
 // unpack: buffer -> field receive slab.  A slot filled by a peer GPU is read
 // only after its flag reached this call's epoch (bounded spin; a timeout sets
 // *err and is reported by igg_check).
-__global__ void __launch_bounds__(kCopyThreads) unpack_kernel(const __grid_constant__ CopyList L) {
+template <int N>
+__global__ void __launch_bounds__(kCopyThreads) unpack_kernel(const __grid_constant__ CopyListT<N> L) {
     const CopyDesc &d = L.d[blockIdx.y];
     if (d.flag_slot >= 0) {
         if (threadIdx.x == 0) {
@@ -693,7 +815,8 @@ __global__ void __launch_bounds__(kCopyThreads) unpack_kernel(const __grid_const
 // one CTA waits for every peer flag of this axis (bounded spin), so the
 // unpack CTAs that follow never occupy SM slots while the peers are still
 // packing (they would starve the concurrent inner-box kernel)
-__global__ void flag_wait_kernel(const __grid_constant__ CopyList L) {
+template <int N>
+__global__ void flag_wait_kernel(const __grid_constant__ CopyListT<N> L) {
     const int t = threadIdx.x;
     if (t < L.nsignal) {
         const unsigned long long *f = L.wait[t];
@@ -717,26 +840,45 @@ static int copy_blocks(const CopyDesc *d, int n) {
     return (int)b;
 }
 
-int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s) {
+template <int N>
+static void fill_list(CopyListT<N> &L, const CopyList &proto) {
+    L.n = 0;
+    L.blocks_per_desc = proto.blocks_per_desc;
+    L.nsignal = proto.nsignal;
+    for (int q = 0; q < kMaxSignal; ++q) {
+        L.signal[q] = proto.signal[q];
+        L.wait[q] = proto.wait[q];
+    }
+    L.ticket = proto.ticket;
+    L.ticket_total = proto.ticket_total;
+    L.epoch = proto.epoch;
+    L.timeout_cycles = proto.timeout_cycles;
+    L.err = proto.err;
+}
+
+template <int N>
+static int launch_copies_n(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s) {
     const int n = (int)descs.size();
-    if (n == 0) return 0;
     // total blocks of all chunks: the pack block that draws the last ticket
     // (necessarily in the last chunk, stream order) publishes the flags
     unsigned total = 0;
-    for (int c = 0; c < n; c += kMaxCopy) {
-        const int m = std::min(kMaxCopy, n - c);
+    for (int c = 0; c < n; c += N) {
+        const int m = std::min(N, n - c);
         total += (unsigned)copy_blocks(descs.data() + c, m) * m;
     }
     int launches = 0;
     const bool waits = op == 1 && proto.nsignal > 0;
     if (waits) {
-        flag_wait_kernel<<<1, 32, 0, s>>>(proto);
+        CopyListT<N> W;
+        fill_list(W, proto);
+        flag_wait_kernel<N><<<1, 32, 0, s>>>(W);
         IGG_CUDA(cudaGetLastError());
         ++launches;
     }
-    for (int c = 0; c < n; c += kMaxCopy) {
-        CopyList L = proto;
-        L.n = std::min(kMaxCopy, n - c);
+    for (int c = 0; c < n; c += N) {
+        CopyListT<N> L;
+        fill_list(L, proto);
+        L.n = std::min(N, n - c);
         for (int j = 0; j < L.n; ++j) {
             L.d[j] = descs[c + j];
             if (waits) L.d[j].flag_slot = -1;   // already waited above
@@ -744,13 +886,96 @@ int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &pr
         L.ticket_total = total;
         dim3 grid(copy_blocks(L.d, L.n), L.n);
         if (op == 0)
-            pack_kernel<<<grid, kCopyThreads, 0, s>>>(L);
+            pack_kernel<N><<<grid, kCopyThreads, 0, s>>>(L);
         else
-            unpack_kernel<<<grid, kCopyThreads, 0, s>>>(L);
+            unpack_kernel<N><<<grid, kCopyThreads, 0, s>>>(L);
         IGG_CUDA(cudaGetLastError());
         ++launches;
     }
     return launches;
+}
+
+int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &proto, cudaStream_t s) {
+    if (descs.empty()) return 0;
+    return descs.size() <= (size_t)kSmallCopy ? launch_copies_n<kSmallCopy>(op, descs, proto, s)
+                                              : launch_copies_n<kMaxCopy>(op, descs, proto, s);
+}
+
+// ============================================================== cooperative update_halo
+// One launch per update_halo call when no NCCL message is involved: all CTAs are
+// co-resident (cooperative launch), so the axis phases are separated by grid
+// barriers instead of kernel boundaries, and the peer flags are published and
+// awaited inside the kernel (removes ~6 dependent launches per call).
+template <bool PACK>
+__device__ __forceinline__ void copy_face_grid(const CopyDesc &d) {
+    const long long nthreads = (long long)gridDim.x * blockDim.x;
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    for (long long base = 0; base < d.count; base += nthreads * kCopyILP) {
+        double v[kCopyILP];
+#pragma unroll
+        for (int u = 0; u < kCopyILP; ++u) {
+            const long long i = base + u * nthreads + gtid;
+            if (i < d.count) v[u] = PACK ? __ldcg(d.field + face_index(d, i)) : __ldcg(d.buf + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kCopyILP; ++u) {
+            const long long i = base + u * nthreads + gtid;
+            if (i < d.count) {
+                if (PACK)
+                    d.buf[i] = v[u];
+                else
+                    d.field[face_index(d, i)] = v[u];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kCopyThreads) halo_coop_kernel(const __grid_constant__ CoopPlan C) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    for (int a = 0; a < 3; ++a) {
+        if (C.pk0[a] == C.pk1[a] && C.up0[a] == C.up1[a]) continue;   // uniform
+        for (int j = C.pk0[a]; j < C.pk1[a]; ++j) copy_face_grid<true>(C.d[j]);
+        if (C.nsignal[a] > 0) __threadfence_system();   // my peer stores, before the barrier
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x < C.nsignal[a]) {
+            __threadfence_system();
+            st_release_sys(C.signal[a][threadIdx.x], C.epoch);
+        }
+        if (C.nwait[a] > 0) {
+            if (blockIdx.x == 0 && threadIdx.x < C.nwait[a]) {
+                const unsigned long long *f = C.wait[a][threadIdx.x];
+                const long long t0 = clock64();
+                while (ld_acquire_sys(f) < C.epoch) {
+                    if (clock64() - t0 > C.timeout_cycles) {
+                        atomicExch(C.err, 1);
+                        break;
+                    }
+                    __nanosleep(32);
+                }
+            }
+            grid.sync();
+        }
+        for (int j = C.up0[a]; j < C.up1[a]; ++j) copy_face_grid<false>(C.d[j]);
+        grid.sync();   // the next axis packs the halos written here (edges and corners)
+    }
+}
+
+void launch_halo_coop(const CoopPlan &C, cudaStream_t s) {
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, halo_coop_kernel, kCopyThreads, 0));
+        int dev = 0;
+        IGG_CUDA(cudaGetDevice(&dev));
+        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    long long mx = 1;
+    for (int a = 0; a < 3; ++a)
+        for (int j = C.pk0[a]; j < C.up1[a]; ++j) mx = std::max(mx, C.d[j].count);
+    long long want = (mx + (long long)kCopyThreads * kCopyILP - 1) / ((long long)kCopyThreads * kCopyILP);
+    const int grid = (int)std::max(1LL, std::min<long long>(want, (long long)occ * nsm));
+    void *args[] = {(void *)&C};
+    IGG_CUDA(cudaLaunchCooperativeKernel((const void *)halo_coop_kernel, dim3(grid), dim3(kCopyThreads), args, 0, s));
 }
 
 // ============================================================== max reduction
