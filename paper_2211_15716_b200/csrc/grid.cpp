@@ -309,7 +309,7 @@ static void launch_regions(igg_grid *g, const std::vector<HeatRegion> &regs, con
     if (rs.empty()) return;
     if (main) prof_begin(g, s);
     const int v = g->stencil_kernel;
-    if (((v >= 2 && v < 30) || v == 0) && vec && main) {   // 0: launch_heat_box's default (variant 20)
+    if (((v >= 2 && v < 30) || (v >= 50 && v < 60) || v == 0) && vec && main) {   // 0: launch_heat_box's default (variant 20)
         for (const HeatRegion &R : rs) {
             launch_heat_box(R, k, s, v);
             g->launches++;
@@ -320,7 +320,7 @@ static void launch_regions(igg_grid *g, const std::vector<HeatRegion> &regs, con
         std::vector<HeatRegion> narrow, wide;
         for (const HeatRegion &R : rs) {
             const bool is_narrow = (R.x0 + R.wx - (R.x0 & ~1)) <= 32;
-            (((v == 0 || v >= 30) && !is_narrow) ? wide : narrow).push_back(R);
+            (((v == 0 || (v >= 30 && v < 40)) && !is_narrow) ? wide : narrow).push_back(R);
         }
         for (int pass = 0; pass < 2; ++pass) {
             const std::vector<HeatRegion> &part = pass == 0 ? wide : narrow;

@@ -417,6 +417,108 @@ static void launch_box_async(const HeatRegion &r, const HeatCoef &k, cudaStream_
     IGG_CUDA(cudaGetLastError());
 }
 
+// ------------------------------------------------------------- wide tiles (ablation)
+// heat_box_async_kernel with WX warps side by side along x (tile (64*WX) x TY):
+// a CTA streams whole 4-KB rows when WX = 8 (DRAM page locality experiment).
+template <int WX, int TY, int D>
+__global__ void __launch_bounds__(32 * WX * TY)
+    heat_box_wide_kernel(const double *__restrict__ T, const double *__restrict__ Ci, double *__restrict__ T2,
+                         int sx, int sy, int x0, int y0, int z0, int wx, int wy, int wz, int ax0, int xtiles,
+                         int ytiles, int kc1, int nbig, int kc2, const HeatCoef k) {
+    constexpr int NT = 32 * WX * TY;
+    __shared__ double2 sT[D][NT];
+    __shared__ double2 sC[D][NT];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wxi = warp % WX, wyi = warp / WX;
+    const int ntiles = xtiles * ytiles;
+    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    int zs, ze;
+    if (chunk < nbig) {
+        zs = z0 + chunk * kc1;
+        ze = min(zs + kc1, z0 + wz);
+    } else {
+        zs = z0 + nbig * kc1 + (chunk - nbig) * kc2;
+        ze = min(zs + kc2, z0 + wz);
+    }
+    const int tx = tile % xtiles, ty = tile / xtiles;
+    const int y = y0 + ty * TY + wyi;
+    if (y >= y0 + wy || zs >= ze) return;
+    const int p = ax0 + (tx * WX + wxi) * 64 + 2 * lane;
+    const int xend = x0 + wx;
+    const bool pair_in = p < sx;
+    const bool w0 = pair_in && p >= x0 && p < xend;
+    const bool w1 = pair_in && p + 1 >= x0 && p + 1 < xend;
+    const long long sxy = (long long)sx * sy;
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+        if (pair_in && zs + q < ze) {
+            cp_async16(&sT[q][tid], T + i + (q + 1) * sxy);
+            cp_async16(&sC[q][tid], Ci + i + q * sxy);
+        }
+        cp_async_commit();
+    }
+    const double2 zero2 = make_double2(0.0, 0.0);
+    double2 zm = pair_in ? ldg2(T + i - sxy) : zero2;
+    double2 c = pair_in ? ldg2(T + i) : zero2;
+    int slot = 0;
+    for (int z = zs; z < ze; ++z, i += sxy) {
+        cp_async_wait<D - 1>();
+        double2 ym = zero2, yp = zero2;
+        if (pair_in) {
+            ym = ldg2(T + i - sx);
+            yp = ldg2(T + i + sx);
+        }
+        const double2 zp = sT[slot][tid];
+        const double2 ci = sC[slot][tid];
+        double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
+        double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+        if (lane == 0 && w0) xm = __ldg(T + i - 1);
+        if (lane == 31 && w1) xp = __ldg(T + i + 2);
+        const double r0 = heat_cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, k);
+        const double r1 = heat_cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, k);
+        if (w0 && w1) {
+            *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+        } else {
+            if (w0) T2[i] = r0;
+            if (w1) T2[i + 1] = r1;
+        }
+        zm = c;
+        c = zp;
+        if (pair_in && z + D < ze) {
+            cp_async16(&sT[slot][tid], T + i + (D + 1) * sxy);
+            cp_async16(&sC[slot][tid], Ci + i + D * sxy);
+        }
+        cp_async_commit();
+        slot = slot + 1 == D ? 0 : slot + 1;
+    }
+    cp_async_wait<0>();
+}
+
+template <int WX, int TY, int D>
+static void launch_box_wide(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int kc1, int kc2) {
+    const int ax0 = r.x0 & ~63;
+    const int xtiles = (r.x0 + r.wx - ax0 + 64 * WX - 1) / (64 * WX);
+    const int ytiles = (r.wy + TY - 1) / TY;
+    const int ntiles = xtiles * ytiles;
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, heat_box_wide_kernel<WX, TY, D>, 32 * WX * TY, 0));
+        int dev = 0;
+        IGG_CUDA(cudaGetDevice(&dev));
+        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const long long conc = (long long)occ * nsm;
+    int small = (int)((2 * conc * kc2 + ntiles - 1) / ntiles);
+    small = std::min(((small + kc2 - 1) / kc2) * kc2, r.wz);
+    const int nbig = (r.wz - small) / kc1;
+    const int rest = r.wz - nbig * kc1;
+    const long long blocks = (long long)ntiles * (nbig + (rest + kc2 - 1) / kc2);
+    heat_box_wide_kernel<WX, TY, D><<<(unsigned)blocks, 32 * WX * TY, 0, s>>>(
+        r.T, r.Ci, r.T2, r.sx, r.sy, r.x0, r.y0, r.z0, r.wx, r.wy, r.wz, ax0, xtiles, ytiles, kc1, nbig, kc2, k);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ------------------------------------------------------------- row-staged pipeline (ablation)
 // Like heat_box_async_kernel, but the CTA stages whole planes of its tile --
 // T rows y0-1 .. y0+TY and Ci rows y0 .. y0+TY-1 -- with cp.async into a ring
@@ -705,6 +807,13 @@ void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int
         case 27: launch_box_rows<8, 3>(r, k, s, 64, 8); break;
         case 28: launch_box_rows<8, 4>(r, k, s, 64, 8); break;
         case 29: launch_box_rows<4, 2>(r, k, s, 64, 8); break;
+        case 50: launch_box_wide<8, 1, 3>(r, k, s, 64, 8); break;
+        case 51: launch_box_wide<4, 1, 3>(r, k, s, 64, 8); break;
+        case 52: launch_box_wide<2, 2, 3>(r, k, s, 64, 8); break;
+        case 53: launch_box_wide<8, 1, 4>(r, k, s, 64, 8); break;
+        case 54: launch_box_wide<4, 2, 3>(r, k, s, 64, 8); break;
+        case 55: launch_box_wide<2, 1, 3>(r, k, s, 64, 8); break;
+        case 56: launch_box_wide<1, 4, 3>(r, k, s, 64, 8); break;
         case 3: launch_box_variant<8, 32, true>(r, k, s); break;
         default: launch_box_async<4, 3, true>(r, k, s, 64, 8); break;   // 0 = 20: the measured best
     }
