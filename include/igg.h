@@ -213,6 +213,15 @@ igg_status igg_global_max(igg_grid *grid, double local, double *out);
 igg_status igg_field_global_max(igg_grid *grid, const double *const *f, long long count,
                                 double *out, igg_stream_t stream);
 
+/* gather: assemble the global field on process root_proc, in host
+ * memory of the global size (igg_n_g per axis, x fastest), from every rank's OWNED layers: interior
+ * ranks own local layers [h + ol%2, s - h) per axis, the first rank also the lower halo layers, the last
+ * the upper ones (non-periodic), a shared middle layer (odd field overlap) the lower rank.  fields:
+ * local_ranks device pointers of one field shape.  host_out is ignored on other processes.
+ * Collective and synchronous (a utility, not on the hot path). */
+igg_status igg_gather(igg_grid *grid, const igg_field *fields, int root_proc, double *host_out,
+                      igg_stream_t stream);
+
 /* ------------------------------------------------------------------ control */
 enum {
     IGG_OPT_SKIP_COMM = 1,       /* timing-only: skip pack/exchange/unpack (results INVALID) */

@@ -70,6 +70,7 @@ SIGNATURES = {
     "igg_field_global_max": [ctypes.c_void_p, c_dbl_pp, ctypes.c_longlong, c_dbl_p, ctypes.c_void_p],
     "igg_set_option": [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong],
     "igg_check": [ctypes.c_void_p],
+    "igg_gather": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
     "igg_profile_stencil": [ctypes.c_void_p, c_dbl_p, c_ll_p, c_ll_p],
     "igg_profile_timeline": [ctypes.c_void_p, c_dbl_p],
 }

@@ -679,6 +679,111 @@ IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *
     IGG_CATCH
 }
 
+// ------------------------------------------------------------------ gather
+namespace igg {
+// owned layers [lo, hi) of a rank at axis coordinate c for a field of size s: interior ranks own
+// [h + ol%2, s - h); the first rank also owns the lower halo layers, the last the upper ones;
+// a shared middle layer (odd field overlap) belongs to the lower rank.  Periodic axes: every rank
+// is interior.  Global index of local layer l: c(n-o) + l (periodic: shifted by o/2 mod the period).
+static void owned_range(const igg_grid *g, int a, int c, long long s, int *lo, int *hi) {
+    HaloSpec hs;
+    halo_spec(g->n[a], g->o[a], s, &hs);
+    const bool first = !g->periods[a] && c == 0, last = !g->periods[a] && c == g->dims[a] - 1;
+    *lo = first ? 0 : hs.h + (hs.ol % 2);
+    *hi = last ? (int)s : (int)s - hs.h;
+}
+}  // namespace igg
+
+IGG_API igg_status igg_gather(igg_grid *g, const igg_field *fields, int root_proc, double *host_out,
+                              igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_gather");
+    if (!fields || root_proc < 0 || root_proc >= g->nproc_procs) fail(IGG_E_ARG, "igg_gather: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long sz[3] = {fields[0].size[0], fields[0].size[1], fields[0].size[2]};
+    long long N[3];
+    for (int a = 0; a < 3; ++a) {
+        igg::HaloSpec hs;
+        if (!igg::halo_spec(g->n[a], g->o[a], sz[a], &hs)) fail(IGG_E_STAGGER, "igg_gather: field size out of range");
+        N[a] = g->periods[a] ? g->ng[a] : g->ng[a] + (sz[a] - g->n[a]);
+    }
+    const bool is_root = g->proc == root_proc;
+    if (is_root && !host_out) fail(IGG_E_ARG, "igg_gather: host_out is NULL on the root");
+    // boxes of every rank, in rank order
+    struct Box {
+        int b0[3], b1[3];
+        long long count, off;
+    };
+    std::vector<Box> boxes(g->nprocs);
+    long long total = 0;
+    for (int r = 0; r < g->nprocs; ++r) {
+        int c[3];
+        igg::coords_of_rank(g->dims, r, c);
+        Box &B = boxes[r];
+        B.count = 1;
+        for (int a = 0; a < 3; ++a) {
+            igg::owned_range(g, a, c[a], sz[a], &B.b0[a], &B.b1[a]);
+            B.count *= std::max(0, B.b1[a] - B.b0[a]);
+        }
+        B.off = total;
+        total += B.count;
+    }
+    // pack my ranks' boxes into one device buffer (mine are contiguous in rank order)
+    long long mine = 0, mine_off = boxes[g->rank0].off;
+    for (int lr = 0; lr < g->nlocal; ++lr) mine += boxes[g->rank0 + lr].count;
+    double *dbuf = nullptr;
+    IGG_CUDA(cudaMalloc(&dbuf, sizeof(double) * (is_root ? total : std::max(mine, 1LL))));
+    double *dst = dbuf + (is_root ? mine_off : 0);
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        const Box &B = boxes[g->rank0 + lr];
+        igg::launch_box_pack(fields[lr].ptr, dst + (B.off - mine_off), sz[0], sz[1], B.b0, B.b1, s);
+    }
+    if (g->nproc_procs > 1) {
+        IGG_NCCL(ncclGroupStart());
+        if (is_root) {
+            for (int p = 0; p < g->nproc_procs; ++p) {
+                if (p == g->proc) continue;
+                long long cnt = 0;
+                for (int lr = 0; lr < g->nlocal; ++lr) cnt += boxes[p * g->nlocal + lr].count;
+                if (cnt) IGG_NCCL(ncclRecv(dbuf + boxes[p * g->nlocal].off, (size_t)cnt, ncclDouble, p, g->comm, s));
+            }
+        } else if (mine) {
+            IGG_NCCL(ncclSend(dbuf, (size_t)mine, ncclDouble, root_proc, g->comm, s));
+        }
+        IGG_NCCL(ncclGroupEnd());
+    }
+    IGG_CUDA(cudaStreamSynchronize(s));
+    if (is_root) {
+        std::vector<double> h(total);
+        IGG_CUDA(cudaMemcpy(h.data(), dbuf, sizeof(double) * total, cudaMemcpyDeviceToHost));
+        for (int r = 0; r < g->nprocs; ++r) {
+            const Box &B = boxes[r];
+            int c[3];
+            igg::coords_of_rank(g->dims, r, c);
+            const int nx = B.b1[0] - B.b0[0], ny = B.b1[1] - B.b0[1], nz = B.b1[2] - B.b0[2];
+            if (nx <= 0 || ny <= 0 || nz <= 0) continue;
+            long long gl[3][1];
+            (void)gl;
+            // global index of local layer l on axis a
+            auto gidx = [&](int a, int l) {
+                long long v = (long long)c[a] * (g->n[a] - g->o[a]) + l;
+                if (g->periods[a]) v = ((v - g->o[a] / 2) % N[a] + N[a]) % N[a];
+                return v;
+            };
+            const double *src = h.data() + B.off;
+            for (int z = 0; z < nz; ++z)
+                for (int y = 0; y < ny; ++y) {
+                    const long long gz = gidx(2, B.b0[2] + z), gy = gidx(1, B.b0[1] + y);
+                    const double *row = src + ((long long)z * ny + y) * nx;
+                    for (int x = 0; x < nx; ++x)
+                        host_out[(gz * N[1] + gy) * N[0] + gidx(0, B.b0[0] + x)] = row[x];
+                }
+        }
+    }
+    IGG_CUDA(cudaFree(dbuf));
+    IGG_CATCH
+}
+
 IGG_API igg_status igg_global_max(igg_grid *g, double local, double *out) {
     IGG_TRY
     igg::check_live(g, "igg_global_max");

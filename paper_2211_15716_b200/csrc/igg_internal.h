@@ -187,6 +187,9 @@ void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant);
 // vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field
 bool heat_box_vectorizable(const HeatRegion &r);
 void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant);
+// sub-box [b0, b1) of a field -> contiguous buffer (x fastest)
+void launch_box_pack(const double *f, double *out, long long sx, long long sy, const int b0[3], const int b1[3],
+                     cudaStream_t s);
 // max over `count` doubles of each of n pointers -> partials -> *out_dev (one double)
 void launch_field_max(const double *const *ptrs, int n, long long count, double *scratch,
                       int scratch_len, double *out_dev, cudaStream_t s);

@@ -1087,6 +1087,30 @@ void launch_halo_coop(const CoopPlan &C, cudaStream_t s) {
     IGG_CUDA(cudaLaunchCooperativeKernel((const void *)halo_coop_kernel, dim3(grid), dim3(kCopyThreads), args, 0, s));
 }
 
+// ============================================================== box pack (gather)
+// Copies the sub-box [b0, b1) of a (sx, sy, sz) field into a contiguous buffer, x fastest.
+__global__ void __launch_bounds__(256) box_pack_kernel(const double *__restrict__ f, double *__restrict__ out,
+                                                       long long sx, long long sy, int x0, int y0, int z0, int nx,
+                                                       int ny, int nz) {
+    const long long n = (long long)nx * ny * nz;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(t % nx);
+        const long long r = t / nx;
+        const int y = (int)(r % ny), z = (int)(r / ny);
+        out[t] = f[((long long)(z0 + z) * sy + (y0 + y)) * sx + x0 + x];
+    }
+}
+
+void launch_box_pack(const double *f, double *out, long long sx, long long sy, const int b0[3], const int b1[3],
+                     cudaStream_t s) {
+    const int nx = b1[0] - b0[0], ny = b1[1] - b0[1], nz = b1[2] - b0[2];
+    if (nx <= 0 || ny <= 0 || nz <= 0) return;
+    const long long n = (long long)nx * ny * nz;
+    const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+    box_pack_kernel<<<blocks, 256, 0, s>>>(f, out, sx, sy, b0[0], b0[1], b0[2], nx, ny, nz);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ============================================================== max reduction
 constexpr int kMaxThreads = 256;
 constexpr int kMaxPartials = 1184;   // 148 SMs x 8

@@ -243,6 +243,24 @@ class Grid:
         _ok(L.lib().igg_heat_run_host(self._handle(), hp(T_host), hp(Ci_host), lam, dt, dx, dy, dz, nt,
                                       _i3(bw), _stream(stream)))
 
+    # -- gather
+    def gather(self, field, root: int = 0, stream=None):
+        """Global field (numpy, (Nz, Ny, Nx)) assembled on process `root` from the owned layers of every
+        rank; None on other processes.  field: a tensor or a list of local_ranks tensors."""
+        import numpy as np
+        ts = _as_list(field, self.local_ranks)
+        arr = (L.igg_field * self.local_ranks)()
+        for r, t in enumerate(ts):
+            arr[r].ptr = _dev_ptr(t)
+            sz, sy, sx = t.shape
+            arr[r].size[0], arr[r].size[1], arr[r].size[2] = sx, sy, sz
+        sz, sy, sx = ts[0].shape
+        shape = (self.n_global(2, sz), self.n_global(1, sy), self.n_global(0, sx))
+        me_root = (self.rank0 // self.local_ranks) == root
+        out = np.empty(shape, dtype=np.float64) if me_root else None
+        _ok(L.lib().igg_gather(self._handle(), arr, root, out.ctypes.data if me_root else None, _stream(stream)))
+        return out
+
     # -- reductions (PAPER.md:73)
     def global_max(self, local: float) -> float:
         out = ctypes.c_double()

@@ -87,6 +87,20 @@ def halo_case(path, n, dims, per, local, sizes, seed, repeat=2):
     log("halo OK", path, dims, per, "local", local)
 
 
+def gather_case(path, n, dims, per, s):
+    g = P.init_global_grid(*n, dims=dims, periods=per, path=path, device=int(os.environ["LOCAL_RANK"]))
+    try:
+        N = [OG.field_global_size(n[i], 2, dims[i], per[i], s[i]) for i in range(3)]
+        G = SI.random_field((N[2], N[1], N[0]), 77)
+        W = OG.window(G, OG.coords_of_rank(g.rank0, dims), dims, n, (2, 2, 2), per, s)
+        out = g.gather(torch.from_numpy(W).cuda(), root=0)
+        if dist.get_rank() == 0 and not np.array_equal(out, G):
+            raise AssertionError(f"gather {dims} per={per} s={s}")
+    finally:
+        g.finalize()
+    log("gather OK", dims, per, s)
+
+
 def main():
     local_rank = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local_rank)
@@ -118,6 +132,8 @@ def main():
             heat_case(path, (24, 20, 18), (2, 2, 2), (0, 0, 0), 8 // world, (4, 2, 2))
             halo_case(path, (24, 20, 18), (2, 2, 2), (1, 0, 1), 8 // world,
                       [(24, 20, 18), (25, 20, 18), (24, 21, 18), (24, 20, 19)], seed=3)
+    gather_case(paths[0], (20, 18, 16), dims, (0, 0, 0), (21, 18, 16))
+    gather_case(paths[0], (20, 18, 16), dims, (1, 0, 1), (20, 17, 16))
     dist.barrier()
     if dist.get_rank() == 0:
         print("MULTI-GPU PARITY OK", world, paths, flush=True)

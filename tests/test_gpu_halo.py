@@ -112,3 +112,40 @@ def test_full_size_staggered_update_512():
     n = (512, 512, 512)
     sizes = [n, (513, 512, 512), (512, 513, 512), (512, 512, 513)]
     _run_case((2, 1, 1), (1, 0, 0), (2, 2, 2), n, sizes, seed=12)
+
+
+def test_gather_spec_example():
+    """n=4, o=2, dims (2,1,1), each rank filled with its rank id -> (0,0,0,1,1,1) along x."""
+    import torch
+    g = P.init_global_grid(4, 4, 4, dims=(2, 1, 1), local_ranks=2, device=0)
+    try:
+        A = [torch.full((4, 4, 4), float(r), dtype=torch.float64, device="cuda") for r in range(2)]
+        G = g.gather(A)
+        assert G.shape == (4, 4, 6)
+        assert np.array_equal(G[0, 0], np.array([0, 0, 0, 1, 1, 1], dtype=np.float64))
+    finally:
+        g.finalize()
+
+
+def test_gather_inverts_windows():
+    """gather(window(G, rank)) == G for random global fields (the window map is the oracle)."""
+    import torch
+    rng = random.Random(21)
+    for case in range(25):
+        dims = tuple(rng.randint(1, 3) for _ in range(3))
+        o = tuple(rng.choice((2, 4)) for _ in range(3))
+        n = tuple(rng.randint(o[i] + 2, o[i] + 7) for i in range(3))
+        per = tuple(rng.random() < 0.4 for _ in range(3))
+        s = tuple(n[i] + rng.choice((-1, 0, 1)) for i in range(3))
+        N = [OG.field_global_size(n[i], o[i], dims[i], per[i], s[i]) for i in range(3)]
+        G = SI.random_field((N[2], N[1], N[0]), case)
+        nprocs = dims[0] * dims[1] * dims[2]
+        g = P.init_global_grid(*n, dims=dims, periods=per, overlaps=o, local_ranks=nprocs, device=0)
+        try:
+            loc = [torch.from_numpy(OG.window(G, OG.coords_of_rank(r, dims), dims, n, o, per, s)).cuda()
+                   for r in range(nprocs)]
+            out = g.gather(loc)
+            assert out.shape == G.shape
+            assert np.array_equal(out, G), (case, dims, o, n, per, s)
+        finally:
+            g.finalize()
