@@ -193,6 +193,22 @@ igg_status igg_heat_step(igg_grid *grid, double *const *T2, const double *const 
                          const double *const *Ci, double lam, double dt,
                          double dx, double dy, double dz, const int bw[3], igg_stream_t stream);
 
+/* ------------------------------------------------------------------ generic hide_communication
+ * A user stencil for igg_hide_communication: compute the cells of the box [lo, hi) (0-based, of the
+ * canonical local grid of hosted rank `local_rank`) by enqueuing work on `stream`; it must write only
+ * cells inside the box and read only values the step does not write. */
+typedef void (*igg_region_fn)(void *user, int local_rank, const int lo[3], const int hi[3], igg_stream_t stream);
+
+/* @hide_communication bw begin <user step>; update_halo!(fields...) end (
+ * SPEC.md:330-338) for any stencil: the six boundary slabs of the computed box [1, n-1)^3 are
+ * requested first on the library's high-priority stream, update_halo(fields) follows them there, and
+ * the inner box [max(1,b), n-b) is requested on the low-priority stream concurrently; everything is
+ * joined to `stream`.  bw = {0,0,0} or an empty inner box: sequential (full box, then update_halo).
+ * An exchanged axis needs b_d >= ol_d of every exchanged field (IGG_E_WIDTH).  fields: local_ranks *
+ * nfields entries, rank-major, as for igg_update_halo.  fn is called on this thread before return. */
+igg_status igg_hide_communication(igg_grid *grid, const int bw[3], igg_region_fn fn, void *user,
+                                  const igg_field *fields, int nfields, igg_stream_t stream);
+
 /* Fig. 1 end to end from HOST memory: copies T (initial, local_ranks*nx*ny*nz
  * doubles, rank-major) and Ci to the device, sets T2 = copy(T), runs nt heat
  * steps with swap, and copies the final T back into T_host.

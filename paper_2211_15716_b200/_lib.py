@@ -42,6 +42,9 @@ class igg_plan_entry(ctypes.Structure):
                 ("lo", ctypes.c_int), ("h", ctypes.c_int), ("count", ctypes.c_longlong), ("order", ctypes.c_int)]
 
 
+REGION_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                             ctypes.POINTER(ctypes.c_int), ctypes.c_void_p)
+
 # name -> (argtypes); every entry point returns igg_status (int) except igg_last_error
 SIGNATURES = {
     "igg_dims_create": [ctypes.c_int, c_int_p, c_int_p],
@@ -70,6 +73,8 @@ SIGNATURES = {
     "igg_field_global_max": [ctypes.c_void_p, c_dbl_pp, ctypes.c_longlong, c_dbl_p, ctypes.c_void_p],
     "igg_set_option": [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong],
     "igg_check": [ctypes.c_void_p],
+    "igg_hide_communication": [ctypes.c_void_p, c_int_p, REGION_FN, ctypes.c_void_p, ctypes.POINTER(igg_field),
+                               ctypes.c_int, ctypes.c_void_p],
     "igg_gather": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
     "igg_profile_stencil": [ctypes.c_void_p, c_dbl_p, c_ll_p, c_ll_p],
     "igg_profile_timeline": [ctypes.c_void_p, c_dbl_p],

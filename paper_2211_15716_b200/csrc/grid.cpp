@@ -642,6 +642,68 @@ IGG_API igg_status igg_heat_step(igg_grid *g, double *const *T2, const double *c
     IGG_CATCH
 }
 
+IGG_API igg_status igg_hide_communication(igg_grid *g, const int bw_in[3], igg_region_fn fn, void *user,
+                                          const igg_field *fields, int nfields, igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_hide_communication");
+    if (!fn || !fields || nfields < 1) fail(IGG_E_ARG, "igg_hide_communication: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int zero[3] = {0, 0, 0};
+    const int *bw = bw_in ? bw_in : zero;
+    bool exch[3] = {false, false, false};
+    for (int a = 0; a < 3; ++a)
+        for (int lr = 0; lr < g->nlocal; ++lr)
+            if (g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0) exch[a] = true;
+    const bool seq = bw[0] == 0 && bw[1] == 0 && bw[2] == 0;
+    int lo[3], hi[3];
+    bool degenerate = false;
+    for (int a = 0; a < 3; ++a) {
+        if (bw[a] < 0) fail(IGG_E_ARG, "igg_hide_communication: negative boundary width");
+        if (!seq && exch[a])
+            for (int f = 0; f < nfields; ++f) {
+                igg::HaloSpec hs;
+                if (!igg::halo_spec(g->n[a], g->o[a], fields[f].size[a], &hs))
+                    fail(IGG_E_STAGGER, "igg_hide_communication: field size out of range");
+                if (hs.h > 0 && bw[a] < hs.ol)
+                    fail(IGG_E_WIDTH, "igg_hide_communication: boundary width " + std::to_string(bw[a]) +
+                                          " on axis " + std::to_string(a) + " is below a field overlap " +
+                                          std::to_string(hs.ol));
+            }
+        const int b = exch[a] ? bw[a] : 0;
+        lo[a] = std::max(1, b);
+        hi[a] = std::min(g->n[a] - 1, g->n[a] - b);
+        if (hi[a] <= lo[a]) degenerate = true;
+    }
+    const int full_lo[3] = {1, 1, 1}, full_hi[3] = {g->n[0] - 1, g->n[1] - 1, g->n[2] - 1};
+    IGG_CUDA(cudaEventRecord(g->ev_start, s));
+    IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
+    if (seq || degenerate) {
+        for (int lr = 0; lr < g->nlocal; ++lr) fn(user, lr, full_lo, full_hi, (igg_stream_t)g->s_comm);
+        igg::exchange(g, fields, nfields, g->s_comm);
+        IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+        IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+        return IGG_OK;
+    }
+    IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
+    const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
+    // the six slabs x-lo, x-hi, y-lo, y-hi, z-lo, z-hi, each cell exactly once
+    const int slab[6][6] = {{1, lo[0], 1, n1 - 1, 1, n2 - 1},           {hi[0], n0 - 1, 1, n1 - 1, 1, n2 - 1},
+                            {lo[0], hi[0], 1, lo[1], 1, n2 - 1},         {lo[0], hi[0], hi[1], n1 - 1, 1, n2 - 1},
+                            {lo[0], hi[0], lo[1], hi[1], 1, lo[2]},      {lo[0], hi[0], lo[1], hi[1], hi[2], n2 - 1}};
+    for (int lr = 0; lr < g->nlocal; ++lr)
+        for (int k = 0; k < 6; ++k) {
+            const int a0[3] = {slab[k][0], slab[k][2], slab[k][4]}, a1[3] = {slab[k][1], slab[k][3], slab[k][5]};
+            if (a1[0] > a0[0] && a1[1] > a0[1] && a1[2] > a0[2]) fn(user, lr, a0, a1, (igg_stream_t)g->s_comm);
+        }
+    for (int lr = 0; lr < g->nlocal; ++lr) fn(user, lr, lo, hi, (igg_stream_t)g->s_inner);
+    igg::exchange(g, fields, nfields, g->s_comm);
+    IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+    IGG_CUDA(cudaEventRecord(g->ev_inner, g->s_inner));
+    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
+    IGG_CATCH
+}
+
 IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *Ci_host, double lam, double dt,
                                      double dx, double dy, double dz, int nt, const int bw[3], igg_stream_t stream) {
     IGG_TRY

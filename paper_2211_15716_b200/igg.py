@@ -243,6 +243,40 @@ class Grid:
         _ok(L.lib().igg_heat_run_host(self._handle(), hp(T_host), hp(Ci_host), lam, dt, dx, dy, dz, nt,
                                       _i3(bw), _stream(stream)))
 
+    # -- generic @hide_communication
+    def hide_communication(self, bw, step, *fields, stream=None) -> None:
+        """Run a user stencil `step(local_rank, lo, hi, stream)` -- which must enqueue the computation of
+        the box [lo, hi) on the given torch stream -- with the boundary slabs first and update_halo(fields)
+        overlapped with the inner box.  bw = (0, 0, 0): sequential."""
+        import torch
+        per = [_as_list(f, self.local_ranks) for f in fields]
+        nf = len(per)
+        arr = (L.igg_field * (nf * self.local_ranks))()
+        for r in range(self.local_ranks):
+            for f in range(nf):
+                t = per[f][r]
+                e = arr[r * nf + f]
+                e.ptr = _dev_ptr(t)
+                sz, sy, sx = t.shape
+                e.size[0], e.size[1], e.size[2] = sx, sy, sz
+        streams = {}
+        errors = []
+
+        def _cb(user, lr, lo, hi, st):
+            try:
+                if st not in streams:
+                    streams[st] = torch.cuda.ExternalStream(st)
+                s_ = streams[st]
+                with torch.cuda.stream(s_):
+                    step(lr, (lo[0], lo[1], lo[2]), (hi[0], hi[1], hi[2]), s_)
+            except Exception as ex:  # never raise through C
+                errors.append(ex)
+
+        cb = L.REGION_FN(_cb)
+        _ok(L.lib().igg_hide_communication(self._handle(), _i3(bw), cb, None, arr, nf, _stream(stream)))
+        if errors:
+            raise errors[0]
+
     # -- gather (SPEC.md:128-136)
     def gather(self, field, root: int = 0, stream=None):
         """Global field (numpy, (Nz, Ny, Nx)) assembled on process `root` from the owned layers of every
