@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--fused-mode", type=int, default=2, help="ablation bits of the fused path")
     ap.add_argument("--kc2", type=int, default=0, help="fused path: tail z-chunk planes (0 auto)")
     ap.add_argument("--ncomm", type=int, default=1, help="fused path: CTAs per receive/forward kernel")
+    ap.add_argument("--dims", default="", help="override the process topology, e.g. 1,2,1")
     ap.add_argument("--schedule", type=int, default=0, help="0 concurrent, 1 boundary first (paper order)")
     ap.add_argument("--timeline", action="store_true", help="record the overlap timeline (extra events)")
     ap.add_argument("--xalign", type=int, default=64, help="x boundary-slab alignment in cells (1 = exact bw)")
@@ -203,7 +204,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dims = DIMS.get(world) or P.dims_create(world)
+    dims = tuple(int(x) for x in a.dims.split(",")) if a.dims else (DIMS.get(world) or P.dims_create(world))
     bw = tuple(int(x) for x in a.bw.split(","))
     n = a.n
     periods = tuple(int(x) for x in a.periodic.split(","))
@@ -262,6 +263,11 @@ def main():
     barrier()
     launches = g.kernel_launches() - l0
     ms = e0.elapsed_time(e1) / a.steps
+    per_rank_ms = [ms]
+    if world > 1:
+        allms = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(world)]
+        dist.all_gather(allms, torch.tensor([ms], dtype=torch.float64, device="cuda"))
+        per_rank_ms = [float(t.item()) for t in allms]
     ms = max_over_ranks(ms)
     k_ms, k_n, k_cells = g.profile_stencil()
     timeline = g.profile_timeline() if a.timeline else None
@@ -376,7 +382,7 @@ def main():
                        "frac_of_stream_2r1w": per_gpu / stream_ref if stream_ref else None,
                        "stencil_variant": a.kernel},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk, "exposed_halo": exposed, "timeline_ms": timeline,
+            "clocks": clk, "exposed_halo": exposed, "timeline_ms": timeline, "per_rank_ms": per_rank_ms,
         }
         print(json.dumps(line))
     if world > 1:

@@ -110,6 +110,7 @@ __device__ __forceinline__ int2 ext_range(const FusedParams &F, int c) {
 }
 
 constexpr int kFTY = 4;    // rows per CTA (one warp each)
+__device__ __forceinline__ bool pair_in_x(int p, int sx) { return p < sx; }
 constexpr unsigned g_poll_ns = 1000;   // flag polling period of the waiting CTAs
 constexpr int kFD = 3;     // planes in flight per thread
 constexpr int kFKC = 64;   // longest z-chunk
@@ -228,44 +229,76 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const int xlo = max(tx0, 1), xhi = min(tx0 + 64, sx - 1);   // inner x of this tile
     const int yhi = min(ty0 + kFTY, sy - 1);
     bool did[6] = {false, false, false, false, false, false};
+    // Each warp copies its own row's part of every face the tile holds, with all loads of a
+    // batch issued before its stores (the cells were just written by this CTA: L2 hits).
+    const int yrow = ty0 + warp;               // my warp's row
+    const bool rowv = yrow < yhi;
 #pragma unroll
     for (int rs = 0; rs < 2 && !F.nostore; ++rs) {
         // rs = 0: the upper neighbour's lower halo layer 0; rs = 1: the lower neighbour's layer s-1
-        // x face: the layer column of my rows over the chunk -> peer T2 x halo
+        // x face: my row's layer cell over the chunk's planes -> the peer's x halo (lanes along z)
         const FusedFace &fx = F.face[0][rs];
         if (fx.active && fx.layer >= xlo && fx.layer < xhi) {
             const int hx = rs == 0 ? 0 : sx - 1;
-            for (int t = tid; t < kFTY * nz; t += blockDim.x) {
-                const int w = t / nz, zz = zs + (t - w * nz);
-                const int yy = ty0 + w;
-                if (yy < yhi) {
-                    const long long row = (long long)zz * sxy + (long long)yy * sx;
-                    fx.dst[row + hx] = XS ? xs[XS ? w : 0][XS ? zz - zs : 0] : T2[row + fx.layer];
+            if (rowv) {
+                double v[kFKC / 32];
+#pragma unroll
+                for (int u = 0; u < kFKC / 32; ++u) {
+                    const int zz = zs + lane + 32 * u;
+                    v[u] = zz < ze ? T2[(long long)zz * sxy + (long long)yrow * sx + fx.layer] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < kFKC / 32; ++u) {
+                    const int zz = zs + lane + 32 * u;
+                    if (zz < ze) fx.dst[(long long)zz * sxy + (long long)yrow * sx + hx] = v[u];
                 }
             }
             did[rs] = true;
         }
-        // y face: the layer row over the chunk -> peer T2 y halo row (512-B runs)
+        // y face: the layer row over the chunk's planes -> the peer's y halo row; the warps
+        // take planes round-robin, lanes the row segment as 16-B pairs
         const FusedFace &fy = F.face[1][rs];
         if (fy.active && fy.layer >= ty0 && fy.layer < yhi) {
             const int hy = rs == 0 ? 0 : sy - 1;
-            const int w = xhi - xlo;
-            for (int t = tid; t < w * nz; t += blockDim.x) {
-                const int zz = zs + t / w, xx = xlo + t % w;
-                fy.dst[(long long)zz * sxy + (long long)hy * sx + xx] =
-                    T2[(long long)zz * sxy + (long long)fy.layer * sx + xx];
+            constexpr int U = 4;
+            for (int zb = zs + warp; zb < ze; zb += kFTY * U) {
+                double2 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int zz = zb + kFTY * u;
+                    v[u] = (zz < ze && pair_in_x(p, sx))
+                               ? *reinterpret_cast<const double2 *>(T2 + (long long)zz * sxy + (long long)fy.layer * sx + p)
+                               : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int zz = zb + kFTY * u;
+                    if (zz >= ze) continue;
+                    double *d = fy.dst + (long long)zz * sxy + (long long)hy * sx + p;
+                    if (p >= xlo && p + 1 < xhi) {
+                        *reinterpret_cast<double2 *>(d) = v[u];
+                    } else {
+                        if (p >= xlo && p < xhi) d[0] = v[u].x;
+                        if (p + 1 >= xlo && p + 1 < xhi) d[1] = v[u].y;
+                    }
+                }
             }
             did[2 + rs] = true;
         }
-        // z face: the layer plane's rows of this tile -> peer T2 z halo plane
+        // z face: my row of the layer plane -> the peer's z halo plane
         const FusedFace &fz = F.face[2][rs];
         if (fz.active && F.zchunk[rs] == td.z) {
             const int hz = rs == 0 ? 0 : F.s[2] - 1;
-            const int w = xhi - xlo;
-            for (int t = tid; t < w * (yhi - ty0); t += blockDim.x) {
-                const int yy = ty0 + t / w, xx = xlo + t % w;
-                fz.dst[(long long)hz * sxy + (long long)yy * sx + xx] =
-                    T2[(long long)fz.layer * sxy + (long long)yy * sx + xx];
+            if (rowv && pair_in_x(p, sx)) {
+                const double2 v =
+                    *reinterpret_cast<const double2 *>(T2 + (long long)fz.layer * sxy + (long long)yrow * sx + p);
+                double *d = fz.dst + (long long)hz * sxy + (long long)yrow * sx + p;
+                if (p >= xlo && p + 1 < xhi) {
+                    *reinterpret_cast<double2 *>(d) = v;
+                } else {
+                    if (p >= xlo && p < xhi) d[0] = v.x;
+                    if (p + 1 >= xlo && p + 1 < xhi) d[1] = v.y;
+                }
             }
             did[4 + rs] = true;
         }
@@ -629,7 +662,8 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
             f.active = act[a][rs];
             if (f.active) {
                 const int pp = proc_of(g, nb);
-                f.dst = peer[pp];
+                // mode bit 16 (timing experiment, INVALID halos): the face stores go to my own T2
+                f.dst = (g->fused_mode & 16) ? T2 : peer[pp];
                 f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
             }
             const int hb = g->nbr[0][a][rs];   // my halo side rs is filled by my neighbour on side rs
