@@ -75,3 +75,18 @@ def random_field(shape, seed: int) -> np.ndarray:
     """An arbitrary random float64 field (e.g. per-rank halo-test data)."""
     n = int(np.prod(shape))
     return uniform01(seed, np.arange(n, dtype=np.uint64)).reshape(shape) * 2.0 - 1.0
+
+
+SEED_ACOUSTIC = 102
+
+
+def global_acoustic_fields(shapes, seed: int = SEED_ACOUSTIC):
+    """Second workload: random global (P, Vx, Vy, Vz) of the given
+    (z, y, x) shapes: P = 1 + u, V = 0.1*(2u - 1), u per field from its own seed and
+    the field's own global linear index."""
+    out = []
+    for f, (sz, sy, sx) in enumerate(shapes):
+        g = linear_index(np.arange(sx), np.arange(sy), np.arange(sz), sx, sy)
+        u = uniform01(seed * 8 + f, g)
+        out.append(1.0 + u if f == 0 else 0.1 * (2.0 * u - 1.0))
+    return out
