@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["heat", "acoustic"], default="heat",
+                    help="heat: the north-star Fig. 1 step (default); acoustic: the staggered second workload")
     ap.add_argument("--n", type=int, default=512)
     ap.add_argument("--bw", default="16,2,2")
     ap.add_argument("--path", choices=["nccl", "p2p"], default="p2p")
@@ -188,6 +190,8 @@ def run_reference(a):
 
 def main():
     a = parse()
+    if a.workload == "acoustic":
+        return run_acoustic(a)
     if a.impl == "reference":
         return run_reference(a)
 
@@ -385,6 +389,170 @@ def main():
             "clocks": clk, "exposed_halo": exposed, "timeline_ms": timeline, "per_rank_ms": per_rank_ms,
         }
         print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ second workload
+AC_METRIC = "T_eff GB/s per GPU of the staggered acoustic step (P, Vx, Vy, Vz read+written once: 64 B/cell)"
+AC_BYTES_PER_CELL = 64      # effective: 4 fields x (read + write) x 8 B
+AC_V_BYTES_PER_CELL = 56    # compute_V kernel: P, Vx, Vy, Vz read; Vx, Vy, Vz written
+
+
+def acoustic_cpu_baseline(n: int, steps: int = 0, target_s: float = 12.0):
+    """The acoustic oracle as it stands (numpy, one host thread for its elementwise ops) on a bounded
+    sample: a full 512 x 512 extent with 34 z-planes per step, as many steps as fit in ~target_s."""
+    import numpy as np
+    import synthetic_inputs as SI
+    from oracle import acoustic3d as OA
+    nz = min(n, 34)
+    N = (n, n, nz)
+    F = SI.global_acoustic_fields(OA.field_shapes(N, (0, 0, 0)))
+    d = 1.0 / n
+    dt = d / 2.0 / 3 ** 0.5
+    co = OA.coefficients(dt, 1.0, 1.0, d, d, d)
+    times = []
+    t_end = time.perf_counter() + target_s
+    while len(times) < max(2, steps) and (steps or time.perf_counter() < t_end or len(times) < 2):
+        t0 = time.perf_counter()
+        OA.step(*F, (0, 0, 0), co)
+        times.append(time.perf_counter() - t0)
+        if not steps and len(times) >= 50:
+            break
+    t = statistics.median(times)
+    cells = n * n * nz
+    return {"value": AC_BYTES_PER_CELL * cells / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{len(times)} acoustic oracle steps (numpy) on a {n}x{n}x{nz} slab of the {n}^3 workload, "
+                      f"median {t:.3f} s/step, T_eff = 64 B x cells / t"}, times
+
+
+def run_acoustic(a):
+    """--workload acoustic: one step = igg_acoustic_step (compute_V under @hide_communication with
+    update_halo!(Vx, Vy, Vz), then compute_P) on 512^3 cells per GPU, random fields."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = a.n
+    bw = tuple(int(x) for x in a.bw.split(",")) if a.bw != "16,2,2" else (16, 4, 4)
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        cpu, times = acoustic_cpu_baseline(n, steps=a.warmup + a.steps)
+        t = sum(times[a.warmup:])
+        val = cpu["value"]
+        print(json.dumps({
+            "impl": "reference", "metric": AC_METRIC, "value": val, "unit": "GB/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t / a.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"acoustic staggered step Float64, {n}^3 local, CPU oracle sample"},
+            "cpu_baseline": cpu, "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2211_15716_b200 as P
+    from paper_2211_15716_b200 import acoustic3d as ac
+
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dims = tuple(int(x) for x in a.dims.split(",")) if a.dims else (DIMS.get(world) or P.dims_create(world))
+    g = P.init_global_grid(n, n, n, dims=dims, path=a.path, device=local)
+    F = ac.alloc_fields(g)
+    ac.init_random(g, F)
+    d = ac.spacing(g)
+    dt = ac.stable_dt(d)
+    stream = torch.cuda.current_stream()
+
+    def steps(k):
+        for _ in range(k):
+            g.acoustic_step(*F, dt, ac.RHO, ac.K, *d, bw=bw)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    steps(max(a.warmup, 3))
+    barrier()
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.4)
+    g.set_option(P.OPT_PROFILE, 1)
+    g.profile_stencil()
+    l0 = g.kernel_launches()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    steps(a.steps)
+    e1.record(stream)
+    barrier()
+    launches = g.kernel_launches() - l0
+    ms = max_over_ranks(e0.elapsed_time(e1) / a.steps)
+    k_ms, k_n, k_cells = g.profile_stencil()
+    g.set_option(P.OPT_PROFILE, 0)
+    clk = clocks.stop() if clocks else None
+    g.check()
+    per_gpu = AC_BYTES_PER_CELL * n ** 3 / (ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak()
+    k_avg_ms = k_ms / max(k_n, 1)
+    k_bytes = AC_V_BYTES_PER_CELL * k_cells / max(k_n, 1)
+    achieved = k_bytes / (k_avg_ms * 1e-3) / 1e9 if k_n else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None, "traffic": None,
+                "kernel": "acoustic_v_kernel (" + ("inner box" if world > 1 else "whole box") + ")",
+                "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_avg_ms, "launches": k_n,
+                "peak_source": peak_src, "share_of_step": k_avg_ms * (k_n / a.steps) / ms if k_n else None}
+
+    e2e = None
+    if not a.no_e2e:   # pinned host fields -> device, nt steps through the public API, fields -> host
+        nt = 20
+        host = [torch.empty(f[0].shape, dtype=torch.float64).pin_memory() for f in F]
+        for h, f in zip(host, F):
+            h.copy_(f[0])
+        barrier()
+        e0.record(stream)
+        for h, f in zip(host, F):
+            f[0].copy_(h, non_blocking=True)
+        steps(nt)
+        for h, f in zip(host, F):
+            h.copy_(f[0], non_blocking=True)
+        e1.record(stream)
+        barrier()
+        t_call = max_over_ranks(e0.elapsed_time(e1))
+        nbytes = sum(h.numel() * 8 for h in host)
+        e2e = {"value": world * AC_BYTES_PER_CELL * n ** 3 * nt / (t_call * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": nbytes / nt, "d2h_bytes_per_step": nbytes / nt,
+               "call": f"H2D P,Vx,Vy,Vz from pinned host + {nt} igg_acoustic_step + D2H all four", "nt_per_call": nt,
+               "ms_per_call": t_call}
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu, _ = acoustic_cpu_baseline(n)
+    g.finalize()
+    if rank == 0:
+        print(json.dumps({
+            "metric": AC_METRIC, "value": per_gpu * world, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
+            "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"staggered acoustic step Float64 (P {n}^3, Vx {n + 1}x{n}x{n}, Vy, Vz) per GPU, "
+                                   f"dims {dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw}",
+                       "n_local": n, "dims": list(dims), "bw": list(bw), "path": a.path,
+                       "t_eff_per_gpu_gbs": per_gpu, "cells_per_s": world * n ** 3 / (ms * 1e-3),
+                       "l2": "inputs 4 x 1 GiB per GPU > 126 MB L2; no flush needed",
+                       "frac_of_measured_peak": per_gpu / peak},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}))
     if world > 1:
         dist.destroy_process_group()
 

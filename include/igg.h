@@ -209,6 +209,23 @@ typedef void (*igg_region_fn)(void *user, int local_rank, const int lo[3], const
 igg_status igg_hide_communication(igg_grid *grid, const int bw[3], igg_region_fn fn, void *user,
                                   const igg_field *fields, int nfields, igg_stream_t stream);
 
+/* ------------------------------------------------------------------ second workload
+ * One leapfrog step of linear acoustics on the staggered grid -- the multi-field staggered kind of
+ * solver the paper scales -- in the paper's stencil notation:
+ *   @hide_communication bw begin compute_V!; update_halo!(Vx, Vy, Vz) end; compute_P!
+ *   compute_V: Vx[k,j,i] -= cVx*(P[k,j,i] - P[k,j,i-1]) on i in [1,nx), j in [1,ny-1), k in [1,nz-1)
+ *              (Vy, Vz likewise along their own axis)
+ *   compute_P: P -= cP*((((Vx[i+1]-Vx[i])*rx) + ((Vy[j+1]-Vy[j])*ry)) + ((Vz[k+1]-Vz[k])*rz)), every cell
+ *   cV_d = (dt/rho)/d_d, cP = dt*K, r_d = 1.0/d_d; binary64, no FMA (readings A1-A3).
+ * P, Vx, Vy, Vz: local_ranks device pointers each; P (nz,ny,nx), Vx (nz,ny,nx+1), Vy (nz,ny+1,nx),
+ * Vz (nz+1,ny,nx), x fastest (config B:10's field set).  bw: boundary widths of the velocity step;
+ * an exchanged axis needs b_d >= 3 (the staggered overlap, IGG_E_WIDTH); {0,0,0} = sequential.
+ * Stream-ordered on `stream`.  Errors: IGG_E_ARG (null pointer, rho or a spacing zero, n_d < 3),
+ * IGG_E_WIDTH, IGG_E_STATE. */
+igg_status igg_acoustic_step(igg_grid *grid, double *const *P, double *const *Vx, double *const *Vy,
+                             double *const *Vz, double dt, double rho, double K, double dx, double dy,
+                             double dz, const int bw[3], igg_stream_t stream);
+
 /* Fig. 1 end to end from HOST memory: copies T (initial, local_ranks*nx*ny*nz
  * doubles, rank-major) and Ci to the device, sets T2 = copy(T), runs nt heat
  * steps with swap, and copies the final T back into T_host.

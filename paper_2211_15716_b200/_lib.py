@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libigg.so")
+# IGG_LIBRARY: load another build of the same ABI (A/B timing of two builds on one box)
+SO_PATH = os.environ.get("IGG_LIBRARY") or os.path.join(HERE, "libigg.so")
 
 c_int_p = ctypes.POINTER(ctypes.c_int)
 c_ll_p = ctypes.POINTER(ctypes.c_longlong)
@@ -75,6 +76,9 @@ SIGNATURES = {
     "igg_check": [ctypes.c_void_p],
     "igg_hide_communication": [ctypes.c_void_p, c_int_p, REGION_FN, ctypes.c_void_p, ctypes.POINTER(igg_field),
                                ctypes.c_int, ctypes.c_void_p],
+    "igg_acoustic_step": [ctypes.c_void_p, c_dbl_pp, c_dbl_pp, c_dbl_pp, c_dbl_pp, ctypes.c_double,
+                          ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                          c_int_p, ctypes.c_void_p],
     "igg_gather": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
     "igg_profile_stencil": [ctypes.c_void_p, c_dbl_p, c_ll_p, c_ll_p],
     "igg_profile_timeline": [ctypes.c_void_p, c_dbl_p],

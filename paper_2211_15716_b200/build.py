@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libigg.so")
-SOURCES = ["topology.cpp", "plan.cpp", "grid.cpp", "kernels.cu", "fused.cu"]
+SOURCES = ["topology.cpp", "plan.cpp", "grid.cpp", "kernels.cu", "fused.cu", "acoustic.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,0 +1,184 @@
+// acoustic.cu -- the second workload: one leapfrog step of
+// linear acoustics on the implicit global staggered grid, the multi-field
+// staggered kind of solver the paper scales, written in the
+// @inn/@all/@d_xi/@d_xa form of its stencil notation:
+//
+//   compute_V:  Vx[k,j,i] = Vx[k,j,i] - cVx*(P[k,j,i] - P[k,j,i-1])    (likewise Vy, Vz)
+//               on i in [1,nx) and the inner layers [1,n-1) of the other axes
+//   update_halo!(Vx, Vy, Vz)                                            (staggered: nx+1 ...)
+//   compute_P:  P = P - cP*((((Vx[i+1]-Vx[i])*rx) + ((Vy[j+1]-Vy[j])*ry)) + ((Vz[k+1]-Vz[k])*rz))
+//               on every cell (@all)
+//
+// with cV_d = (dt/rho)/d_d, cP = dt*K, r_d = 1/d_d (reading A2).  Every
+// operation is an explicitly rounded binary64 op (no FMA contraction), so the
+// result is bit-identical to the oracle (oracle/acoustic3d.py) and to itself
+// under any decomposition.
+//
+// Both kernels are HBM-bound z-sweeps: one thread per x cell, a warp per row
+// segment of 32 cells, 4 rows per CTA, a chunk of planes per CTA with the
+// z-neighbour in a register queue and the next plane's loads issued one
+// iteration ahead.  Algorithmic bytes per cell: compute_V reads P, Vx, Vy, Vz and
+// writes Vx, Vy, Vz (56 B); compute_P reads P, Vx, Vy, Vz and writes P (40 B).
+#include "igg_internal.h"
+
+namespace igg {
+namespace {
+
+constexpr int kAcTY = 4;    // rows per CTA (one warp each)
+constexpr int kAcKC = 32;   // planes per CTA
+
+__device__ __forceinline__ double ldg(const double *p) { return __ldg(p); }
+
+// V -= c*(p - pm)
+__device__ __forceinline__ double vupd(double v, double c, double p, double pm) {
+    return __dsub_rn(v, __dmul_rn(c, __dsub_rn(p, pm)));
+}
+
+// compute_V on the box [lo, hi) of the velocity cells (x in [1,nx), y in [1,ny), z in [1,nz)):
+// component d is written where its own range holds (module comment).
+__global__ void __launch_bounds__(32 * kAcTY) acoustic_v_kernel(const __grid_constant__ AcousticFields F,
+                                                                const __grid_constant__ AcousticCoef C,
+                                                                int3 lo, int3 hi) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int i = lo.x + blockIdx.x * 32 + lane;
+    const int j = lo.y + blockIdx.y * kAcTY + warp;
+    const int z0 = lo.z + blockIdx.z * kAcKC;
+    const int z1 = min(z0 + kAcKC, hi.z);
+    if (j >= hi.y) return;   // warp-uniform
+    const bool act = i < hi.x;
+    const int nx = F.n[0], ny = F.n[1], nz = F.n[2];
+    const long long sxyP = (long long)nx * ny;
+    const long long sxX = nx + 1, sxyX = (long long)(nx + 1) * ny;
+    const long long sxyY = (long long)nx * (ny + 1);
+    const bool wx = act && j < ny - 1, wy = act && i < nx - 1, wxy = act && i < nx - 1 && j < ny - 1;
+    const double *__restrict__ P = F.P;
+    double *__restrict__ Vx = F.Vx;
+    double *__restrict__ Vy = F.Vy;
+    double *__restrict__ Vz = F.Vz;
+    long long ip = (long long)z0 * sxyP + (long long)j * nx + i;   // P, Vz (same x/y strides)
+    long long ix = (long long)z0 * sxyX + (long long)j * sxX + i;  // Vx
+    long long iy = (long long)z0 * sxyY + (long long)j * nx + i;   // Vy
+    double pzm = act ? ldg(P + ip - sxyP) : 0.0;
+    // current plane's loads; the next plane's are issued before this plane's math
+    double p = 0.0, pym = 0.0, pxm = 0.0, vx = 0.0, vy = 0.0, vz = 0.0;
+    if (act && z0 < z1) {
+        p = ldg(P + ip);
+        pym = ldg(P + ip - nx);
+        if (lane == 0) pxm = ldg(P + ip - 1);
+        vx = Vx[ix];
+        vy = Vy[iy];
+        vz = Vz[ip];
+    }
+    for (int z = z0; z < z1; ++z) {
+        const bool more = act && z + 1 < z1;
+        double np = 0.0, npym = 0.0, npxm = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
+        if (more) {
+            np = ldg(P + ip + sxyP);
+            npym = ldg(P + ip + sxyP - nx);
+            if (lane == 0) npxm = ldg(P + ip + sxyP - 1);
+            nvx = Vx[ix + sxyX];
+            nvy = Vy[iy + sxyY];
+            nvz = Vz[ip + sxyP];
+        }
+        double xm = __shfl_up_sync(0xffffffffu, p, 1);
+        if (lane == 0) xm = pxm;
+        const bool zin = z < nz - 1;
+        if (wx && zin) Vx[ix] = vupd(vx, C.cV[0], p, xm);
+        if (wy && zin) Vy[iy] = vupd(vy, C.cV[1], p, pym);
+        if (wxy) Vz[ip] = vupd(vz, C.cV[2], p, pzm);
+        pzm = p;
+        p = np;
+        pym = npym;
+        pxm = npxm;
+        vx = nvx;
+        vy = nvy;
+        vz = nvz;
+        ip += sxyP;
+        ix += sxyX;
+        iy += sxyY;
+    }
+}
+
+// compute_P on every cell [0,nx) x [0,ny) x [z-chunk)
+__global__ void __launch_bounds__(32 * kAcTY) acoustic_p_kernel(const __grid_constant__ AcousticFields F,
+                                                                const __grid_constant__ AcousticCoef C) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nx = F.n[0], ny = F.n[1], nz = F.n[2];
+    const int i = blockIdx.x * 32 + lane;
+    const int j = blockIdx.y * kAcTY + warp;
+    const int z0 = blockIdx.z * kAcKC;
+    const int z1 = min(z0 + kAcKC, nz);
+    if (j >= ny) return;   // warp-uniform
+    const bool act = i < nx;
+    const bool edge = act && (lane == 31 || i + 1 == nx);   // loads its x+1 face itself
+    const long long sxyP = (long long)nx * ny;
+    const long long sxX = nx + 1, sxyX = (long long)(nx + 1) * ny;
+    const long long sxyY = (long long)nx * (ny + 1);
+    double *__restrict__ P = F.P;
+    const double *__restrict__ Vx = F.Vx;
+    const double *__restrict__ Vy = F.Vy;
+    const double *__restrict__ Vz = F.Vz;
+    long long ip = (long long)z0 * sxyP + (long long)j * nx + i;
+    long long ix = (long long)z0 * sxyX + (long long)j * sxX + i;
+    long long iy = (long long)z0 * sxyY + (long long)j * nx + i;
+    double vzk = act ? ldg(Vz + ip) : 0.0;
+    double p = 0.0, vx = 0.0, vxe = 0.0, vy = 0.0, vyp = 0.0, vzp = 0.0;
+    if (act && z0 < z1) {
+        p = P[ip];
+        vx = ldg(Vx + ix);
+        if (edge) vxe = ldg(Vx + ix + 1);
+        vy = ldg(Vy + iy);
+        vyp = ldg(Vy + iy + nx);
+        vzp = ldg(Vz + ip + sxyP);
+    }
+    for (int z = z0; z < z1; ++z) {
+        const bool more = act && z + 1 < z1;
+        double np = 0.0, nvx = 0.0, nvxe = 0.0, nvy = 0.0, nvyp = 0.0, nvzp = 0.0;
+        if (more) {
+            np = P[ip + sxyP];
+            nvx = ldg(Vx + ix + sxyX);
+            if (edge) nvxe = ldg(Vx + ix + sxyX + 1);
+            nvy = ldg(Vy + iy + sxyY);
+            nvyp = ldg(Vy + iy + sxyY + nx);
+            nvzp = ldg(Vz + ip + 2 * sxyP);
+        }
+        double vxp = __shfl_down_sync(0xffffffffu, vx, 1);
+        if (edge) vxp = vxe;
+        if (act) {
+            const double div = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(vxp, vx), C.r[0]),
+                                                   __dmul_rn(__dsub_rn(vyp, vy), C.r[1])),
+                                         __dmul_rn(__dsub_rn(vzp, vzk), C.r[2]));
+            P[ip] = __dsub_rn(p, __dmul_rn(C.cP, div));
+        }
+        vzk = vzp;
+        p = np;
+        vx = nvx;
+        vxe = nvxe;
+        vy = nvy;
+        vyp = nvyp;
+        vzp = nvzp;
+        ip += sxyP;
+        ix += sxyX;
+        iy += sxyY;
+    }
+}
+
+}  // namespace
+
+void launch_acoustic_v(const AcousticFields &f, const AcousticCoef &c, const int lo[3], const int hi[3],
+                       cudaStream_t s) {
+    const int wx = hi[0] - lo[0], wy = hi[1] - lo[1], wz = hi[2] - lo[2];
+    if (wx <= 0 || wy <= 0 || wz <= 0) return;
+    const dim3 grid((wx + 31) / 32, (wy + kAcTY - 1) / kAcTY, (wz + kAcKC - 1) / kAcKC);
+    acoustic_v_kernel<<<grid, 32 * kAcTY, 0, s>>>(f, c, make_int3(lo[0], lo[1], lo[2]),
+                                                  make_int3(hi[0], hi[1], hi[2]));
+    IGG_CUDA(cudaGetLastError());
+}
+
+void launch_acoustic_p(const AcousticFields &f, const AcousticCoef &c, cudaStream_t s) {
+    const dim3 grid((f.n[0] + 31) / 32, (f.n[1] + kAcTY - 1) / kAcTY, (f.n[2] + kAcKC - 1) / kAcKC);
+    acoustic_p_kernel<<<grid, 32 * kAcTY, 0, s>>>(f, c);
+    IGG_CUDA(cudaGetLastError());
+}
+
+}  // namespace igg

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <array>
 #include <cstring>
+#include <type_traits>
 
 #include "igg_internal.h"
 
@@ -56,14 +57,6 @@ __device__ __forceinline__ double cell(double c, double xm, double xp, double ym
     const double lap =
         __dadd_rn(__dadd_rn(__dmul_rn(d2x, k.rdx2), __dmul_rn(d2y, k.rdy2)), __dmul_rn(d2z, k.rdz2));
     return __dadd_rn(c, __dmul_rn(k.dt, __dmul_rn(__dmul_rn(k.lam, ci), lap)));
-}
-
-// face index of a cell on a face normal to axis a.  y- and z-faces: x fastest
-// (z*sx + x, y*sx + x).  The x-face is stored z fastest (y*sz + z)
-// so a tile's x-face cells of one chunk are contiguous runs (sender and
-// receiver of the fused path share this layout).
-__device__ __forceinline__ long long fidx(int a, int x, int y, int z, const int *s) {
-    return a == 0 ? (long long)y * s[2] + z : (a == 1 ? (long long)z * s[0] + x : (long long)y * s[0] + x);
 }
 
 __device__ __forceinline__ void contribute(const FusedParams &F, int a, int rs, int c) {
@@ -117,67 +110,18 @@ constexpr int kFKC = 64;   // longest z-chunk
 
 }  // namespace
 
-// One launch over all tiles, the 1-GPU loop unchanged.  A CTA whose tile holds
-// send-layer cells (x layer of its rows, a y layer row, or a z layer plane in
-// its chunk) re-reads them from T2 after its sweep (its own just-written, L2-hot
-// values) and stores them into the receivers' slots as contiguous runs, then
-// counts itself on the (face, chunk) counters.  Keeping the face work out of the
-// z loop keeps the loop's instruction stream identical to the 1-GPU kernel.
-template <bool XS>   // XS: capture the x send layer in smem during the sweep (else re-read T2)
-__global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
-    __shared__ double2 sT[kFD][32 * kFTY];
-    __shared__ double2 sC[kFD][32 * kFTY];
-    __shared__ double xs[XS ? kFTY : 1][XS ? kFKC : 1];   // my rows' x send-layer cells over the chunk
-    // tile from the block index (x-tiles fastest, then y-tiles, then chunks in visit order);
-    // the last chunks' tiles are re-ordered, face tiles first, from the parameter table
-    int4 td;
-    {
-        const int b = blockIdx.x;
-        if (b < F.bmain) {
-            td.x = b % F.xtiles;
-            const int r = b / F.xtiles;
-            td.y = r % F.ytiles;
-            td.z = r / F.ytiles;
-        } else {
-            const unsigned e = F.tail[b - F.bmain];
-            td.x = e & 15u;
-            td.y = (e >> 4) & 1023u;
-            td.z = F.bmain / (F.xtiles * F.ytiles) + (int)(e >> 14);
-        }
-    }
-    const int2 zr = chunk_range(F, td.z);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int sx = F.s[0], sy = F.s[1];
-    const int y = 1 + td.y * kFTY + warp;
-    const int p = td.x * 64 + 2 * lane;
-    const bool pair_in = y < sy - 1 && p < sx;
-    const bool w0 = pair_in && p >= 1 && p < sx - 1;
-    const bool w1 = pair_in && p + 1 >= 1 && p + 1 < sx - 1;
-    const int zs = zr.x, ze = zr.y;
-    const long long sxy = (long long)sx * sy;
+// The z sweep of one tile (cp.async ring of kFD planes of T and Ci, x neighbours by shuffle, z by a
+// register queue).  CAP: the lane xl holding an x send-layer cell of its row (cell xodd of its pair)
+// stores it straight into the neighbour's halo every plane (xdst + i), while the receiver's own
+// stores of the same 32-B sector (its cells 1-3 or s-4..s-2) are still in its L2.
+template <bool CAP>
+__device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[32 * kFTY], double2 (*sC)[32 * kFTY],
+                                            double *xdst, int tid, int lane, int zs, int ze, long long i,
+                                            long long sxy, int sx, bool pair_in, bool w0, bool w1, int xl,
+                                            bool xodd) {
     const double *__restrict__ T = F.T;
     const double *__restrict__ Ci = F.Ci;
     double *__restrict__ T2 = F.T2;
-    bool face_tile = false;   // this tile holds send-layer cells
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        const int xl = F.face[0][rs].layer, yl = F.face[1][rs].layer;
-        face_tile |= F.face[0][rs].active && xl >= max(td.x * 64, 1) && xl < min(td.x * 64 + 64, sx - 1);
-        face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
-        face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
-    }
-    long long i = (long long)zs * sxy + (long long)y * sx + p;
-    // the lane holding an x send-layer cell of my row (-1: none) and which of its two cells
-    int xlane = -1;
-    bool xodd = false;
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        const int L = F.face[0][rs].layer;
-        if (F.face[0][rs].active && pair_in && ((w0 && p == L) || (w1 && p + 1 == L))) {
-            xlane = lane;
-            xodd = p + 1 == L;
-        }
-    }
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
@@ -190,41 +134,73 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
     int slot = 0;
-    for (int z = zs; z < ze; ++z, i += sxy) {
-        cp_wait<kFD - 1>();
-        double2 ym = zero2, yp = zero2;
-        if (pair_in) {
-            ym = ldg2f(T + i - sx);
-            yp = ldg2f(T + i + sx);
+    {
+#pragma unroll 2
+        for (int z = zs; z < ze; ++z, i += sxy) {
+            cp_wait<kFD - 1>();
+            double2 ym = zero2, yp = zero2;
+            if (pair_in) {
+                ym = ldg2f(T + i - sx);
+                yp = ldg2f(T + i + sx);
+            }
+            const double2 zp = sT[slot][tid];
+            const double2 ci = sC[slot][tid];
+            double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
+            double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+            if (lane == 0 && w0) xm = __ldg(T + i - 1);
+            if (lane == 31 && w1) xp = __ldg(T + i + 2);
+            const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
+            const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
+            if (w0 && w1) {   // plain stores (streaming stores measured no faster; face cells stay in L2)
+                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+            } else {
+                if (w0) T2[i] = r0;
+                if (w1) T2[i + 1] = r1;
+            }
+            if (CAP && lane == xl) xdst[i] = xodd ? r1 : r0;
+            zm = c;
+            c = zp;
+            if (pair_in && z + kFD < ze) {
+                cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
+                cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
+            }
+            cp_commit();
+            slot = slot + 1 == kFD ? 0 : slot + 1;
         }
-        const double2 zp = sT[slot][tid];
-        const double2 ci = sC[slot][tid];
-        double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
-        double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
-        if (lane == 0 && w0) xm = __ldg(T + i - 1);
-        if (lane == 31 && w1) xp = __ldg(T + i + 2);
-        const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
-        const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (w0 && w1) {   // plain stores (streaming stores measured no faster; face cells stay in L2)
-            *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
-        } else {
-            if (w0) T2[i] = r0;
-            if (w1) T2[i + 1] = r1;
-        }
-        if (XS && lane == xlane) xs[warp][z - zs] = xodd ? r1 : r0;   // predicated, no branch
-        zm = c;
-        c = zp;
-        if (pair_in && z + kFD < ze) {
-            cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
-            cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
-        }
-        cp_commit();
-        slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
-    if (!face_tile) return;   // CTA-uniform
+}
+
+// tile of this CTA from the block index (x-tiles fastest, then y-tiles, then chunks in visit
+// order); the last chunks' tiles are re-ordered, face tiles first, from the parameter table
+__device__ __forceinline__ int4 fused_tile(const FusedParams &F) {
+    int4 td;
+    const int b = blockIdx.x;
+    if (b < F.bmain) {
+        td.x = b % F.xtiles;
+        const int r = b / F.xtiles;
+        td.y = r % F.ytiles;
+        td.z = r / F.ytiles;
+    } else {
+        const unsigned e = F.tail[b - F.bmain];
+        td.x = e & 15u;
+        td.y = (e >> 4) & 1023u;
+        td.z = F.bmain / (F.xtiles * F.ytiles) + (int)(e >> 14);
+    }
+    td.w = 0;
+    return td;
+}
+
+// The face work of a face tile after its sweep (called CTA-uniformly).  Each warp copies its own
+// row's part of every face the tile holds, loads of a batch before its stores.
+template <bool XS>
+__device__ __forceinline__ void fused_faces(const FusedParams &F, int4 td, int zs, int ze) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sx = F.s[0], sy = F.s[1];
+    const int p = td.x * 64 + 2 * lane;
+    const long long sxy = (long long)sx * sy;
+    const double *__restrict__ T2 = F.T2;
     __syncthreads();          // the CTA's T2 stores are visible to the CTA
-    const int nz = ze - zs;
     const int tx0 = td.x * 64, ty0 = 1 + td.y * kFTY;
     const int xlo = max(tx0, 1), xhi = min(tx0 + 64, sx - 1);   // inner x of this tile
     const int yhi = min(ty0 + kFTY, sy - 1);
@@ -245,12 +221,13 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
 #pragma unroll
                 for (int u = 0; u < kFKC / 32; ++u) {
                     const int zz = zs + lane + 32 * u;
-                    v[u] = zz < ze ? T2[(long long)zz * sxy + (long long)yrow * sx + fx.layer] : 0.0;
+                    v[u] = (!XS && zz < ze) ? T2[(long long)zz * sxy + (long long)yrow * sx + fx.layer] : 0.0;
                 }
 #pragma unroll
                 for (int u = 0; u < kFKC / 32; ++u) {
                     const int zz = zs + lane + 32 * u;
-                    if (zz < ze) fx.dst[(long long)zz * sxy + (long long)yrow * sx + hx] = v[u];
+                    if (XS || zz >= ze) continue;   // XS: stored from the sweep
+                    fx.dst[(long long)zz * sxy + (long long)yrow * sx + hx] = v[u];
                 }
             }
             did[rs] = true;
@@ -315,6 +292,55 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     if (tid == 0)
         for (int f = 0; f < 6; ++f)
             if (did[f]) contribute(F, f >> 1, f & 1, f < 4 ? td.z : 0);
+}
+
+// One launch over all tiles, the 1-GPU loop unchanged.  A CTA whose tile holds
+// send-layer cells (x layer of its rows, a y layer row, or a z layer plane in
+// its chunk) re-reads them from T2 after its sweep (its own just-written
+// values) and stores them into the receivers' halos, then counts itself on the
+// (face, chunk) counters (fused_faces).  Keeping the face work out of the z loop
+// keeps the loop's instruction stream identical to the 1-GPU kernel.
+template <bool XS>   // XS: the x send layer goes to the neighbour from the sweep (else re-read from T2)
+__global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
+    __shared__ double2 sT[kFD][32 * kFTY];
+    __shared__ double2 sC[kFD][32 * kFTY];
+    const int4 td = fused_tile(F);
+    const int2 zr = chunk_range(F, td.z);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sx = F.s[0], sy = F.s[1];
+    const int y = 1 + td.y * kFTY + warp;
+    const int p = td.x * 64 + 2 * lane;
+    const bool pair_in = y < sy - 1 && p < sx;
+    const bool w0 = pair_in && p >= 1 && p < sx - 1;
+    const bool w1 = pair_in && p + 1 >= 1 && p + 1 < sx - 1;
+    const int zs = zr.x, ze = zr.y;
+    const long long sxy = (long long)sx * sy;
+    bool face_tile = false;   // this tile holds send-layer cells
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        const int xl = F.face[0][rs].layer, yl = F.face[1][rs].layer;
+        face_tile |= F.face[0][rs].active && xl >= max(td.x * 64, 1) && xl < min(td.x * 64 + 64, sx - 1);
+        face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
+        face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
+    }
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+    // XS: the x send-layer cell of my row (lane xl, cell xodd of its pair) goes to the neighbour
+    // plane by plane from the sweep (xdst + i = its halo cell of my row and plane)
+    int xl = -1;
+    bool xodd = false;
+    double *xdst = nullptr;
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        const int L = F.face[0][rs].layer - td.x * 64;
+        if (XS && !F.nostore && F.face[0][rs].active && y < sy - 1 && L >= 0 && L < 64 && L + td.x * 64 >= 1 &&
+            L + td.x * 64 < sx - 1) {
+            xl = L >> 1;
+            xodd = L & 1;
+            if (lane == xl) xdst = F.face[0][rs].dst + ((rs == 0 ? 0 : sx - 1) - p);
+        }
+    }
+    fused_sweep<XS>(F, sT, sC, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd);
+    if (face_tile) fused_faces<XS>(F, td, zs, ze);   // CTA-uniform
 }
 
 // Face cells the stencil does not compute (on other axes' halo/boundary layers):

@@ -7,6 +7,7 @@
 // transfers are performed on non-blocking high-priority streams"  PAPER.md:94.
 // @hide_communication (16,2,2): PAPER.md:75.
 #include <algorithm>
+#include <functional>
 #include <cstring>
 
 #include "igg_internal.h"
@@ -642,12 +643,15 @@ IGG_API igg_status igg_heat_step(igg_grid *g, double *const *T2, const double *c
     IGG_CATCH
 }
 
-IGG_API igg_status igg_hide_communication(igg_grid *g, const int bw_in[3], igg_region_fn fn, void *user,
-                                          const igg_field *fields, int nfields, igg_stream_t stream) {
-    IGG_TRY
-    igg::check_live(g, "igg_hide_communication");
-    if (!fn || !fields || nfields < 1) fail(IGG_E_ARG, "igg_hide_communication: bad argument");
-    cudaStream_t s = (cudaStream_t)stream;
+namespace igg {
+using RegionFn = std::function<void(int lr, const int lo[3], const int hi[3], cudaStream_t st)>;
+
+// @hide_communication bw begin <step>; update_halo!(fields) end for any stencil given as a
+// box callback: the six boundary slabs of [1, n-1)^3 first on
+// the high-priority comm stream, the exchange behind them there, the inner box concurrently on the
+// low-priority stream; both joined to s.
+static void hide_comm(igg_grid *g, const int bw_in[3], const RegionFn &fn, const igg_field *fields, int nfields,
+                      cudaStream_t s, const char *who) {
     const int zero[3] = {0, 0, 0};
     const int *bw = bw_in ? bw_in : zero;
     bool exch[3] = {false, false, false};
@@ -658,14 +662,14 @@ IGG_API igg_status igg_hide_communication(igg_grid *g, const int bw_in[3], igg_r
     int lo[3], hi[3];
     bool degenerate = false;
     for (int a = 0; a < 3; ++a) {
-        if (bw[a] < 0) fail(IGG_E_ARG, "igg_hide_communication: negative boundary width");
+        if (bw[a] < 0) fail(IGG_E_ARG, std::string(who) + ": negative boundary width");
         if (!seq && exch[a])
             for (int f = 0; f < nfields; ++f) {
-                igg::HaloSpec hs;
-                if (!igg::halo_spec(g->n[a], g->o[a], fields[f].size[a], &hs))
-                    fail(IGG_E_STAGGER, "igg_hide_communication: field size out of range");
+                HaloSpec hs;
+                if (!halo_spec(g->n[a], g->o[a], fields[f].size[a], &hs))
+                    fail(IGG_E_STAGGER, std::string(who) + ": field size out of range");
                 if (hs.h > 0 && bw[a] < hs.ol)
-                    fail(IGG_E_WIDTH, "igg_hide_communication: boundary width " + std::to_string(bw[a]) +
+                    fail(IGG_E_WIDTH, std::string(who) + ": boundary width " + std::to_string(bw[a]) +
                                           " on axis " + std::to_string(a) + " is below a field overlap " +
                                           std::to_string(hs.ol));
             }
@@ -678,11 +682,11 @@ IGG_API igg_status igg_hide_communication(igg_grid *g, const int bw_in[3], igg_r
     IGG_CUDA(cudaEventRecord(g->ev_start, s));
     IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
     if (seq || degenerate) {
-        for (int lr = 0; lr < g->nlocal; ++lr) fn(user, lr, full_lo, full_hi, (igg_stream_t)g->s_comm);
-        igg::exchange(g, fields, nfields, g->s_comm);
+        for (int lr = 0; lr < g->nlocal; ++lr) fn(lr, full_lo, full_hi, g->s_comm);
+        exchange(g, fields, nfields, g->s_comm);
         IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
         IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
-        return IGG_OK;
+        return;
     }
     IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
     const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
@@ -693,14 +697,84 @@ IGG_API igg_status igg_hide_communication(igg_grid *g, const int bw_in[3], igg_r
     for (int lr = 0; lr < g->nlocal; ++lr)
         for (int k = 0; k < 6; ++k) {
             const int a0[3] = {slab[k][0], slab[k][2], slab[k][4]}, a1[3] = {slab[k][1], slab[k][3], slab[k][5]};
-            if (a1[0] > a0[0] && a1[1] > a0[1] && a1[2] > a0[2]) fn(user, lr, a0, a1, (igg_stream_t)g->s_comm);
+            if (a1[0] > a0[0] && a1[1] > a0[1] && a1[2] > a0[2]) fn(lr, a0, a1, g->s_comm);
         }
-    for (int lr = 0; lr < g->nlocal; ++lr) fn(user, lr, lo, hi, (igg_stream_t)g->s_inner);
-    igg::exchange(g, fields, nfields, g->s_comm);
+    for (int lr = 0; lr < g->nlocal; ++lr) fn(lr, lo, hi, g->s_inner);
+    exchange(g, fields, nfields, g->s_comm);
     IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
     IGG_CUDA(cudaEventRecord(g->ev_inner, g->s_inner));
     IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
     IGG_CUDA(cudaStreamWaitEvent(s, g->ev_inner, 0));
+}
+}  // namespace igg
+
+IGG_API igg_status igg_hide_communication(igg_grid *g, const int bw_in[3], igg_region_fn fn, void *user,
+                                          const igg_field *fields, int nfields, igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_hide_communication");
+    if (!fn || !fields || nfields < 1) fail(IGG_E_ARG, "igg_hide_communication: bad argument");
+    igg::hide_comm(
+        g, bw_in,
+        [&](int lr, const int lo[3], const int hi[3], cudaStream_t st) { fn(user, lr, lo, hi, (igg_stream_t)st); },
+        fields, nfields, (cudaStream_t)stream, "igg_hide_communication");
+    IGG_CATCH
+}
+
+// second workload (acoustic.cu): compute_V under @hide_communication with
+// update_halo!(Vx, Vy, Vz), then compute_P on every cell
+IGG_API igg_status igg_acoustic_step(igg_grid *g, double *const *P, double *const *Vx, double *const *Vy,
+                                     double *const *Vz, double dt, double rho, double K, double dx, double dy,
+                                     double dz, const int bw[3], igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_acoustic_step");
+    if (!P || !Vx || !Vy || !Vz) fail(IGG_E_ARG, "igg_acoustic_step: null field list");
+    if (!(rho != 0.0) || !(dx != 0.0) || !(dy != 0.0) || !(dz != 0.0))
+        fail(IGG_E_ARG, "igg_acoustic_step: rho and the spacings must be non-zero");
+    for (int a = 0; a < 3; ++a)
+        if (g->n[a] < 3) fail(IGG_E_ARG, "igg_acoustic_step: every local size must be >= 3");
+    cudaStream_t s = (cudaStream_t)stream;
+    igg::AcousticCoef c;
+    const double adt = dt / rho;   // reading A2: cV_d = (dt/rho)/d_d, cP = dt*K, r_d = 1/d_d
+    c.cV[0] = adt / dx;
+    c.cV[1] = adt / dy;
+    c.cV[2] = adt / dz;
+    c.cP = dt * K;
+    c.r[0] = 1.0 / dx;
+    c.r[1] = 1.0 / dy;
+    c.r[2] = 1.0 / dz;
+    const long long n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
+    std::vector<igg_field> fl(3 * g->nlocal);
+    std::vector<igg::AcousticFields> af(g->nlocal);
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        if (!P[lr] || !Vx[lr] || !Vy[lr] || !Vz[lr]) fail(IGG_E_ARG, "igg_acoustic_step: null field pointer");
+        fl[3 * lr + 0] = igg_field{Vx[lr], {n0 + 1, n1, n2}};
+        fl[3 * lr + 1] = igg_field{Vy[lr], {n0, n1 + 1, n2}};
+        fl[3 * lr + 2] = igg_field{Vz[lr], {n0, n1, n2 + 1}};
+        af[lr] = igg::AcousticFields{P[lr], Vx[lr], Vy[lr], Vz[lr], {g->n[0], g->n[1], g->n[2]}};
+    }
+    // the velocity cells are [1, n) per axis: a box ending at n-1 (the stencil box's end) extends to n
+    igg::hide_comm(
+        g, bw,
+        [&](int lr, const int lo[3], const int hi[3], cudaStream_t st) {
+            int h[3];
+            bool full = true;
+            for (int a = 0; a < 3; ++a) {
+                h[a] = hi[a] == g->n[a] - 1 ? g->n[a] : hi[a];
+                full = full && lo[a] == 1 && h[a] == g->n[a];
+            }
+            // OPT_PROFILE brackets the main velocity launch (the inner box, or the whole box)
+            const bool main_box = st == g->s_inner || full;
+            if (main_box) igg::prof_begin(g, st);
+            igg::launch_acoustic_v(af[lr], c, lo, h, st);
+            if (main_box)
+                igg::prof_end(g, st, (long long)(h[0] - lo[0]) * (h[1] - lo[1]) * (h[2] - lo[2]));
+            g->launches++;
+        },
+        fl.data(), 3, s, "igg_acoustic_step");
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        igg::launch_acoustic_p(af[lr], c, s);
+        g->launches++;
+    }
     IGG_CATCH
 }
 

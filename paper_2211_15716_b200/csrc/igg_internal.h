@@ -195,6 +195,22 @@ void launch_field_max(const double *const *ptrs, int n, long long count, double 
                       int scratch_len, double *out_dev, cudaStream_t s);
 int field_max_scratch_len();
 
+// second workload (acoustic.cu): one rank's staggered fields P (n), Vx (n+1 in x), Vy, Vz
+struct AcousticFields {
+    double *P, *Vx, *Vy, *Vz;
+    int n[3];
+};
+struct AcousticCoef {
+    double cV[3];   // (dt/rho)/d
+    double cP;      // dt*K
+    double r[3];    // 1/d
+};
+// compute_V on the velocity box [lo, hi) (x in [1,nx), y in [1,ny), z in [1,nz))
+void launch_acoustic_v(const AcousticFields &f, const AcousticCoef &c, const int lo[3], const int hi[3],
+                       cudaStream_t s);
+// compute_P on every cell
+void launch_acoustic_p(const AcousticFields &f, const AcousticCoef &c, cudaStream_t s);
+
 // ---------------------------------------------------------------- geometry and exchange plan (plan.cpp)
 // Validated grid geometry of one process (host only, no CUDA).
 struct Geom {

@@ -243,6 +243,21 @@ class Grid:
         _ok(L.lib().igg_heat_run_host(self._handle(), hp(T_host), hp(Ci_host), lam, dt, dx, dy, dz, nt,
                                       _i3(bw), _stream(stream)))
 
+    # -- second workload: staggered acoustic leapfrog step
+    def acoustic_step(self, P, Vx, Vy, Vz, dt: float, rho: float, K: float, dx: float, dy: float, dz: float,
+                      bw=(16, 4, 4), stream=None) -> None:
+        """@hide_communication bw begin compute_V!; update_halo!(Vx,Vy,Vz) end; compute_P! (include/igg.h)."""
+        n = self.local_ranks
+        nx, ny, nz = self.n
+        want = [(nz, ny, nx), (nz, ny, nx + 1), (nz, ny + 1, nx), (nz + 1, ny, nx)]
+        lists = [_as_list(x, n) for x in (P, Vx, Vy, Vz)]
+        for f, lst in enumerate(lists):
+            for x in lst:
+                if tuple(x.shape) != want[f]:
+                    raise ValueError(f"acoustic_step field {f} must have shape {want[f]}, got {tuple(x.shape)}")
+        _ok(L.lib().igg_acoustic_step(self._handle(), *(_ptr_array(l) for l in lists), dt, rho, K, dx, dy, dz,
+                                      _i3(bw), _stream(stream)))
+
     # -- generic @hide_communication (PAPER.md:75, :94; SPEC.md:330-338)
     def hide_communication(self, bw, step, *fields, stream=None) -> None:
         """Run a user stencil `step(local_rank, lo, hi, stream)` -- which must enqueue the computation of

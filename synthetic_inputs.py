@@ -80,13 +80,16 @@ def random_field(shape, seed: int) -> np.ndarray:
 SEED_ACOUSTIC = 102
 
 
+def acoustic_values(f: int, gx, gy, gz, Sx: int, Sy: int, seed: int = SEED_ACOUSTIC) -> np.ndarray:
+    """Field f (0 = P, 1..3 = Vx, Vy, Vz) at global indices (gz, gy, gx) of a field whose
+    global x/y sizes are Sx, Sy: P = 1 + u, V = 0.1*(2u - 1), u from the field's own seed
+    and global linear index."""
+    u = uniform01(seed * 8 + f, linear_index(gx, gy, gz, Sx, Sy))
+    return 1.0 + u if f == 0 else 0.1 * (2.0 * u - 1.0)
+
+
 def global_acoustic_fields(shapes, seed: int = SEED_ACOUSTIC):
     """Second workload: random global (P, Vx, Vy, Vz) of the given
-    (z, y, x) shapes: P = 1 + u, V = 0.1*(2u - 1), u per field from its own seed and
-    the field's own global linear index."""
-    out = []
-    for f, (sz, sy, sx) in enumerate(shapes):
-        g = linear_index(np.arange(sx), np.arange(sy), np.arange(sz), sx, sy)
-        u = uniform01(seed * 8 + f, g)
-        out.append(1.0 + u if f == 0 else 0.1 * (2.0 * u - 1.0))
-    return out
+    (z, y, x) shapes (acoustic_values over every global index)."""
+    return [acoustic_values(f, np.arange(sx), np.arange(sy), np.arange(sz), sx, sy, seed)
+            for f, (sz, sy, sx) in enumerate(shapes)]

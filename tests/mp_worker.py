@@ -13,7 +13,9 @@ import torch
 import torch.distributed as dist
 
 import paper_2211_15716_b200 as P
+from paper_2211_15716_b200 import acoustic3d as ac
 from paper_2211_15716_b200 import heat3d as app
+from oracle import acoustic3d as OA
 from oracle import grid as OG
 from oracle import halo as OHL
 from oracle import heat3d as OH
@@ -101,6 +103,32 @@ def gather_case(path, n, dims, per, s):
     log("gather OK", dims, per, s)
 
 
+def acoustic_case(path, n, dims, per, local, bw, nt=5):
+    """Second workload: staggered P, Vx, Vy, Vz with update_halo!(Vx, Vy, Vz)."""
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
+                           device=int(os.environ["LOCAL_RANK"]))
+    try:
+        F = ac.alloc_fields(g)
+        ac.init_random(g, F)
+        d = ac.spacing(g)
+        dt = ac.stable_dt(d)
+        ac.run(g, F, nt, dt, d, bw=bw)
+        torch.cuda.synchronize()
+        g.check()
+        N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+        ref = OA.run(*SI.global_acoustic_fields(OA.field_shapes(N, per)), nt, per, dt, ac.RHO, ac.K, *d)
+        sizes = [n, (n[0] + 1, n[1], n[2]), (n[0], n[1] + 1, n[2]), (n[0], n[1], n[2] + 1)]
+        for lr in range(local):
+            c = OG.coords_of_rank(g.rank0 + lr, dims)
+            for f in range(4):
+                W = OG.window(ref[f], c, dims, n, (2, 2, 2), per, sizes[f])
+                if not np.array_equal(F[f][lr].cpu().numpy(), W):
+                    raise AssertionError(f"acoustic {path} {dims} per={per} rank {g.rank0 + lr} field {f}")
+    finally:
+        g.finalize()
+    log("acoustic OK", path, dims, per, "local", local)
+
+
 def main():
     local_rank = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local_rank)
@@ -120,12 +148,16 @@ def main():
                 heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), opts=o)
             heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=12)
             heat_case(path, (66, 40, 36), dims, (0, 1, 0), 1, (16, 2, 2), nt=9)
+            # register/smem capture of the x send layer (fused mode bit 1)
+            heat_case(path, (130, 36, 70), dims, (1, 1, 1), 1, (16, 2, 2), nt=5, opts={P.OPT_FUSED_MODE: 3})
             # the fused put path on every split axis (z faces, corner forwarding x->y->z)
             extra = {2: [(1, 2, 1), (1, 1, 2)], 4: [(2, 1, 2), (1, 2, 2), (4, 1, 1), (1, 1, 4)]}.get(world, [])
             for d2 in extra:
                 heat_case(path, (130, 36, 34), d2, (0, 0, 0), 1, (16, 2, 2), nt=7)
                 heat_case(path, (130, 36, 34), d2, (1, 1, 1), 1, (16, 2, 2), nt=7)
         halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
+        acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4))
+        acoustic_case(path, n, dims, (1, 0, 1), 1, (4, 4, 4))
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
         # 8 ranks as virtual ranks over the processes (2x2x2 correctness on fewer GPUs)
         if 8 % world == 0 and world < 8:
