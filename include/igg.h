@@ -271,8 +271,11 @@ enum {
                                     send layers straight into the neighbours' halos over NVLink, chunk
                                     by chunk; 0 = boundary/inner kernels + pack/exchange/unpack;
                                     -1 (default) = fused whenever eligible */
-    IGG_OPT_FUSED_MODE = 8,      /* ablation bits of the fused path: 1 = capture x send layer in smem,
-                                    2 = stencil on the low-priority inner stream (default) */
+    IGG_OPT_FUSED_MODE = 8,      /* ablation bits of the fused path: 1 = the x send layer is stored to the
+                                    neighbour from inside the z sweep, 2 = stencil on the low-priority inner
+                                    stream (default), 4/8/16 = timing experiments (INVALID halos: no
+                                    receive side / no face stores / stores to own T2), 32 = no tail
+                                    re-order table, 64 = natural chunk order with z faces */
     IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8 with one
                                     exchanging axis, 16 with more) */
     IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */

@@ -191,15 +191,57 @@ __device__ __forceinline__ int4 fused_tile(const FusedParams &F) {
     return td;
 }
 
-// The face work of a face tile after its sweep (called CTA-uniformly).  Each warp copies its own
-// row's part of every face the tile holds, loads of a batch before its stores.
-template <bool XS>
-__device__ __forceinline__ void fused_faces(const FusedParams &F, int4 td, int zs, int ze) {
+// One launch over all tiles, the 1-GPU loop unchanged.  A CTA whose tile holds
+// send-layer cells (x layer of its rows, a y layer row, or a z layer plane in
+// its chunk) re-reads them from T2 after its sweep (its own just-written
+// values) and stores them into the receivers' halos, then counts itself on the
+// (face, chunk) counters.  Keeping the face work out of the z loop keeps the
+// loop's instruction stream identical to the 1-GPU kernel.  (Measured: the face
+// epilogue must stay inline with face_tile computed before the sweep; outlining it
+// or recomputing the tile after the sweep adds spills around the loop and costs
+// 2-13 % of the step.)
+template <bool XS>   // XS: the x send layer goes to the neighbour from the sweep (else re-read from T2)
+__global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
+    __shared__ double2 sT[kFD][32 * kFTY];
+    __shared__ double2 sC[kFD][32 * kFTY];
+    const int4 td = fused_tile(F);
+    const int2 zr = chunk_range(F, td.z);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sx = F.s[0], sy = F.s[1];
+    const int y = 1 + td.y * kFTY + warp;
     const int p = td.x * 64 + 2 * lane;
+    const bool pair_in = y < sy - 1 && p < sx;
+    const bool w0 = pair_in && p >= 1 && p < sx - 1;
+    const bool w1 = pair_in && p + 1 >= 1 && p + 1 < sx - 1;
+    const int zs = zr.x, ze = zr.y;
     const long long sxy = (long long)sx * sy;
-    const double *__restrict__ T2 = F.T2;
+    bool face_tile = false;   // this tile holds send-layer cells
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        const int xl = F.face[0][rs].layer, yl = F.face[1][rs].layer;
+        face_tile |= F.face[0][rs].active && xl >= max(td.x * 64, 1) && xl < min(td.x * 64 + 64, sx - 1);
+        face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
+        face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
+    }
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+    // XS: the x send-layer cell of my row (lane xl, cell xodd of its pair) goes to the neighbour
+    // plane by plane from the sweep (xdst + i = its halo cell of my row and plane)
+    int xl = -1;
+    bool xodd = false;
+    double *xdst = nullptr;
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        const int L = F.face[0][rs].layer - td.x * 64;
+        if (XS && !F.nostore && F.face[0][rs].active && y < sy - 1 && L >= 0 && L < 64 && L + td.x * 64 >= 1 &&
+            L + td.x * 64 < sx - 1) {
+            xl = L >> 1;
+            xodd = L & 1;
+            if (lane == xl) xdst = F.face[0][rs].dst + ((rs == 0 ? 0 : sx - 1) - p);
+        }
+    }
+    fused_sweep<XS>(F, sT, sC, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd);
+    if (!face_tile) return;   // CTA-uniform
+    double *__restrict__ T2 = F.T2;
     __syncthreads();          // the CTA's T2 stores are visible to the CTA
     const int tx0 = td.x * 64, ty0 = 1 + td.y * kFTY;
     const int xlo = max(tx0, 1), xhi = min(tx0 + 64, sx - 1);   // inner x of this tile
@@ -292,55 +334,6 @@ __device__ __forceinline__ void fused_faces(const FusedParams &F, int4 td, int z
     if (tid == 0)
         for (int f = 0; f < 6; ++f)
             if (did[f]) contribute(F, f >> 1, f & 1, f < 4 ? td.z : 0);
-}
-
-// One launch over all tiles, the 1-GPU loop unchanged.  A CTA whose tile holds
-// send-layer cells (x layer of its rows, a y layer row, or a z layer plane in
-// its chunk) re-reads them from T2 after its sweep (its own just-written
-// values) and stores them into the receivers' halos, then counts itself on the
-// (face, chunk) counters (fused_faces).  Keeping the face work out of the z loop
-// keeps the loop's instruction stream identical to the 1-GPU kernel.
-template <bool XS>   // XS: the x send layer goes to the neighbour from the sweep (else re-read from T2)
-__global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
-    __shared__ double2 sT[kFD][32 * kFTY];
-    __shared__ double2 sC[kFD][32 * kFTY];
-    const int4 td = fused_tile(F);
-    const int2 zr = chunk_range(F, td.z);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int sx = F.s[0], sy = F.s[1];
-    const int y = 1 + td.y * kFTY + warp;
-    const int p = td.x * 64 + 2 * lane;
-    const bool pair_in = y < sy - 1 && p < sx;
-    const bool w0 = pair_in && p >= 1 && p < sx - 1;
-    const bool w1 = pair_in && p + 1 >= 1 && p + 1 < sx - 1;
-    const int zs = zr.x, ze = zr.y;
-    const long long sxy = (long long)sx * sy;
-    bool face_tile = false;   // this tile holds send-layer cells
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        const int xl = F.face[0][rs].layer, yl = F.face[1][rs].layer;
-        face_tile |= F.face[0][rs].active && xl >= max(td.x * 64, 1) && xl < min(td.x * 64 + 64, sx - 1);
-        face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
-        face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
-    }
-    long long i = (long long)zs * sxy + (long long)y * sx + p;
-    // XS: the x send-layer cell of my row (lane xl, cell xodd of its pair) goes to the neighbour
-    // plane by plane from the sweep (xdst + i = its halo cell of my row and plane)
-    int xl = -1;
-    bool xodd = false;
-    double *xdst = nullptr;
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        const int L = F.face[0][rs].layer - td.x * 64;
-        if (XS && !F.nostore && F.face[0][rs].active && y < sy - 1 && L >= 0 && L < 64 && L + td.x * 64 >= 1 &&
-            L + td.x * 64 < sx - 1) {
-            xl = L >> 1;
-            xodd = L & 1;
-            if (lane == xl) xdst = F.face[0][rs].dst + ((rs == 0 ? 0 : sx - 1) - p);
-        }
-    }
-    fused_sweep<XS>(F, sT, sC, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd);
-    if (face_tile) fused_faces<XS>(F, td, zs, ze);   // CTA-uniform
 }
 
 // Face cells the stencil does not compute (on other axes' halo/boundary layers):
@@ -526,9 +519,12 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
     for (int z = 1 + nbig * kc1; z < 1 + wz; z += kc2) zc.push_back(make_int2(z, std::min(z + kc2, 1 + wz)));
     const int nch = (int)zc.size();
     if (nch > kMaxChunks) fail(IGG_E_UNSUPPORTED, "fused step: too many z-chunks");
+    // natural chunk order (measured best); fused_mode bit 64: visit the chunk holding the upper z send
+    // layer second (ablation)
     int cz = 0;
-    for (int c = 0; c < nch; ++c)
-        if (n2 - 2 >= zc[c].x && n2 - 2 < zc[c].y) cz = c;
+    if ((act[2][0] || act[2][1]) && (g->fused_mode & 64))
+        for (int c = 0; c < nch; ++c)
+            if (n2 - 2 >= zc[c].x && n2 - 2 < zc[c].y) cz = c;
     // visit order position of each chunk id (mirror of chunk_id() on the device)
     auto id_of = [&](int oc) { return (cz <= 1 || oc == 0) ? oc : (oc == 1 ? cz : (oc - 1 < cz ? oc - 1 : oc)); };
     g->fused_zchunk[0] = g->fused_zchunk[1] = -1;
@@ -569,7 +565,10 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
     g->fused_bmain = g->fused_ntiles;
     int ntail_ch = 0;
     while (ntail_ch < std::min(4, nch - 1) && (long long)(ntail_ch + 1) * ntile <= kMaxTail) ++ntail_ch;
-    if (xtiles <= 16 && ytiles <= 1024 && ntail_ch > 0) {
+    bool any_face = false;
+    for (int a = 0; a < 3; ++a) any_face = any_face || act[a][0] || act[a][1];
+    // no faces: nothing to reorder (natural order, no table); fused_mode bit 32: no table (ablation)
+    if (any_face && !(g->fused_mode & 32) && xtiles <= 16 && ytiles <= 1024 && ntail_ch > 0) {
         const int c0 = nch - ntail_ch;
         std::vector<unsigned short> face_t, rest_t;
         for (int oc = c0; oc < nch; ++oc) {

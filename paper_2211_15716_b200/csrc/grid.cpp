@@ -960,7 +960,10 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_X_ALIGN: g->x_align = (int)(value < 1 ? 1 : value); break;
         case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
         case IGG_OPT_FUSED: g->fused = (int)value; break;
-        case IGG_OPT_FUSED_MODE: g->fused_mode = (int)value; break;
+        case IGG_OPT_FUSED_MODE:
+            g->fused_mode = (int)value;
+            g->fused_key = -1;   // bits 32/64 change the tile layout
+            break;
         case IGG_OPT_COOP_HALO: g->coop = value != 0; break;
         case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
         case IGG_OPT_FUSED_COMM_CTAS:

@@ -37,8 +37,7 @@ def stcs(s):
                      "                __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));")
 
 
-VARIANTS = {"cur": [], "inl": [inline_all], "noinl": [noinline], "lb9": [lb9], "stcs": [stcs],
-            "inl_lb9": [inline_all, lb9], "inl_stcs": [inline_all, stcs]}
+VARIANTS = {"cur": [], "lb9": [lb9], "stcs": [stcs]}   # (inline_all/noinline applied to an older layout)
 
 
 def build(name, fns):
