@@ -193,6 +193,16 @@ igg_status igg_heat_step(igg_grid *grid, double *const *T2, const double *const 
                          const double *const *Ci, double lam, double dt,
                          double dx, double dy, double dz, const int bw[3], igg_stream_t stream);
 
+/* Fig. 1's time loop on the device: nt heat steps, each followed by the swap
+ * T, T2 = T2, T.  T, T2: arrays of local_ranks device pointers that the library swaps in place, so on
+ * return T[lr] holds the state after nt steps and T2[lr] the state before it.  Results are identical
+ * to nt igg_heat_step calls; on the fused P2P path consecutive steps are pipelined (a step's tiles that
+ * read halo cells wait in-kernel for the previous step's faces; only the last step waits for all of
+ * them).  Stream-ordered on `stream`; complete for any later work on it.  Errors as igg_heat_step. */
+igg_status igg_heat_run(igg_grid *grid, double **T, double **T2, const double *const *Ci, double lam,
+                        double dt, double dx, double dy, double dz, int nt, const int bw[3],
+                        igg_stream_t stream);
+
 /* ------------------------------------------------------------------ generic hide_communication
  * A user stencil for igg_hide_communication: compute the cells of the box [lo, hi) (0-based, of the
  * canonical local grid of hosted rank `local_rank`) by enqueuing work on `stream`; it must write only
@@ -275,7 +285,10 @@ enum {
                                     neighbour from inside the z sweep, 2 = stencil on the low-priority inner
                                     stream (default), 4/8/16 = timing experiments (INVALID halos: no
                                     receive side / no face stores / stores to own T2), 32 = no tail
-                                    re-order table, 64 = natural chunk order with z faces */
+                                    re-order table, 64 = visit the upper z-face chunk second,
+                                    128 = legacy multi-stream schedule (rim / receive kernels on
+                                    comm streams joined by events) instead of the pipelined one,
+                                    256 = x faces pulled by the receiver instead of pushed */
     IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8 with one
                                     exchanging axis, 16 with more) */
     IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */

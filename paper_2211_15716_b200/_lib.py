@@ -67,6 +67,8 @@ SIGNATURES = {
     "igg_update_halo": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p],
     "igg_heat_step": [ctypes.c_void_p, c_dbl_pp, c_dbl_pp, c_dbl_pp, ctypes.c_double, ctypes.c_double,
                       ctypes.c_double, ctypes.c_double, ctypes.c_double, c_int_p, ctypes.c_void_p],
+    "igg_heat_run": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, c_dbl_pp, ctypes.c_double, ctypes.c_double,
+                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_int_p, ctypes.c_void_p],
     "igg_heat_run_host": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_int_p,
                           ctypes.c_void_p],

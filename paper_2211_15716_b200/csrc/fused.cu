@@ -69,6 +69,29 @@ __device__ __forceinline__ void contribute(const FusedParams &F, int a, int rs, 
     }
 }
 
+// rim / forwarded cells of (face, chunk) on the pipelined schedule: their own counters and flags
+__device__ __forceinline__ void contribute_x(const FusedParams &F, int a, int rs, int c) {
+    const int i = (a * 2 + rs) * kMaxChunks + c;
+    const unsigned old = atomicAdd(F.ctr_x + i, 1u);
+    if (old == F.tgt_x[i] - 1) {
+        __threadfence_system();
+        st_rel_sys(F.face[a][rs].xflag + c, F.epoch);
+        atomicExch(F.ctr_x + i, 0u);
+    }
+}
+
+// thread 0 spins (bounded) until *fl >= v; the caller synchronises the CTA
+__device__ __forceinline__ void spin_geq(const FusedParams &F, const unsigned long long *fl, unsigned long long v) {
+    const long long t0 = clock64();
+    while (ld_acq_sys(fl) < v) {
+        if (clock64() - t0 > F.timeout_cycles) {
+            atomicExch(F.err, 1);
+            break;
+        }
+        __nanosleep(200);
+    }
+}
+
 // the earlier axis whose unpack writes this cell last in the dimension-sequential
 // exchange (-1: none) -- that unpack forwards the cell to face a
 __device__ __forceinline__ int forward_phase(const FusedParams &F, int a, const int *c) {
@@ -78,6 +101,19 @@ __device__ __forceinline__ int forward_phase(const FusedParams &F, int a, const 
         if (c[b] == F.s[b] - 1 && F.halo[b][1].active) fwd = b;
     }
     return fwd;
+}
+
+// a later axis whose exchange writes this cell's receiver copy last: the cell is sent by that
+// axis' phase (face or forwarding), never by this one -- so every receiver cell has ONE writer
+__device__ __forceinline__ bool later_halo(const FusedParams &F, int a, const int *c) {
+    for (int b = a + 1; b < 3; ++b)
+        if ((c[b] == 0 && F.halo[b][0].active) || (c[b] == F.s[b] - 1 && F.halo[b][1].active)) return true;
+    return false;
+}
+
+// staging buffer offset of (epoch parity, halo side, y, z)
+__device__ __forceinline__ long long xstg_at(const FusedParams &F, unsigned long long epoch, int side, int y, int z) {
+    return ((long long)((int)(epoch & 1) * 2 + side) * F.s[1] + y) * F.s[2] + z;
 }
 
 // chunk visited at order position oc: 0, cz, then the others ascending
@@ -112,8 +148,8 @@ constexpr int kFKC = 64;   // longest z-chunk
 
 // The z sweep of one tile (cp.async ring of kFD planes of T and Ci, x neighbours by shuffle, z by a
 // register queue).  CAP: the lane xl holding an x send-layer cell of its row (cell xodd of its pair)
-// stores it straight into the neighbour's halo every plane (xdst + i), while the receiver's own
-// stores of the same 32-B sector (its cells 1-3 or s-4..s-2) are still in its L2.
+// stores it into the receiver's staging row every plane (xdst[z]), so the face epilogue need not
+// re-read the column from DRAM.
 template <bool CAP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[32 * kFTY], double2 (*sC)[32 * kFTY],
                                             double *xdst, int tid, int lane, int zs, int ze, long long i,
@@ -157,7 +193,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[
                 if (w0) T2[i] = r0;
                 if (w1) T2[i + 1] = r1;
             }
-            if (CAP && lane == xl) xdst[i] = xodd ? r1 : r0;
+            if (CAP && lane == xl) xdst[z] = xodd ? r1 : r0;   // the receiver's staging row
             zm = c;
             c = zp;
             if (pair_in && z + kFD < ze) {
@@ -173,9 +209,8 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[
 
 // tile of this CTA from the block index (x-tiles fastest, then y-tiles, then chunks in visit
 // order); the last chunks' tiles are re-ordered, face tiles first, from the parameter table
-__device__ __forceinline__ int4 fused_tile(const FusedParams &F) {
+__device__ __forceinline__ int4 fused_tile(const FusedParams &F, int b) {
     int4 td;
-    const int b = blockIdx.x;
     if (b < F.bmain) {
         td.x = b % F.xtiles;
         const int r = b / F.xtiles;
@@ -191,6 +226,54 @@ __device__ __forceinline__ int4 fused_tile(const FusedParams &F) {
     return td;
 }
 
+// Pipelined schedule, before the sweep: a tile that reads halo cells waits until the previous
+// epoch's faces covering them have arrived (x: first/last x-tile of the chunk, y: first/last y-tile,
+// z: the chunks holding planes 1 and s_z-2).  The same wait orders my face stores of this epoch
+// after the neighbour's reads of the halo they overwrite: the neighbour's tiles that read that halo
+// are the ones that published the awaited face (hazard argument).
+__device__ __forceinline__ void fused_wait_halos(const FusedParams &F, int4 td, int zs, int ze) {
+    const bool xlo = F.halo[0][0].active && td.x == 0, xhi = F.halo[0][1].active && td.x == F.xtiles - 1;
+    if (threadIdx.x == 0) {
+        const unsigned long long prev = F.epoch - 1;
+        if (xlo) spin_geq(F, F.halo[0][0].flag + td.z, prev);
+        if (xhi) spin_geq(F, F.halo[0][1].flag + td.z, prev);
+        if (F.halo[1][0].active && td.y == 0) spin_geq(F, F.halo[1][0].flag + td.z, prev);
+        if (F.halo[1][1].active && td.y == F.ytiles - 1) spin_geq(F, F.halo[1][1].flag + td.z, prev);
+        if (F.halo[2][0].active && zs == 1) spin_geq(F, F.halo[2][0].flag, prev);
+        if (F.halo[2][1].active && ze == F.s[2] - 1) spin_geq(F, F.halo[2][1].flag, prev);
+    }
+    __syncthreads();
+    if (F.xstage && (xlo || xhi)) {
+        // my x halo column of this tile (its rows, its chunk's planes), staged by the neighbour in the
+        // previous epoch -- final since the awaited flag -- into my T, just before the sweep reads it
+        // (writing whole 32-B sectors instead, halo cell plus its row neighbours, measured slower)
+        const int sx = F.s[0], sy = F.s[1];
+        const long long sxy = (long long)sx * sy;
+        const int ty0 = 1 + td.y * kFTY, nrow = min(ty0 + kFTY, sy - 1) - ty0, nz = ze - zs;
+        double *Tw = const_cast<double *>(F.T);
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            if (!(side == 0 ? xlo : xhi)) continue;
+            const int hx = side == 0 ? 0 : sx - 1;
+            constexpr int U = kFKC / 32;   // cells per thread (4 rows x 64 planes / 128 threads)
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = threadIdx.x + u * 32 * kFTY;
+                v[u] = t < nrow * nz ? __ldcg(F.xstg + xstg_at(F, F.epoch - 1, side, ty0 + t / nz, zs + t % nz)) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = threadIdx.x + u * 32 * kFTY;
+                if (t < nrow * nz) Tw[(long long)(zs + t % nz) * sxy + (long long)(ty0 + t / nz) * sx + hx] = v[u];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __noinline__ void fused_extra(const FusedParams &F, int b);
+
 // One launch over all tiles, the 1-GPU loop unchanged.  A CTA whose tile holds
 // send-layer cells (x layer of its rows, a y layer row, or a z layer plane in
 // its chunk) re-reads them from T2 after its sweep (its own just-written
@@ -204,7 +287,15 @@ template <bool XS>   // XS: the x send layer goes to the neighbour from the swee
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
-    const int4 td = fused_tile(F);
+    int b = blockIdx.x;
+    if (F.pipe) {   // pipelined schedule: rim blocks first, forwarders last (CTA-uniform)
+        if (b < F.nrim || b >= F.nrim + F.nstencil) {
+            fused_extra(F, b);
+            return;
+        }
+        b -= F.nrim;
+    }
+    const int4 td = fused_tile(F, b);
     const int2 zr = chunk_range(F, td.z);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sx = F.s[0], sy = F.s[1];
@@ -223,6 +314,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
         face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
     }
+    if (F.wait_prev) fused_wait_halos(F, td, zs, ze);   // CTA-uniform
     long long i = (long long)zs * sxy + (long long)y * sx + p;
     // XS: the x send-layer cell of my row (lane xl, cell xodd of its pair) goes to the neighbour
     // plane by plane from the sweep (xdst + i = its halo cell of my row and plane)
@@ -232,11 +324,11 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
 #pragma unroll
     for (int rs = 0; rs < 2; ++rs) {
         const int L = F.face[0][rs].layer - td.x * 64;
-        if (XS && !F.nostore && F.face[0][rs].active && y < sy - 1 && L >= 0 && L < 64 && L + td.x * 64 >= 1 &&
-            L + td.x * 64 < sx - 1) {
+        if (XS && !F.nostore && F.xstage && F.face[0][rs].active && y < sy - 1 && L >= 0 && L < 64 &&
+            L + td.x * 64 >= 1 && L + td.x * 64 < sx - 1) {
             xl = L >> 1;
             xodd = L & 1;
-            if (lane == xl) xdst = F.face[0][rs].dst + ((rs == 0 ? 0 : sx - 1) - p);
+            if (lane == xl) xdst = F.xstg_peer[rs] + xstg_at(F, F.epoch, rs, y, 0);
         }
     }
     fused_sweep<XS>(F, sT, sC, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd);
@@ -263,13 +355,18 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
 #pragma unroll
                 for (int u = 0; u < kFKC / 32; ++u) {
                     const int zz = zs + lane + 32 * u;
-                    v[u] = (!XS && zz < ze) ? T2[(long long)zz * sxy + (long long)yrow * sx + fx.layer] : 0.0;
+                    v[u] = ((!XS || !F.xstage) && zz < ze) ? T2[(long long)zz * sxy + (long long)yrow * sx + fx.layer]
+                                                           : 0.0;
                 }
+                // staged: the receiver's staging row (lanes along z: whole sectors); else its T2 column
+                double *const dst = F.xstage ? F.xstg_peer[rs] + xstg_at(F, F.epoch, rs, yrow, 0)
+                                             : fx.dst + (long long)yrow * sx + hx;
+                const long long zstride = F.xstage ? 1 : sxy;
 #pragma unroll
                 for (int u = 0; u < kFKC / 32; ++u) {
                     const int zz = zs + lane + 32 * u;
-                    if (XS || zz >= ze) continue;   // XS: stored from the sweep
-                    fx.dst[(long long)zz * sxy + (long long)yrow * sx + hx] = v[u];
+                    if ((XS && F.xstage) || zz >= ze) continue;   // XS: staged from the sweep
+                    dst[(long long)zz * zstride] = v[u];
                 }
             }
             did[rs] = true;
@@ -329,11 +426,14 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             did[4 + rs] = F.face[2][rs].active && F.zchunk[rs] == td.z;
         }
     }
-    __threadfence_system();
+    // one system-scope release for the CTA: the barrier orders every warp's face stores before
+    // thread 0's fence, which is cumulative (PTX memory model), then the counters
     __syncthreads();
-    if (tid == 0)
+    if (tid == 0) {
+        __threadfence_system();
         for (int f = 0; f < 6; ++f)
             if (did[f]) contribute(F, f >> 1, f & 1, f < 4 ? td.z : 0);
+    }
 }
 
 // Face cells the stencil does not compute (on other axes' halo/boundary layers):
@@ -363,7 +463,7 @@ __global__ void fused_rim_kernel(const __grid_constant__ FusedParams F, unsigned
             c[a] = fc.layer;
             c[b1] = u;
             c[b2] = v;
-            if (forward_phase(F, a, c) >= 0) continue;
+            if (forward_phase(F, a, c) >= 0 || later_halo(F, a, c)) continue;
             const long long gi = ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0];
             const double val = F.T2[gi];
             c[a] = rs == 0 ? 0 : F.s[a] - 1;   // the receiver's halo layer
@@ -426,18 +526,24 @@ __device__ __forceinline__ void wait_flags(const FusedParams &F, int b, int idx)
 }
 
 // forward my fresh halo line (axis b, side) x (face a, rs) over the third axis range [lo, hi)
-__device__ __forceinline__ bool forward_line(const FusedParams &F, int b, int side, int a, int rs, int lo, int hi) {
+__device__ __forceinline__ bool forward_line(const FusedParams &F, int b, int side, int a, int rs, int lo, int hi,
+                                             int part, int nparts) {
     const FusedFace &fc = F.face[a][rs];
     if (!fc.active || !F.halo[b][side].active) return false;
     const int third = 3 - a - b;
     bool any = false;
-    for (int t = lo + blockIdx.x * blockDim.x + threadIdx.x; t < hi; t += gridDim.x * blockDim.x) {
+    for (int t = lo + part * blockDim.x + threadIdx.x; t < hi; t += nparts * blockDim.x) {
         int c[3];
         c[b] = side == 0 ? 0 : F.s[b] - 1;
         c[a] = fc.layer;
         c[third] = t;
-        if (forward_phase(F, a, c) != b) continue;
-        const double v = __ldcg(F.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
+        if (forward_phase(F, a, c) != b || later_halo(F, a, c)) continue;
+        double v;
+        if (b == 0 && F.xstage && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1) {
+            v = __ldcg(F.xstg + xstg_at(F, F.epoch, side, c[1], c[2]));   // staged, not yet in T2
+        } else {
+            v = __ldcg(F.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
+        }
         c[a] = rs == 0 ? 0 : F.s[a] - 1;
         fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v;
         any = true;
@@ -455,9 +561,9 @@ __global__ void __launch_bounds__(128) fused_comm_kernel(const __grid_constant__
             bool fwd = false;
             for (int side = 0; side < 2; ++side)
                 for (int rs = 0; rs < 2; ++rs) {
-                    if (b == 0) fwd |= forward_line(F, 0, side, 1, rs, zr.x, zr.y);   // x halo -> y faces
+                    if (b == 0) fwd |= forward_line(F, 0, side, 1, rs, zr.x, zr.y, blockIdx.x, gridDim.x);   // x -> y faces
                     if (F.face[2][rs].layer >= zr.x && F.face[2][rs].layer < zr.y)   // -> z faces
-                        fwd |= forward_line(F, b, side, 2, rs, 0, F.s[b == 0 ? 1 : 0]);
+                        fwd |= forward_line(F, b, side, 2, rs, 0, F.s[b == 0 ? 1 : 0], blockIdx.x, gridDim.x);
                 }
             if (__syncthreads_or(fwd)) __threadfence_system();
             __syncthreads();
@@ -475,17 +581,135 @@ __global__ void __launch_bounds__(128) fused_comm_kernel(const __grid_constant__
     }
 }
 
+// The rim and forwarding roles of the pipelined schedule, as extra blocks of the stencil launch.
+// Rim (blocks [0, nrim), six faces x nrim/6 blocks): the rim cells of every face (fused_rim_kernel's
+// work); the last rim block counts once on every (face, chunk).  Forwarders (the last nfwd blocks):
+// per chunk, wait for the x (then y) halo of the chunk -- its data and its rim/forwarded cells --
+// forward the edge lines (fused_comm_kernel's work) and count on the later faces' xflags.
+__device__ __noinline__ void fused_extra(const FusedParams &F, int b) {
+    if (b < F.nrim) {
+        const int per = F.nrim / 6;
+        const int f = b / per, part = b % per, a = f >> 1, rs = f & 1;
+        const FusedFace &fc = F.face[a][rs];
+        if (fc.active) {
+            const int b1 = a == 0 ? 1 : 0, b2 = a == 2 ? 1 : 2;
+            const int S1 = F.s[b1], S2 = F.s[b2];
+            const long long nrim = 2LL * S2 + 2LL * (S1 - 2);
+            for (long long t = (long long)part * blockDim.x + threadIdx.x; t < nrim;
+                 t += (long long)per * blockDim.x) {
+                int u, v;
+                if (t < 2LL * S2) {
+                    u = t < S2 ? 0 : S1 - 1;
+                    v = (int)(t % S2);
+                } else {
+                    const long long r = t - 2LL * S2;
+                    u = 1 + (int)(r % (S1 - 2));
+                    v = r < (S1 - 2) ? 0 : S2 - 1;
+                }
+                int c[3];
+                c[a] = fc.layer;
+                c[b1] = u;
+                c[b2] = v;
+                if (forward_phase(F, a, c) >= 0 || later_halo(F, a, c)) continue;
+                const double val = F.T2[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]];
+                c[a] = rs == 0 ? 0 : F.s[a] - 1;
+                fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = val;
+            }
+            __threadfence_system();
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(F.rim_ticket, 1u) == (unsigned)F.nrim - 1) {
+            __threadfence_system();
+            for (int g = 0; g < 6; ++g) {
+                const int ga = g >> 1, grs = g & 1;
+                if (!F.face[ga][grs].active) continue;
+                if (ga == 2)
+                    contribute_x(F, 2, grs, 0);
+                else
+                    for (int ch = 0; ch < F.nchunks; ++ch) contribute_x(F, ga, grs, ch);
+            }
+            atomicExch(F.rim_ticket, 0u);
+        }
+        return;
+    }
+    const int q = b - F.nrim - F.nstencil;   // forwarder q of nfwd
+    for (int ch = 0; ch < F.nchunks; ++ch) {
+        const int2 zr = ext_range(F, ch);
+        for (int hb = 0; hb < 2; ++hb) {
+            if (!(F.halo[hb][0].active || F.halo[hb][1].active)) continue;
+            if (threadIdx.x == 0)
+                for (int side = 0; side < 2; ++side)
+                    if (F.halo[hb][side].active) {
+                        spin_geq(F, F.halo[hb][side].flag + ch, F.epoch);
+                        spin_geq(F, F.halo[hb][side].xflag + ch, F.epoch);
+                    }
+            __syncthreads();
+            bool fwd = false;
+            for (int side = 0; side < 2; ++side)
+                for (int rs = 0; rs < 2; ++rs) {
+                    if (hb == 0) fwd |= forward_line(F, 0, side, 1, rs, zr.x, zr.y, q, F.nfwd);
+                    if (F.face[2][rs].layer >= zr.x && F.face[2][rs].layer < zr.y)
+                        fwd |= forward_line(F, hb, side, 2, rs, 0, F.s[hb == 0 ? 1 : 0], q, F.nfwd);
+                }
+            if (__syncthreads_or(fwd)) __threadfence_system();
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int a = hb + 1; a < 3; ++a)
+                    for (int rs = 0; rs < 2; ++rs) {
+                        if (!F.face[a][rs].active) continue;
+                        if (a == 1)
+                            contribute_x(F, 1, rs, ch);
+                        else if (F.face[2][rs].layer >= zr.x && F.face[2][rs].layer < zr.y)
+                            contribute_x(F, 2, rs, 0);
+                    }
+        }
+    }
+}
+
+// Pipelined schedule, after the last step of a run: every incoming face (data and rim/forwarded
+// cells) of the epoch has arrived -- the step is complete for any later work on the stream.
+// Staged x faces: also copies the last epoch's staged x halo columns (inner rows and planes) into T2,
+// every block its share after the x data flags.
+__global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
+    if (blockIdx.x == 0)
+        for (int f = threadIdx.x; f < 6 * F.nchunks; f += blockDim.x) {
+            const int a = f / (2 * F.nchunks), rs = (f / F.nchunks) & 1, ch = f % F.nchunks;
+            const FusedHalo &h = F.halo[a][rs];
+            if (!h.active || (a == 2 && ch > 0)) continue;
+            spin_geq(F, h.flag + ch, F.epoch);
+            spin_geq(F, h.xflag + ch, F.epoch);
+        }
+    if (!F.xstage) return;
+    for (int f = threadIdx.x; f < 2 * F.nchunks; f += blockDim.x)
+        if (F.halo[0][f / F.nchunks].active) spin_geq(F, F.halo[0][f / F.nchunks].flag + f % F.nchunks, F.epoch);
+    __syncthreads();
+    const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
+    const long long sxy = (long long)sx * sy, ncell = (long long)(sy - 2) * (sz - 2);
+    for (int side = 0; side < 2; ++side) {
+        if (!F.halo[0][side].active) continue;
+        const int hx = side == 0 ? 0 : sx - 1;
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
+             t += (long long)gridDim.x * blockDim.x) {
+            const int z = 1 + (int)(t % (sz - 2)), y = 1 + (int)(t / (sz - 2));
+            F.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(F.xstg + xstg_at(F, F.epoch, side, y, z));
+        }
+    }
+}
+
 // ------------------------------------------------------------------ host side
 bool fused_eligible(const igg_grid *g) {
     if (g->fused == 2 && g->nlocal == 1) return true;   // ablation/profiling: force the fused kernel
-    // fused = 3/5: timing experiments on the same path (see fused_step)
-    if (g->path != IGG_PATH_P2P || g->nlocal != 1 || g->nproc_procs < 2 || g->fused == 0) return false;
-
+    if (g->path != IGG_PATH_P2P || g->nlocal != 1 || g->fused == 0) return false;
+    bool any = false, self = false;
     for (int a = 0; a < 3; ++a)
         for (int k = 0; k < 2; ++k) {
             const int nb = g->nbr[0][a][k];
-            if (nb >= 0 && proc_of(g, nb) == g->proc) return false;   // self-wrap: stream-ordered path
+            if (nb < 0) continue;
+            any = true;
+            self = self || proc_of(g, nb) == g->proc;   // a periodic axis wrapping onto this process
         }
+    if (!any) return false;                               // nothing to exchange: the plain stencil
+    if (self && (g->fused_mode & 128)) return false;      // legacy schedule: stream-ordered path
     if (g->n[0] < 66 || g->n[1] < 6 || g->n[2] < 6) return false;   // one x send layer per 64-cell segment
     return true;
 }
@@ -558,6 +782,41 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
         g->allocs++;
     }
     IGG_CUDA(cudaMemcpy(g->fused_tgt, tgt.data(), tgt.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+    // pipelined schedule: face tiles complete the data flags; the rim (1) and the in-kernel forwarders
+    // complete the xflags (forwarders exist only when a later face takes an earlier axis' halo lines)
+    bool xh = false, yh = false;
+    for (int sd = 0; sd < 2; ++sd) {
+        xh = xh || g->nbr[0][0][sd] >= 0;
+        yh = yh || g->nbr[0][1][sd] >= 0;
+    }
+    const bool yf = act[1][0] || act[1][1], zf = act[2][0] || act[2][1];
+    const bool need_fwd = (xh && (yf || zf)) || (yh && zf);
+    g->fused_nfwd = need_fwd ? g->fused_ncomm : 0;
+    const unsigned nf = (unsigned)g->fused_nfwd;
+    std::vector<unsigned> tgt_d(6 * kMaxChunks, 0u), tgt_x(6 * kMaxChunks, 0u);
+    for (int rs = 0; rs < 2; ++rs) {
+        for (int c = 0; c < nch; ++c) {
+            if (act[0][rs]) {
+                tgt_d[(0 * 2 + rs) * kMaxChunks + c] = ytiles;
+                tgt_x[(0 * 2 + rs) * kMaxChunks + c] = 1;
+            }
+            if (act[1][rs]) {
+                tgt_d[(1 * 2 + rs) * kMaxChunks + c] = xtiles;
+                tgt_x[(1 * 2 + rs) * kMaxChunks + c] = 1 + (xh ? nf : 0);
+            }
+        }
+        if (act[2][rs]) {
+            tgt_d[(2 * 2 + rs) * kMaxChunks] = xtiles * ytiles;
+            tgt_x[(2 * 2 + rs) * kMaxChunks] = 1 + (xh ? nf : 0) + (yh ? nf : 0);
+        }
+    }
+    for (auto *pp : {&g->fused_tgt_pipe, &g->fused_tgt_x})
+        if (!*pp) {
+            IGG_CUDA(cudaMalloc(pp, 6 * kMaxChunks * sizeof(unsigned)));
+            g->allocs++;
+        }
+    IGG_CUDA(cudaMemcpy(g->fused_tgt_pipe, tgt_d.data(), tgt_d.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
+    IGG_CUDA(cudaMemcpy(g->fused_tgt_x, tgt_x.data(), tgt_x.size() * sizeof(unsigned), cudaMemcpyHostToDevice));
     g->fused_ntiles = (int)(ntile * nch);
     // tail: the last chunks' tiles (about 2-3 waves), face tiles first, so the last faces
     // leave a couple of waves before the stencil ends and the forwarding chain is hidden
@@ -611,6 +870,10 @@ typedef int (*MemGetAddressRangeFn)(unsigned long long *, size_t *, unsigned lon
 static const std::vector<double *> &peer_arrays(igg_grid *g, double *T2) {
     for (const auto &m : g->fused_peer_maps)
         if (m.first == (const void *)T2) return m.second;
+    if (g->nproc_procs == 1) {   // self-wrap on one process: my own array
+        g->fused_peer_maps.push_back({(const void *)T2, std::vector<double *>(1, T2)});
+        return g->fused_peer_maps.back().second;
+    }
     static MemGetAddressRangeFn range_fn = nullptr;
     if (!range_fn) {
         void *fn = nullptr;
@@ -652,15 +915,16 @@ static const std::vector<double *> &peer_arrays(igg_grid *g, double *T2) {
     return g->fused_peer_maps.back().second;
 }
 
-void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s) {
-    if (!g->fused_ctr) {
-        IGG_CUDA(cudaMalloc(&g->fused_ctr, (6 * kMaxChunks + 8) * sizeof(unsigned int)));
-        IGG_CUDA(cudaMemset(g->fused_ctr, 0, (6 * kMaxChunks + 8) * sizeof(unsigned int)));
+void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s,
+                bool wait_prev, bool drain) {
+    if (!g->fused_ctr) {   // [data ctr | rim/forward ctr] x 6 x kMaxChunks, then tickets
+        IGG_CUDA(cudaMalloc(&g->fused_ctr, (12 * kMaxChunks + 8) * sizeof(unsigned int)));
+        IGG_CUDA(cudaMemset(g->fused_ctr, 0, (12 * kMaxChunks + 8) * sizeof(unsigned int)));
         g->allocs++;
     }
     const bool comm = !g->skip_comm;
     static const std::vector<double *> none;
-    const std::vector<double *> &peer = (comm && g->nproc_procs > 1) ? peer_arrays(g, T2) : none;
+    const std::vector<double *> peer = comm ? peer_arrays(g, T2) : none;   // a copy: the map may grow
     g->epoch++;
     FusedParams F{};
     F.T = T;
@@ -690,12 +954,14 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
                 // mode bit 16 (timing experiment, INVALID halos): the face stores go to my own T2
                 f.dst = (g->fused_mode & 16) ? T2 : peer[pp];
                 f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
+                f.xflag = g->peer_flags[pp] + (6 + a * 2 + rs) * kMaxChunks;   // (one rank per process)
             }
             const int hb = g->nbr[0][a][rs];   // my halo side rs is filled by my neighbour on side rs
             FusedHalo &h = F.halo[a][rs];
             h.active = comm && hb >= 0;
             h.layer = rs == 0 ? 0 : g->n[a] - 1;
             h.flag = g->flags + (a * 2 + rs) * kMaxChunks;
+            h.xflag = g->flags + (6 + a * 2 + rs) * kMaxChunks;
         }
     int key = 0;
     for (int a = 0; a < 3; ++a)
@@ -717,6 +983,51 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
     F.zchunk[1] = g->fused_zchunk[1];
     F.tgt = g->fused_tgt;
 
+    if (!(g->fused_mode & 128)) {
+        // pipelined schedule (default): ONE launch on the caller's stream -- rim blocks, stencil
+        // tiles, forwarders -- and, when the step must be complete on return, a one-block drain
+        const bool recv = comm && !(g->fused_mode & 4);   // mode bit 4: timing without receive side
+        F.pipe = 1;
+        F.wait_prev = (wait_prev && recv) ? 1 : 0;
+        F.nrim = comm ? 48 : 0;
+        F.nstencil = g->fused_ntiles;
+        F.nfwd = recv ? g->fused_nfwd : 0;
+        F.tgt = g->fused_tgt_pipe;
+        F.ctr_x = g->fused_ctr + 6 * kMaxChunks;
+        F.tgt_x = g->fused_tgt_x;
+        F.rim_ticket = g->fused_ctr + 12 * kMaxChunks;
+        // x faces staged in the receiver's compact buffer (default) or stored straight into its T2
+        // column (fused_mode bit 256, ablation: one 8-B value per 32-B sector)
+        F.xstage = (recv && !(g->fused_mode & 256) && (F.halo[0][0].active || F.halo[0][1].active)) ? 1 : 0;
+        if (F.xstage) {
+            if (!g->fused_xstg) {
+                IGG_CUDA(cudaMalloc(&g->fused_xstg, sizeof(double) * 4 * (size_t)g->n[1] * g->n[2]));
+                g->allocs++;
+            }
+            const std::vector<double *> pstg = peer_arrays(g, g->fused_xstg);
+            F.xstg = g->fused_xstg;
+            for (int rs = 0; rs < 2; ++rs)
+                if (F.face[0][rs].active) F.xstg_peer[rs] = pstg[proc_of(g, g->nbr[0][0][rs == 0 ? 1 : 0])];
+        }
+        const int blocks = F.nrim + F.nstencil + F.nfwd;
+        prof_begin(g, s);
+        if (g->fused_mode & 1)
+            heat_fused_kernel<true><<<blocks, 32 * kFTY, 0, s>>>(F);
+        else
+            heat_fused_kernel<false><<<blocks, 32 * kFTY, 0, s>>>(F);
+        IGG_CUDA(cudaGetLastError());
+        g->launches++;
+        prof_end(g, s, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2));
+        if (drain && recv) {
+            fused_drain_kernel<<<F.xstage ? 2 * g->sm_count : 1, 128, 0, s>>>(F);
+            IGG_CUDA(cudaGetLastError());
+            g->launches++;
+        }
+        return;
+    }
+
+    // legacy schedule (fused_mode bit 128, ablation): rim and receive/forward kernels on the comm
+    // streams, the stencil on the inner stream, joined by events
     IGG_CUDA(cudaEventRecord(g->ev_start, s));
     IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
     tl_mark(g, s, 0);

@@ -351,7 +351,8 @@ static void launch_full(igg_grid *g, double *const *T2, const double *const *T, 
 }
 
 void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, double lam,
-               double dt, double dx, double dy, double dz, const int bw[3], cudaStream_t s) {
+               double dt, double dx, double dy, double dz, const int bw[3], cudaStream_t s, bool wait_prev,
+               bool drain) {
     for (int lr = 0; lr < g->nlocal; ++lr)
         if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "heat_step: NULL field pointer");
     for (int a = 0; a < 3; ++a)
@@ -396,7 +397,7 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
     if (!sequential_req && g->stencil_kernel == 0 && fused_eligible(g)) {
         HeatRegion R = make_region(g, 0, T2, T, Ci, 1, g->n[0] - 1, 1, g->n[1] - 1, 1, g->n[2] - 1);
         if (heat_box_vectorizable(R)) {   // one kernel: stencil + exchange in peer memory
-            fused_step(g, T2[0], T[0], Ci[0], k, s);
+            fused_step(g, T2[0], T[0], Ci[0], k, s, wait_prev, drain);
             return;
         }
     }
@@ -490,7 +491,8 @@ IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_
             IGG_NCCL(ncclCommInitRank(&g->comm, g->nproc_procs, id, g->proc));
         }
         // receive flags (P2P), last-block tickets, error word, reduction scratch
-        const size_t flag_bytes = sizeof(unsigned long long) * g->nlocal * 6 * igg::kMaxChunks;
+        // [data | rim+forwarded] x nlocal x 6 faces x kMaxChunks
+        const size_t flag_bytes = 2 * sizeof(unsigned long long) * g->nlocal * 6 * igg::kMaxChunks;
         g->flags = (unsigned long long *)igg::dev_alloc(g, flag_bytes);
         IGG_CUDA(cudaMemset(g->flags, 0, flag_bytes));
         g->tickets = (unsigned int *)igg::dev_alloc(g, sizeof(unsigned int) * 4);
@@ -547,7 +549,7 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->fused_tgt, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->fused_xstg, (void *)g->fused_tgt, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
@@ -778,6 +780,22 @@ IGG_API igg_status igg_acoustic_step(igg_grid *g, double *const *P, double *cons
     IGG_CATCH
 }
 
+IGG_API igg_status igg_heat_run(igg_grid *g, double **T, double **T2, const double *const *Ci, double lam,
+                                double dt, double dx, double dy, double dz, int nt, const int bw[3],
+                                igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_heat_run");
+    if (!T || !T2 || !Ci || nt < 0) fail(IGG_E_ARG, "igg_heat_run: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int it = 0; it < nt; ++it) {
+        // consecutive steps pipelined on the fused path (the previous step's faces awaited tile by
+        // tile); the last one drains, so the run is complete on the stream like nt single steps
+        igg::heat_step(g, T2, T, Ci, lam, dt, dx, dy, dz, bw, s, it > 0, it == nt - 1);
+        for (int lr = 0; lr < g->nlocal; ++lr) std::swap(T[lr], T2[lr]);   // T, T2 = T2, T
+    }
+    IGG_CATCH
+}
+
 IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *Ci_host, double lam, double dt,
                                      double dx, double dy, double dz, int nt, const int bw[3], igg_stream_t stream) {
     IGG_TRY
@@ -806,7 +824,7 @@ IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *
     }
     for (int it = 0; it < nt; ++it) {
         std::vector<const double *> ac(a.begin(), a.end());
-        igg::heat_step(g, b.data(), ac.data(), c.data(), lam, dt, dx, dy, dz, bw, s);
+        igg::heat_step(g, b.data(), ac.data(), c.data(), lam, dt, dx, dy, dz, bw, s, it > 0, it == nt - 1);
         std::swap(a, b);   // T, T2 = T2, T
     }
     for (int lr = 0; lr < g->nlocal; ++lr)

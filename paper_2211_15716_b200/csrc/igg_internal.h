@@ -127,11 +127,13 @@ constexpr int kMaxTail = 6144;       // tiles of the last chunks, re-ordered fac
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // the receiver's T2 (peer-mapped); the face lands in its halo layer
     unsigned long long *flag;        // receiver's flags of (axis, side): [kMaxChunks] (z faces: [0])
+    unsigned long long *xflag;       // receiver's flags of the rim/forwarded cells (pipelined schedule)
     int layer;                       // my send layer along the axis
     int active;
 };
 struct FusedHalo {                   // one halo side I receive
     const unsigned long long *flag;  // my flags [kMaxChunks]
+    const unsigned long long *xflag; // my rim/forwarded-cell flags [kMaxChunks] (pipelined schedule)
     int layer;                       // halo layer (0 or s-1)
     int active;
 };
@@ -155,6 +157,23 @@ struct FusedParams {
     long long timeout_cycles;
     int *err;
     HeatCoef k;
+    // pipelined schedule (one launch per step on the caller's stream): blocks [0, nrim) send the rim,
+    // [nrim, nrim + nstencil) are the stencil tiles, the last nfwd forward the edge lines; face tiles
+    // count on ctr/tgt (data flags), rim and forwarders on ctr_x/tgt_x (xflags)
+    int pipe;
+    int wait_prev;                   // tiles reading halos wait for the previous epoch's data flags
+    int nrim, nstencil, nfwd;
+    unsigned int *ctr_x;
+    const unsigned int *tgt_x;
+    unsigned int *rim_ticket;
+    // x faces staged (pipelined schedule): the sender's face tiles store their x layer into the
+    // receiver's compact staging buffer [epoch parity][halo side][y][z] (z fastest: whole 32-B
+    // sectors, not one 8-B value per sector of a T2 column); the receiver's first/last x-tiles copy
+    // the previous epoch's values into their T column before their sweep, the forwarders read the
+    // current epoch's, the drain copies the last epoch's into T2
+    int xstage;
+    double *xstg;                    // mine
+    double *xstg_peer[2];            // the receivers' (indexed like face[0][rs])
 };
 
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
@@ -297,7 +316,7 @@ struct igg_grid : igg::Geom {
     bool coop = false;                                   // IGG_OPT_COOP_HALO
     bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
     std::list<std::pair<std::vector<long long>, igg::Plan>> plan_cache;   // field-list shape -> plan
-    unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr;
+    unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr, *fused_tgt_x = nullptr, *fused_tgt_pipe = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
     std::vector<std::pair<const void *, std::vector<double *>>> fused_peer_maps;   // local T2 -> peers' T2
     std::vector<unsigned short> fused_tail;                                       // tail tile order
@@ -306,6 +325,8 @@ struct igg_grid : igg::Geom {
     int fused_ntiles = 0, fused_nchunks = 0, fused_key = -1;
     int fused_zchunk[2] = {-1, -1};
     int fused_zafter = 1;
+    int fused_nfwd = 0;                                  // in-kernel forwarders (pipelined)
+    double *fused_xstg = nullptr;                        // x-face staging buffer (pipelined)
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
@@ -315,12 +336,16 @@ void exchange(igg_grid *g, const igg_field *fields, int nfields, cudaStream_t st
 void check_live(const igg_grid *g, const char *what);
 void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
                double lam, double dt, double dx, double dy, double dz, const int bw[3],
-               cudaStream_t s);
+               cudaStream_t s, bool wait_prev = false,
+               bool drain = true);
 void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap);
 int local_index(const igg_grid *g, int global_rank);   // -1 if not hosted here
 std::vector<char> allgather_bytes_pub(igg_grid *g, const void *mine, size_t bytes);
 bool fused_eligible(const igg_grid *g);
-void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s);
+// one fused step; pipelined schedule: wait_prev = the previous step of the same run was fused (its
+// halos are awaited tile by tile), drain = wait for every incoming face at the end (step complete)
+void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s,
+                bool wait_prev = false, bool drain = true);
 void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
 void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step

@@ -73,8 +73,12 @@ def init_random(grid: Grid, T, T2, Ci, seed_T=None, seed_C=None) -> None:
         T2[r].copy_(T[r])
 
 
-def run(grid: Grid, T, T2, Ci, nt: int, dt: float, d: tuple, lam: float = LAM, bw=BW, stream=None):
-    """The time loop; returns the lists (T, T2) after the swaps."""
+def run(grid: Grid, T, T2, Ci, nt: int, dt: float, d: tuple, lam: float = LAM, bw=BW, stream=None,
+        per_step: bool = False):
+    """The time loop; returns the lists (T, T2) after the swaps.  Default: one
+    igg_heat_run call (consecutive steps pipelined on the fused path); per_step: nt igg_heat_step calls."""
+    if not per_step:
+        return grid.heat_run(T, T2, Ci, lam, dt, d[0], d[1], d[2], nt, bw=bw, stream=stream)
     for _ in range(nt):
         grid.heat_step(T2, T, Ci, lam, dt, d[0], d[1], d[2], bw=bw, stream=stream)
         T, T2 = T2, T

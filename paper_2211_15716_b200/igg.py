@@ -231,6 +231,21 @@ class Grid:
         _ok(L.lib().igg_heat_step(self._handle(), _ptr_array(t2), _ptr_array(t), _ptr_array(c),
                                   lam, dt, dx, dy, dz, _i3(bw), _stream(stream)))
 
+    def heat_run(self, T, T2, Ci, lam: float, dt: float, dx: float, dy: float, dz: float, nt: int,
+                 bw=(16, 2, 2), stream=None):
+        """Fig. 1's time loop on the device (igg_heat_run): nt steps with the swap; returns the lists
+        (T, T2) after the swaps (T = the state after nt steps)."""
+        n = self.local_ranks
+        t, t2, c = (_as_list(x, n) for x in (T, T2, Ci))
+        for x in t2 + t + c:
+            if tuple(x.shape) != (self.n[2], self.n[1], self.n[0]):
+                raise ValueError("heat_run fields must have the canonical local shape (nz, ny, nx)")
+        pt, pt2 = _ptr_array(t), _ptr_array(t2)
+        _ok(L.lib().igg_heat_run(self._handle(), pt, pt2, _ptr_array(c), lam, dt, dx, dy, dz, int(nt), _i3(bw),
+                                 _stream(stream)))
+        swapped = nt % 2 == 1
+        return (list(t2), list(t)) if swapped else (list(t), list(t2))
+
     def heat_run_host(self, T_host, Ci_host, lam, dt, dx, dy, dz, nt: int, bw=(16, 2, 2), stream=None) -> None:
         """Fig. 1 end to end from host memory (numpy arrays or CPU tensors, ideally pinned);
         T_host is overwritten with the final T."""

@@ -28,7 +28,7 @@ def log(*a):
     print(f"[rank {dist.get_rank()}]", *a, flush=True)
 
 
-def heat_case(path, n, dims, per, local, bw, nt=8, opts=None):
+def heat_case(path, n, dims, per, local, bw, nt=8, opts=None, per_step=False):
     world = dist.get_world_size()
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
                            device=int(os.environ["LOCAL_RANK"]))
@@ -39,7 +39,7 @@ def heat_case(path, n, dims, per, local, bw, nt=8, opts=None):
         app.init_random(g, T, T2, Ci)
         d = app.spacing(g)
         dt = app.stable_dt(g, Ci, *d)
-        T, T2 = app.run(g, T, T2, Ci, nt, dt, d, bw=bw)
+        T, T2 = app.run(g, T, T2, Ci, nt, dt, d, bw=bw, per_step=per_step)
         torch.cuda.synchronize()
         g.check()
         N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
@@ -57,7 +57,7 @@ def heat_case(path, n, dims, per, local, bw, nt=8, opts=None):
                                      f"{int((got != W).sum())} cells differ")
     finally:
         g.finalize()
-    log("heat OK", path, dims, per, "local", local, "world", world, "opts", opts)
+    log("heat OK", path, dims, per, "local", local, "world", world, "opts", opts, "per_step", per_step)
 
 
 def halo_case(path, n, dims, per, local, sizes, seed, repeat=2):
@@ -148,7 +148,11 @@ def main():
                 heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), opts=o)
             heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=12)
             heat_case(path, (66, 40, 36), dims, (0, 1, 0), 1, (16, 2, 2), nt=9)
-            # register/smem capture of the x send layer (fused mode bit 1)
+            # single igg_heat_step calls (each drained) and the legacy multi-stream fused schedule
+            heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=5, per_step=True)
+            heat_case(path, (130, 36, 34), dims, (1, 0, 1), 1, (16, 2, 2), nt=5, opts={P.OPT_FUSED_MODE: 130})
+            heat_case(path, (130, 36, 34), dims, (1, 1, 0), 1, (16, 2, 2), nt=6, opts={P.OPT_FUSED_MODE: 258})
+            # the x send layer stored from inside the sweep (fused mode bit 1)
             heat_case(path, (130, 36, 70), dims, (1, 1, 1), 1, (16, 2, 2), nt=5, opts={P.OPT_FUSED_MODE: 3})
             # the fused put path on every split axis (z faces, corner forwarding x->y->z)
             extra = {2: [(1, 2, 1), (1, 1, 2)], 4: [(2, 1, 2), (1, 2, 2), (4, 1, 1), (1, 1, 4)]}.get(world, [])

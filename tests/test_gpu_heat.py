@@ -186,3 +186,32 @@ def test_box_kernel_variants_bit_exact(variant):
                             options={P.OPT_STENCIL_KERNEL: variant})
     can1, _ = oracle_global((130, 44, 70), per, 5)
     assert np.array_equal(out1[0], can1)
+
+
+@pytest.mark.parametrize("per", [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1)])
+@pytest.mark.parametrize("mode", [2, 258])
+def test_fused_self_wrap_one_gpu(per, mode):
+    """Periodic axes wrapping onto the one process run the fused P2P path with the rank as its own
+    neighbour (faces stored into its own halos; staged or direct x faces); heat_run (pipelined) and
+    single steps both bit-exact vs the periodic global oracle."""
+    import torch
+    n = (130, 36, 34)
+    N = tuple(OG.global_size(n[i], 2, 1, bool(per[i])) for i in range(3))
+    ref, dtr = oracle_global(N, per, 7)
+    for per_step in (False, True):
+        g = P.init_global_grid(*n, periods=per, local_ranks=1, device=0, path=P.PATH_P2P)
+        try:
+            g.set_option(P.OPT_FUSED_MODE, mode)
+            T, T2, Ci = app.alloc_fields(g)
+            app.init_random(g, T, T2, Ci)
+            d = app.spacing(g)
+            dt = app.stable_dt(g, Ci, *d)
+            assert dt == dtr
+            l0 = g.kernel_launches()
+            T, T2 = app.run(g, T, T2, Ci, 7, dt, d, per_step=per_step)
+            torch.cuda.synchronize()
+            g.check()
+            assert g.kernel_launches() - l0 <= (7 * 2 if per_step else 8)   # one launch per step (+ drains)
+            assert_windows([T[0].cpu().numpy()], ref, (1, 1, 1), n, (2, 2, 2), per)
+        finally:
+            g.finalize()
