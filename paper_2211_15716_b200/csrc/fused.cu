@@ -43,6 +43,10 @@ __device__ __forceinline__ void cp_async16f(void *smem, const void *gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -152,23 +156,30 @@ constexpr int kFKC = 64;   // longest z-chunk
 // re-read the column from DRAM.
 template <bool CAP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[32 * kFTY], double2 (*sC)[32 * kFTY],
-                                            double *xdst, int tid, int lane, int zs, int ze, long long i,
-                                            long long sxy, int sx, bool pair_in, bool w0, bool w1, int xl,
-                                            bool xodd) {
+                                            double (*sH)[kFTY], double *xdst, int tid, int lane, int zs, int ze,
+                                            long long i, long long sxy, int sx, bool pair_in, bool w0, bool w1,
+                                            int xl, bool xodd, const double *xr, int xrl, bool xrhi) {
     const double *__restrict__ T = F.T;
     const double *__restrict__ Ci = F.Ci;
     double *__restrict__ T2 = F.T2;
+    const int warp = tid >> 5;
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
             cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
             cp_async16f(&sC[q][tid], Ci + i + q * sxy);
+            // CAP, halo-reading lane: its x halo cell of plane zs+q+1 from the staging row (not in T)
+            if (CAP && lane == xrl) cp_async8(&sH[q][warp], xr + zs + q + 1);
         }
         cp_commit();
     }
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
+    if (CAP && lane == xrl) {
+        const double h = __ldcg(xr + zs);
+        if (xrhi) c.y = h; else c.x = h;
+    }
     int slot = 0;
     {
 #pragma unroll 2
@@ -196,9 +207,14 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[
             if (CAP && lane == xl) xdst[z] = xodd ? r1 : r0;   // the receiver's staging row
             zm = c;
             c = zp;
+            if (CAP && lane == xrl) {
+                const double h = sH[slot][warp];
+                if (xrhi) c.y = h; else c.x = h;
+            }
             if (pair_in && z + kFD < ze) {
                 cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
                 cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
+                if (CAP && lane == xrl) cp_async8(&sH[slot][warp], xr + z + kFD + 1);
             }
             cp_commit();
             slot = slot + 1 == kFD ? 0 : slot + 1;
@@ -231,6 +247,7 @@ __device__ __forceinline__ int4 fused_tile(const FusedParams &F, int b) {
 // z: the chunks holding planes 1 and s_z-2).  The same wait orders my face stores of this epoch
 // after the neighbour's reads of the halo they overwrite: the neighbour's tiles that read that halo
 // are the ones that published the awaited face (hazard argument).
+template <bool XS>
 __device__ __forceinline__ void fused_wait_halos(const FusedParams &F, int4 td, int zs, int ze) {
     const bool xlo = F.halo[0][0].active && td.x == 0, xhi = F.halo[0][1].active && td.x == F.xtiles - 1;
     if (threadIdx.x == 0) {
@@ -243,7 +260,7 @@ __device__ __forceinline__ void fused_wait_halos(const FusedParams &F, int4 td, 
         if (F.halo[2][1].active && ze == F.s[2] - 1) spin_geq(F, F.halo[2][1].flag, prev);
     }
     __syncthreads();
-    if (F.xstage && (xlo || xhi)) {
+    if (!XS && F.xstage && (xlo || xhi)) {   // (XS: read from the staging row inside the sweep)
         // my x halo column of this tile (its rows, its chunk's planes), staged by the neighbour in the
         // previous epoch -- final since the awaited flag -- into my T, just before the sweep reads it
         // (writing whole 32-B sectors instead, halo cell plus its row neighbours, measured slower)
@@ -287,6 +304,7 @@ template <bool XS>   // XS: the x send layer goes to the neighbour from the swee
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
+    __shared__ double sH[XS ? kFD : 1][kFTY];   // XS: the halo-reading lanes' staged x halo cells
     int b = blockIdx.x;
     if (F.pipe) {   // pipelined schedule: rim blocks first, forwarders last (CTA-uniform)
         if (b < F.nrim || b >= F.nrim + F.nstencil) {
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         face_tile |= F.face[1][rs].active && yl >= 1 + td.y * kFTY && yl < min(1 + (td.y + 1) * kFTY, sy - 1);
         face_tile |= F.face[2][rs].active && F.zchunk[rs] == td.z;
     }
-    if (F.wait_prev) fused_wait_halos(F, td, zs, ze);   // CTA-uniform
+    if (F.wait_prev) fused_wait_halos<XS>(F, td, zs, ze);   // CTA-uniform
     long long i = (long long)zs * sxy + (long long)y * sx + p;
     // XS: the x send-layer cell of my row (lane xl, cell xodd of its pair) goes to the neighbour
     // plane by plane from the sweep (xdst + i = its halo cell of my row and plane)
@@ -331,7 +349,23 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             if (lane == xl) xdst = F.xstg_peer[rs] + xstg_at(F, F.epoch, rs, y, 0);
         }
     }
-    fused_sweep<XS>(F, sT, sC, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd);
+    // XS with staged x faces and a previous epoch: the halo-reading lane takes its x halo cell from the
+    // staging row inside the sweep (no copy into T in the prologue)
+    const double *xr = nullptr;
+    int xrl = -1;
+    bool xrhi = false;
+    if (XS && F.xstage && F.wait_prev && y < sy - 1) {
+        if (F.halo[0][0].active && td.x == 0) {
+            xrl = 0;
+            xr = F.xstg + xstg_at(F, F.epoch - 1, 0, y, 0);
+        } else if (F.halo[0][1].active && td.x == F.xtiles - 1) {
+            const int L = sx - 1 - td.x * 64;
+            xrl = L >> 1;
+            xrhi = L & 1;
+            xr = F.xstg + xstg_at(F, F.epoch - 1, 1, y, 0);
+        }
+    }
+    fused_sweep<XS>(F, sT, sC, sH, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd, xr, xrl, xrhi);
     if (!face_tile) return;   // CTA-uniform
     double *__restrict__ T2 = F.T2;
     __syncthreads();          // the CTA's T2 stores are visible to the CTA
