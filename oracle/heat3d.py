@@ -80,7 +80,11 @@ def set_threads(n: int) -> None:
 
 def spacing(l: float, N: int, periodic: bool) -> float:
     """dx = lx/(nx_g()-1) on non-periodic axes; dx = lx/N on a
-    periodic axis, where N is the period (reading 11)."""
+    periodic axis, where N is the period (reading 11); an axis of
+    size 1 (1-D/2-D grid) has no spacing: inf, so it drops out of
+    stable_dt's minimum (reading 23)."""
+    if N == 1 and not periodic:
+        return float("inf")
     return l / N if periodic else l / (N - 1)
 
 

@@ -31,6 +31,10 @@
  *     (reading 11 / SPEC.md:98).
  *   - IEEE binary64, round to nearest even, compiled with -ffp-contract=off
  *     (no FMA contraction) and without -ffast-math (reading 8).
+ *   - 1-D/2-D grids are 3-D grids with size-1 axes: an axis with
+ *     N == 1 has no second difference (its term is absent from the sum, the
+ *     others keep their x, y, z order) and its single layer is updated
+ *     (reading 23).
  *
  * Layout: x fastest: index(x,y,z) = (z*Ny + y)*Nx + x.
  * OpenMP (if compiled with -fopenmp) splits the z loop only; it never changes
@@ -64,9 +68,11 @@ void oracle_heat_step(double *T2, const double *T, const double *Ci,
                       double lam, double dt, double dx, double dy, double dz,
                       int mode)
 {
-    const long xa = px ? 0 : 1, xb = px ? Nx : Nx - 1;
-    const long ya = py ? 0 : 1, yb = py ? Ny : Ny - 1;
-    const long za = pz ? 0 : 1, zb = pz ? Nz : Nz - 1;
+    /* an axis of size 1 (a 1-D/2-D grid) is updated on its one layer, without a term */
+    const int ax = Nx > 1, ay = Ny > 1, az = Nz > 1;
+    const long xa = (px || !ax) ? 0 : 1, xb = (px || !ax) ? Nx : Nx - 1;
+    const long ya = (py || !ay) ? 0 : 1, yb = (py || !ay) ? Ny : Ny - 1;
+    const long za = (pz || !az) ? 0 : 1, zb = (pz || !az) ? Nz : Nz - 1;
     const double dx2 = dx * dx, dy2 = dy * dy, dz2 = dz * dz;
     const double rdx2 = 1.0 / dx2, rdy2 = 1.0 / dy2, rdz2 = 1.0 / dz2;
     long z;
@@ -75,21 +81,34 @@ void oracle_heat_step(double *T2, const double *T, const double *Ci,
         for (long y = ya; y < yb; ++y) {
             for (long x = xa; x < xb; ++x) {
                 const double c  = T[IDX(x, y, z, Nx, Ny)];
-                const double xm = T[IDX(nb(x, -1, Nx, px), y, z, Nx, Ny)];
-                const double xp = T[IDX(nb(x, +1, Nx, px), y, z, Nx, Ny)];
-                const double ym = T[IDX(x, nb(y, -1, Ny, py), z, Nx, Ny)];
-                const double yp = T[IDX(x, nb(y, +1, Ny, py), z, Nx, Ny)];
-                const double zm = T[IDX(x, y, nb(z, -1, Nz, pz), Nx, Ny)];
-                const double zp = T[IDX(x, y, nb(z, +1, Nz, pz), Nx, Ny)];
-                /* @d2_xi, @d2_yi, @d2_zi */
-                const double d2x = (xp - c) - (c - xm);
-                const double d2y = (yp - c) - (c - ym);
-                const double d2z = (zp - c) - (c - zm);
-                double lap;
-                if (mode == 0)
-                    lap = ((d2x / dx2) + (d2y / dy2)) + (d2z / dz2);
-                else
-                    lap = ((d2x * rdx2) + (d2y * rdy2)) + (d2z * rdz2);
+                /* @d2_xi, @d2_yi, @d2_zi, each as (a/d^2) or (a*r) by mode,
+                   summed left to right over the axes that have extent */
+                double lap = 0.0;
+                int first = 1;
+                if (ax) {
+                    const double xm = T[IDX(nb(x, -1, Nx, px), y, z, Nx, Ny)];
+                    const double xp = T[IDX(nb(x, +1, Nx, px), y, z, Nx, Ny)];
+                    const double d2x = (xp - c) - (c - xm);
+                    const double t = mode == 0 ? d2x / dx2 : d2x * rdx2;
+                    lap = first ? t : lap + t;
+                    first = 0;
+                }
+                if (ay) {
+                    const double ym = T[IDX(x, nb(y, -1, Ny, py), z, Nx, Ny)];
+                    const double yp = T[IDX(x, nb(y, +1, Ny, py), z, Nx, Ny)];
+                    const double d2y = (yp - c) - (c - ym);
+                    const double t = mode == 0 ? d2y / dy2 : d2y * rdy2;
+                    lap = first ? t : lap + t;
+                    first = 0;
+                }
+                if (az) {
+                    const double zm = T[IDX(x, y, nb(z, -1, Nz, pz), Nx, Ny)];
+                    const double zp = T[IDX(x, y, nb(z, +1, Nz, pz), Nx, Ny)];
+                    const double d2z = (zp - c) - (c - zm);
+                    const double t = mode == 0 ? d2z / dz2 : d2z * rdz2;
+                    lap = first ? t : lap + t;
+                    first = 0;
+                }
                 const double ci = Ci[IDX(x, y, z, Nx, Ny)];
                 T2[IDX(x, y, z, Nx, Ny)] = c + dt * ((lam * ci) * lap);
             }

@@ -173,3 +173,56 @@ def test_c_oracle_matches_pure_python_transcription(per, mode):
     a = H.heat_run(T0, Ci, 3, per, 1.0, dt, *d, mode)
     b = H.heat_run_py(T0, Ci, 3, per, 1.0, dt, *d, mode)
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("N,k,per", [((14, 12, 1), (1, 2, 0), (0, 0, 0)),      # 2-D (size-1 z)
+                                     ((20, 1, 1), (3, 0, 0), (0, 0, 0)),       # 1-D
+                                     ((12, 1, 9), (2, 0, 1), (1, 0, 0)),       # 2-D x-z, x periodic
+                                     ((1, 16, 11), (0, 2, 1), (0, 0, 0))])     # 2-D y-z
+@pytest.mark.parametrize("mode", [H.LITERAL, H.CANONICAL])
+def test_fourier_mode_low_dimensional(N, k, per, mode):
+    """1-D/2-D grids as size-1 axes (reading 23): the discrete mode decays with only the extended
+    axes' factors; a size-1 axis contributes no term and its one layer is updated."""
+    L = (1.0, 0.8, 1.2); lam = 1.1; c = 0.5; nt = 80; A = 0.3
+    d = [H.spacing(L[i], N[i], bool(per[i])) for i in range(3)]
+    prof = []
+    for i in range(3):
+        g = np.arange(N[i])
+        if N[i] == 1:
+            prof.append(np.ones(1))
+        elif per[i]:
+            prof.append(np.cos(2 * np.pi * k[i] * g / N[i]))
+        else:
+            s = np.sin(k[i] * np.pi * g / (N[i] - 1)); s[[0, -1]] = 0.0
+            prof.append(s)
+    M = prof[2][:, None, None] * prof[1][None, :, None] * prof[0][None, None, :]
+    T0 = 1.7 + A * M
+    Ci = np.full(T0.shape, c)
+    dt = H.stable_dt(d[0], d[1], d[2], lam, Ci)
+    assert dt == min(d[i] ** 2 for i in range(3) if N[i] > 1) / lam / c / 6.1
+    out = H.heat_run(T0, Ci, nt, per, lam, dt, d[0], d[1], d[2], mode)
+    lamk = 0.0
+    for i in range(3):
+        if N[i] == 1:
+            continue
+        arg = math.pi * k[i] / N[i] if per[i] else k[i] * math.pi / (2 * (N[i] - 1))
+        lamk += 4.0 / d[i] ** 2 * math.sin(arg) ** 2
+    Gf = 1.0 - dt * lam * c * lamk
+    expect = 1.7 + A * Gf ** nt * M
+    assert Gf ** nt < 0.9
+    assert np.max(np.abs(out - expect)) <= 1e-14
+
+
+def test_size1_axis_equals_lower_dimensional_grid():
+    """A 3-D grid with a size-1 z equals the same 2-D grid embedded with nz = 3 whose z neighbours
+    equal the middle layer (d2z = 0 exactly): every cell, bit for bit, in canonical mode."""
+    rng = np.random.default_rng(3)
+    T2d = 1.7 + rng.random((1, 9, 11)); C2d = 0.5 + 0.2 * rng.random((1, 9, 11))
+    d = (0.1, 0.13, float("inf"))
+    dt = H.stable_dt(*d, 1.0, C2d)
+    a = H.heat_run(T2d, C2d, 5, (0, 0, 0), 1.0, dt, *d, H.CANONICAL)
+    T3 = np.repeat(T2d, 3, axis=0); C3 = np.repeat(C2d, 3, axis=0)
+    # z periodic with three equal layers: d2z = (c - c) - (c - c) = 0 exactly, x/y terms identical
+    b = H.heat_run(T3, C3, 5, (0, 0, 1), 1.0, dt, d[0], d[1], 1.0, H.CANONICAL)
+    # the 3-D sum adds (d2z*rdz2) = +0.0 last: x + y + 0.0 == x + y exactly
+    assert np.array_equal(a[0], b[1])
