@@ -306,12 +306,12 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     __shared__ double2 sC[kFD][32 * kFTY];
     __shared__ double sH[XS ? kFD : 1][kFTY];   // XS: the halo-reading lanes' staged x halo cells
     int b = blockIdx.x;
-    if (F.pipe) {   // pipelined schedule: rim blocks first, forwarders last (CTA-uniform)
-        if (b < F.nrim || b >= F.nrim + F.nstencil) {
+    if (F.pipe) {   // pipelined schedule: rim blocks, then the forwarders, then the tiles (CTA-uniform)
+        if (b < F.nrim + F.nfwd) {
             fused_extra(F, b);
             return;
         }
-        b -= F.nrim;
+        b -= F.nrim + F.nfwd;
     }
     const int4 td = fused_tile(F, b);
     const int2 zr = chunk_range(F, td.z);
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(128) fused_comm_kernel(const __grid_constant__
 
 // The rim and forwarding roles of the pipelined schedule, as extra blocks of the stencil launch.
 // Rim (blocks [0, nrim), six faces x nrim/6 blocks): the rim cells of every face (fused_rim_kernel's
-// work); the last rim block counts once on every (face, chunk).  Forwarders (the last nfwd blocks):
+// work); the last rim block counts once on every (face, chunk).  Forwarders (the next nfwd blocks):
 // per chunk, wait for the x (then y) halo of the chunk -- its data and its rim/forwarded cells --
 // forward the edge lines (fused_comm_kernel's work) and count on the later faces' xflags.
 __device__ __noinline__ void fused_extra(const FusedParams &F, int b) {
@@ -666,7 +666,8 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, int b) {
         }
         return;
     }
-    const int q = b - F.nrim - F.nstencil;   // forwarder q of nfwd
+    const int q = b - F.nrim;   // forwarder q of nfwd (launched right after the rim: they wait chunk by
+                                // chunk, so each edge line leaves as soon as its halo has arrived)
     for (int ch = 0; ch < F.nchunks; ++ch) {
         const int2 zr = ext_range(F, ch);
         for (int hb = 0; hb < 2; ++hb) {

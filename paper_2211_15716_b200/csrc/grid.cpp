@@ -355,10 +355,29 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
                bool drain) {
     for (int lr = 0; lr < g->nlocal; ++lr)
         if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "heat_step: NULL field pointer");
-    for (int a = 0; a < 3; ++a)
-        if (g->n[a] < 3) fail(IGG_E_ARG, "heat_step: every axis needs at least 3 cells");
+    bool lowdim = false;
+    for (int a = 0; a < 3; ++a) {
+        if (g->n[a] == 2) fail(IGG_E_ARG, "heat_step: an axis needs 1 (size-1 axis) or at least 3 cells");
+        lowdim = lowdim || g->n[a] == 1;
+    }
     // reciprocals computed once on the host (reading 9, canonical form)
     const HeatCoef k{lam, dt, 1.0 / (dx * dx), 1.0 / (dy * dy), 1.0 / (dz * dz)};
+    if (lowdim) {
+        // 1-D/2-D grid (size-1 axes, reading 23): the low-dimensional stencil on the
+        // whole updated box, then update_halo (sequential schedule)
+        std::vector<igg_field> f(g->nlocal);
+        for (int lr = 0; lr < g->nlocal; ++lr) f[lr] = igg_field{T2[lr], {g->n[0], g->n[1], g->n[2]}};
+        IGG_CUDA(cudaEventRecord(g->ev_start, s));
+        IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
+        for (int lr = 0; lr < g->nlocal; ++lr) {
+            launch_heat_lowdim(T2[lr], T[lr], Ci[lr], g->n, k, g->s_comm);
+            g->launches++;
+        }
+        exchange(g, f.data(), 1, g->s_comm);
+        IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+        IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+        return;
+    }
     bool exch[3] = {false, false, false};
     bool any = false;
     for (int a = 0; a < 3; ++a)
@@ -678,9 +697,19 @@ static void hide_comm(igg_grid *g, const int bw_in[3], const RegionFn &fn, const
         const int b = exch[a] ? bw[a] : 0;
         lo[a] = std::max(1, b);
         hi[a] = std::min(g->n[a] - 1, g->n[a] - b);
+        if (g->n[a] == 1) {   // a size-1 axis (1-D/2-D grid): its one layer, no slabs along it
+            lo[a] = 0;
+            hi[a] = 1;
+        }
         if (hi[a] <= lo[a]) degenerate = true;
     }
-    const int full_lo[3] = {1, 1, 1}, full_hi[3] = {g->n[0] - 1, g->n[1] - 1, g->n[2] - 1};
+    // the computed box per axis: inner layers, or the one layer of a size-1 axis
+    int L[3], H[3];
+    for (int a = 0; a < 3; ++a) {
+        L[a] = g->n[a] == 1 ? 0 : 1;
+        H[a] = g->n[a] == 1 ? 1 : g->n[a] - 1;
+    }
+    const int full_lo[3] = {L[0], L[1], L[2]}, full_hi[3] = {H[0], H[1], H[2]};
     IGG_CUDA(cudaEventRecord(g->ev_start, s));
     IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
     if (seq || degenerate) {
@@ -691,11 +720,10 @@ static void hide_comm(igg_grid *g, const int bw_in[3], const RegionFn &fn, const
         return;
     }
     IGG_CUDA(cudaStreamWaitEvent(g->s_inner, g->ev_start, 0));
-    const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
     // the six slabs x-lo, x-hi, y-lo, y-hi, z-lo, z-hi, each cell exactly once
-    const int slab[6][6] = {{1, lo[0], 1, n1 - 1, 1, n2 - 1},           {hi[0], n0 - 1, 1, n1 - 1, 1, n2 - 1},
-                            {lo[0], hi[0], 1, lo[1], 1, n2 - 1},         {lo[0], hi[0], hi[1], n1 - 1, 1, n2 - 1},
-                            {lo[0], hi[0], lo[1], hi[1], 1, lo[2]},      {lo[0], hi[0], lo[1], hi[1], hi[2], n2 - 1}};
+    const int slab[6][6] = {{L[0], lo[0], L[1], H[1], L[2], H[2]},       {hi[0], H[0], L[1], H[1], L[2], H[2]},
+                            {lo[0], hi[0], L[1], lo[1], L[2], H[2]},     {lo[0], hi[0], hi[1], H[1], L[2], H[2]},
+                            {lo[0], hi[0], lo[1], hi[1], L[2], lo[2]},   {lo[0], hi[0], lo[1], hi[1], hi[2], H[2]}};
     for (int lr = 0; lr < g->nlocal; ++lr)
         for (int k = 0; k < 6; ++k) {
             const int a0[3] = {slab[k][0], slab[k][2], slab[k][4]}, a1[3] = {slab[k][1], slab[k][3], slab[k][5]};

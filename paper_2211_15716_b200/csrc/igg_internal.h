@@ -158,7 +158,7 @@ struct FusedParams {
     int *err;
     HeatCoef k;
     // pipelined schedule (one launch per step on the caller's stream): blocks [0, nrim) send the rim,
-    // [nrim, nrim + nstencil) are the stencil tiles, the last nfwd forward the edge lines; face tiles
+    // the next nfwd forward the edge lines, the rest are the stencil tiles; face tiles
     // count on ctr/tgt (data flags), rim and forwarders on ctr_x/tgt_x (xflags)
     int pipe;
     int wait_prev;                   // tiles reading halos wait for the previous epoch's data flags
@@ -203,6 +203,9 @@ void launch_heat_slabs(HeatRegionList &L, cudaStream_t s);
 // the production stencil: cp.async-pipelined z-sweep over a list of box regions
 // (all local ranks' inner boxes, or the boundary slabs), one launch
 void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant);
+// 1-D/2-D grid (size-1 axes): the stencil without the size-1 axes' terms on the updated box
+void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int n[3], const HeatCoef &k,
+                        cudaStream_t s);
 // vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field
 bool heat_box_vectorizable(const HeatRegion &r);
 void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant);

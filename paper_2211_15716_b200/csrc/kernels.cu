@@ -30,6 +30,56 @@ __device__ __forceinline__ double heat_cell(double c, double xm, double xp, doub
     return __dadd_rn(c, __dmul_rn(k.dt, __dmul_rn(__dmul_rn(k.lam, ci), lap)));
 }
 
+// ============================================================== 1-D / 2-D grids
+// A size-1 axis (reading 23) has no second difference: the Laplacian sums the
+// extended axes' terms in x, y, z order (left to right), and its one layer is updated.  One thread per
+// cell of the updated box (inner layers of the extended axes), x fastest.
+__global__ void __launch_bounds__(256) heat_lowdim_kernel(double *__restrict__ T2, const double *__restrict__ T,
+                                                          const double *__restrict__ Ci, int nx, int ny, int nz,
+                                                          const HeatCoef k) {
+    const int ax = nx > 1, ay = ny > 1, az = nz > 1;
+    const int wx = ax ? nx - 2 : 1, wy = ay ? ny - 2 : 1, wz = az ? nz - 2 : 1;
+    const long long cells = (long long)wx * wy * wz;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < cells;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(t % wx) + ax, y = (int)((t / wx) % wy) + ay, z = (int)(t / ((long long)wx * wy)) + az;
+        const long long sx = nx, sxy = (long long)nx * ny;
+        const long long i = z * sxy + y * sx + x;
+        const double c = T[i];
+        double lap = 0.0;
+        bool first = true;
+        if (ax) {
+            const double d2 = __dsub_rn(__dsub_rn(T[i + 1], c), __dsub_rn(c, T[i - 1]));
+            const double tt = __dmul_rn(d2, k.rdx2);
+            lap = first ? tt : __dadd_rn(lap, tt);
+            first = false;
+        }
+        if (ay) {
+            const double d2 = __dsub_rn(__dsub_rn(T[i + sx], c), __dsub_rn(c, T[i - sx]));
+            const double tt = __dmul_rn(d2, k.rdy2);
+            lap = first ? tt : __dadd_rn(lap, tt);
+            first = false;
+        }
+        if (az) {
+            const double d2 = __dsub_rn(__dsub_rn(T[i + sxy], c), __dsub_rn(c, T[i - sxy]));
+            const double tt = __dmul_rn(d2, k.rdz2);
+            lap = first ? tt : __dadd_rn(lap, tt);
+            first = false;
+        }
+        T2[i] = __dadd_rn(c, __dmul_rn(k.dt, __dmul_rn(__dmul_rn(k.lam, Ci[i]), lap)));
+    }
+}
+
+void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int n[3], const HeatCoef &k,
+                        cudaStream_t s) {
+    const long long cells = (long long)(n[0] > 1 ? n[0] - 2 : 1) * (n[1] > 1 ? n[1] - 2 : 1) *
+                            (n[2] > 1 ? n[2] - 2 : 1);
+    if (cells <= 0) return;
+    const int blocks = (int)std::min<long long>((cells + 255) / 256, 148LL * 16);
+    heat_lowdim_kernel<<<blocks, 256, 0, s>>>(T2, T, Ci, n[0], n[1], n[2], k);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ============================================================== generic region kernel
 // One thread per (x,y) column of a region, sweeping a chunk of kRegKc planes in
 // z with a register queue (T[z-1], T[z], T[z+1]); x/y neighbours come through

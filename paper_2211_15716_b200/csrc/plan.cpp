@@ -24,6 +24,10 @@ Geom make_geom(const igg_init_args *A) {
         g.periods[a] = A->periods[a] ? 1 : 0;
         if (g.o[a] < 2 || g.o[a] % 2)
             fail(IGG_E_ARG, "init: overlap must be even and >= 2 (axis " + std::to_string(a) + ")");
+        if (n[a] == 1) {   // a 1-D/2-D grid: a size-1 axis, one process along it, no halo
+            if (g.periods[a]) fail(IGG_E_ARG, "init: a size-1 axis cannot be periodic (axis " + std::to_string(a) + ")");
+            continue;
+        }
         if (n[a] <= g.o[a])
             fail(IGG_E_ARG, "init: local size " + std::to_string(n[a]) + " must exceed the overlap " +
                                 std::to_string(g.o[a]) + " (axis " + std::to_string(a) + ")");
@@ -33,6 +37,10 @@ Geom make_geom(const igg_init_args *A) {
         fail(IGG_E_ARG, "init: inconsistent nprocs/rank0/local_ranks");
     if (A->path != IGG_PATH_NCCL && A->path != IGG_PATH_P2P) fail(IGG_E_ARG, "init: unknown path");
     int d[3] = {A->dims[0], A->dims[1], A->dims[2]};
+    for (int a = 0; a < 3; ++a) {
+        if (n[a] == 1 && d[a] == 0) d[a] = 1;   // a size-1 axis is never split
+        if (n[a] == 1 && d[a] != 1) fail(IGG_E_ARG, "init: a size-1 axis must have dims 1 (axis " + std::to_string(a) + ")");
+    }
     if (d[0] == 0 || d[1] == 0 || d[2] == 0) {   // automatic topology
         if (dims_create(A->nprocs, d, d) != 0) fail(IGG_E_ARG, "init: no topology honours the given dims");
     }

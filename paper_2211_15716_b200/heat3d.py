@@ -24,7 +24,10 @@ def spacing(grid: Grid, lengths=(LX, LY, LZ)) -> tuple:
     out = []
     for a in range(3):
         N = grid.n_global(a)
-        out.append(lengths[a] / N if grid.periods[a] else lengths[a] / (N - 1))
+        if N == 1 and not grid.periods[a]:   # a size-1 axis (1-D/2-D grid): no spacing (reading 23)
+            out.append(float("inf"))
+        else:
+            out.append(lengths[a] / N if grid.periods[a] else lengths[a] / (N - 1))
     return tuple(out)
 
 

@@ -215,3 +215,35 @@ def test_fused_self_wrap_one_gpu(per, mode):
             assert_windows([T[0].cpu().numpy()], ref, (1, 1, 1), n, (2, 2, 2), per)
         finally:
             g.finalize()
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=(24, 20, 1), dims=(2, 2, 1), per=(0, 1, 0)),   # 2-D (x-y), y periodic
+    dict(n=(30, 1, 1), dims=(3, 1, 1), per=(1, 0, 0)),    # 1-D, periodic
+    dict(n=(1, 18, 16), dims=(1, 2, 2), per=(0, 0, 0)),   # 2-D (y-z)
+    dict(n=(70, 36, 1), dims=(1, 1, 1), per=(0, 0, 0)),   # 2-D, one rank
+    dict(n=(20, 1, 14), dims=(2, 1, 1), per=(0, 0, 1)),   # 2-D (x-z), z periodic self-wrap
+])
+def test_low_dimensional_grids(case):
+    """1-D/2-D grids as size-1 axes (reading 23): heat steps with update_halo on virtual
+    topologies, bit-exact vs the canonical oracle on the global grid."""
+    n, dims, per = case["n"], case["dims"], case["per"]
+    N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+    out, dt, _, _ = gpu_run(P, app, n, dims, per, (2, 2, 2), 6, (4, 2, 2))
+    ref, dtr = oracle_global(N, per, 6)
+    assert dt == dtr
+    assert_windows(out, ref, dims, n, (2, 2, 2), per)
+
+
+def test_low_dimensional_init_rules():
+    g = P.init_global_grid(24, 20, 1, local_ranks=4, device=0)   # automatic dims never split a size-1 axis
+    try:
+        assert g.dims[2] == 1 and g.dims[0] * g.dims[1] == 4 and g.nz_g() == 1
+    finally:
+        g.finalize()
+    with pytest.raises(P.IggError) as e:
+        P.init_global_grid(24, 20, 1, periods=(0, 0, 1), local_ranks=1, device=0)
+    assert e.value.name == "IGG_E_ARG"
+    with pytest.raises(P.IggError) as e:
+        P.init_global_grid(24, 20, 1, dims=(1, 1, 2), local_ranks=2, device=0)
+    assert e.value.name == "IGG_E_ARG"
