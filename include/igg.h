@@ -288,9 +288,12 @@ enum {
                                     re-order table, 64 = visit the upper z-face chunk second,
                                     128 = legacy multi-stream schedule (rim / receive kernels on
                                     comm streams joined by events) instead of the pipelined one,
-                                    256 = x faces pulled by the receiver instead of pushed */
-    IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8 with one
-                                    exchanging axis, 16 with more) */
+                                    256 = x faces stored straight into the receiver's T2 column
+                                    instead of its staging buffer, 512 = no forwarders (timing,
+                                    INVALID edge cells), 1024 = single forwarding steps stay on the
+                                    pipelined schedule */
+    IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8; 16 on the
+                                    legacy schedule with more than one exchanging axis) */
     IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */
     IGG_OPT_COOP_HALO = 11,      /* 1: update_halo without NCCL messages runs as one cooperative kernel
                                     (grid barriers between axes); 0 (default, measured faster): per-axis launches */

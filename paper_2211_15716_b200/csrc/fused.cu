@@ -764,11 +764,13 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
         IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false>, 32 * kFTY, 0));
         IGG_CUDA(cudaDeviceGetAttribute(&g_fused_nsm, cudaDevAttrMultiProcessorCount, g->device));
     }
-    // tail chunk planes: short chunks shorten the last wave, but every chunk adds one hop to the
-    // per-chunk forwarding chain when several axes exchange (measured: 8 for one axis, 16 for more)
+    // tail chunk planes: short chunks shorten the last wave; on the legacy schedule every chunk also
+    // adds one hop to the receive side's forwarding chain when several axes exchange (measured there:
+    // 8 for one axis, 16 for more); the pipelined schedule keeps forwarding off the critical path: 8
     int naxes = 0;
     for (int a = 0; a < 3; ++a) naxes += (act[a][0] || act[a][1]) ? 1 : 0;
-    const int kc1 = kFKC, kc2 = g->fused_kc2 > 0 ? g->fused_kc2 : (naxes <= 1 ? 8 : 16);
+    const bool legacy = (g->fused_mode & 128) != 0;
+    const int kc1 = kFKC, kc2 = g->fused_kc2 > 0 ? g->fused_kc2 : ((naxes <= 1 || !legacy) ? 8 : 16);
     const long long ntile = (long long)xtiles * ytiles;
     int small = (int)((2LL * g_fused_occ * g_fused_nsm * kc2 + ntile - 1) / ntile);
     small = std::min(((small + kc2 - 1) / kc2) * kc2, wz);
@@ -825,7 +827,8 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
         yh = yh || g->nbr[0][1][sd] >= 0;
     }
     const bool yf = act[1][0] || act[1][1], zf = act[2][0] || act[2][1];
-    const bool need_fwd = (xh && (yf || zf)) || (yh && zf);
+    // (fused_mode bit 512: timing experiment without forwarders -- edge/corner halo cells INVALID)
+    const bool need_fwd = ((xh && (yf || zf)) || (yh && zf)) && !(g->fused_mode & 512);
     g->fused_nfwd = need_fwd ? g->fused_ncomm : 0;
     const unsigned nf = (unsigned)g->fused_nfwd;
     std::vector<unsigned> tgt_d(6 * kMaxChunks, 0u), tgt_x(6 * kMaxChunks, 0u);
@@ -1018,15 +1021,20 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
     F.zchunk[1] = g->fused_zchunk[1];
     F.tgt = g->fused_tgt;
 
-    if (!(g->fused_mode & 128)) {
-        // pipelined schedule (default): ONE launch on the caller's stream -- rim blocks, stencil
-        // tiles, forwarders -- and, when the step must be complete on return, a one-block drain
+    // a single complete step that needs edge forwarding runs the multi-stream schedule (its receive
+    // kernels forward while the stencil runs; measured faster than in-kernel forwarders for one step)
+    const bool single_fwd = !wait_prev && drain && g->fused_nfwd > 0 && !(g->fused_mode & 1024);
+    if (!(g->fused_mode & 128) && !single_fwd) {
+        // pipelined schedule (default): ONE launch on the caller's stream and, when the step must be
+        // complete on return, a drain.  The rim cells and the forwarded edge lines are never read by
+        // the stencil, so only the step that completes a run sends them (rim blocks + forwarders in
+        // its launch); the steps before it move only the faces the next step's tiles read.
         const bool recv = comm && !(g->fused_mode & 4);   // mode bit 4: timing without receive side
         F.pipe = 1;
         F.wait_prev = (wait_prev && recv) ? 1 : 0;
-        F.nrim = comm ? 48 : 0;
+        F.nrim = (comm && drain) ? 48 : 0;
         F.nstencil = g->fused_ntiles;
-        F.nfwd = recv ? g->fused_nfwd : 0;
+        F.nfwd = (recv && drain) ? g->fused_nfwd : 0;
         F.tgt = g->fused_tgt_pipe;
         F.ctr_x = g->fused_ctr + 6 * kMaxChunks;
         F.tgt_x = g->fused_tgt_x;

@@ -211,7 +211,9 @@ def test_fused_self_wrap_one_gpu(per, mode):
             T, T2 = app.run(g, T, T2, Ci, 7, dt, d, per_step=per_step)
             torch.cuda.synchronize()
             g.check()
-            assert g.kernel_launches() - l0 <= (7 * 2 if per_step else 8)   # one launch per step (+ drains)
+            # one launch per step and one drain per run; single steps with edge forwarding use the
+            # multi-stream schedule (rim, stencil, two receive kernels)
+            assert g.kernel_launches() - l0 <= (7 * 4 if per_step else 10)
             assert_windows([T[0].cpu().numpy()], ref, (1, 1, 1), n, (2, 2, 2), per)
         finally:
             g.finalize()
