@@ -291,7 +291,8 @@ enum {
                                     256 = x faces stored straight into the receiver's T2 column
                                     instead of its staging buffer, 512 = no forwarders (timing,
                                     INVALID edge cells), 1024 = single forwarding steps stay on the
-                                    pipelined schedule */
+                                    pipelined schedule, 2048 = dedicated x sender/receiver blocks
+                                    move the staged x columns (ablation, measured slower) */
     IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8; 16 on the
                                     legacy schedule with more than one exchanging axis) */
     IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */

@@ -73,6 +73,33 @@ __device__ __forceinline__ void contribute(const FusedParams &F, int a, int rs, 
     }
 }
 
+__device__ __forceinline__ void st_rel_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acq_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// thread 0 spins (bounded) until the local *fl >= v
+__device__ __forceinline__ void spin_geq_gpu(const FusedParams &F, const unsigned long long *fl, unsigned long long v) {
+    const long long t0 = clock64();
+    while (ld_acq_gpu(fl) < v) {
+        if (clock64() - t0 > F.timeout_cycles) {
+            atomicExch(F.err, 1);
+            break;
+        }
+        __nanosleep(100);
+    }
+}
+// count one of `target` contributions on a local counter; the last one publishes the epoch (gpu scope)
+__device__ __forceinline__ void count_local(const FusedParams &F, int i, unsigned target) {
+    if (atomicAdd(F.xcnt + i, 1u) == target - 1) {
+        atomicExch(F.xcnt + i, 0u);
+        st_rel_gpu(F.xev + i, F.epoch);
+    }
+}
+
 // rim / forwarded cells of (face, chunk) on the pipelined schedule: their own counters and flags
 __device__ __forceinline__ void contribute_x(const FusedParams &F, int a, int rs, int c) {
     const int i = (a * 2 + rs) * kMaxChunks + c;
@@ -252,15 +279,20 @@ __device__ __forceinline__ void fused_wait_halos(const FusedParams &F, int4 td, 
     const bool xlo = F.halo[0][0].active && td.x == 0, xhi = F.halo[0][1].active && td.x == F.xtiles - 1;
     if (threadIdx.x == 0) {
         const unsigned long long prev = F.epoch - 1;
-        if (xlo) spin_geq(F, F.halo[0][0].flag + td.z, prev);
-        if (xhi) spin_geq(F, F.halo[0][1].flag + td.z, prev);
+        if (F.xblk) {   // my receiver blocks copied the column into this T (last step's T2)
+            if (xlo) spin_geq_gpu(F, F.xev + 2 * kMaxChunks + td.z, prev);
+            if (xhi) spin_geq_gpu(F, F.xev + 3 * kMaxChunks + td.z, prev);
+        } else {
+            if (xlo) spin_geq(F, F.halo[0][0].flag + td.z, prev);
+            if (xhi) spin_geq(F, F.halo[0][1].flag + td.z, prev);
+        }
         if (F.halo[1][0].active && td.y == 0) spin_geq(F, F.halo[1][0].flag + td.z, prev);
         if (F.halo[1][1].active && td.y == F.ytiles - 1) spin_geq(F, F.halo[1][1].flag + td.z, prev);
         if (F.halo[2][0].active && zs == 1) spin_geq(F, F.halo[2][0].flag, prev);
         if (F.halo[2][1].active && ze == F.s[2] - 1) spin_geq(F, F.halo[2][1].flag, prev);
     }
     __syncthreads();
-    if (!XS && F.xstage && (xlo || xhi)) {   // (XS: read from the staging row inside the sweep)
+    if (!XS && F.xstage && !F.xblk && (xlo || xhi)) {   // (XS: read from the staging row in the sweep)
         // my x halo column of this tile (its rows, its chunk's planes), staged by the neighbour in the
         // previous epoch -- final since the awaited flag -- into my T, just before the sweep reads it
         // (writing whole 32-B sectors instead, halo cell plus its row neighbours, measured slower)
@@ -306,12 +338,12 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     __shared__ double2 sC[kFD][32 * kFTY];
     __shared__ double sH[XS ? kFD : 1][kFTY];   // XS: the halo-reading lanes' staged x halo cells
     int b = blockIdx.x;
-    if (F.pipe) {   // pipelined schedule: rim blocks, then the forwarders, then the tiles (CTA-uniform)
-        if (b < F.nrim + F.nfwd) {
+    if (F.pipe) {   // pipelined schedule: rim, forwarders, x senders/receivers, then the tiles (CTA-uniform)
+        if (b < F.nrim + F.nfwd + 4 * F.nxb) {
             fused_extra(F, b);
             return;
         }
-        b -= F.nrim + F.nfwd;
+        b -= F.nrim + F.nfwd + 4 * F.nxb;
     }
     const int4 td = fused_tile(F, b);
     const int2 zr = chunk_range(F, td.z);
@@ -384,7 +416,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         const FusedFace &fx = F.face[0][rs];
         if (fx.active && fx.layer >= xlo && fx.layer < xhi) {
             const int hx = rs == 0 ? 0 : sx - 1;
-            if (rowv) {
+            if (rowv && !F.xblk) {   // (x blocks: the sender blocks move the column)
                 double v[kFKC / 32];
 #pragma unroll
                 for (int u = 0; u < kFKC / 32; ++u) {
@@ -465,8 +497,13 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     __syncthreads();
     if (tid == 0) {
         __threadfence_system();
-        for (int f = 0; f < 6; ++f)
-            if (did[f]) contribute(F, f >> 1, f & 1, f < 4 ? td.z : 0);
+        for (int f = 0; f < 6; ++f) {
+            if (!did[f]) continue;
+            if (f < 2 && F.xblk)   // x face with sender blocks: my chunk's layer cells are computed
+                count_local(F, f * kMaxChunks + td.z, F.ytiles);
+            else
+                contribute(F, f >> 1, f & 1, f < 4 ? td.z : 0);
+        }
     }
 }
 
@@ -666,6 +703,70 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, int b) {
         }
         return;
     }
+    if (b >= F.nrim + F.nfwd) {   // x blocks: [senders face 0 | face 1 | receivers halo 0 | halo 1] x nxb
+        const int e = b - F.nrim - F.nfwd, role = e / F.nxb, part = e % F.nxb;
+        const int sx = F.s[0], sy = F.s[1];
+        const long long sxy = (long long)sx * sy;
+        if (role < 2) {   // sender of face rs: my layer column -> the receiver's staging, data flag
+            const int rs = role;
+            const FusedFace &fx = F.face[0][rs];
+            if (!fx.active) return;
+            double *dst = F.xstg_peer[rs];
+            for (int ch = 0; ch < F.nchunks; ++ch) {
+                if (threadIdx.x == 0) spin_geq_gpu(F, F.xev + rs * kMaxChunks + ch, F.epoch);
+                __syncthreads();
+                const int2 zr = chunk_range(F, ch);
+                const int nz = zr.y - zr.x;
+                const long long ncell = (long long)(sy - 2) * nz;
+                constexpr int U = 4;
+                for (long long t0 = (long long)part * blockDim.x * U + threadIdx.x; t0 < ncell;
+                     t0 += (long long)F.nxb * blockDim.x * U) {
+                    double v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {   // z fastest: whole sectors of the staging rows
+                        const long long t = t0 + (long long)u * blockDim.x;
+                        const int y = 1 + (int)(t / nz), z = zr.x + (int)(t % nz);
+                        v[u] = t < ncell ? __ldcg(F.T2 + (long long)z * sxy + (long long)y * sx + fx.layer) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const long long t = t0 + (long long)u * blockDim.x;
+                        if (t >= ncell) continue;
+                        const int y = 1 + (int)(t / nz), z = zr.x + (int)(t % nz);
+                        dst[xstg_at(F, F.epoch, rs, y, z)] = v[u];
+                    }
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence_system();
+                    contribute(F, 0, rs, ch);
+                }
+            }
+        } else {   // receiver of halo side: the staged column -> my T2 column, xready (local)
+            const int side = role - 2;
+            const FusedHalo &h = F.halo[0][side];
+            if (!h.active) return;
+            const int hx = side == 0 ? 0 : sx - 1;
+            for (int ch = 0; ch < F.nchunks; ++ch) {
+                if (threadIdx.x == 0) spin_geq(F, h.flag + ch, F.epoch);
+                __syncthreads();
+                const int2 zr = chunk_range(F, ch);
+                const int nz = zr.y - zr.x;
+                const long long ncell = (long long)(sy - 2) * nz;
+                for (long long t = (long long)part * blockDim.x + threadIdx.x; t < ncell;
+                     t += (long long)F.nxb * blockDim.x) {
+                    const int y = 1 + (int)(t / nz), z = zr.x + (int)(t % nz);
+                    F.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(F.xstg + xstg_at(F, F.epoch, side, y, z));
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    count_local(F, (2 + side) * kMaxChunks + ch, F.nxb);
+                }
+            }
+        }
+        return;
+    }
     const int q = b - F.nrim;   // forwarder q of nfwd (launched right after the rim: they wait chunk by
                                 // chunk, so each edge line leaves as soon as its halo has arrived)
     for (int ch = 0; ch < F.nchunks; ++ch) {
@@ -714,7 +815,7 @@ __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
             spin_geq(F, h.flag + ch, F.epoch);
             spin_geq(F, h.xflag + ch, F.epoch);
         }
-    if (!F.xstage) return;
+    if (!F.xstage || F.xblk) return;   // (x blocks: the receiver blocks already wrote the columns)
     for (int f = threadIdx.x; f < 2 * F.nchunks; f += blockDim.x)
         if (F.halo[0][f / F.nchunks].active) spin_geq(F, F.halo[0][f / F.nchunks].flag + f % F.nchunks, F.epoch);
     __syncthreads();
@@ -831,11 +932,13 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
     const bool need_fwd = ((xh && (yf || zf)) || (yh && zf)) && !(g->fused_mode & 512);
     g->fused_nfwd = need_fwd ? g->fused_ncomm : 0;
     const unsigned nf = (unsigned)g->fused_nfwd;
+    // staged x faces moved by dedicated sender blocks (their count completes the data flag)
+    const bool xblk = (g->fused_mode & 2048) && !(g->fused_mode & (4 | 128 | 256));
     std::vector<unsigned> tgt_d(6 * kMaxChunks, 0u), tgt_x(6 * kMaxChunks, 0u);
     for (int rs = 0; rs < 2; ++rs) {
         for (int c = 0; c < nch; ++c) {
             if (act[0][rs]) {
-                tgt_d[(0 * 2 + rs) * kMaxChunks + c] = ytiles;
+                tgt_d[(0 * 2 + rs) * kMaxChunks + c] = xblk ? (unsigned)g->fused_nxb : ytiles;
                 tgt_x[(0 * 2 + rs) * kMaxChunks + c] = 1;
             }
             if (act[1][rs]) {
@@ -1051,8 +1154,23 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
             F.xstg = g->fused_xstg;
             for (int rs = 0; rs < 2; ++rs)
                 if (F.face[0][rs].active) F.xstg_peer[rs] = pstg[proc_of(g, g->nbr[0][0][rs == 0 ? 1 : 0])];
+            // dedicated x sender/receiver blocks (fused_mode bit 2048, ablation: measured slower -- a few
+            // blocks cannot keep up with one scattered 8-B read per row and plane; the face tiles, spread
+            // over the whole grid, move the column faster)
+            F.xblk = (g->fused_mode & 2048) ? 1 : 0;
+            if (F.xblk) {
+                if (!g->fused_xsync) {
+                    const size_t bytes = 4 * kMaxChunks * (sizeof(unsigned int) + sizeof(unsigned long long));
+                    IGG_CUDA(cudaMalloc(&g->fused_xsync, bytes));
+                    IGG_CUDA(cudaMemset(g->fused_xsync, 0, bytes));
+                    g->allocs++;
+                }
+                F.xev = static_cast<unsigned long long *>(g->fused_xsync);
+                F.xcnt = reinterpret_cast<unsigned int *>(F.xev + 4 * kMaxChunks);
+                F.nxb = g->fused_nxb;
+            }
         }
-        const int blocks = F.nrim + F.nstencil + F.nfwd;
+        const int blocks = F.nrim + F.nfwd + 4 * F.nxb + F.nstencil;
         prof_begin(g, s);
         if (g->fused_mode & 1)
             heat_fused_kernel<true><<<blocks, 32 * kFTY, 0, s>>>(F);
@@ -1062,7 +1180,7 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
         g->launches++;
         prof_end(g, s, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2));
         if (drain && recv) {
-            fused_drain_kernel<<<F.xstage ? 2 * g->sm_count : 1, 128, 0, s>>>(F);
+            fused_drain_kernel<<<(F.xstage && !F.xblk) ? 2 * g->sm_count : 1, 128, 0, s>>>(F);
             IGG_CUDA(cudaGetLastError());
             g->launches++;
         }

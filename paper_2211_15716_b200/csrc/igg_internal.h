@@ -174,6 +174,13 @@ struct FusedParams {
     int xstage;
     double *xstg;                    // mine
     double *xstg_peer[2];            // the receivers' (indexed like face[0][rs])
+    // dedicated x blocks (staged schedule, default): the face tiles only count their chunk as computed
+    // (xcomp -> xcompe); nxb sender blocks per x face copy the layer column into the receiver's
+    // staging and publish the data flag; nxb receiver blocks per x halo copy the staged column into
+    // my T2 and publish xready (local), which the next step's halo tiles await
+    int xblk, nxb;
+    unsigned int *xcnt;              // [4][kMaxChunks]: 0..1 face-tile counts, 2..3 receiver-block counts
+    unsigned long long *xev;         // [4][kMaxChunks]: 0..1 chunk computed (epoch), 2..3 halo ready (epoch)
 };
 
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
@@ -329,7 +336,9 @@ struct igg_grid : igg::Geom {
     int fused_zchunk[2] = {-1, -1};
     int fused_zafter = 1;
     int fused_nfwd = 0;                                  // in-kernel forwarders (pipelined)
+    int fused_nxb = 4;                                   // x sender/receiver blocks per face (pipelined)
     double *fused_xstg = nullptr;                        // x-face staging buffer (pipelined)
+    void *fused_xsync = nullptr;                         // x-block counters and epochs
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };

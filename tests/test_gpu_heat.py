@@ -189,7 +189,7 @@ def test_box_kernel_variants_bit_exact(variant):
 
 
 @pytest.mark.parametrize("per", [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1)])
-@pytest.mark.parametrize("mode", [2, 3, 258])
+@pytest.mark.parametrize("mode", [2, 3, 258, 2050])
 def test_fused_self_wrap_one_gpu(per, mode):
     """Periodic axes wrapping onto the one process run the fused P2P path with the rank as its own
     neighbour (faces stored into its own halos; staged or direct x faces); heat_run (pipelined) and
