@@ -55,6 +55,12 @@ def lib():
                                       ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int]
         L.oracle_heat_run.restype = ctypes.c_int
+        fp = ctypes.POINTER(ctypes.c_float)
+        L.oracle_heat_run_f32.argtypes = [fp, fp, ctypes.c_long, ctypes.c_long, ctypes.c_long,
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                          ctypes.c_float, ctypes.c_float, ctypes.c_int]
+        L.oracle_heat_run_f32.restype = ctypes.c_int
         L.oracle_max.argtypes = [dp, ctypes.c_long]
         L.oracle_max.restype = ctypes.c_double
         L.oracle_set_threads.argtypes = [ctypes.c_int]
@@ -120,6 +126,21 @@ def heat_run(T0: np.ndarray, Ci: np.ndarray, nt: int, periodic, lam, dt, dx, dy,
                                lam, dt, dx, dy, dz, nt, mode)
     if rc != 0:
         raise MemoryError("oracle_heat_run: allocation failed")
+    return T
+
+
+def heat_run_f32(T0: np.ndarray, Ci: np.ndarray, nt: int, periodic, lam, dt, dx, dy, dz) -> np.ndarray:
+    """The binary32 variant of the time loop (reading 24): inputs rounded to float32 once, every
+    operation in binary32, canonical association, r_d = 1/(d*d) computed in float."""
+    T = np.array(T0, dtype=np.float32, order="C", copy=True)
+    C = np.ascontiguousarray(Ci, dtype=np.float32)
+    Nz, Ny, Nx = T.shape
+    fp = ctypes.POINTER(ctypes.c_float)
+    rc = lib().oracle_heat_run_f32(T.ctypes.data_as(fp), C.ctypes.data_as(fp), Nx, Ny, Nz,
+                                   int(periodic[0]), int(periodic[1]), int(periodic[2]),
+                                   lam, dt, dx, dy, dz, nt)
+    if rc != 0:
+        raise MemoryError("oracle_heat_run_f32: allocation failed")
     return T
 
 

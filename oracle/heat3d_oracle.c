@@ -117,6 +117,73 @@ void oracle_heat_step(double *T2, const double *T, const double *Ci,
 }
 
 /*
+ * The binary32 variant (reading 24): the same step with every
+ * operation in binary32 -- inputs rounded to float once (lam, dt, dx, dy, dz, T, Ci), the
+ * reciprocals r_d = 1.0f/(d*d) computed in float, canonical association only:
+ *   T2 = T + dt*((lam*Ci)*(((d2x*rdx2) + (d2y*rdy2)) + (d2z*rdz2)))
+ * A size-1 axis drops its term as in the binary64 step (reading 23).
+ */
+void oracle_heat_step_f32(float *T2, const float *T, const float *Ci,
+                          long Nx, long Ny, long Nz,
+                          int px, int py, int pz,
+                          float lam, float dt, float dx, float dy, float dz)
+{
+    const int ax = Nx > 1, ay = Ny > 1, az = Nz > 1;
+    const long xa = (px || !ax) ? 0 : 1, xb = (px || !ax) ? Nx : Nx - 1;
+    const long ya = (py || !ay) ? 0 : 1, yb = (py || !ay) ? Ny : Ny - 1;
+    const long za = (pz || !az) ? 0 : 1, zb = (pz || !az) ? Nz : Nz - 1;
+    const float rdx2 = 1.0f / (dx * dx), rdy2 = 1.0f / (dy * dy), rdz2 = 1.0f / (dz * dz);
+    long z;
+#pragma omp parallel for schedule(static)
+    for (z = za; z < zb; ++z) {
+        for (long y = ya; y < yb; ++y) {
+            for (long x = xa; x < xb; ++x) {
+                const float c = T[IDX(x, y, z, Nx, Ny)];
+                float lap = 0.0f;
+                int first = 1;
+                if (ax) {
+                    const float d2 = (T[IDX(nb(x, +1, Nx, px), y, z, Nx, Ny)] - c) - (c - T[IDX(nb(x, -1, Nx, px), y, z, Nx, Ny)]);
+                    const float t = d2 * rdx2;
+                    lap = first ? t : lap + t;
+                    first = 0;
+                }
+                if (ay) {
+                    const float d2 = (T[IDX(x, nb(y, +1, Ny, py), z, Nx, Ny)] - c) - (c - T[IDX(x, nb(y, -1, Ny, py), z, Nx, Ny)]);
+                    const float t = d2 * rdy2;
+                    lap = first ? t : lap + t;
+                    first = 0;
+                }
+                if (az) {
+                    const float d2 = (T[IDX(x, y, nb(z, +1, Nz, pz), Nx, Ny)] - c) - (c - T[IDX(x, y, nb(z, -1, Nz, pz), Nx, Ny)]);
+                    const float t = d2 * rdz2;
+                    lap = first ? t : lap + t;
+                    first = 0;
+                }
+                T2[IDX(x, y, z, Nx, Ny)] = c + dt * ((lam * Ci[IDX(x, y, z, Nx, Ny)]) * lap);
+            }
+        }
+    }
+}
+
+/* the binary32 time loop: T2 = copy(T), nt steps with swap; T holds the result */
+int oracle_heat_run_f32(float *T, const float *Ci, long Nx, long Ny, long Nz, int px, int py, int pz,
+                        float lam, float dt, float dx, float dy, float dz, int nt)
+{
+    const size_t n = (size_t)Nx * (size_t)Ny * (size_t)Nz;
+    float *T2 = (float *)malloc(n * sizeof(float));
+    if (!T2) return -1;
+    memcpy(T2, T, n * sizeof(float));
+    float *a = T, *b = T2;
+    for (int it = 0; it < nt; ++it) {
+        oracle_heat_step_f32(b, a, Ci, Nx, Ny, Nz, px, py, pz, lam, dt, dx, dy, dz);
+        float *t = a; a = b; b = t;
+    }
+    if (a != T) memcpy(T, a, n * sizeof(float));
+    free(T2);
+    return 0;
+}
+
+/*
  * The time loop of Fig. 1: T2 = copy(T); nt times
  * { step!(T2, T, ...); T, T2 = T2, T }.  T (in) is the initial field and on
  * return holds the final T.  Returns 0 on success, -1 on allocation failure.

@@ -226,3 +226,42 @@ def test_size1_axis_equals_lower_dimensional_grid():
     b = H.heat_run(T3, C3, 5, (0, 0, 1), 1.0, dt, d[0], d[1], 1.0, H.CANONICAL)
     # the 3-D sum adds (d2z*rdz2) = +0.0 last: x + y + 0.0 == x + y exactly
     assert np.array_equal(a[0], b[1])
+
+
+# ---------------------------------------------------------------- binary32 variant (reading 24)
+def test_f32_fixed_point_exact():
+    T = np.full((6, 7, 8), 1.7, dtype=np.float32); Ci = np.full(T.shape, 0.5, dtype=np.float32)
+    out = H.heat_run_f32(T, Ci, 20, (0, 1, 0), 1.0, 1e-3, 0.1, 0.1, 0.1)
+    assert out.dtype == np.float32 and np.array_equal(out, T)
+
+
+@pytest.mark.parametrize("per", [(0, 0, 0), (1, 0, 1)])
+def test_f32_tracks_f64_within_float_precision(per):
+    N = (12, 10, 9)
+    T0, Ci = SI_fields(N)
+    d = [H.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+    dt = H.stable_dt(*d, 1.0, Ci)
+    a = H.heat_run(T0, Ci, 30, per, 1.0, dt, *d, H.CANONICAL)
+    b = H.heat_run_f32(T0, Ci, 30, per, 1.0, dt, *d)
+    rel = np.max(np.abs(b.astype(np.float64) - a) / np.abs(a))
+    assert 1e-9 < rel < 2e-6          # really binary32, and as accurate as binary32 allows
+
+
+def test_f32_fourier_mode_decay():
+    N = (14, 12, 10); L = (1.0, 0.7, 1.3); k = (1, 2, 1); lam = 1.3; c = 0.45; nt = 60; A = 0.25
+    d = [H.spacing(L[i], N[i], False) for i in range(3)]
+    M = _dirichlet_mode(N, L, k)
+    T0 = 1.7 + A * M
+    Ci = np.full(T0.shape, c)
+    dt = H.stable_dt(d[0], d[1], d[2], lam, Ci)
+    out = H.heat_run_f32(T0, Ci, nt, (0, 0, 0), lam, dt, *d)
+    Gf = 1.0 - dt * lam * c * sum(4.0 / d[i] ** 2 * math.sin(k[i] * math.pi / (2 * (N[i] - 1))) ** 2
+                                  for i in range(3))
+    expect = 1.7 + A * Gf ** nt * M
+    assert Gf ** nt < 0.9
+    assert np.max(np.abs(out - expect)) <= 2e-5
+
+
+def SI_fields(N):
+    import synthetic_inputs as SI
+    return SI.global_heat_fields(*N)
