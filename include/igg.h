@@ -160,8 +160,10 @@ igg_status igg_buffer_allocs(const igg_grid *grid, long long *count_out);
 
 /* ------------------------------------------------------------------ halo update */
 typedef struct igg_field {
-    double *ptr;             /* device pointer, x fastest */
+    double *ptr;             /* device pointer, x fastest (a float array when elsize == 4) */
     long long size[3];       /* (sx, sy, sz): n_d-o_d <= s_d <= n_d+o_d; staggered fields are n+1 */
+    int elsize;              /* bytes per element: 0 or 8 = binary64, 4 = binary32 (
+                                igg_update_halo and igg_hide_communication; igg_gather: 8 only) */
 } igg_field;
 
 /* update_halo! (listing 38).  Collective.
@@ -192,6 +194,14 @@ igg_status igg_update_halo(igg_grid *grid, const igg_field *fields, int nfields,
 igg_status igg_heat_step(igg_grid *grid, double *const *T2, const double *const *T,
                          const double *const *Ci, double lam, double dt,
                          double dx, double dy, double dz, const int bw[3], igg_stream_t stream);
+
+/* The binary32 heat step (reading 24): the same step with float fields and
+ * every operation in binary32 (inputs as given, reciprocals 1.0f/(d*d) in float, no FMA, canonical
+ * association), then update_halo of T2 as a binary32 field.  Sequential schedule (bw accepted for
+ * symmetry).  Size-1 axes allowed as in igg_heat_step.  Errors: IGG_E_ARG, IGG_E_STATE. */
+igg_status igg_heat_step_f32(igg_grid *grid, float *const *T2, const float *const *T, const float *const *Ci,
+                             float lam, float dt, float dx, float dy, float dz, const int bw[3],
+                             igg_stream_t stream);
 
 /* Fig. 1's time loop on the device: nt heat steps, each followed by the swap
  * T, T2 = T2, T.  T, T2: arrays of local_ranks device pointers that the library swaps in place, so on

@@ -28,7 +28,7 @@ class igg_init_args(ctypes.Structure):
 
 
 class igg_field(ctypes.Structure):
-    _fields_ = [("ptr", ctypes.c_void_p), ("size", ctypes.c_longlong * 3)]
+    _fields_ = [("ptr", ctypes.c_void_p), ("size", ctypes.c_longlong * 3), ("elsize", ctypes.c_int)]
 
 
 class igg_halo_spec(ctypes.Structure):
@@ -67,6 +67,8 @@ SIGNATURES = {
     "igg_update_halo": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p],
     "igg_heat_step": [ctypes.c_void_p, c_dbl_pp, c_dbl_pp, c_dbl_pp, ctypes.c_double, ctypes.c_double,
                       ctypes.c_double, ctypes.c_double, ctypes.c_double, c_int_p, ctypes.c_void_p],
+    "igg_heat_step_f32": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float,
+                          ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, c_int_p, ctypes.c_void_p],
     "igg_heat_run": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, c_dbl_pp, ctypes.c_double, ctypes.c_double,
                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_int_p, ctypes.c_void_p],
     "igg_heat_run_host": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,

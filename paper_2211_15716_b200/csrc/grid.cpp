@@ -106,27 +106,36 @@ void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap) {
 // receiver's arena slot: local, peer-mapped over NVLink, or the NCCL send
 // arena), the grouped NCCL send/recv of that axis, one unpack launch.
 // plans depend only on the field sizes: built once per field-list shape
-const Plan &cached_plan(igg_grid *g, const std::vector<long long> &sizes) {
+// key: nf*3 sizes then nf element sizes
+const Plan &cached_plan(igg_grid *g, const std::vector<long long> &key, int nf) {
     for (const auto &e : g->plan_cache)
-        if (e.first == sizes) return e.second;
-    g->plan_cache.push_back({sizes, build_plan(*g, sizes.data(), (int)(sizes.size() / 3))});
+        if (e.first == key) return e.second;
+    std::vector<int> esz(nf);
+    for (int f = 0; f < nf; ++f) esz[f] = (int)key[3 * nf + f];
+    g->plan_cache.push_back({key, build_plan(*g, key.data(), nf, esz.data())});
     return g->plan_cache.back().second;
 }
 
 void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, bool allow_coop) {
     if (nf < 1 || !fields) fail(IGG_E_ARG, "update_halo: need at least one field");
     const int L = g->nlocal;
-    std::vector<long long> sizes(nf * 3);
-    for (int f = 0; f < nf; ++f)
+    std::vector<long long> sizes(nf * 4);   // nf*3 sizes, then nf element sizes (the plan key)
+    for (int f = 0; f < nf; ++f) {
         for (int a = 0; a < 3; ++a) sizes[f * 3 + a] = fields[f].size[a];
+        const int e = fields[f].elsize == 0 ? 8 : fields[f].elsize;
+        if (e != 8 && e != 4) fail(IGG_E_ARG, "update_halo: elsize must be 0, 8 or 4");
+        sizes[3 * nf + f] = e;
+    }
     for (int r = 0; r < L; ++r)
         for (int f = 0; f < nf; ++f) {
             const igg_field &F = fields[r * nf + f];
             if (!F.ptr) fail(IGG_E_ARG, "update_halo: NULL field pointer");
             for (int a = 0; a < 3; ++a)
                 if (F.size[a] != sizes[f * 3 + a]) fail(IGG_E_ARG, "update_halo: local ranks disagree on a field size");
+            if ((F.elsize == 0 ? 8 : F.elsize) != sizes[3 * nf + f])
+                fail(IGG_E_ARG, "update_halo: local ranks disagree on a field element size");
         }
-    const Plan &plan = cached_plan(g, sizes);
+    const Plan &plan = cached_plan(g, sizes, nf);
     const size_t half = (size_t)L * plan.block * sizeof(double);
     ensure_arena(g, half, plan.any_nccl ? half : 0);
 
@@ -154,6 +163,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
             d.sy = F.size[1];
             d.sz = F.size[2];
             d.count = m.count;
+            d.esz = (int)sizes[3 * nf + m.field];
             d.axis = a;
             d.lo = m.lo;
             d.h = m.h;
@@ -234,9 +244,9 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
             std::sort(recvs[a].begin(), recvs[a].end(), by_order);
             IGG_NCCL(ncclGroupStart());
             for (const PlanMsg *m : sends[a])
-                IGG_NCCL(ncclSend(sendb + m->sbuf, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
+                IGG_NCCL(ncclSend(sendb + m->sbuf, (size_t)m->words, ncclDouble, m->peer_proc, g->comm, st));
             for (const PlanMsg *m : recvs[a])
-                IGG_NCCL(ncclRecv(recv + m->slot, (size_t)m->count, ncclDouble, m->peer_proc, g->comm, st));
+                IGG_NCCL(ncclRecv(recv + m->slot, (size_t)m->words, ncclDouble, m->peer_proc, g->comm, st));
             IGG_NCCL(ncclGroupEnd());
         }
         g->launches += launch_copies(1, ud[a], U[a], st);
@@ -808,6 +818,33 @@ IGG_API igg_status igg_acoustic_step(igg_grid *g, double *const *P, double *cons
     IGG_CATCH
 }
 
+IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci,
+                                     float lam, float dt, float dx, float dy, float dz, const int bw[3],
+                                     igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_heat_step_f32");
+    if (!T2 || !T || !Ci) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field list");
+    for (int a = 0; a < 3; ++a)
+        if (g->n[a] == 2) fail(IGG_E_ARG, "igg_heat_step_f32: an axis needs 1 or at least 3 cells");
+    (void)bw;   // the binary32 step runs the sequential schedule: stencil, then update_halo
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<igg_field> f(g->nlocal);
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field pointer");
+        f[lr] = igg_field{reinterpret_cast<double *>(T2[lr]), {g->n[0], g->n[1], g->n[2]}, 4};
+    }
+    IGG_CUDA(cudaEventRecord(g->ev_start, s));
+    IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        igg::launch_heat_f32(T2[lr], T[lr], Ci[lr], g->n, lam, dt, dx, dy, dz, g->s_comm);
+        g->launches++;
+    }
+    igg::exchange(g, f.data(), 1, g->s_comm);
+    IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
+    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    IGG_CATCH
+}
+
 IGG_API igg_status igg_heat_run(igg_grid *g, double **T, double **T2, const double *const *Ci, double lam,
                                 double dt, double dx, double dy, double dz, int nt, const int bw[3],
                                 igg_stream_t stream) {
@@ -881,6 +918,9 @@ IGG_API igg_status igg_gather(igg_grid *g, const igg_field *fields, int root_pro
     IGG_TRY
     igg::check_live(g, "igg_gather");
     if (!fields || root_proc < 0 || root_proc >= g->nproc_procs) fail(IGG_E_ARG, "igg_gather: bad argument");
+    for (int lr = 0; lr < g->nlocal; ++lr)
+        if (fields[lr].elsize != 0 && fields[lr].elsize != 8)
+            fail(IGG_E_UNSUPPORTED, "igg_gather: binary64 fields only");
     cudaStream_t s = (cudaStream_t)stream;
     const long long sz[3] = {fields[0].size[0], fields[0].size[1], fields[0].size[2]};
     long long N[3];

@@ -65,12 +65,13 @@ bool halo_spec(int n, int o, long long s, HaloSpec *out);             // false: 
 // one face copy: the slab [lo, lo+h) of `axis` of a field <-> a contiguous buffer,
 // buffer layout x fastest, then y, then z, restricted to the slab
 struct CopyDesc {
-    double *field;
+    double *field;                   // element type by esz (8: double, 4: float)
     double *buf;
     long long sx, sy, sz;
-    long long count;                 // h * (other two sizes)
+    long long count;                 // h * (other two sizes), elements
     int axis, lo, h;
     int flag_slot;                   // unpack: index into WaitList flags (-1 = no wait)
+    int esz;                         // bytes per element
 };
 
 constexpr int kMaxCopy = 48;
@@ -210,6 +211,9 @@ void launch_heat_slabs(HeatRegionList &L, cudaStream_t s);
 // the production stencil: cp.async-pipelined z-sweep over a list of box regions
 // (all local ranks' inner boxes, or the boundary slabs), one launch
 void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant);
+// binary32 heat step on the updated box (size-1 axes allowed); coefficients rounded to float by the caller
+void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], float lam, float dt, float dx,
+                     float dy, float dz, cudaStream_t s);
 // 1-D/2-D grid (size-1 axes): the stencil without the size-1 axes' terms on the updated box
 void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int n[3], const HeatCoef &k,
                         cudaStream_t s);
@@ -257,9 +261,10 @@ enum Transport { kLocal = 0, kNccl = 1, kP2P = 2 };
 struct PlanMsg {
     int op, lr, field, recv_side, peer, peer_proc, peer_lr, transport;
     int lo, h;
-    long long count;
-    long long slot;    // element offset in the receive-arena half of the RECEIVING process
-    long long sbuf;    // op 0, NCCL: element offset in the send arena
+    long long count;   // elements
+    long long words;   // 8-byte words the face occupies in the arenas (NCCL message size)
+    long long slot;    // word offset in the receive-arena half of the RECEIVING process
+    long long sbuf;    // op 0, NCCL: word offset in the send arena
     int order;         // NCCL: posting position among this axis' sends (op 0) / recvs (op 1); else -1
 };
 struct Plan {
@@ -268,7 +273,8 @@ struct Plan {
     std::vector<PlanMsg> msgs[3];                          // per axis: all packs, then all unpacks
     bool any_nccl = false;
 };
-Plan build_plan(const Geom &G, const long long *sizes /* nf*3, (sx,sy,sz) */, int nf);
+Plan build_plan(const Geom &G, const long long *sizes /* nf*3, (sx,sy,sz) */, int nf,
+                const int *esz = nullptr /* nf bytes per element, default 8 */);
 
 }  // namespace igg
 
@@ -362,5 +368,5 @@ void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
 void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step
 int proc_of(const igg_grid *g, int global_rank);
-const Plan &cached_plan(igg_grid *g, const std::vector<long long> &sizes);
+const Plan &cached_plan(igg_grid *g, const std::vector<long long> &key, int nf);
 }  // namespace igg

@@ -80,6 +80,65 @@ void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int
     IGG_CUDA(cudaGetLastError());
 }
 
+// ============================================================== binary32 variant
+// DESIGN.md reading 24: every operation in binary32 with explicit rounding (no FMA), canonical
+// association, reciprocals 1/(d*d) computed in float on the host; size-1 axes drop their term
+// (reading 23).  One thread per cell of the updated box, x fastest, a z-chunk of planes per thread
+// with the z neighbours in registers.
+struct HeatCoefF {
+    float lam, dt, rdx2, rdy2, rdz2;
+};
+constexpr int kF32Kc = 16;
+__global__ void __launch_bounds__(256) heat_f32_kernel(float *__restrict__ T2, const float *__restrict__ T,
+                                                       const float *__restrict__ Ci, int nx, int ny, int nz,
+                                                       const HeatCoefF k) {
+    const int ax = nx > 1, ay = ny > 1, az = nz > 1;
+    const int wx = ax ? nx - 2 : 1, wy = ay ? ny - 2 : 1, wz = az ? nz - 2 : 1;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x + ax;
+    const int y = blockIdx.y + ay;
+    const int z0 = blockIdx.z * kF32Kc + az, z1 = min(z0 + kF32Kc, az + wz);
+    if (x >= ax + wx) return;
+    const long long sx = nx, sxy = (long long)nx * ny;
+    long long i = (long long)z0 * sxy + (long long)y * sx + x;
+    float zm = az ? __ldg(T + i - sxy) : 0.f, c = __ldg(T + i);
+    for (int z = z0; z < z1; ++z, i += sxy) {
+        const float zp = az ? __ldg(T + i + sxy) : 0.f;
+        float lap = 0.f;
+        bool first = true;
+        if (ax) {
+            const float t = __fmul_rn(__fsub_rn(__fsub_rn(__ldg(T + i + 1), c), __fsub_rn(c, __ldg(T + i - 1))), k.rdx2);
+            lap = t;
+            first = false;
+        }
+        if (ay) {
+            const float t = __fmul_rn(__fsub_rn(__fsub_rn(__ldg(T + i + sx), c), __fsub_rn(c, __ldg(T + i - sx))), k.rdy2);
+            lap = first ? t : __fadd_rn(lap, t);
+            first = false;
+        }
+        if (az) {
+            const float t = __fmul_rn(__fsub_rn(__fsub_rn(zp, c), __fsub_rn(c, zm)), k.rdz2);
+            lap = first ? t : __fadd_rn(lap, t);
+        }
+        T2[i] = __fadd_rn(c, __fmul_rn(k.dt, __fmul_rn(__fmul_rn(k.lam, __ldg(Ci + i)), lap)));
+        zm = c;
+        c = zp;
+    }
+}
+
+void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], float lam, float dt, float dx,
+                     float dy, float dz, cudaStream_t s) {
+    HeatCoefF k;
+    k.lam = lam;
+    k.dt = dt;
+    k.rdx2 = 1.0f / (dx * dx);   // in float, as the binary32 oracle (reading 24)
+    k.rdy2 = 1.0f / (dy * dy);
+    k.rdz2 = 1.0f / (dz * dz);
+    const int wx = n[0] > 1 ? n[0] - 2 : 1, wy = n[1] > 1 ? n[1] - 2 : 1, wz = n[2] > 1 ? n[2] - 2 : 1;
+    const dim3 grid((wx + 255) / 256, wy, (wz + kF32Kc - 1) / kF32Kc);
+    heat_f32_kernel<<<grid, 256, 0, s>>>(T2, T, Ci, n[0], n[1], n[2], k);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ============================================================== generic region kernel
 // One thread per (x,y) column of a region, sweeping a chunk of kRegKc planes in
 // z with a register queue (T[z-1], T[z], T[z+1]); x/y neighbours come through
@@ -902,27 +961,37 @@ constexpr int kCopyILP = 8;   // elements per thread, all loads issued before th
 // Copies of the faces run concurrently with the bandwidth-bound inner box: each
 // thread issues kCopyILP independent loads before storing, so a CTA finishes
 // in about one memory round trip and holds its SM slot as briefly as possible.
-template <bool PACK>
-__device__ __forceinline__ void copy_face(const CopyDesc &d) {
+template <bool PACK, typename E>
+__device__ __forceinline__ void copy_face_t(const CopyDesc &d) {
+    E *field = reinterpret_cast<E *>(d.field);
+    E *buf = reinterpret_cast<E *>(d.buf);
     const long long chunk = (long long)kCopyThreads * kCopyILP;
     for (long long base = (long long)blockIdx.x * chunk; base < d.count; base += (long long)gridDim.x * chunk) {
-        double v[kCopyILP];
+        E v[kCopyILP];
 #pragma unroll
         for (int u = 0; u < kCopyILP; ++u) {
             const long long i = base + u * kCopyThreads + threadIdx.x;
-            if (i < d.count) v[u] = PACK ? __ldcg(d.field + face_index(d, i)) : __ldcg(d.buf + i);
+            if (i < d.count) v[u] = PACK ? __ldcg(field + face_index(d, i)) : __ldcg(buf + i);
         }
 #pragma unroll
         for (int u = 0; u < kCopyILP; ++u) {
             const long long i = base + u * kCopyThreads + threadIdx.x;
             if (i < d.count) {
                 if (PACK)
-                    d.buf[i] = v[u];
+                    buf[i] = v[u];
                 else
-                    d.field[face_index(d, i)] = v[u];
+                    field[face_index(d, i)] = v[u];
             }
         }
     }
+}
+// binary64 or binary32 elements (a bit copy either way; CTA-uniform branch)
+template <bool PACK>
+__device__ __forceinline__ void copy_face(const CopyDesc &d) {
+    if (d.esz == 4)
+        copy_face_t<PACK, float>(d);
+    else
+        copy_face_t<PACK, double>(d);
 }
 
 // pack: field slab -> buffer (own send buffer, a local rank's receive slot, or a
@@ -1065,28 +1134,37 @@ int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &pr
 // co-resident (cooperative launch), so the axis phases are separated by grid
 // barriers instead of kernel boundaries, and the peer flags are published and
 // awaited inside the kernel (removes ~6 dependent launches per call).
-template <bool PACK>
-__device__ __forceinline__ void copy_face_grid(const CopyDesc &d) {
+template <bool PACK, typename E>
+__device__ __forceinline__ void copy_face_grid_t(const CopyDesc &d) {
+    E *field = reinterpret_cast<E *>(d.field);
+    E *buf = reinterpret_cast<E *>(d.buf);
     const long long nthreads = (long long)gridDim.x * blockDim.x;
     const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     for (long long base = 0; base < d.count; base += nthreads * kCopyILP) {
-        double v[kCopyILP];
+        E v[kCopyILP];
 #pragma unroll
         for (int u = 0; u < kCopyILP; ++u) {
             const long long i = base + u * nthreads + gtid;
-            if (i < d.count) v[u] = PACK ? __ldcg(d.field + face_index(d, i)) : __ldcg(d.buf + i);
+            if (i < d.count) v[u] = PACK ? __ldcg(field + face_index(d, i)) : __ldcg(buf + i);
         }
 #pragma unroll
         for (int u = 0; u < kCopyILP; ++u) {
             const long long i = base + u * nthreads + gtid;
             if (i < d.count) {
                 if (PACK)
-                    d.buf[i] = v[u];
+                    buf[i] = v[u];
                 else
-                    d.field[face_index(d, i)] = v[u];
+                    field[face_index(d, i)] = v[u];
             }
         }
     }
+}
+template <bool PACK>
+__device__ __forceinline__ void copy_face_grid(const CopyDesc &d) {
+    if (d.esz == 4)
+        copy_face_grid_t<PACK, float>(d);
+    else
+        copy_face_grid_t<PACK, double>(d);
 }
 
 __global__ void __launch_bounds__(kCopyThreads) halo_coop_kernel(const __grid_constant__ CoopPlan C) {

@@ -78,7 +78,7 @@ Geom make_geom(const igg_init_args *A) {
     return g;
 }
 
-Plan build_plan(const Geom &G, const long long *sizes, int nf) {
+Plan build_plan(const Geom &G, const long long *sizes, int nf, const int *esz) {
     if (nf < 1) fail(IGG_E_ARG, "update_halo: need at least one field");
     if (!sizes) fail(IGG_E_ARG, "update_halo: sizes is NULL");
     Plan P;
@@ -96,7 +96,7 @@ Plan build_plan(const Geom &G, const long long *sizes, int nf) {
         }
     // receive-slot layout of one rank: [field][axis][side]; face = h * (other two sizes)
     std::vector<std::array<std::array<long long, 2>, 3>> off(nf);
-    std::vector<std::array<long long, 3>> face(nf);
+    std::vector<std::array<long long, 3>> face(nf), words(nf);
     long long block = 0;
     for (int f = 0; f < nf; ++f)
         for (int a = 0; a < 3; ++a) {
@@ -104,9 +104,11 @@ Plan build_plan(const Geom &G, const long long *sizes, int nf) {
             for (int b = 0; b < 3; ++b)
                 if (b != a) other *= P.sz[f][b];
             face[f][a] = hs[f][a].h * other;
+            const long long e = esz ? esz[f] : 8;
+            words[f][a] = (face[f][a] * e + 7) / 8;   // slots in 8-byte words (binary32 faces packed)
             for (int side = 0; side < 2; ++side) {
                 off[f][a][side] = block;
-                block += face[f][a];
+                block += words[f][a];
             }
         }
     P.block = block;
@@ -133,6 +135,7 @@ Plan build_plan(const Geom &G, const long long *sizes, int nf) {
                     m.lo = k == 0 ? H.send_up[0] : H.send_lo[0];
                     m.h = H.h;
                     m.count = face[f][a];
+                    m.words = words[f][a];
                     m.slot = (long long)m.peer_lr * block + off[f][a][k];
                     m.sbuf = (long long)lr * block + off[f][a][k];
                     m.order = -1;
@@ -153,6 +156,7 @@ Plan build_plan(const Geom &G, const long long *sizes, int nf) {
                     m.lo = side == 0 ? H.recv_lo[0] : H.recv_up[0];
                     m.h = H.h;
                     m.count = face[f][a];
+                    m.words = words[f][a];
                     m.slot = (long long)lr * block + off[f][a][side];
                     m.sbuf = -1;
                     m.order = -1;

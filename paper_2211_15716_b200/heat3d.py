@@ -38,11 +38,13 @@ def stable_dt(grid: Grid, Ci, dx: float, dy: float, dz: float, lam: float = LAM)
     return min(dx * dx, dy * dy, dz * dz) / lam / mx / 6.1
 
 
-def alloc_fields(grid: Grid, device=None):
-    """(T, T2, Ci) per local rank, canonical local shape (nz, ny, nx)."""
+def alloc_fields(grid: Grid, device=None, dtype=None):
+    """(T, T2, Ci) per local rank, canonical local shape (nz, ny, nx); float64 unless dtype is given
+    (torch.float32: the binary32 variant)."""
     import torch
     nx, ny, nz = grid.n
-    mk = lambda: [torch.empty((nz, ny, nx), dtype=torch.float64, device=device or "cuda")
+    dt_ = dtype or torch.float64
+    mk = lambda: [torch.empty((nz, ny, nx), dtype=dt_, device=device or "cuda")
                   for _ in range(grid.local_ranks)]
     return mk(), mk(), mk()
 
@@ -71,7 +73,7 @@ def init_random(grid: Grid, T, T2, Ci, seed_T=None, seed_C=None) -> None:
         gy = grid.global_indices(rank, 1, ny)
         gz = grid.global_indices(rank, 2, nz)
         g = SI.linear_index(gx, gy, gz, Nx, Ny)
-        T[r].copy_(torch.from_numpy(SI.heat_T(g, seed_T)))
+        T[r].copy_(torch.from_numpy(SI.heat_T(g, seed_T)))     # (rounded once if float32)
         Ci[r].copy_(torch.from_numpy(SI.heat_Ci(g, seed_C)))
         T2[r].copy_(T[r])
 

@@ -131,13 +131,19 @@ def _as_list(x, n: int) -> list:
     return lst
 
 
-def _dev_ptr(t) -> int:
+def _dev_ptr(t, allow_f32: bool = False) -> int:
     import torch
     if not isinstance(t, torch.Tensor):
         raise TypeError("fields must be torch tensors")
-    if not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous() or t.dim() != 3:
-        raise ValueError("fields must be contiguous 3-D float64 CUDA tensors of shape (sz, sy, sx)")
+    ok_dtype = t.dtype == torch.float64 or (allow_f32 and t.dtype == torch.float32)
+    if not t.is_cuda or not ok_dtype or not t.is_contiguous() or t.dim() != 3:
+        raise ValueError("fields must be contiguous 3-D float64%s CUDA tensors of shape (sz, sy, sx)"
+                         % (" or float32" if allow_f32 else ""))
     return t.data_ptr()
+
+
+def _elsize(t) -> int:
+    return t.element_size()
 
 
 def _ptr_array(ts) -> ctypes.Array:
@@ -215,7 +221,8 @@ class Grid:
             for f in range(nf):
                 t = per[f][r]
                 e = arr[r * nf + f]
-                e.ptr = _dev_ptr(t)
+                e.ptr = _dev_ptr(t, allow_f32=True)   # binary64 or binary32
+                e.elsize = _elsize(t)
                 sz, sy, sx = t.shape
                 e.size[0], e.size[1], e.size[2] = sx, sy, sz
         _ok(L.lib().igg_update_halo(self._handle(), arr, nf, _stream(stream)))
@@ -225,6 +232,15 @@ class Grid:
                   bw=(16, 2, 2), stream=None) -> None:
         n = self.local_ranks
         t2, t, c = (_as_list(x, n) for x in (T2, T, Ci))
+        import torch
+        if t2[0].dtype == torch.float32:   # the binary32 variant (igg_heat_step_f32)
+            for x in t2 + t + c:
+                if tuple(x.shape) != (self.n[2], self.n[1], self.n[0]) or x.dtype != torch.float32:
+                    raise ValueError("binary32 heat_step fields must be float32 of the canonical local shape")
+            arr = lambda ts: (ctypes.c_void_p * len(ts))(*[_dev_ptr(q, allow_f32=True) for q in ts])
+            _ok(L.lib().igg_heat_step_f32(self._handle(), arr(t2), arr(t), arr(c), lam, dt, dx, dy, dz, _i3(bw),
+                                          _stream(stream)))
+            return
         for x in t2 + t + c:
             if tuple(x.shape) != (self.n[2], self.n[1], self.n[0]):
                 raise ValueError("heat_step fields must have the canonical local shape (nz, ny, nx)")
@@ -286,7 +302,8 @@ class Grid:
             for f in range(nf):
                 t = per[f][r]
                 e = arr[r * nf + f]
-                e.ptr = _dev_ptr(t)
+                e.ptr = _dev_ptr(t, allow_f32=True)
+                e.elsize = _elsize(t)
                 sz, sy, sx = t.shape
                 e.size[0], e.size[1], e.size[2] = sx, sy, sz
         streams = {}

@@ -103,6 +103,31 @@ def gather_case(path, n, dims, per, s):
     log("gather OK", dims, per, s)
 
 
+def heat_f32_case(path, n, dims, per, nt=5):
+    """The binary32 variant (igg_heat_step_f32, float halos through NCCL / NVLink) vs the binary32 oracle."""
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=1, path=path,
+                           device=int(os.environ["LOCAL_RANK"]))
+    try:
+        N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+        T0g, Cig = SI.global_heat_fields(*N)
+        d = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+        dt = OH.stable_dt(*d, 1.0, Cig)
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
+        app.init_random(g, T, T2, Ci)
+        for _ in range(nt):
+            g.heat_step(T2, T, Ci, 1.0, dt, *d)
+            T, T2 = T2, T
+        torch.cuda.synchronize()
+        g.check()
+        ref = OH.heat_run_f32(T0g, Cig, nt, per, 1.0, dt, *d)
+        W = OG.window(ref, OG.coords_of_rank(g.rank0, dims), dims, n, (2, 2, 2), per, n)
+        if not np.array_equal(T[0].cpu().numpy(), W):
+            raise AssertionError(f"heat f32 {path} {dims} per={per}")
+    finally:
+        g.finalize()
+    log("heat f32 OK", path, dims, per)
+
+
 def acoustic_case(path, n, dims, per, local, bw, nt=5):
     """Second workload: staggered P, Vx, Vy, Vz with update_halo!(Vx, Vy, Vz)."""
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
@@ -162,6 +187,7 @@ def main():
                 heat_case(path, (130, 36, 34), d2, (1, 1, 1), 1, (16, 2, 2), nt=7)
         halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
         acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4))
+        heat_f32_case(path, n, dims, (1, 0, 1))
         acoustic_case(path, n, dims, (1, 0, 1), 1, (4, 4, 4))
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
         # 8 ranks as virtual ranks over the processes (2x2x2 correctness on fewer GPUs)

@@ -9,6 +9,7 @@ import paper_2211_15716_b200 as P
 from paper_2211_15716_b200 import heat3d as app
 from oracle import grid as OG
 from oracle import heat3d as OH
+import synthetic_inputs as SI
 
 from _heat_cases import assert_windows, gpu_run, oracle_global
 
@@ -249,3 +250,36 @@ def test_low_dimensional_init_rules():
     with pytest.raises(P.IggError) as e:
         P.init_global_grid(24, 20, 1, dims=(1, 1, 2), local_ranks=2, device=0)
     assert e.value.name == "IGG_E_ARG"
+
+
+@pytest.mark.parametrize("case", [
+    dict(n=(24, 20, 18), dims=(2, 2, 1), per=(1, 0, 0)),
+    dict(n=(30, 26, 1), dims=(2, 1, 1), per=(0, 0, 0)),      # 2-D
+    dict(n=(40, 22, 20), dims=(1, 1, 1), per=(0, 1, 1)),     # self-wrap
+])
+def test_binary32_heat_vs_oracle(case):
+    """The binary32 variant (reading 24): igg_heat_step_f32 with update_halo of a
+    float field, bit-exact vs the binary32 oracle on the global grid."""
+    import torch
+    n, dims, per = case["n"], case["dims"], case["per"]
+    nprocs = dims[0] * dims[1] * dims[2]
+    N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+    T0g, Cig = SI.global_heat_fields(*N)
+    d = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+    dt = OH.stable_dt(*d, 1.0, Cig)
+    ref = OH.heat_run_f32(T0g, Cig, 6, per, 1.0, dt, *d)
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=nprocs, device=0)
+    try:
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
+        app.init_random(g, T, T2, Ci)
+        for _ in range(6):
+            g.heat_step(T2, T, Ci, 1.0, dt, *d)
+            T, T2 = T2, T
+        torch.cuda.synchronize()
+        g.check()
+        for r in range(nprocs):
+            W = OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)
+            got = T[r].cpu().numpy()
+            assert got.dtype == np.float32 and np.array_equal(got, W), (case, r)
+    finally:
+        g.finalize()
