@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=["f64", "f32"], default="f64",
+                    help="heat workload: f64 (the paper's Float64, default) or the binary32 variant (f4)")
     ap.add_argument("--workload", choices=["heat", "acoustic"], default="heat",
                     help="heat: the north-star Fig. 1 step (default); acoustic: the staggered second workload")
     ap.add_argument("--n", type=int, default=512)
@@ -70,10 +72,10 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def dram_traffic_per_launch():
+def dram_traffic_per_launch(name="traffic.json"):
     """ncu dram__bytes_read+write per launch of the dominant kernel, from the
     committed summary of this round's `ncu --set full` capture, else None."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+    p = os.path.join(ROOT, "profiles", name)
     try:
         d = json.load(open(p))
         return d
@@ -123,13 +125,28 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_oracle_baseline(n: int, target_s: float = 12.0):
+def cpu_oracle_baseline(n: int, target_s: float = 12.0, f32: bool = False):
     """The oracle as it stands (plain C, OpenMP) on this host: full n^3 paper
     workload, as many single steps as fit in ~target_s (at least 2)."""
     import numpy as np
     from oracle import heat3d as OH
     OH.build()
     OH.set_threads(len(os.sched_getaffinity(0)))   # all host cores (torchrun sets OMP_NUM_THREADS=1)
+    if f32:   # the binary32 oracle: one-step runs (the copy T2 = T inside is part of the sample)
+        T = np.full((n, n, n), 1.7, dtype=np.float32)
+        Ci = np.full((n, n, n), 0.5, dtype=np.float32)
+        d = 1.0 / (n - 1)
+        dt = d * d / 0.5 / 6.1
+        times = []
+        t_end = time.perf_counter() + target_s
+        while len(times) < 2 or (time.perf_counter() < t_end and len(times) < 30):
+            t0 = time.perf_counter()
+            T = OH.heat_run_f32(T, Ci, 1, (0, 0, 0), 1.0, dt, d, d, d)
+            times.append(time.perf_counter() - t0)
+        t = statistics.median(times)
+        return {"value": 12 * n ** 3 / t / 1e9, "unit": "GB/s", "cores": OH.num_threads(), "kind": "oracle",
+                "sample": f"{len(times)} binary32 oracle steps (full {n}^3 grid, each with its T2 = copy(T)), "
+                          f"median {t:.3f} s/step, T_eff = 12 B x {n}^3 / t"}
     T = np.full((n, n, n), 1.7)
     T2 = T.copy()
     Ci = np.full((n, n, n), 0.5)
@@ -230,9 +247,14 @@ def main():
     dt = app.stable_dt(g, Ci, *d)
     stream = torch.cuda.current_stream()
 
+    f32 = a.dtype == "f32"
+    if f32:   # the binary32 variant (igg_heat_step_f32): same fields rounded to float once
+        T, T2, Ci = (list(x) for x in app.alloc_fields(g, dtype=torch.float32))
+        (app.init_paper if a.init == "paper" else app.init_random)(g, T, T2, Ci)
+
     def steps(k):   # Fig. 1's time loop through the public API (igg_heat_run; --per-step: igg_heat_step x k)
         nonlocal T, T2
-        T, T2 = app.run(g, T, T2, Ci, k, dt, d, app.LAM, bw=bw, per_step=a.per_step)
+        T, T2 = app.run(g, T, T2, Ci, k, dt, d, app.LAM, bw=bw, per_step=a.per_step or f32)
 
     def barrier():
         torch.cuda.synchronize()
@@ -282,7 +304,8 @@ def main():
     g.set_option(P.OPT_PROFILE, 0)
     g.check()
 
-    per_gpu = BYTES_PER_CELL * n ** 3 / (ms * 1e-3) / 1e9
+    bpc = BYTES_PER_CELL // 2 if f32 else BYTES_PER_CELL   # binary32: 3 x 4 B per cell
+    per_gpu = bpc * n ** 3 / (ms * 1e-3) / 1e9
     value = per_gpu * world
 
     # ---------------- in-run streaming reference: torch fp64 a+b->c over 1 GiB arrays (2 reads + 1 write)
@@ -322,22 +345,23 @@ def main():
     # ---------------- roofline of the dominant kernel (the full-region / inner-box stencil)
     peak, peak_src = measured_peak()
     k_avg_ms = k_ms / max(k_n, 1)
-    k_bytes = BYTES_PER_CELL * k_cells / max(k_n, 1)
+    k_bytes = bpc * k_cells / max(k_n, 1)
     achieved = k_bytes / (k_avg_ms * 1e-3) / 1e9 if k_n else None
-    tr = dram_traffic_per_launch()
+    tr = dram_traffic_per_launch("traffic_f32.json" if f32 else "traffic.json")
     traffic = None
     if tr and tr.get("n") == n and tr.get("dims") == list(dims):
         traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
-                "kernel": "heat_box_kernel (inner box)" if world > 1 else "heat_box_kernel (full region)",
+                "kernel": ("heat_f32_async_kernel (full region)" if f32 else
+                           "heat_box_kernel (inner box)" if world > 1 else "heat_box_kernel (full region)"),
                 "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_avg_ms, "launches": k_n,
                 "peak_source": peak_src, "share_of_step": k_avg_ms * (k_n / prof_steps) / ms if k_n else None,
                 "measured_in": f"a separate pass of {prof_steps} steps with events around the kernel"}
 
     # ---------------- end to end through the C ABI from pinned host buffers
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and not f32:   # (igg_heat_run_host is the binary64 entry point)
         nt = 100
         cells = n ** 3
         Th = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
@@ -370,15 +394,15 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = cpu_oracle_baseline(n)
+        cpu = cpu_oracle_baseline(n, f32=f32)
 
     g.finalize()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": a.steps,
             "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"3-D heat diffusion Float64, local {n}^3 per GPU, dims "
+            "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
+            "config": {"workload": f"3-D heat diffusion {'Float32 variant' if f32 else 'Float64'}, local {n}^3 per GPU, dims "
                                    f"{dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw} (paper Fig. 1)",
                        "n_local": n, "dims": list(dims), "bw": list(bw), "path": a.path, "init": a.init,
                        "x_align": a.xalign, "periods": list(periods), "schedule": a.schedule, "fused": a.fused,

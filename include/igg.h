@@ -197,8 +197,9 @@ igg_status igg_heat_step(igg_grid *grid, double *const *T2, const double *const 
 
 /* The binary32 heat step (reading 24): the same step with float fields and
  * every operation in binary32 (inputs as given, reciprocals 1.0f/(d*d) in float, no FMA, canonical
- * association), then update_halo of T2 as a binary32 field.  Sequential schedule (bw accepted for
- * symmetry).  Size-1 axes allowed as in igg_heat_step.  Errors: IGG_E_ARG, IGG_E_STATE. */
+ * association), then update_halo of T2 as a binary32 field.  bw as in igg_heat_step: {0,0,0} (or NULL)
+ * = sequential, else boundary slabs + exchange on the high-priority stream with the inner box
+ * concurrent.  Size-1 axes allowed as in igg_heat_step.  Errors: IGG_E_ARG, IGG_E_STATE, IGG_E_WIDTH. */
 igg_status igg_heat_step_f32(igg_grid *grid, float *const *T2, const float *const *T, const float *const *Ci,
                              float lam, float dt, float dx, float dy, float dz, const int bw[3],
                              igg_stream_t stream);

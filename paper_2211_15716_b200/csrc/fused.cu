@@ -47,6 +47,17 @@ __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
+// L2 eviction-priority hint: evict_last for the rows of the x-face tiles, whose send-layer cells the
+// face epilogue re-reads after the sweep (fused_mode bit 4096, experiment)
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st2_hint(double *ptr, double a, double b, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(a), "d"(b), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -185,7 +196,8 @@ template <bool CAP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[32 * kFTY], double2 (*sC)[32 * kFTY],
                                             double (*sH)[kFTY], double *xdst, int tid, int lane, int zs, int ze,
                                             long long i, long long sxy, int sx, bool pair_in, bool w0, bool w1,
-                                            int xl, bool xodd, const double *xr, int xrl, bool xrhi) {
+                                            int xl, bool xodd, const double *xr, int xrl, bool xrhi,
+                                            unsigned long long pol) {
     const double *__restrict__ T = F.T;
     const double *__restrict__ Ci = F.Ci;
     double *__restrict__ T2 = F.T2;
@@ -226,7 +238,10 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, double2 (*sT)[
             const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
             const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
             if (w0 && w1) {   // plain stores (streaming stores measured no faster; face cells stay in L2)
-                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+                if (pol)      // (CTA-uniform)
+                    st2_hint(T2 + i, r0, r1, pol);
+                else
+                    *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
             } else {
                 if (w0) T2[i] = r0;
                 if (w1) T2[i + 1] = r1;
@@ -397,7 +412,17 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             xr = F.xstg + xstg_at(F, F.epoch - 1, 1, y, 0);
         }
     }
-    fused_sweep<XS>(F, sT, sC, sH, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd, xr, xrl, xrhi);
+    unsigned long long pol = 0;
+    if (F.xhint) {   // x-face tile: keep its rows in L2 until the face epilogue re-reads the layer
+        bool xface = false;
+        for (int rs = 0; rs < 2; ++rs) {
+            const int xlr = F.face[0][rs].layer;
+            xface |= F.face[0][rs].active && xlr >= max(td.x * 64, 1) && xlr < min(td.x * 64 + 64, sx - 1);
+        }
+        if (xface) pol = policy_evict_last();
+    }
+    fused_sweep<XS>(F, sT, sC, sH, xdst, tid, lane, zs, ze, i, sxy, sx, pair_in, w0, w1, xl, xodd, xr, xrl, xrhi,
+                    pol);
     if (!face_tile) return;   // CTA-uniform
     double *__restrict__ T2 = F.T2;
     __syncthreads();          // the CTA's T2 stores are visible to the CTA
@@ -1145,6 +1170,7 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
         // x faces staged in the receiver's compact buffer (default) or stored straight into its T2
         // column (fused_mode bit 256, ablation: one 8-B value per 32-B sector)
         F.xstage = (recv && !(g->fused_mode & 256) && (F.halo[0][0].active || F.halo[0][1].active)) ? 1 : 0;
+        F.xhint = (g->fused_mode & 4096) ? 1 : 0;
         if (F.xstage) {
             if (!g->fused_xstg) {
                 IGG_CUDA(cudaMalloc(&g->fused_xstg, sizeof(double) * 4 * (size_t)g->n[1] * g->n[2]));

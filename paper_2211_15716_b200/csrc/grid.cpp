@@ -826,22 +826,28 @@ IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float 
     if (!T2 || !T || !Ci) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field list");
     for (int a = 0; a < 3; ++a)
         if (g->n[a] == 2) fail(IGG_E_ARG, "igg_heat_step_f32: an axis needs 1 or at least 3 cells");
-    (void)bw;   // the binary32 step runs the sequential schedule: stencil, then update_halo
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<igg_field> f(g->nlocal);
     for (int lr = 0; lr < g->nlocal; ++lr) {
         if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field pointer");
         f[lr] = igg_field{reinterpret_cast<double *>(T2[lr]), {g->n[0], g->n[1], g->n[2]}, 4};
     }
-    IGG_CUDA(cudaEventRecord(g->ev_start, s));
-    IGG_CUDA(cudaStreamWaitEvent(g->s_comm, g->ev_start, 0));
-    for (int lr = 0; lr < g->nlocal; ++lr) {
-        igg::launch_heat_f32(T2[lr], T[lr], Ci[lr], g->n, lam, dt, dx, dy, dz, g->s_comm);
-        g->launches++;
-    }
-    igg::exchange(g, f.data(), 1, g->s_comm);
-    IGG_CUDA(cudaEventRecord(g->ev_comm, g->s_comm));
-    IGG_CUDA(cudaStreamWaitEvent(s, g->ev_comm, 0));
+    const igg::HeatCoefF k = igg::heat_coef_f32(lam, dt, dx, dy, dz);
+    // @hide_communication bw: boundary slabs, then update_halo!(T2) on the comm stream
+    // behind them, the inner box concurrently; bw = 0 (or NULL) is the sequential schedule
+    igg::hide_comm(
+        g, bw,
+        [&](int lr, const int lo[3], const int hi[3], cudaStream_t st) {
+            bool full = true;
+            for (int a = 0; a < 3; ++a) full = full && lo[a] == (g->n[a] > 1 ? 1 : 0);
+            const bool main_box = st == g->s_inner || full;   // OPT_PROFILE: the inner (or whole) box
+            if (main_box) igg::prof_begin(g, st);
+            igg::launch_heat_f32(T2[lr], T[lr], Ci[lr], g->n, lo, hi, k, st, g->stencil_kernel);
+            if (main_box)
+                igg::prof_end(g, st, (long long)(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]));
+            g->launches++;
+        },
+        f.data(), 1, s, "igg_heat_step_f32");
     IGG_CATCH
 }
 

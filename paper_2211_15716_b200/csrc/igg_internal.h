@@ -180,6 +180,7 @@ struct FusedParams {
     // staging and publish the data flag; nxb receiver blocks per x halo copy the staged column into
     // my T2 and publish xready (local), which the next step's halo tiles await
     int xblk, nxb;
+    int xhint;                       // x-face tiles store with an L2 evict_last hint (experiment)
     unsigned int *xcnt;              // [4][kMaxChunks]: 0..1 face-tile counts, 2..3 receiver-block counts
     unsigned long long *xev;         // [4][kMaxChunks]: 0..1 chunk computed (epoch), 2..3 halo ready (epoch)
 };
@@ -211,9 +212,13 @@ void launch_heat_slabs(HeatRegionList &L, cudaStream_t s);
 // the production stencil: cp.async-pipelined z-sweep over a list of box regions
 // (all local ranks' inner boxes, or the boundary slabs), one launch
 void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant);
-// binary32 heat step on the updated box (size-1 axes allowed); coefficients rounded to float by the caller
-void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], float lam, float dt, float dx,
-                     float dy, float dz, cudaStream_t s);
+// binary32 heat step on the box [lo, hi) (size-1 axes allowed); coefficients rounded to float by the caller
+struct HeatCoefF {
+    float lam, dt, rdx2, rdy2, rdz2;
+};
+HeatCoefF heat_coef_f32(float lam, float dt, float dx, float dy, float dz);
+void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], const int lo[3], const int hi[3],
+                     const HeatCoefF &k, cudaStream_t s, int variant);
 // 1-D/2-D grid (size-1 axes): the stencil without the size-1 axes' terms on the updated box
 void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int n[3], const HeatCoef &k,
                         cudaStream_t s);

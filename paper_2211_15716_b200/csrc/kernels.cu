@@ -85,23 +85,20 @@ void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int
 // association, reciprocals 1/(d*d) computed in float on the host; size-1 axes drop their term
 // (reading 23).  One thread per cell of the updated box, x fastest, a z-chunk of planes per thread
 // with the z neighbours in registers.
-struct HeatCoefF {
-    float lam, dt, rdx2, rdy2, rdz2;
-};
 constexpr int kF32Kc = 16;
 __global__ void __launch_bounds__(256) heat_f32_kernel(float *__restrict__ T2, const float *__restrict__ T,
                                                        const float *__restrict__ Ci, int nx, int ny, int nz,
+                                                       int x0, int y0, int z0, int wx, int wy, int wz,
                                                        const HeatCoefF k) {
     const int ax = nx > 1, ay = ny > 1, az = nz > 1;
-    const int wx = ax ? nx - 2 : 1, wy = ay ? ny - 2 : 1, wz = az ? nz - 2 : 1;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x + ax;
-    const int y = blockIdx.y + ay;
-    const int z0 = blockIdx.z * kF32Kc + az, z1 = min(z0 + kF32Kc, az + wz);
-    if (x >= ax + wx) return;
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // (x, y) flattened: thin x slabs
+    if (t >= (long long)wx * wy) return;                                    // keep every lane busy
+    const int x = x0 + (int)(t % wx), y = y0 + (int)(t / wx);
+    const int zb = z0 + blockIdx.z * kF32Kc, z1 = min(zb + kF32Kc, z0 + wz);
     const long long sx = nx, sxy = (long long)nx * ny;
-    long long i = (long long)z0 * sxy + (long long)y * sx + x;
+    long long i = (long long)zb * sxy + (long long)y * sx + x;
     float zm = az ? __ldg(T + i - sxy) : 0.f, c = __ldg(T + i);
-    for (int z = z0; z < z1; ++z, i += sxy) {
+    for (int z = zb; z < z1; ++z, i += sxy) {
         const float zp = az ? __ldg(T + i + sxy) : 0.f;
         float lap = 0.f;
         bool first = true;
@@ -125,17 +122,197 @@ __global__ void __launch_bounds__(256) heat_f32_kernel(float *__restrict__ T2, c
     }
 }
 
-void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], float lam, float dt, float dx,
-                     float dy, float dz, cudaStream_t s) {
+// 3-D binary32 grids with 16-B aligned rows: the binary64 cp.async pipeline (heat_box_async_kernel)
+// with four floats per lane, so a warp row is again 512 B (128 cells) and every DRAM stream moves
+// the same sectors per instruction as the Float64 kernel.  T[z+1] and Ci[z] are fetched D planes
+// ahead into a per-thread smem ring; rows y+-1 are L2 hits from the neighbouring warps' streams.
+// Box [x0, x0+wx) x [y0, y0+wy) x [z0, z0+wz); x-tiles start at the 512-B boundary below x0.
+__device__ __forceinline__ float heat_cell_f(float c, float xm, float xp, float ym, float yp, float zm, float zp,
+                                             float ci, const HeatCoefF &k) {
+    const float tx = __fmul_rn(__fsub_rn(__fsub_rn(xp, c), __fsub_rn(c, xm)), k.rdx2);
+    const float ty = __fmul_rn(__fsub_rn(__fsub_rn(yp, c), __fsub_rn(c, ym)), k.rdy2);
+    const float tz = __fmul_rn(__fsub_rn(__fsub_rn(zp, c), __fsub_rn(c, zm)), k.rdz2);
+    return __fadd_rn(c, __fmul_rn(k.dt, __fmul_rn(__fmul_rn(k.lam, ci), __fadd_rn(__fadd_rn(tx, ty), tz))));
+}
+template <int V>   // V floats global -> shared (16 B: L1-bypassing .cg; 8 B: .ca, the only 8-B form)
+__device__ __forceinline__ void cp_async_f(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    if (V == 4)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+template <int V> struct VecF;
+template <> struct VecF<2> { using T = float2; };
+template <> struct VecF<4> { using T = float4; };
+template <int V>
+__device__ __forceinline__ void ldv(float (&r)[V], const float *p) {
+    const typename VecF<V>::T v = __ldg(reinterpret_cast<const typename VecF<V>::T *>(p));
+    memcpy(r, &v, sizeof(v));
+}
+// TY warps per CTA (one y row each), D planes of cp.async prefetch, V floats per lane (a warp row is
+// 32*V cells), ST streaming stores of T2
+template <int TY, int D, int V, bool ST>
+__global__ void __launch_bounds__(32 * TY)
+    heat_f32_async_kernel(const float *__restrict__ T, const float *__restrict__ Ci, float *__restrict__ T2, int sx,
+                          int sy, int x0, int y0, int z0, int wx, int wy, int wz, int ax0, int xtiles, int ytiles,
+                          int kc1, int nbig, int kc2, const HeatCoefF k) {
+    using VT = typename VecF<V>::T;
+    __shared__ VT sT[D][32 * TY], sC[D][32 * TY];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ntiles = xtiles * ytiles;
+    const int tile = blockIdx.x % ntiles, chunk = blockIdx.x / ntiles;
+    int zs, ze;
+    if (chunk < nbig) {
+        zs = z0 + chunk * kc1;
+        ze = min(zs + kc1, z0 + wz);
+    } else {
+        zs = z0 + nbig * kc1 + (chunk - nbig) * kc2;
+        ze = min(zs + kc2, z0 + wz);
+    }
+    const int tx = tile % xtiles, ty = tile / xtiles;
+    const int y = y0 + ty * TY + warp;
+    if (y >= y0 + wy || zs >= ze) return;            // per-thread pipeline: no CTA barrier
+    const int p = ax0 + tx * 32 * V + V * lane;      // cells p..p+V-1 (rows are 16-B aligned: sx % 4 == 0)
+    const bool in = p < sx;
+    bool w[V], wall = true;
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+        w[j] = in && p + j >= x0 && p + j < x0 + wx;
+        wall = wall && w[j];
+    }
+    const long long sxy = (long long)sx * sy;
+    long long i = (long long)zs * sxy + (long long)y * sx + p;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {                    // stage q: T[zs+q+1], Ci[zs+q]
+        if (in && zs + q < ze) {
+            cp_async_f<V>(&sT[q][tid], T + i + (q + 1) * sxy);
+            cp_async_f<V>(&sC[q][tid], Ci + i + q * sxy);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    float zm[V] = {}, c[V] = {};
+    if (in) {
+        ldv<V>(zm, T + i - sxy);
+        ldv<V>(c, T + i);
+    }
+    int slot = 0;
+    for (int z = zs; z < ze; ++z, i += sxy) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
+        float ym[V] = {}, yp[V] = {}, zp[V], ci[V];
+        if (in) {
+            ldv<V>(ym, T + i - sx);
+            ldv<V>(yp, T + i + sx);
+        }
+        {
+            const VT a = sT[slot][tid], b = sC[slot][tid];
+            memcpy(zp, &a, sizeof(a));
+            memcpy(ci, &b, sizeof(b));
+        }
+        float xm = __shfl_up_sync(0xffffffffu, c[V - 1], 1);
+        float xp = __shfl_down_sync(0xffffffffu, c[0], 1);
+        if (lane == 0 && w[0]) xm = __ldg(T + i - 1);
+        if (lane == 31 && w[V - 1]) xp = __ldg(T + i + V);
+        float r[V];
+#pragma unroll
+        for (int j = 0; j < V; ++j)
+            r[j] = heat_cell_f(c[j], j == 0 ? xm : c[j - 1], j == V - 1 ? xp : c[j + 1], ym[j], yp[j], zm[j], zp[j],
+                               ci[j], k);
+        if (wall) {
+            VT rv;
+            memcpy(&rv, r, sizeof(rv));
+            if (ST)   // streaming store: T2 is not re-read this step
+                __stcs(reinterpret_cast<VT *>(T2 + i), rv);
+            else
+                *reinterpret_cast<VT *>(T2 + i) = rv;
+        } else {
+#pragma unroll
+            for (int j = 0; j < V; ++j)
+                if (w[j]) T2[i + j] = r[j];
+        }
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+            zm[j] = c[j];
+            c[j] = zp[j];
+        }
+        if (in && z + D < ze) {                      // refill this slot with plane z+D
+            cp_async_f<V>(&sT[slot][tid], T + i + (D + 1) * sxy);
+            cp_async_f<V>(&sC[slot][tid], Ci + i + D * sxy);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        slot = slot + 1 == D ? 0 : slot + 1;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+HeatCoefF heat_coef_f32(float lam, float dt, float dx, float dy, float dz) {
     HeatCoefF k;
     k.lam = lam;
     k.dt = dt;
     k.rdx2 = 1.0f / (dx * dx);   // in float, as the binary32 oracle (reading 24)
     k.rdy2 = 1.0f / (dy * dy);
     k.rdz2 = 1.0f / (dz * dz);
-    const int wx = n[0] > 1 ? n[0] - 2 : 1, wy = n[1] > 1 ? n[1] - 2 : 1, wz = n[2] > 1 ? n[2] - 2 : 1;
-    const dim3 grid((wx + 255) / 256, wy, (wz + kF32Kc - 1) / kF32Kc);
-    heat_f32_kernel<<<grid, 256, 0, s>>>(T2, T, Ci, n[0], n[1], n[2], k);
+    return k;
+}
+
+template <int TY, int D, int V, bool ST>
+static void launch_f32_async(float *T2, const float *T, const float *Ci, const int n[3], const int lo[3],
+                             const int hi[3], const HeatCoefF &k, cudaStream_t s, int kc1, int kc2) {
+    static int occ = -1, nsm = 0;
+    if (occ < 0) {
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, heat_f32_async_kernel<TY, D, V, ST>, 32 * TY, 0));
+        int dev = 0;
+        IGG_CUDA(cudaGetDevice(&dev));
+        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int wx = hi[0] - lo[0], wy = hi[1] - lo[1], wz = hi[2] - lo[2];
+    constexpr int TW = 32 * V;                       // tile width in cells
+    const int ax0 = lo[0] & ~(TW - 1);
+    const int xtiles = (hi[0] - ax0 + TW - 1) / TW, ytiles = (wy + TY - 1) / TY, ntiles = xtiles * ytiles;
+    // z-chunks of kc1 planes; about two waves' worth of tile-planes at the end in kc2-plane chunks
+    const long long conc = (long long)occ * nsm;
+    int small = (int)((2 * conc * kc2 + ntiles - 1) / ntiles);
+    small = std::min(((small + kc2 - 1) / kc2) * kc2, wz);
+    const int nbig = (wz - small) / kc1;             // whole big chunks only; the rest goes in small ones
+    const int nsmall = (wz - nbig * kc1 + kc2 - 1) / kc2;
+    heat_f32_async_kernel<TY, D, V, ST><<<(unsigned)((long long)ntiles * (nbig + nsmall)), 32 * TY, 0, s>>>(
+        T, Ci, T2, n[0], n[1], lo[0], lo[1], lo[2], wx, wy, wz, ax0, xtiles, ytiles, kc1, nbig, kc2, k);
+    IGG_CUDA(cudaGetLastError());
+}
+
+// variant (IGG_OPT_STENCIL_KERNEL): 0 = default (TY 4, D 3, float4 lanes, streaming stores, z-chunks 64
+// with an 8-plane tail); 101.. = the ablations measured in profiles/; 1 = the scalar kernel
+void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], const int lo[3], const int hi[3],
+                     const HeatCoefF &k, cudaStream_t s, int variant) {
+    const int wx = hi[0] - lo[0], wy = hi[1] - lo[1], wz = hi[2] - lo[2];
+    if (wx <= 0 || wy <= 0 || wz <= 0) return;
+    const bool aligned = n[0] % 4 == 0 && (((uintptr_t)T | (uintptr_t)T2 | (uintptr_t)Ci) & 15) == 0;
+    if (n[0] > 1 && n[1] > 1 && n[2] > 1 && aligned && wx >= 64 && variant != 1) {
+        switch (variant) {
+            case 101: launch_f32_async<8, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 102: launch_f32_async<4, 4, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 103: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 104: launch_f32_async<4, 3, 4, false>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 105: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 128, 16); break;
+            case 106: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 32, 8); break;
+            case 107: launch_f32_async<4, 3, 2, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 108: launch_f32_async<8, 3, 2, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 109: launch_f32_async<4, 4, 2, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 110: launch_f32_async<8, 4, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 111: launch_f32_async<2, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 112: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 4); break;
+            case 113: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 32, 8); break;
+            case 114: launch_f32_async<4, 4, 4, true>(T2, T, Ci, n, lo, hi, k, s, 32, 8); break;
+            case 115: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
+            case 116: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 24, 8); break;
+            case 117: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 16, 8); break;
+            case 118: launch_f32_async<2, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 32, 8); break;
+            default: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+        }
+        return;
+    }
+    const dim3 grid((unsigned)(((long long)wx * wy + 255) / 256), 1, (wz + kF32Kc - 1) / kF32Kc);
+    heat_f32_kernel<<<grid, 256, 0, s>>>(T2, T, Ci, n[0], n[1], n[2], lo[0], lo[1], lo[2], wx, wy, wz, k);
     IGG_CUDA(cudaGetLastError());
 }
 

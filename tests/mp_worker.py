@@ -103,7 +103,7 @@ def gather_case(path, n, dims, per, s):
     log("gather OK", dims, per, s)
 
 
-def heat_f32_case(path, n, dims, per, nt=5):
+def heat_f32_case(path, n, dims, per, nt=5, bw=(16, 2, 2)):
     """The binary32 variant (igg_heat_step_f32, float halos through NCCL / NVLink) vs the binary32 oracle."""
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=1, path=path,
                            device=int(os.environ["LOCAL_RANK"]))
@@ -115,7 +115,7 @@ def heat_f32_case(path, n, dims, per, nt=5):
         T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
         app.init_random(g, T, T2, Ci)
         for _ in range(nt):
-            g.heat_step(T2, T, Ci, 1.0, dt, *d)
+            g.heat_step(T2, T, Ci, 1.0, dt, *d, bw=bw)
             T, T2 = T2, T
         torch.cuda.synchronize()
         g.check()
@@ -125,7 +125,7 @@ def heat_f32_case(path, n, dims, per, nt=5):
             raise AssertionError(f"heat f32 {path} {dims} per={per}")
     finally:
         g.finalize()
-    log("heat f32 OK", path, dims, per)
+    log("heat f32 OK", path, n, dims, per, bw)
 
 
 def acoustic_case(path, n, dims, per, local, bw, nt=5):
@@ -188,6 +188,8 @@ def main():
         halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
         acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4))
         heat_f32_case(path, n, dims, (1, 0, 1))
+        heat_f32_case(path, (264, 36, 34), dims, (0, 0, 0), bw=(16, 2, 2))   # hide_communication, float4 kernel
+        heat_f32_case(path, (264, 36, 34), dims, (1, 1, 0), bw=(0, 0, 0))
         acoustic_case(path, n, dims, (1, 0, 1), 1, (4, 4, 4))
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
         # 8 ranks as virtual ranks over the processes (2x2x2 correctness on fewer GPUs)

@@ -256,10 +256,14 @@ def test_low_dimensional_init_rules():
     dict(n=(24, 20, 18), dims=(2, 2, 1), per=(1, 0, 0)),
     dict(n=(30, 26, 1), dims=(2, 1, 1), per=(0, 0, 0)),      # 2-D
     dict(n=(40, 22, 20), dims=(1, 1, 1), per=(0, 1, 1)),     # self-wrap
+    dict(n=(264, 21, 75), dims=(1, 1, 1), per=(0, 0, 0)),    # 3 x-tiles of the float4 kernel, ragged y/z
+    dict(n=(132, 9, 40), dims=(2, 1, 1), per=(0, 0, 1)),     # 2 x-tiles on each of 2 ranks
+    dict(n=(30, 20, 18), dims=(1, 2, 1), per=(0, 0, 0)),     # rows not 16-B aligned: the scalar kernel
 ])
-def test_binary32_heat_vs_oracle(case):
+@pytest.mark.parametrize("bw", [(0, 0, 0), (4, 2, 2), (16, 2, 2)])
+def test_binary32_heat_vs_oracle(case, bw):
     """The binary32 variant (reading 24): igg_heat_step_f32 with update_halo of a
-    float field, bit-exact vs the binary32 oracle on the global grid."""
+    float field (sequential and hide_communication schedules), bit-exact vs the binary32 oracle."""
     import torch
     n, dims, per = case["n"], case["dims"], case["per"]
     nprocs = dims[0] * dims[1] * dims[2]
@@ -273,7 +277,7 @@ def test_binary32_heat_vs_oracle(case):
         T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
         app.init_random(g, T, T2, Ci)
         for _ in range(6):
-            g.heat_step(T2, T, Ci, 1.0, dt, *d)
+            g.heat_step(T2, T, Ci, 1.0, dt, *d, bw=bw)
             T, T2 = T2, T
         torch.cuda.synchronize()
         g.check()
@@ -281,5 +285,61 @@ def test_binary32_heat_vs_oracle(case):
             W = OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)
             got = T[r].cpu().numpy()
             assert got.dtype == np.float32 and np.array_equal(got, W), (case, r)
+    finally:
+        g.finalize()
+
+
+@pytest.mark.gpu
+def test_binary32_full_size_512():
+    """The f32 bench configuration (512^3 local, one GPU, the float4 cp.async kernel with its 64-plane
+    chunks and 8-plane tail), nt = 2, every cell bit-exact vs the binary32 oracle (reading 24)."""
+    import torch
+    n, nt = (512, 512, 512), 2
+    N = tuple(OG.global_size(n[i], 2, 1, False) for i in range(3))
+    T0g, Cig = SI.global_heat_fields(*N)
+    d = [OH.spacing(1.0, N[i], False) for i in range(3)]
+    dt = OH.stable_dt(*d, 1.0, Cig)
+    ref = OH.heat_run_f32(T0g, Cig, nt, (0, 0, 0), 1.0, dt, *d)
+    del T0g, Cig
+    g = P.init_global_grid(*n, local_ranks=1, device=0)
+    try:
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
+        app.init_random(g, T, T2, Ci)
+        for _ in range(nt):
+            g.heat_step(T2, T, Ci, 1.0, dt, *d)
+            T, T2 = T2, T
+        torch.cuda.synchronize()
+        g.check()
+        got = T[0].cpu().numpy()
+        assert got.dtype == np.float32 and np.array_equal(got, ref)
+    finally:
+        g.finalize()
+
+
+@pytest.mark.parametrize("variant", [0, 1] + list(range(101, 119)))
+def test_binary32_kernel_variants_bit_exact(variant):
+    """Every binary32 stencil variant (IGG_OPT_STENCIL_KERNEL; 1 = the scalar kernel, 101.. = the
+    float4/float2 cp.async ablations) is valid: 2 virtual ranks, hide_communication (16,2,2) (inner
+    box starting off a tile boundary, slabs through the scalar kernel), bit-exact vs the binary32 oracle."""
+    import torch
+    n, dims, per = (264, 21, 75), (2, 1, 1), (0, 0, 1)
+    N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+    T0g, Cig = SI.global_heat_fields(*N)
+    d = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+    dt = OH.stable_dt(*d, 1.0, Cig)
+    ref = OH.heat_run_f32(T0g, Cig, 4, per, 1.0, dt, *d)
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=2, device=0)
+    try:
+        g.set_option(P.OPT_STENCIL_KERNEL, variant)
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
+        app.init_random(g, T, T2, Ci)
+        for _ in range(4):
+            g.heat_step(T2, T, Ci, 1.0, dt, *d, bw=(16, 2, 2))
+            T, T2 = T2, T
+        torch.cuda.synchronize()
+        g.check()
+        for r in range(2):
+            W = OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)
+            assert np.array_equal(T[r].cpu().numpy(), W), (variant, r)
     finally:
         g.finalize()
