@@ -682,7 +682,7 @@ using RegionFn = std::function<void(int lr, const int lo[3], const int hi[3], cu
 // the high-priority comm stream, the exchange behind them there, the inner box concurrently on the
 // low-priority stream; both joined to s.
 static void hide_comm(igg_grid *g, const int bw_in[3], const RegionFn &fn, const igg_field *fields, int nfields,
-                      cudaStream_t s, const char *who) {
+                      cudaStream_t s, const char *who, int x_align = 1) {
     const int zero[3] = {0, 0, 0};
     const int *bw = bw_in ? bw_in : zero;
     bool exch[3] = {false, false, false};
@@ -707,6 +707,12 @@ static void hide_comm(igg_grid *g, const int bw_in[3], const RegionFn &fn, const
         const int b = exch[a] ? bw[a] : 0;
         lo[a] = std::max(1, b);
         hi[a] = std::min(g->n[a] - 1, g->n[a] - b);
+        if (a == 0 && exch[0] && x_align > 1) {
+            // x-boundaries on whole row segments of the caller's tile (as heat_step's x_align): the
+            // boundary phase grows, every cell is still computed exactly once
+            lo[0] = ((lo[0] + x_align - 1) / x_align) * x_align;
+            hi[0] = (hi[0] / x_align) * x_align;
+        }
         if (g->n[a] == 1) {   // a size-1 axis (1-D/2-D grid): its one layer, no slabs along it
             lo[a] = 0;
             hi[a] = 1;
@@ -847,7 +853,10 @@ IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float 
                 igg::prof_end(g, st, (long long)(hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]));
             g->launches++;
         },
-        f.data(), 1, s, "igg_heat_step_f32");
+        f.data(), 1, s, "igg_heat_step_f32",
+        // IGG_OPT_X_ALIGN counts binary64 cells (64 = a 512-B row segment); the binary32 kernel's
+        // 512-B segment is twice as many cells
+        g->x_align > 1 ? 2 * g->x_align : 1);
     IGG_CATCH
 }
 

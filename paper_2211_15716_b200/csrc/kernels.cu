@@ -280,8 +280,9 @@ static void launch_f32_async(float *T2, const float *T, const float *Ci, const i
     IGG_CUDA(cudaGetLastError());
 }
 
-// variant (IGG_OPT_STENCIL_KERNEL): 0 = default (TY 4, D 3, float4 lanes, streaming stores, z-chunks 64
-// with an 8-plane tail); 101.. = the ablations measured in profiles/; 1 = the scalar kernel
+// variant (IGG_OPT_STENCIL_KERNEL): 0 = default (TY 4, D 2, float4 lanes, streaming stores, z-chunks 48
+// with an 8-plane tail: the measured best, profiles/r01_f32_variant_sweep.txt); 100.. = ablations;
+// 1 = the scalar kernel
 void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], const int lo[3], const int hi[3],
                      const HeatCoefF &k, cudaStream_t s, int variant) {
     const int wx = hi[0] - lo[0], wy = hi[1] - lo[1], wz = hi[2] - lo[2];
@@ -307,7 +308,16 @@ void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3],
             case 116: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 24, 8); break;
             case 117: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 16, 8); break;
             case 118: launch_f32_async<2, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 32, 8); break;
-            default: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
+            case 119: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 40, 8); break;
+            case 120: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 56, 8); break;
+            case 121: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 4); break;
+            case 122: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 16); break;
+            case 123: launch_f32_async<8, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
+            case 124: launch_f32_async<4, 1, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
+            case 125: launch_f32_async<4, 2, 4, false>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
+            case 126: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
+            case 100: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;   // = f64 default
+            default: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;   // 0 = 115
         }
         return;
     }

@@ -259,6 +259,7 @@ def test_low_dimensional_init_rules():
     dict(n=(264, 21, 75), dims=(1, 1, 1), per=(0, 0, 0)),    # 3 x-tiles of the float4 kernel, ragged y/z
     dict(n=(132, 9, 40), dims=(2, 1, 1), per=(0, 0, 1)),     # 2 x-tiles on each of 2 ranks
     dict(n=(30, 20, 18), dims=(1, 2, 1), per=(0, 0, 0)),     # rows not 16-B aligned: the scalar kernel
+    dict(n=(520, 13, 40), dims=(2, 1, 1), per=(0, 0, 0)),    # x boundary slabs on 512-B segments (x_align)
 ])
 @pytest.mark.parametrize("bw", [(0, 0, 0), (4, 2, 2), (16, 2, 2)])
 def test_binary32_heat_vs_oracle(case, bw):
@@ -316,7 +317,7 @@ def test_binary32_full_size_512():
         g.finalize()
 
 
-@pytest.mark.parametrize("variant", [0, 1] + list(range(101, 119)))
+@pytest.mark.parametrize("variant", [0, 1] + list(range(100, 127)))
 def test_binary32_kernel_variants_bit_exact(variant):
     """Every binary32 stencil variant (IGG_OPT_STENCIL_KERNEL; 1 = the scalar kernel, 101.. = the
     float4/float2 cp.async ablations) is valid: 2 virtual ranks, hide_communication (16,2,2) (inner
@@ -331,6 +332,7 @@ def test_binary32_kernel_variants_bit_exact(variant):
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=2, device=0)
     try:
         g.set_option(P.OPT_STENCIL_KERNEL, variant)
+        g.set_option(P.OPT_X_ALIGN, 1)   # exact bw: the inner box starts off a tile boundary
         T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
         app.init_random(g, T, T2, Ci)
         for _ in range(4):
