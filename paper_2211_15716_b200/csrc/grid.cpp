@@ -840,9 +840,16 @@ IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float 
     }
     const igg::HeatCoefF k = igg::heat_coef_f32(lam, dt, dx, dy, dz);
     // @hide_communication bw: boundary slabs, then update_halo!(T2) on the comm stream
-    // behind them, the inner box concurrently; bw = 0 (or NULL) is the sequential schedule
+    // behind them, the inner box concurrently; bw = 0 (or NULL) is the sequential schedule.  With an
+    // exchanged x axis the x slabs cut every row into 15 + inner + 15 cells, which costs more than the
+    // exposed exchange (2x1x1 at 512^3: 0.306 ms hidden vs 0.287 ms sequential), so the
+    // step runs sequentially there (same cells, same result); fused_mode bit 16384 keeps the slabs.
+    bool xex = false;
+    for (int lr = 0; lr < g->nlocal; ++lr) xex = xex || g->nbr[lr][0][0] >= 0 || g->nbr[lr][0][1] >= 0;
+    const int zero[3] = {0, 0, 0};
+    const int *bw_eff = (xex && !(g->fused_mode & 16384)) ? zero : bw;
     igg::hide_comm(
-        g, bw,
+        g, bw_eff,
         [&](int lr, const int lo[3], const int hi[3], cudaStream_t st) {
             bool full = true;
             for (int a = 0; a < 3; ++a) full = full && lo[a] == (g->n[a] > 1 ? 1 : 0);
@@ -854,9 +861,10 @@ IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float 
             g->launches++;
         },
         f.data(), 1, s, "igg_heat_step_f32",
-        // IGG_OPT_X_ALIGN counts binary64 cells (64 = a 512-B row segment); the binary32 kernel's
-        // 512-B segment is twice as many cells
-        g->x_align > 1 ? 2 * g->x_align : 1);
+        // exact bw in x: growing the x slabs to whole 512-B segments (128 binary32 cells) measured
+        // slower on a 2x1x1 split (0.313 vs 0.306 ms/step, profiles/r01_f32_scaling.txt); fused_mode
+        // bit 8192 restores it for the ablation
+        (g->fused_mode & 8192) ? 128 : 1);
     IGG_CATCH
 }
 

@@ -103,7 +103,7 @@ def gather_case(path, n, dims, per, s):
     log("gather OK", dims, per, s)
 
 
-def heat_f32_case(path, n, dims, per, nt=5, bw=(16, 2, 2)):
+def heat_f32_case(path, n, dims, per, nt=5, bw=(16, 2, 2), opts=None):
     """The binary32 variant (igg_heat_step_f32, float halos through NCCL / NVLink) vs the binary32 oracle."""
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=1, path=path,
                            device=int(os.environ["LOCAL_RANK"]))
@@ -112,6 +112,8 @@ def heat_f32_case(path, n, dims, per, nt=5, bw=(16, 2, 2)):
         T0g, Cig = SI.global_heat_fields(*N)
         d = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
         dt = OH.stable_dt(*d, 1.0, Cig)
+        for key, val in (opts or {}).items():
+            g.set_option(key, val)
         T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
         app.init_random(g, T, T2, Ci)
         for _ in range(nt):
@@ -189,6 +191,7 @@ def main():
         acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4))
         heat_f32_case(path, n, dims, (1, 0, 1))
         heat_f32_case(path, (520, 20, 34), dims, (0, 0, 0), bw=(16, 2, 2))   # hide_communication, float4 kernel
+        heat_f32_case(path, (520, 20, 34), dims, (0, 1, 0), bw=(16, 2, 2), opts={P.OPT_FUSED_MODE: 2 | 16384})
         heat_f32_case(path, (264, 36, 34), dims, (1, 1, 0), bw=(0, 0, 0))
         acoustic_case(path, n, dims, (1, 0, 1), 1, (4, 4, 4))
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)

@@ -259,7 +259,7 @@ def test_low_dimensional_init_rules():
     dict(n=(264, 21, 75), dims=(1, 1, 1), per=(0, 0, 0)),    # 3 x-tiles of the float4 kernel, ragged y/z
     dict(n=(132, 9, 40), dims=(2, 1, 1), per=(0, 0, 1)),     # 2 x-tiles on each of 2 ranks
     dict(n=(30, 20, 18), dims=(1, 2, 1), per=(0, 0, 0)),     # rows not 16-B aligned: the scalar kernel
-    dict(n=(520, 13, 40), dims=(2, 1, 1), per=(0, 0, 0)),    # x boundary slabs on 512-B segments (x_align)
+    dict(n=(520, 13, 40), dims=(2, 1, 1), per=(0, 0, 0)),    # non-degenerate x split: float4 inner box
 ])
 @pytest.mark.parametrize("bw", [(0, 0, 0), (4, 2, 2), (16, 2, 2)])
 def test_binary32_heat_vs_oracle(case, bw):
@@ -332,7 +332,7 @@ def test_binary32_kernel_variants_bit_exact(variant):
     g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=2, device=0)
     try:
         g.set_option(P.OPT_STENCIL_KERNEL, variant)
-        g.set_option(P.OPT_X_ALIGN, 1)   # exact bw: the inner box starts off a tile boundary
+        g.set_option(P.OPT_FUSED_MODE, 2 | 16384)   # keep the x slabs (hide_communication in x)
         T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
         app.init_random(g, T, T2, Ci)
         for _ in range(4):
@@ -343,5 +343,31 @@ def test_binary32_kernel_variants_bit_exact(variant):
         for r in range(2):
             W = OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)
             assert np.array_equal(T[r].cpu().numpy(), W), (variant, r)
+    finally:
+        g.finalize()
+
+
+def test_binary32_aligned_x_slabs():
+    """fused_mode bits 16384 + 8192 (ablation): binary32 x boundary slabs kept, grown to whole 512-B segments."""
+    import torch
+    n, dims, per = (520, 13, 40), (2, 1, 1), (1, 0, 0)
+    N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+    T0g, Cig = SI.global_heat_fields(*N)
+    d = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+    dt = OH.stable_dt(*d, 1.0, Cig)
+    ref = OH.heat_run_f32(T0g, Cig, 4, per, 1.0, dt, *d)
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=2, device=0)
+    try:
+        g.set_option(P.OPT_FUSED_MODE, 2 | 8192 | 16384)
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
+        app.init_random(g, T, T2, Ci)
+        for _ in range(4):
+            g.heat_step(T2, T, Ci, 1.0, dt, *d, bw=(16, 2, 2))
+            T, T2 = T2, T
+        torch.cuda.synchronize()
+        g.check()
+        for r in range(2):
+            W = OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)
+            assert np.array_equal(T[r].cpu().numpy(), W), r
     finally:
         g.finalize()
