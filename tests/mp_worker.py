@@ -156,12 +156,80 @@ def acoustic_case(path, n, dims, per, local, bw, nt=5):
     log("acoustic OK", path, dims, per, "local", local)
 
 
+def full_size_case(path, dtype, nt=3):
+    """The bench configuration (512^3 per GPU, dims DIMS[world], bw (16,2,2); binary64 through
+    igg_heat_run -- the pipelined fused path bench.py times --, binary32 through igg_heat_step) at full
+    size: sub-boxes at the exchanged faces, corners and centre are re-run by the oracle as grids of their
+    own from the same seeded initial values; cells farther than nt+1 layers (the domain of dependence)
+    from a sub-box edge that is not a global boundary agree bit for bit."""
+    n = (512, 512, 512)
+    world = dist.get_world_size()
+    dims = DIMS[world]
+    g = P.init_global_grid(*n, dims=dims, local_ranks=1, path=path, device=int(os.environ["LOCAL_RANK"]))
+    try:
+        f32 = dtype == "f32"
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32 if f32 else None)
+        app.init_random(g, T, T2, Ci)
+        T0 = T[0].clone()
+        d = app.spacing(g)
+        if f32:   # dt of the float fields as the binary32 bench takes it: global max(Ci) on the device
+            mx = Ci[0].max().double()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dt = min(x * x for x in d) / 1.0 / float(mx) / 6.1
+        else:
+            dt = app.stable_dt(g, Ci, *d)
+        if f32:
+            for _ in range(nt):
+                g.heat_step(T2, T, Ci, 1.0, dt, *d, bw=(16, 2, 2))
+                T, T2 = T2, T
+        else:
+            T, T2 = app.run(g, T, T2, Ci, nt, dt, d, app.LAM, bw=(16, 2, 2))
+        torch.cuda.synchronize()
+        g.check()
+        Ng = [g.n_global(a) for a in range(3)]
+        gi = [g.global_indices(g.rank0, a, n[a]) for a in range(3)]
+        m, L = nt + 1, 36
+        for z0 in (0, 251, 512 - L):
+            for y0 in (0, 300, 512 - L):
+                for x0 in (0, 8, 240, 512 - L):
+                    st = (z0, y0, x0)
+                    box = tuple(slice(st[a], st[a] + L) for a in range(3))
+                    sT0 = T0[box].cpu().numpy()
+                    sC = Ci[0][box].cpu().numpy()
+                    got = T[0][box].cpu().numpy()
+                    if f32:
+                        ref = OH.heat_run_f32(sT0, sC, nt, (0, 0, 0), 1.0, dt, *d)
+                    else:
+                        ref = OH.heat_run(sT0, sC, nt, (0, 0, 0), app.LAM, dt, *d, mode=OH.CANONICAL)
+                    # array axis k (z, y, x) is grid axis 2-k; a side is exact where it is a global boundary
+                    cut = []
+                    for k in range(3):
+                        a = 2 - k
+                        g_lo = gi[a][st[k]]
+                        g_hi = gi[a][st[k] + L - 1]
+                        cut.append(slice(0 if g_lo == 0 else m, L - (0 if g_hi == Ng[a] - 1 else m)))
+                    cut = tuple(cut)
+                    if not np.array_equal(ref[cut], got[cut]):
+                        raise AssertionError(f"full-size {dtype} {path} rank {g.rank0} box {st}")
+    finally:
+        g.finalize()
+    log("full-size OK", dtype, path, dims)
+
+
 def main():
     local_rank = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local_rank)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     world = dist.get_world_size()
     paths = sys.argv[1].split(",") if len(sys.argv) > 1 else ["nccl", "p2p"]
+    if len(sys.argv) > 2 and sys.argv[2] == "full":   # the bench configuration at full size
+        for dtype in ("f64", "f32"):
+            full_size_case(paths[0], dtype)
+        dist.barrier()
+        if dist.get_rank() == 0:
+            print("MULTI-GPU FULL-SIZE OK", world, paths, flush=True)
+        dist.destroy_process_group()
+        return
     dims = DIMS[world]
     n = (40, 36, 34)
     sizes = [n, (41, 36, 34), (40, 37, 34), (40, 36, 35)]

@@ -37,3 +37,20 @@ def test_torchrun_parity(path):
     sys.stderr.write(r.stderr[-4000:])
     assert r.returncode == 0
     assert "MULTI-GPU PARITY OK" in r.stdout
+
+
+def test_torchrun_full_size_bench_config():
+    """512^3 per GPU in the bench's launch configuration (fused pipelined binary64 run, binary32 step),
+    sampled sub-boxes vs the oracle (tests/mp_worker.py full_size_case)."""
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = 4 if n >= 4 else 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_worker.py"),
+           "p2p", "full"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    sys.stdout.write(r.stdout[-4000:])
+    sys.stderr.write(r.stderr[-4000:])
+    assert r.returncode == 0
+    assert "MULTI-GPU FULL-SIZE OK" in r.stdout
