@@ -169,3 +169,24 @@ def test_init_without_gpu_fails_loudly():
     with pytest.raises(P.IggError) as e:
         P.init_global_grid(8, 8, 8, dims=(1, 1, 1), device=0)
     assert e.value.name == "IGG_E_CUDA"
+
+
+def test_missing_library_raises_instead_of_falling_back(monkeypatch):
+    """The product path has no CPU fallback: without libigg.so every call
+    raises ImportError (nothing routes through oracle/)."""
+    monkeypatch.setattr(_lib, "SO_PATH", os.path.join(ROOT, "no_such_dir", "libigg.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError, match="no fallback"):
+        _lib.lib()
+    with pytest.raises(ImportError):
+        P.global_size(8, 2, 2, False)
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2211_15716_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
+                src = open(os.path.join(dirpath, f), errors="replace").read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
+                assert "heat3d_oracle" not in src, f
