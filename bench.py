@@ -541,8 +541,12 @@ def run_acoustic(a):
     k_avg_ms = k_ms / max(k_n, 1)
     k_bytes = AC_V_BYTES_PER_CELL * k_cells / max(k_n, 1)
     achieved = k_bytes / (k_avg_ms * 1e-3) / 1e9 if k_n else None
+    tr = dram_traffic_per_launch("traffic_acoustic.json")
+    traffic = None
+    if tr and tr.get("n") == n and tr.get("dims") == list(dims):
+        traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None, "traffic": None,
+                "frac": achieved / peak if achieved else None, "traffic": traffic,
                 "kernel": "acoustic_v_kernel (" + ("inner box" if world > 1 else "whole box") + ")",
                 "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_avg_ms, "launches": k_n,
                 "peak_source": peak_src, "share_of_step": k_avg_ms * (k_n / prof_steps) / ms if k_n else None}

@@ -25,7 +25,7 @@ namespace igg {
 namespace {
 
 constexpr int kAcTY = 4;    // rows per CTA (one warp each)
-constexpr int kAcKC = 32;   // planes per CTA
+constexpr int kAcKC = 8;    // planes per CTA (tiling sweep: 8 beats 12/16/32/64/128, profiles/r01_acoustic_tiling_sweep.txt)
 
 __device__ __forceinline__ double ldg(const double *p) { return __ldg(p); }
 
