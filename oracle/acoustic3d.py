@@ -30,11 +30,15 @@ paper's own stencil notation:
         cV_d = (dt / rho) / d_d,   cP = dt * K,   r_d = 1.0 / d_d.
   * binary64, every operation rounded on its own (numpy never contracts to FMA).
 
-Pins (tests/test_oracle_acoustic.py): the exact evolution of one periodic
-Fourier mode (the 4x4 per-mode amplification matrix raised to the n-th power
-with numpy), conservation of sum(P) with periodic boundaries, exact mirror
-symmetry, the fixed point, a second pure-Python transcription, and
-decomposition independence through oracle.halo.
+Pins (tests/test_oracle_acoustic.py): the coefficients (reading A2) from the
+physics alone -- a travelling periodic mode built from (rho, K, dt, d) only,
+with the leapfrog dispersion relation sin^2(phi/2) = (K/rho) dt^2 sum s_d^2/d_d^2
+and the wave impedance |V|/|P| = 1/sqrt(rho K), is reproduced step by step, and
+the measured sound speed of a standing wave tends to sqrt(K/rho); the exact
+evolution of one periodic Fourier mode (the 4x4 per-mode amplification matrix
+raised to the n-th power with numpy), conservation of sum(P) with periodic
+boundaries, exact mirror symmetry, the fixed point, a second pure-Python
+transcription, and decomposition independence through oracle.halo.
 """
 from __future__ import annotations
 

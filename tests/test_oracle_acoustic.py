@@ -155,3 +155,71 @@ def test_decomposition_independence():
             for f in range(4):
                 W = G.window(ref[f], c, dims, n, o, per, sizes[f])
                 assert np.array_equal(loc[r][f], W), (case, dims, n, per, r, f)
+
+
+# ---------------------------------------------------------------------------------------------------
+# Pins of the coefficients (reading A2) from the physics alone -- no call to A.coefficients().
+#
+# The continuum equations rho dV/dt = -grad P, dP/dt = -K div V (the system the leapfrog discretises)
+# fix two numbers a correct discretisation must reproduce for a periodic mode with phase angles
+# theta_d (s_d = sin(theta_d/2)), written only in terms of (rho, K, dt, d_d):
+#   * the leapfrog dispersion relation  sin^2(phi/2) = (K/rho) dt^2 sum_d s_d^2 / d_d^2   (phi: phase
+#     advance per step; a 2x2 system with determinant 1 for (P, longitudinal V)),
+#   * the wave impedance of a travelling mode  |V| / |P| = 1 / sqrt(rho K), along the discrete wave
+#     vector (s_d/d_d)/S, S = sqrt(sum s_d^2/d_d^2), with V lagging P by half a cell and half a step.
+# A travelling mode initialised from these is reproduced step after step.  A wrong cV (e.g.
+# dt/(rho d^2), or K in place of 1/rho) or a wrong cP / r_d changes phi or the impedance and fails.
+def _travelling_mode(N, m, rho, K, dt, d):
+    theta = [2.0 * math.pi * m[i] / N[i] for i in range(3)]
+    s = [math.sin(t / 2.0) for t in theta]
+    S = math.sqrt(sum(s[i] ** 2 / d[i] ** 2 for i in range(3)))
+    phi = 2.0 * math.asin(math.sqrt(K / rho) * dt * S)
+    Z = math.sqrt(rho * K)
+    z, y, x = np.meshgrid(np.arange(N[2]), np.arange(N[1]), np.arange(N[0]), indexing="ij")
+    phase = theta[0] * x + theta[1] * y + theta[2] * z
+
+    def fields(n):
+        P = np.cos(phase + n * phi)
+        V = [-(1.0 / Z) * (s[dd] / d[dd]) / S * np.cos(phase - theta[dd] / 2 - phi / 2 + n * phi) for dd in range(3)]
+        return [P] + V
+    return fields, phi
+
+
+@pytest.mark.parametrize("N,m,rho,K,d", [
+    ((8, 6, 10), (1, 2, 1), 1.3, 0.7, (0.125, 0.2, 0.09)),
+    ((12, 5, 7), (3, 0, 2), 2.0, 3.5, (0.1, 0.1, 0.1)),
+    ((16, 4, 4), (1, 0, 0), 0.8, 1.9, (0.05, 0.3, 0.3)),
+])
+def test_travelling_mode_dispersion_and_impedance(N, m, rho, K, d):
+    dt = 0.45 * min(d) / math.sqrt(K / rho) / math.sqrt(3.0)
+    fields, phi = _travelling_mode(N, m, rho, K, dt, d)
+    assert phi > 0.05                                   # the mode really moves
+    F0 = fields(0)
+    nt = 17
+    out = A.run(*F0, nt, (1, 1, 1), dt, rho, K, *d)
+    for got, ref in zip(out, fields(nt)):
+        assert np.max(np.abs(got - ref)) < 1e-12
+
+
+def test_sound_speed_continuum_limit():
+    """A standing wave on a fine grid oscillates at omega = c k with c = sqrt(K/rho): the phase
+    advance per step measured from the oracle's P (cos(phi) = (p[n+1] + p[n-1]) / (2 p[n]), the
+    recurrence of a determinant-1 two-level scheme) gives c within the O((k d)^2 + (omega dt)^2)
+    discretisation error."""
+    N, lx, rho, K = (128, 4, 4), 1.0, 1.7, 2.9
+    d = (lx / N[0], 0.5, 0.5)
+    c = math.sqrt(K / rho)
+    dt = 0.2 * d[0] / c
+    k = 2.0 * math.pi / lx
+    x = np.arange(N[0])
+    F = [np.zeros(s) for s in A.field_shapes(N, (1, 1, 1))]
+    F[0][...] = np.cos(k * d[0] * x)[None, None, :]
+    amp = []
+    for _ in range(3):
+        amp.append(float(np.sum(F[0][0, 0, :] * np.cos(k * d[0] * x))) * 2.0 / N[0])
+        F = list(A.run(*F, 1, (1, 1, 1), dt, rho, K, *d))
+    cphi = (amp[2] + amp[0]) / (2.0 * amp[1])
+    c_num = math.acos(cphi) / dt / k
+    assert abs(c_num / c - 1.0) < 2e-3
+    # a scheme with the wrong speed (e.g. K*rho or 1/rho in place of K/rho) is far outside that
+    assert abs(math.sqrt(K * rho) / c - 1.0) > 0.1 and abs(math.sqrt(1.0 / rho) / c - 1.0) > 0.1

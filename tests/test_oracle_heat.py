@@ -265,3 +265,26 @@ def test_f32_fourier_mode_decay():
 def SI_fields(N):
     import synthetic_inputs as SI
     return SI.global_heat_fields(*N)
+
+
+@pytest.mark.parametrize("lx,k", [(0.7, 1), (2.3, 2)])
+def test_periodic_spacing_continuum_decay(lx, k):
+    """Reading 11 (dx = lx/n_g on a periodic axis: the period is the domain length lx) pinned by the
+    physics, not by the oracle's own spacing: a periodic mode of physical wavelength lx/k -- k whole
+    periods over the n_g cells -- decays at the continuum rate lam*c*(2 pi k/lx)^2 of dT/dt =
+    lam*Ci*Laplacian(T) (Ci = c) up to the O((pi k/N)^2) + O(rate dt) discretisation
+    error (~0.2 % here).  Reading dx = lx/(n_g-1) instead misses the rate by 2/N (3 %)."""
+    N = (64, 4, 4); lam, c, A = 1.3, 0.45, 0.2
+    L = (lx, lx, lx)
+    d = [H.spacing(L[i], N[i], True) for i in range(3)]
+    g = np.arange(N[0])
+    M = np.broadcast_to(np.cos(2.0 * math.pi * k * g / N[0])[None, None, :], (N[2], N[1], N[0]))
+    T0 = np.ascontiguousarray(1.7 + A * M)
+    Ci = np.full(T0.shape, c)
+    dt = H.stable_dt(d[0], d[1], d[2], lam, Ci)
+    rate = lam * c * (2.0 * math.pi * k / lx) ** 2          # continuum decay rate, 1/time
+    nt = int(round(1.0 / (rate * dt)))                        # about one e-folding of physical time
+    out = H.heat_run(T0, Ci, nt, (1, 1, 1), lam, dt, d[0], d[1], d[2], H.LITERAL)
+    amp = float(np.sum((out[0, 0, :] - 1.7) * np.cos(2.0 * math.pi * k * g / N[0]))) * 2.0 / N[0]
+    measured = -math.log(amp / A) / (nt * dt)
+    assert abs(measured / rate - 1.0) < 5e-3, (measured, rate)
