@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--periodic", default="0,0,0", help="periodic axes (1-GPU self-wrap experiments)")
     ap.add_argument("--per-step", action="store_true", help="time igg_heat_step calls instead of igg_heat_run")
     ap.add_argument("--skip-comm", action="store_true", help="timing experiment only: no exchange (INVALID results)")
+    ap.add_argument("--samples", type=int, default=20, help="paper statistics: samples of nt=100 steps")
+    ap.add_argument("--no-stats", action="store_true", help="skip the 20-sample statistics pass")
     return ap.parse_args()
 
 
@@ -168,8 +170,8 @@ def cpu_oracle_baseline(n: int, target_s: float = 12.0, f32: bool = False):
 
 def run_reference(a):
     """--impl reference: the CPU oracle timed as it stands on the host cores.
-    Each step = one oracle step on a bounded sample of the workload: the
-    full-x/y 512x512 plane extent with 66 z-planes (64 updated planes)."""
+    Each step = one oracle step (paper-literal C, OpenMP over z) of the SAME workload as our arm's
+    line: the full n^3 local grid of the paper setup (T = 1.7, Ci = 0.5)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -178,10 +180,9 @@ def run_reference(a):
     OH.build()
     OH.set_threads(len(os.sched_getaffinity(0)))   # all host cores (torchrun sets OMP_NUM_THREADS=1)
     n = a.n
-    nz = min(n, 66)
-    T = np.full((nz, n, n), 1.7)
+    T = np.full((n, n, n), 1.7)
     T2 = T.copy()
-    Ci = np.full((nz, n, n), 0.5)
+    Ci = np.full((n, n, n), 0.5)
     d = 1.0 / (n - 1)
     dt = OH.stable_dt(d, d, d, 1.0, Ci)
     for _ in range(a.warmup):
@@ -192,18 +193,43 @@ def run_reference(a):
         OH.heat_step(T, Ci, T2, (0, 0, 0), 1.0, dt, d, d, d, OH.LITERAL)
         T, T2 = T2, T
     el = time.perf_counter() - t0
-    cells = nz * n * n
+    cells = n ** 3
     val = BYTES_PER_CELL * cells * a.steps / el / 1e9
-    sample = f"oracle step on a {n}x{n}x{nz} slab of the {n}^3 workload per step (paper-literal C, OpenMP)"
+    sample = f"{a.steps} oracle steps of the full {n}^3 grid (paper-literal C, OpenMP), after {a.warmup} warm-up"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": "GB/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"heat3d Float64 {n}^3 local, nt-step sample, CPU oracle", "bw": a.bw,
-                   "sample_cells": cells},
+        "config": {"workload": f"3-D heat diffusion Float64, local {n}^3, CPU oracle on the host cores",
+                   "n_local": n, "sample_cells": cells},
         "cpu_baseline": {"value": val, "unit": "GB/s", "cores": OH.num_threads(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def bpc_(f32: bool) -> int:
+    return BYTES_PER_CELL // 2 if f32 else BYTES_PER_CELL
+
+
+def median_ci95(xs):
+    """Median and a distribution-free 95 % confidence interval of the median (order statistics of the
+    binomial(n, 1/2): for n = 20 the 6th and 15th smallest, coverage 95.9 %) -- the paper's statistics
+    of 20 samples (Fig. 2 caption)."""
+    import math
+    v = sorted(xs)
+    n = len(v)
+    if n < 6:
+        return statistics.median(v), [v[0], v[-1]]
+    # largest k with P(Binom(n, 1/2) < k) <= 2.5 %: [v[k-1], v[n-k]]
+    k, acc = 0, 0.0
+    while True:
+        p = math.comb(n, k) / 2 ** n
+        if acc + p > 0.025:
+            break
+        acc += p
+        k += 1
+    k = max(k, 1)
+    return statistics.median(v), [v[k - 1], v[n - k]]
 
 
 def main():
@@ -293,6 +319,32 @@ def main():
         per_rank_ms = [float(t.item()) for t in allms]
     ms = max_over_ranks(ms)
     clk = clocks.stop() if clocks else None
+    g.check()
+
+    def sampled(nsamples, nt):
+        """The paper's statistics: nsamples samples of nt steps, each
+        bracketed by barrier + synchronize, CUDA events on the launching stream, max over ranks."""
+        xs = []
+        for _ in range(nsamples):
+            barrier()
+            e0.record(stream)
+            steps(nt)
+            e1.record(stream)
+            barrier()
+            xs.append(max_over_ranks(e0.elapsed_time(e1) / nt))
+        med, ci = median_ci95(xs)
+        return {"samples": nsamples, "nt": nt, "median_ms": med, "ci95_ms": ci, "min_ms": min(xs),
+                "max_ms": max(xs)}
+
+    stats = None
+    if not a.no_stats:
+        stats = sampled(a.samples, 100)
+        stats["t_eff_per_gpu_gbs_median"] = bpc_(f32) * n ** 3 / (stats["median_ms"] * 1e-3) / 1e9
+        if a.init == "paper":   # B:8 (ii): the same timing on non-trivial (random) data
+            (app.init_random)(g, T, T2, Ci)
+            stats["random_init"] = sampled(a.samples, 100)
+            app.init_paper(g, T, T2, Ci)
+        g.check()
     # roofline pass (not timed above): CUDA events around the main stencil launches on their stream
     g.set_option(P.OPT_PROFILE, 2 if a.timeline else 1)
     g.profile_stencil()
@@ -304,7 +356,7 @@ def main():
     g.set_option(P.OPT_PROFILE, 0)
     g.check()
 
-    bpc = BYTES_PER_CELL // 2 if f32 else BYTES_PER_CELL   # binary32: 3 x 4 B per cell
+    bpc = bpc_(f32)   # binary32: 3 x 4 B per cell
     per_gpu = bpc * n ** 3 / (ms * 1e-3) / 1e9
     value = per_gpu * world
 
@@ -339,22 +391,27 @@ def main():
         barrier()
         ms_nc = max_over_ranks(e0.elapsed_time(e1) / a.steps)
         g.set_option(P.OPT_SKIP_COMM, 0)
+        g.check()
         exposed = {"ms_per_step": ms - ms_nc, "ms_no_comm": ms_nc}
         (app.init_paper if a.init == "paper" else app.init_random)(g, T, T2, Ci)   # results were invalid
 
     # ---------------- roofline of the dominant kernel (the full-region / inner-box stencil)
+    fused_run = (not f32) and a.path == "p2p" and a.fused != 0 and (world > 1 or any(periods)) and not a.kernel
+    kernel_name = ("heat_f32_async_kernel (full region)" if f32 else
+                   "heat_fused_kernel (whole region: stencil + peer stores of the faces)" if fused_run else
+                   "heat_box_list_kernel (full region)" if world == 1 else
+                   "heat_box_list_kernel (inner box)")
     peak, peak_src = measured_peak()
     k_avg_ms = k_ms / max(k_n, 1)
     k_bytes = bpc * k_cells / max(k_n, 1)
     achieved = k_bytes / (k_avg_ms * 1e-3) / 1e9 if k_n else None
-    tr = dram_traffic_per_launch("traffic_f32.json" if f32 else "traffic.json")
+    tr = dram_traffic_per_launch("traffic_f32.json" if f32 else "traffic_fused.json" if fused_run else "traffic.json")
     traffic = None
-    if tr and tr.get("n") == n and tr.get("dims") == list(dims):
+    if tr and tr.get("n") == n and (tr.get("dims") == list(dims) or fused_run):
         traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic,
-                "kernel": ("heat_f32_async_kernel (full region)" if f32 else
-                           "heat_box_kernel (inner box)" if world > 1 else "heat_box_kernel (full region)"),
+                "kernel": kernel_name,
                 "algorithmic_bytes_per_launch": k_bytes, "avg_launch_ms": k_avg_ms, "launches": k_n,
                 "peak_source": peak_src, "share_of_step": k_avg_ms * (k_n / prof_steps) / ms if k_n else None,
                 "measured_in": f"a separate pass of {prof_steps} steps with events around the kernel"}
@@ -368,6 +425,7 @@ def main():
         Ch = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
         Th.copy_(T[0].cpu() if a.init == "random" else torch.full((1,), 1.7, dtype=torch.float64).expand(n, n, n))
         Ch.copy_(Ci[0].cpu())
+        g.release_arrays()   # collective: no peer keeps a mapping of the arrays freed next
         del T, T2   # make room for the library's e2e scratch
         torch.cuda.empty_cache()
         T0h = Th.clone()
@@ -384,6 +442,7 @@ def main():
             barrier()
             tt.append(max_over_ranks(e0.elapsed_time(e1)))
         t_call = statistics.median(tt)
+        g.check()
         h2d = 2 * cells * 8
         d2h = cells * 8
         e2e = {"value": world * BYTES_PER_CELL * cells * nt / (t_call * 1e-3) / 1e9, "unit": "GB/s",
@@ -403,7 +462,11 @@ def main():
             "warmup": max(a.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
             "config": {"workload": f"3-D heat diffusion {'Float32 variant' if f32 else 'Float64'}, local {n}^3 per GPU, dims "
-                                   f"{dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw} (paper Fig. 1)",
+                                   f"{dims[0]}x{dims[1]}x{dims[2]}, hide_communication {bw} (paper Fig. 1)" +
+                                   ("" if (world > 1 or any(periods)) else
+                                    "; one GPU: no axis exchanges, so the step is one full-region stencil launch "
+                                    "(no boundary slabs to schedule)"),
+                       "value_is": "aggregate over all GPUs (N x per-GPU T_eff)",
                        "n_local": n, "dims": list(dims), "bw": list(bw), "path": a.path, "init": a.init,
                        "x_align": a.xalign, "periods": list(periods), "schedule": a.schedule, "fused": a.fused,
                        "skip_comm_INVALID_RESULTS": bool(a.skip_comm),
@@ -415,6 +478,7 @@ def main():
                        "stencil_variant": a.kernel},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk, "exposed_halo": exposed, "timeline_ms": timeline, "per_rank_ms": per_rank_ms,
+            "stats": stats,
         }
         print(json.dumps(line))
     if world > 1:
@@ -422,7 +486,8 @@ def main():
 
 
 # ------------------------------------------------------------------ second workload
-AC_METRIC = "T_eff GB/s per GPU of the staggered acoustic step (P, Vx, Vy, Vz read+written once: 64 B/cell)"
+AC_METRIC = ("T_eff GB/s of the staggered acoustic step, aggregate over GPUs (P, Vx, Vy, Vz read+written once: "
+             "64 B/cell)")
 AC_BYTES_PER_CELL = 64      # effective: 4 fields x (read + write) x 8 B
 AC_V_BYTES_PER_CELL = 56    # compute_V kernel: P, Vx, Vy, Vz read; Vx, Vy, Vz written
 

@@ -50,7 +50,8 @@ typedef enum igg_status {
     IGG_E_CUDA = 5,      /* a CUDA runtime call failed */
     IGG_E_NCCL = 6,      /* an NCCL call failed */
     IGG_E_TIMEOUT = 7,   /* a P2P receive flag did not arrive in time (analog of SPEC.md:273, :308) */
-    IGG_E_UNSUPPORTED = 8
+    IGG_E_UNSUPPORTED = 8,
+    IGG_E_BOOTSTRAP = 9  /* the caller's bootstrap all-gather returned non-zero */
 } igg_status;
 
 enum {
@@ -111,6 +112,13 @@ typedef struct igg_plan_entry {
 igg_status igg_plan_update_halo(const igg_init_args *args, const long long *sizes, int nfields,
                                 igg_plan_entry *out, int capacity, int *count);
 
+/* Host bootstrap (optional, igg_init_args.bootstrap): a collective all-gather over the caller's own
+ * channel (e.g. a torch gloo process group).  Every process passes `bytes` bytes in `mine` and receives
+ * the contributions of all processes, in process order, in `all` (nprocs/local_ranks * bytes).  Called
+ * on the thread that called into the library, only from collective entry points (init, the first use of
+ * an array on the fused path, arena growth, global_max, gather, finalize).  Returns 0 on success. */
+typedef int (*igg_allgather_fn)(void *user, const void *mine, void *all, unsigned long long bytes);
+
 struct igg_init_args {
     int nx, ny, nz;          /* local size of a canonical (non-staggered) field */
     int dims[3];             /* process topology; 0 entries = automatic (igg_dims_create) */
@@ -123,8 +131,17 @@ struct igg_init_args {
     int path;                /* IGG_PATH_NCCL or IGG_PATH_P2P */
     int reserved;
     unsigned char comm_id[128]; /* ncclUniqueId from igg_get_unique_id on process 0, broadcast by
-                                   the caller; unused when one process hosts every rank */
+                                   the caller; unused when one process hosts every rank or when
+                                   `bootstrap` is set */
+    igg_allgather_fn bootstrap; /* NULL (default): host collectives over an NCCL communicator built
+                                   from comm_id.  Set (path must be IGG_PATH_P2P): NO NCCL communicator
+                                   is created; every host-side collective goes through this callback and
+                                   every face moves by CUDA-IPC peer stores.  This is also what lets
+                                   several processes share one GPU (NCCL refuses two ranks on one
+                                   device); IGG_E_ARG with path == IGG_PATH_NCCL. */
+    void *bootstrap_user;       /* passed back to bootstrap */
 };
+
 
 /* Fill out[128] with a fresh NCCL unique id (call on process 0 only). */
 igg_status igg_get_unique_id(unsigned char out[128]);
@@ -313,6 +330,14 @@ enum {
                                     stream joined to the caller's; 1: directly on the caller's stream */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
+
+/* Collective, synchronous.  The fused P2P step maps every rank's T2 array into its neighbours'
+ * address spaces (CUDA IPC) on the array's first use and caches the mapping.  Call this on every
+ * process before freeing (or handing back to an allocator) any array used as T / T2 in a heat step,
+ * so no peer keeps a mapping of freed memory.  igg_heat_run / igg_heat_run_host re-validate the cache
+ * collectively on entry; a single igg_heat_step given an array that was re-allocated at a cached address
+ * fails with IGG_E_STATE instead of storing into the old allocation. */
+igg_status igg_release_arrays(igg_grid *grid);
 
 /* Blocks until all work of the grid's streams is done, then reports a P2P
  * wait timeout (IGG_E_TIMEOUT) or an NCCL asynchronous error. */

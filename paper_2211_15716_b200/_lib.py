@@ -24,7 +24,12 @@ class igg_init_args(ctypes.Structure):
                 ("dims", ctypes.c_int * 3), ("periods", ctypes.c_int * 3), ("overlaps", ctypes.c_int * 3),
                 ("nprocs", ctypes.c_int), ("rank0", ctypes.c_int), ("local_ranks", ctypes.c_int),
                 ("device", ctypes.c_int), ("path", ctypes.c_int), ("reserved", ctypes.c_int),
-                ("comm_id", ctypes.c_ubyte * 128)]
+                ("comm_id", ctypes.c_ubyte * 128), ("bootstrap", ctypes.c_void_p),
+                ("bootstrap_user", ctypes.c_void_p)]
+
+
+# int (*igg_allgather_fn)(void *user, const void *mine, void *all, unsigned long long bytes)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_ulonglong)
 
 
 class igg_field(ctypes.Structure):
@@ -78,6 +83,7 @@ SIGNATURES = {
     "igg_field_global_max": [ctypes.c_void_p, c_dbl_pp, ctypes.c_longlong, c_dbl_p, ctypes.c_void_p],
     "igg_set_option": [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong],
     "igg_check": [ctypes.c_void_p],
+    "igg_release_arrays": [ctypes.c_void_p],
     "igg_hide_communication": [ctypes.c_void_p, c_int_p, REGION_FN, ctypes.c_void_p, ctypes.POINTER(igg_field),
                                ctypes.c_int, ctypes.c_void_p],
     "igg_acoustic_step": [ctypes.c_void_p, c_dbl_pp, c_dbl_pp, c_dbl_pp, c_dbl_pp, ctypes.c_double,

@@ -1026,59 +1026,131 @@ static void build_layout(igg_grid *g, const int layer[3][2], const bool act[3][2
 }
 
 // ------------------------------------------------------------------ peer arrays
-// The caller's T2 lives inside some cudaMalloc allocation (e.g. a torch caching-
-// allocator segment).  Its base is exported with cudaIpcGetMemHandle, every
-// process all-gathers (handle, offset) and opens its neighbours' handles once;
-// the result is cached per local T2 pointer (Fig. 1 alternates two arrays, so
-// two collective exchanges happen, on the first two steps, on every rank).
+// The caller's T2 lives inside some cudaMalloc allocation (e.g. a torch caching-allocator segment).
+// Its base is exported with cudaIpcGetMemHandle, every process all-gathers (handle, offset) and opens
+// its neighbours' handles once; the result is cached per local array (Fig. 1 alternates two arrays,
+// so two collective exchanges happen, on the first two steps, on every rank).  A cached entry records
+// the allocation's identity (base, size, CU_POINTER_ATTRIBUTE_BUFFER_ID -- unique per allocation for
+// the life of the process), so an array freed and re-allocated at the same address is never taken
+// for the old one: a stale entry fails loudly (IGG_E_STATE) on a single step, and igg_heat_run /
+// igg_heat_run_host re-validate every entry collectively (validate_peer_maps) and re-map.
 typedef int (*MemGetAddressRangeFn)(unsigned long long *, size_t *, unsigned long long);
+typedef int (*PointerGetAttributeFn)(void *, int, unsigned long long);
+
+struct AllocId {
+    unsigned long long base = 0, size = 0, buffer_id = 0;
+};
+
+static AllocId alloc_id(const void *p) {
+    static MemGetAddressRangeFn range_fn = nullptr;
+    static PointerGetAttributeFn attr_fn = nullptr;
+    if (!range_fn) {
+        void *fn = nullptr, *fa = nullptr;
+        cudaDriverEntryPointQueryResult q, qa;
+        IGG_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        IGG_CUDA(cudaGetDriverEntryPoint("cuPointerGetAttribute", &fa, cudaEnableDefault, &qa));
+        if (!fn || q != cudaDriverEntryPointSuccess || !fa || qa != cudaDriverEntryPointSuccess)
+            fail(IGG_E_CUDA, "cuMemGetAddressRange / cuPointerGetAttribute unavailable");
+        range_fn = (MemGetAddressRangeFn)fn;
+        attr_fn = (PointerGetAttributeFn)fa;
+    }
+    AllocId id;
+    size_t size = 0;
+    if (range_fn(&id.base, &size, (unsigned long long)(uintptr_t)p) != 0)
+        fail(IGG_E_CUDA, "cuMemGetAddressRange failed on a field array (not device memory?)");
+    id.size = size;
+    constexpr int kBufferIdAttr = 7;   // CU_POINTER_ATTRIBUTE_BUFFER_ID
+    if (attr_fn(&id.buffer_id, kBufferIdAttr, (unsigned long long)(uintptr_t)p) != 0)
+        fail(IGG_E_CUDA, "cuPointerGetAttribute(BUFFER_ID) failed on a field array");
+    return id;
+}
+
+static bool same_alloc(const igg_grid::PeerMap &m, const AllocId &id) {
+    return m.base == id.base && m.size == id.size && m.buffer_id == id.buffer_id;
+}
+
+void release_peer_maps(igg_grid *g) {
+    if (g->nproc_procs > 1) {
+        IGG_CUDA(cudaDeviceSynchronize());   // no kernel of mine still stores through a mapping
+        allgather_bytes_pub(g, "", 1);       // nor any peer's (barrier)
+    }
+    for (auto &o : g->fused_opened) cudaIpcCloseMemHandle(o.second);
+    g->fused_opened.clear();
+    g->fused_peer_maps.clear();
+}
+
+void validate_peer_maps(igg_grid *g) {
+    if (g->nproc_procs == 1) {   // self-wrap on one process: entries are my own arrays; drop stale ones
+        std::vector<igg_grid::PeerMap> keep;
+        for (auto &m : g->fused_peer_maps)
+            if (same_alloc(m, alloc_id(m.ptr))) keep.push_back(m);
+        g->fused_peer_maps.swap(keep);
+        return;
+    }
+    if (g->fused_peer_maps.empty() && g->fused_opened.empty()) {
+        // nothing cached here; the other processes hold nothing either (entries are created collectively)
+        return;
+    }
+    unsigned char ok = 1;
+    for (auto &m : g->fused_peer_maps) ok = ok && same_alloc(m, alloc_id(m.ptr));
+    std::vector<char> all = allgather_bytes_pub(g, &ok, 1);
+    for (char c : all)
+        if (!c) {
+            release_peer_maps(g);
+            return;
+        }
+}
 
 static const std::vector<double *> &peer_arrays(igg_grid *g, double *T2) {
-    for (const auto &m : g->fused_peer_maps)
-        if (m.first == (const void *)T2) return m.second;
+    const AllocId id = alloc_id(T2);
+    for (auto &m : g->fused_peer_maps)
+        if (m.ptr == (const void *)T2) {
+            if (!same_alloc(m, id) && g->nproc_procs == 1) {   // self-wrap: the peer is this array itself
+                m.base = id.base;
+                m.size = id.size;
+                m.buffer_id = id.buffer_id;
+            } else if (!same_alloc(m, id))
+                fail(IGG_E_STATE, "fused step: an array was freed and re-allocated at the same address after its "
+                                  "first fused step; call igg_release_arrays (collective) before reusing it");
+            return m.peers;
+        }
+    igg_grid::PeerMap e;
+    e.ptr = T2;
+    e.base = id.base;
+    e.size = id.size;
+    e.buffer_id = id.buffer_id;
     if (g->nproc_procs == 1) {   // self-wrap on one process: my own array
-        g->fused_peer_maps.push_back({(const void *)T2, std::vector<double *>(1, T2)});
-        return g->fused_peer_maps.back().second;
+        e.peers.assign(1, T2);
+        g->fused_peer_maps.push_back(e);
+        return g->fused_peer_maps.back().peers;
     }
-    static MemGetAddressRangeFn range_fn = nullptr;
-    if (!range_fn) {
-        void *fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        IGG_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) fail(IGG_E_CUDA, "cuMemGetAddressRange unavailable");
-        range_fn = (MemGetAddressRangeFn)fn;
-    }
-    unsigned long long base = 0;
-    size_t size = 0;
-    if (range_fn(&base, &size, (unsigned long long)(uintptr_t)T2) != 0)
-        fail(IGG_E_CUDA, "cuMemGetAddressRange failed on the T2 array");
     struct Entry {
         cudaIpcMemHandle_t h;
         unsigned long long off;
     } mine;
-    IGG_CUDA(cudaIpcGetMemHandle(&mine.h, (void *)(uintptr_t)base));
-    mine.off = (unsigned long long)(uintptr_t)T2 - base;
+    IGG_CUDA(cudaIpcGetMemHandle(&mine.h, (void *)(uintptr_t)id.base));
+    mine.off = (unsigned long long)(uintptr_t)T2 - id.base;
     std::vector<char> all = allgather_bytes_pub(g, &mine, sizeof mine);
-    std::vector<double *> peers(g->nproc_procs, nullptr);
+    e.peers.assign(g->nproc_procs, nullptr);
     for (int p = 0; p < g->nproc_procs; ++p) {
         if (p == g->proc) {
-            peers[p] = T2;
+            e.peers[p] = T2;
             continue;
         }
-        Entry e;
-        std::memcpy(&e, all.data() + p * sizeof e, sizeof e);
-        const std::string key(reinterpret_cast<const char *>(&e.h), sizeof e.h);
+        Entry pe;
+        std::memcpy(&pe, all.data() + p * sizeof pe, sizeof pe);
+        const std::string key(reinterpret_cast<const char *>(&pe.h), sizeof pe.h);
         void *opened = nullptr;
         for (const auto &o : g->fused_opened)
             if (o.first == key) opened = o.second;
         if (!opened) {
-            IGG_CUDA(cudaIpcOpenMemHandle(&opened, e.h, cudaIpcMemLazyEnablePeerAccess));
+            IGG_CUDA(cudaIpcOpenMemHandle(&opened, pe.h, cudaIpcMemLazyEnablePeerAccess));
             g->fused_opened.push_back({key, opened});
         }
-        peers[p] = reinterpret_cast<double *>(static_cast<char *>(opened) + e.off);
+        e.peers[p] = reinterpret_cast<double *>(static_cast<char *>(opened) + pe.off);
     }
-    g->fused_peer_maps.push_back({(const void *)T2, peers});
-    return g->fused_peer_maps.back().second;
+    g->fused_peer_maps.push_back(e);
+    return g->fused_peer_maps.back().peers;
 }
 
 void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s,
@@ -1151,7 +1223,9 @@ void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, cons
 
     // a single complete step that needs edge forwarding runs the multi-stream schedule (its receive
     // kernels forward while the stencil runs; measured faster than in-kernel forwarders for one step)
-    const bool single_fwd = !wait_prev && drain && g->fused_nfwd > 0 && !(g->fused_mode & 1024);
+    // (every schedule is ONE launch on the caller's stream: kernels on other streams that spin on this
+    // launch's flags are never relied on -- nothing guarantees that two launches run at the same time)
+    const bool single_fwd = false;
     if (!(g->fused_mode & 128) && !single_fwd) {
         // pipelined schedule (default): ONE launch on the caller's stream and, when the step must be
         // complete on return, a drain.  The rim cells and the forwarded edge lines are never read by

@@ -29,17 +29,50 @@ static void *dev_alloc(igg_grid *g, size_t bytes) {
     return p;
 }
 
-// all-gather of a small host blob over the NCCL communicator (init-time only)
+// all-gather of a small host blob over the processes (collective entry points only): through the
+// caller's bootstrap callback when one was given, else over the NCCL communicator (a persistent
+// device buffer, so no allocation synchronizes the device); one process: a copy
 static std::vector<char> allgather_bytes(igg_grid *g, const void *mine, size_t bytes) {
     std::vector<char> out(bytes * g->nproc_procs);
-    char *d = nullptr;
-    IGG_CUDA(cudaMalloc(&d, out.size()));
-    IGG_CUDA(cudaMemcpy(d + bytes * g->proc, mine, bytes, cudaMemcpyHostToDevice));
+    if (g->nproc_procs == 1) {
+        std::memcpy(out.data(), mine, bytes);
+        return out;
+    }
+    if (g->boot) {
+        if (g->boot(g->boot_user, mine, out.data(), (unsigned long long)bytes) != 0)
+            fail(IGG_E_BOOTSTRAP, "bootstrap all-gather of " + std::to_string(bytes) + " bytes failed");
+        return out;
+    }
+    if (g->d_gather_bytes < out.size()) {
+        if (g->d_gather) IGG_CUDA(cudaFree(g->d_gather));
+        g->d_gather_bytes = std::max<size_t>(out.size(), 4096);
+        IGG_CUDA(cudaMalloc(&g->d_gather, g->d_gather_bytes));
+    }
+    char *d = g->d_gather;
+    IGG_CUDA(cudaMemcpyAsync(d + bytes * g->proc, mine, bytes, cudaMemcpyHostToDevice, g->s_comm));
     IGG_NCCL(ncclAllGather(d + bytes * g->proc, d, bytes, ncclChar, g->comm, g->s_comm));
+    IGG_CUDA(cudaMemcpyAsync(out.data(), d, out.size(), cudaMemcpyDeviceToHost, g->s_comm));
     IGG_CUDA(cudaStreamSynchronize(g->s_comm));
-    IGG_CUDA(cudaMemcpy(out.data(), d, out.size(), cudaMemcpyDeviceToHost));
-    IGG_CUDA(cudaFree(d));
     return out;
+}
+
+// max over the processes of one double, through allgather_bytes (host bootstrap)
+double host_max(igg_grid *g, double local) {
+    std::vector<char> all = allgather_bytes(g, &local, sizeof local);
+    double m = local;
+    for (int p = 0; p < g->nproc_procs; ++p) {
+        double v;
+        std::memcpy(&v, all.data() + p * sizeof v, sizeof v);
+        m = std::max(m, v);
+    }
+    return m;
+}
+
+void check_device_error(igg_grid *g, const char *who) {
+    IGG_CUDA(cudaDeviceSynchronize());
+    int err = 0;
+    IGG_CUDA(cudaMemcpy(&err, g->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) fail(IGG_E_TIMEOUT, std::string(who) + ": a P2P receive flag wait timed out (halos are invalid)");
 }
 
 std::vector<char> allgather_bytes_pub(igg_grid *g, const void *mine, size_t bytes) {
@@ -514,7 +547,11 @@ IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_inner, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_bnd, cudaEventDisableTiming));
         IGG_CUDA(cudaEventCreateWithFlags(&g->ev_comm2, cudaEventDisableTiming));
-        if (g->nproc_procs > 1) {
+        g->boot = A->bootstrap;
+        g->boot_user = A->bootstrap_user;
+        if (g->nproc_procs > 1 && g->boot && g->path != IGG_PATH_P2P)
+            fail(IGG_E_ARG, "igg_init_global_grid: a host bootstrap needs path IGG_PATH_P2P (no NCCL communicator)");
+        if (g->nproc_procs > 1 && !g->boot) {
             ncclUniqueId id;
             std::memcpy(&id, A->comm_id, sizeof id);
             IGG_NCCL(ncclCommInitRank(&g->comm, g->nproc_procs, id, g->proc));
@@ -572,13 +609,14 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
     igg::process_barrier(g);
     for (auto &o : g->fused_opened) cudaIpcCloseMemHandle(o.second);
     g->fused_opened.clear();
+    g->fused_peer_maps.clear();
     if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
         igg::unmap_peers(g, g->peer_recv);
         for (int p = 0; p < g->nproc_procs; ++p)
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->fused_xsync, (void *)g->fused_xstg, (void *)g->fused_tgt, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->d_gather, (void *)g->fused_xsync, (void *)g->fused_xstg, (void *)g->fused_tgt, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
@@ -621,6 +659,10 @@ IGG_API igg_status igg_local_to_global(const igg_grid *g, int rank, int axis, lo
     igg::check_live(g, "igg_local_to_global");
     if (rank < 0 || rank >= g->nprocs || axis < 0 || axis > 2 || !g_out)
         fail(IGG_E_ARG, "igg_local_to_global: bad argument");
+    // a layer of some field on this axis: fields have at most n+o layers
+    if (l < 0 || l >= (long long)g->n[axis] + g->o[axis])
+        fail(IGG_E_ARG, "igg_local_to_global: local layer " + std::to_string(l) + " outside [0, " +
+                            std::to_string(g->n[axis] + g->o[axis]) + ") on axis " + std::to_string(axis));
     int c[3];
     igg::coords_of_rank(g->dims, rank, c);
     long long v = (long long)c[axis] * (g->n[axis] - g->o[axis]) + l;
@@ -875,6 +917,7 @@ IGG_API igg_status igg_heat_run(igg_grid *g, double **T, double **T2, const doub
     igg::check_live(g, "igg_heat_run");
     if (!T || !T2 || !Ci || nt < 0) fail(IGG_E_ARG, "igg_heat_run: bad argument");
     cudaStream_t s = (cudaStream_t)stream;
+    igg::validate_peer_maps(g);   // collective: every cached peer mapping still names a live allocation
     for (int it = 0; it < nt; ++it) {
         // consecutive steps pipelined on the fused path (the previous step's faces awaited tile by
         // tile); the last one drains, so the run is complete on the stream like nt single steps
@@ -892,7 +935,11 @@ IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *
     cudaStream_t s = (cudaStream_t)stream;
     const size_t cells = (size_t)g->n[0] * g->n[1] * g->n[2];
     const size_t bytes = cells * g->nlocal * sizeof(double);
+    igg::validate_peer_maps(g);
     if (bytes > g->run_bytes) {
+        // the scratch arrays may be mapped by the peers (fused path): drop every mapping first
+        // (collective: every process grows its scratch on the same call)
+        if (g->run_T) igg::release_peer_maps(g);
         for (double *p : {g->run_T, g->run_T2, g->run_Ci})
             if (p) IGG_CUDA(cudaFree(p));
         g->run_T = (double *)igg::dev_alloc(g, bytes);
@@ -918,6 +965,7 @@ IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *
     for (int lr = 0; lr < g->nlocal; ++lr)
         IGG_CUDA(cudaMemcpyAsync(T_host + lr * cells, a[lr], cells * sizeof(double), cudaMemcpyDeviceToHost, s));
     IGG_CUDA(cudaStreamSynchronize(s));
+    igg::check_device_error(g, "igg_heat_run_host");   // a timed-out flag wait invalidates the result
     IGG_CATCH
 }
 
@@ -983,7 +1031,28 @@ IGG_API igg_status igg_gather(igg_grid *g, const igg_field *fields, int root_pro
         const Box &B = boxes[g->rank0 + lr];
         igg::launch_box_pack(fields[lr].ptr, dst + (B.off - mine_off), sz[0], sz[1], B.b0, B.b1, s);
     }
-    if (g->nproc_procs > 1) {
+    if (g->nproc_procs > 1 && g->boot) {
+        // host bootstrap: every process' owned boxes through the all-gather (padded to the largest)
+        long long maxc = 1;
+        for (int p = 0; p < g->nproc_procs; ++p) {
+            long long cnt = 0;
+            for (int lr = 0; lr < g->nlocal; ++lr) cnt += boxes[p * g->nlocal + lr].count;
+            maxc = std::max(maxc, cnt);
+        }
+        std::vector<double> hmine(maxc, 0.0);
+        IGG_CUDA(cudaStreamSynchronize(s));
+        if (mine) IGG_CUDA(cudaMemcpy(hmine.data(), dst, sizeof(double) * mine, cudaMemcpyDeviceToHost));
+        std::vector<char> all = igg::allgather_bytes(g, hmine.data(), sizeof(double) * maxc);
+        if (is_root)
+            for (int p = 0; p < g->nproc_procs; ++p) {
+                if (p == g->proc) continue;
+                long long cnt = 0;
+                for (int lr = 0; lr < g->nlocal; ++lr) cnt += boxes[p * g->nlocal + lr].count;
+                if (cnt)
+                    IGG_CUDA(cudaMemcpy(dbuf + boxes[p * g->nlocal].off, all.data() + sizeof(double) * maxc * p,
+                                        sizeof(double) * cnt, cudaMemcpyHostToDevice));
+            }
+    } else if (g->nproc_procs > 1) {
         IGG_NCCL(ncclGroupStart());
         if (is_root) {
             for (int p = 0; p < g->nproc_procs; ++p) {
@@ -1033,6 +1102,10 @@ IGG_API igg_status igg_global_max(igg_grid *g, double local, double *out) {
     IGG_TRY
     igg::check_live(g, "igg_global_max");
     if (!out) fail(IGG_E_ARG, "igg_global_max: NULL out");
+    if (g->boot) {   // host bootstrap: all-gather the local values, max on the host
+        *out = igg::host_max(g, local);
+        return IGG_OK;
+    }
     double *d = g->d_scratch + igg::field_max_scratch_len();
     IGG_CUDA(cudaMemcpyAsync(d, &local, sizeof(double), cudaMemcpyHostToDevice, g->s_comm));
     if (g->nproc_procs > 1) IGG_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, g->comm, g->s_comm));
@@ -1051,10 +1124,10 @@ IGG_API igg_status igg_field_global_max(igg_grid *g, const double *const *f, lon
     double *d = g->d_scratch + igg::field_max_scratch_len();
     igg::launch_field_max(f, g->nlocal, count, g->d_scratch, igg::field_max_scratch_len(), d, s);
     g->launches += 2;
-    if (g->nproc_procs > 1) IGG_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, g->comm, s));
+    if (g->nproc_procs > 1 && g->comm) IGG_NCCL(ncclAllReduce(d, d, 1, ncclDouble, ncclMax, g->comm, s));
     IGG_CUDA(cudaMemcpyAsync(g->d_pinned_out, d, sizeof(double), cudaMemcpyDeviceToHost, s));
     IGG_CUDA(cudaStreamSynchronize(s));
-    *out = *g->d_pinned_out;
+    *out = g->boot ? igg::host_max(g, *g->d_pinned_out) : *g->d_pinned_out;
     IGG_CATCH
 }
 
@@ -1127,13 +1200,17 @@ IGG_API igg_status igg_profile_timeline(igg_grid *g, double out[5]) {
     IGG_CATCH
 }
 
+IGG_API igg_status igg_release_arrays(igg_grid *g) {
+    IGG_TRY
+    igg::check_live(g, "igg_release_arrays");
+    igg::release_peer_maps(g);
+    IGG_CATCH
+}
+
 IGG_API igg_status igg_check(igg_grid *g) {
     IGG_TRY
     igg::check_live(g, "igg_check");
-    IGG_CUDA(cudaDeviceSynchronize());
-    int err = 0;
-    IGG_CUDA(cudaMemcpy(&err, g->d_err, sizeof(int), cudaMemcpyDeviceToHost));
-    if (err) fail(IGG_E_TIMEOUT, "igg_check: a P2P receive flag wait timed out");
+    igg::check_device_error(g, "igg_check");
     if (g->comm) {
         ncclResult_t r = ncclSuccess;
         IGG_NCCL(ncclCommGetAsyncError(g->comm, &r));

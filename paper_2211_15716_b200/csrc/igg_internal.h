@@ -291,8 +291,12 @@ struct igg_grid : igg::Geom {
     cudaStream_t s_comm = nullptr, s_inner = nullptr, s_comm2 = nullptr;
     cudaEvent_t ev_start = nullptr, ev_comm = nullptr, ev_inner = nullptr, ev_bnd = nullptr, ev_comm2 = nullptr;
 
-    // communicator
+    // communicator: NCCL (comm), or the caller's host bootstrap (boot; then comm stays NULL)
     ncclComm_t comm = nullptr;
+    igg_allgather_fn boot = nullptr;
+    void *boot_user = nullptr;
+    char *d_gather = nullptr;                            // small device buffer of allgather_bytes (NCCL)
+    size_t d_gather_bytes = 0;
 
     // buffer pool: receive arena (two parity halves), send arena (NCCL path)
     char *recv_arena = nullptr;
@@ -339,7 +343,14 @@ struct igg_grid : igg::Geom {
     std::list<std::pair<std::vector<long long>, igg::Plan>> plan_cache;   // field-list shape -> plan
     unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr, *fused_tgt_x = nullptr, *fused_tgt_pipe = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
-    std::vector<std::pair<const void *, std::vector<double *>>> fused_peer_maps;   // local T2 -> peers' T2
+    // peer mappings of arrays the fused path stores into (PeerMap: fused.cu)
+    struct PeerMap {
+        const void *ptr;                 // my array
+        unsigned long long base, size;   // its allocation (cuMemGetAddressRange)
+        unsigned long long buffer_id;    // CU_POINTER_ATTRIBUTE_BUFFER_ID: unique per allocation
+        std::vector<double *> peers;     // per process: the same array of that process, mapped
+    };
+    std::vector<PeerMap> fused_peer_maps;
     std::vector<unsigned short> fused_tail;                                       // tail tile order
     int fused_bmain = 0;
     std::vector<std::pair<std::string, void *>> fused_opened;                     // IPC handle -> mapping
@@ -364,7 +375,16 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
 void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap);
 int local_index(const igg_grid *g, int global_rank);   // -1 if not hosted here
 std::vector<char> allgather_bytes_pub(igg_grid *g, const void *mine, size_t bytes);
+double host_max(igg_grid *g, double local);   // max of one double over the processes (host collective)
 bool fused_eligible(const igg_grid *g);
+// drop every peer mapping of caller arrays (collective: process barrier, close the IPC handles);
+// the next fused step maps its arrays again
+void release_peer_maps(igg_grid *g);
+// collective: do all processes' cached peer mappings still describe live allocations?  If any does
+// not, every process releases them (called once per igg_heat_run / igg_heat_run_host)
+void validate_peer_maps(igg_grid *g);
+// synchronizes the grid's device work and fails with IGG_E_TIMEOUT if a flag wait timed out
+void check_device_error(igg_grid *g, const char *who);
 // one fused step; pipelined schedule: wait_prev = the previous step of the same run was fused (its
 // halos are awaited tile by tile), drain = wait for every incoming face at the end (step complete)
 void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s,

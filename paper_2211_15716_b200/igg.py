@@ -37,7 +37,7 @@ OPT_COOP_HALO = 11
 OPT_HALO_STREAM = 12
 
 STATUS = {0: "IGG_OK", 1: "IGG_E_ARG", 2: "IGG_E_STATE", 3: "IGG_E_STAGGER", 4: "IGG_E_WIDTH",
-          5: "IGG_E_CUDA", 6: "IGG_E_NCCL", 7: "IGG_E_TIMEOUT", 8: "IGG_E_UNSUPPORTED"}
+          5: "IGG_E_CUDA", 6: "IGG_E_NCCL", 7: "IGG_E_TIMEOUT", 8: "IGG_E_UNSUPPORTED", 9: "IGG_E_BOOTSTRAP"}
 
 
 class IggError(RuntimeError):
@@ -375,6 +375,11 @@ class Grid:
     def check(self) -> None:
         _ok(L.lib().igg_check(self._handle()))
 
+    def release_arrays(self) -> None:
+        """Collective: drop the peers' mappings of T / T2 arrays (igg_release_arrays); call before freeing
+        arrays used in heat steps on the fused P2P path."""
+        _ok(L.lib().igg_release_arrays(self._handle()))
+
     # -- finalize_global_grid (PAPER.md:82)
     def finalize_global_grid(self) -> None:
         _ok(L.lib().igg_finalize_global_grid(self._handle()))
@@ -383,12 +388,34 @@ class Grid:
     finalize = finalize_global_grid
 
 
+def _gloo_bootstrap(group):
+    """The host all-gather of igg_init_args.bootstrap over a gloo process group (argument marshalling:
+    bytes in, bytes out)."""
+    import torch
+    dist = torch.distributed
+    world = dist.get_world_size(group)
+
+    def _cb(user, mine, out, nbytes):
+        try:
+            t = torch.frombuffer(bytearray(ctypes.string_at(mine, nbytes)), dtype=torch.uint8)
+            parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, t, group=group)
+            ctypes.memmove(out, b"".join(p.numpy().tobytes() for p in parts), nbytes * world)
+            return 0
+        except Exception:   # never raise through C; the library reports IGG_E_BOOTSTRAP
+            return 1
+    return L.ALLGATHER_FN(_cb)
+
+
 def init_global_grid(nx: int, ny: int, nz: int, dims=(0, 0, 0), periods=(0, 0, 0), overlaps=(2, 2, 2),
                      path: str = "nccl", local_ranks: int = 1, device: int | None = None,
-                     process_group=None) -> Grid:
+                     process_group=None, bootstrap: bool = False) -> Grid:
     """init_global_grid.  With torch.distributed initialised and
     world size > 1 this is collective: process 0's NCCL unique id is broadcast
-    over the process group (gloo or nccl)."""
+    over the process group (gloo or nccl).  bootstrap=True (path "p2p" only):
+    no NCCL communicator; the library's host collectives run over a gloo
+    group of the processes (igg_init_args.bootstrap) -- which also lets
+    several processes share one GPU."""
     import torch
     world, prank = 1, 0
     dist = torch.distributed
@@ -399,7 +426,14 @@ def init_global_grid(nx: int, ny: int, nz: int, dims=(0, 0, 0), periods=(0, 0, 0
         device = int(os.environ.get("LOCAL_RANK", torch.cuda.current_device() if torch.cuda.is_available() else 0))
     a = _init_args(nx, ny, nz, dims, periods, overlaps, world * local_ranks, prank * local_ranks, local_ranks,
                    device, path)
-    if world > 1:
+    boot_cb = None
+    if world > 1 and bootstrap:
+        group = process_group
+        if dist.get_backend(group) != "gloo":
+            group = dist.new_group(ranks=list(range(world)), backend="gloo")
+        boot_cb = _gloo_bootstrap(group)
+        a.bootstrap = ctypes.cast(boot_cb, ctypes.c_void_p)
+    elif world > 1:
         obj = [get_unique_id() if prank == 0 else None]
         dist.broadcast_object_list(obj, src=0, group=process_group)
         ctypes.memmove(a.comm_id, obj[0], 128)
@@ -409,5 +443,7 @@ def init_global_grid(nx: int, ny: int, nz: int, dims=(0, 0, 0), periods=(0, 0, 0
     d = (ctypes.c_int * 3)()
     ng = (ctypes.c_longlong * 3)()
     _ok(L.lib().igg_init_global_grid(ctypes.byref(a), ctypes.byref(h), ctypes.byref(me), c, d, ng))
-    return Grid(h, me.value, tuple(c), tuple(d), tuple(ng), (nx, ny, nz), tuple(int(x) for x in overlaps),
-                tuple(int(bool(p)) for p in periods), a.nprocs, a.rank0, local_ranks, a.path)
+    g = Grid(h, me.value, tuple(c), tuple(d), tuple(ng), (nx, ny, nz), tuple(int(x) for x in overlaps),
+             tuple(int(bool(p)) for p in periods), a.nprocs, a.rank0, local_ranks, a.path)
+    g._boot_cb = boot_cb   # the library calls it until finalize
+    return g

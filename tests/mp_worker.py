@@ -22,6 +22,19 @@ from oracle import heat3d as OH
 import synthetic_inputs as SI
 
 DIMS = {2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+# "boot" mode: one process per GPU, no NCCL communicator at all -- the library's host collectives go
+# through igg_init_args.bootstrap over a gloo group, faces by CUDA-IPC peer stores / the fused kernel.
+# (Never several processes on one GPU: spinning kernels of different contexts are not co-scheduled,
+# B200_PROFILING.md; ranks sharing a GPU are emulated inside one process, tests/test_gpu_virtual_p2p.py.)
+BOOT = False
+
+
+def device():
+    return int(os.environ["LOCAL_RANK"])
+
+
+def init_grid(*n, **kw):
+    return P.init_global_grid(*n, device=device(), bootstrap=BOOT, **kw)
 
 
 def log(*a):
@@ -30,8 +43,7 @@ def log(*a):
 
 def heat_case(path, n, dims, per, local, bw, nt=8, opts=None, per_step=False):
     world = dist.get_world_size()
-    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
-                           device=int(os.environ["LOCAL_RANK"]))
+    g = init_grid(*n, dims=dims, periods=per, local_ranks=local, path=path)
     try:
         for k, v in (opts or {}).items():
             g.set_option(k, v)
@@ -61,8 +73,7 @@ def heat_case(path, n, dims, per, local, bw, nt=8, opts=None, per_step=False):
 
 
 def halo_case(path, n, dims, per, local, sizes, seed, repeat=2):
-    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
-                           device=int(os.environ["LOCAL_RANK"]))
+    g = init_grid(*n, dims=dims, periods=per, local_ranks=local, path=path)
     try:
         nprocs = g.nprocs
         mine = {g.rank0 + lr: [SI.random_field(s[::-1], seed * 1000 + 10 * (g.rank0 + lr) + f)
@@ -90,7 +101,7 @@ def halo_case(path, n, dims, per, local, sizes, seed, repeat=2):
 
 
 def gather_case(path, n, dims, per, s):
-    g = P.init_global_grid(*n, dims=dims, periods=per, path=path, device=int(os.environ["LOCAL_RANK"]))
+    g = init_grid(*n, dims=dims, periods=per, path=path)
     try:
         N = [OG.field_global_size(n[i], 2, dims[i], per[i], s[i]) for i in range(3)]
         G = SI.random_field((N[2], N[1], N[0]), 77)
@@ -105,8 +116,7 @@ def gather_case(path, n, dims, per, s):
 
 def heat_f32_case(path, n, dims, per, nt=5, bw=(16, 2, 2), opts=None):
     """The binary32 variant (igg_heat_step_f32, float halos through NCCL / NVLink) vs the binary32 oracle."""
-    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=1, path=path,
-                           device=int(os.environ["LOCAL_RANK"]))
+    g = init_grid(*n, dims=dims, periods=per, local_ranks=1, path=path)
     try:
         N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
         T0g, Cig = SI.global_heat_fields(*N)
@@ -132,8 +142,7 @@ def heat_f32_case(path, n, dims, per, nt=5, bw=(16, 2, 2), opts=None):
 
 def acoustic_case(path, n, dims, per, local, bw, nt=5):
     """Second workload: staggered P, Vx, Vy, Vz with update_halo!(Vx, Vy, Vz)."""
-    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=local, path=path,
-                           device=int(os.environ["LOCAL_RANK"]))
+    g = init_grid(*n, dims=dims, periods=per, local_ranks=local, path=path)
     try:
         F = ac.alloc_fields(g)
         ac.init_random(g, F)
@@ -165,7 +174,7 @@ def full_size_case(path, dtype, nt=3):
     n = (512, 512, 512)
     world = dist.get_world_size()
     dims = DIMS[world]
-    g = P.init_global_grid(*n, dims=dims, local_ranks=1, path=path, device=int(os.environ["LOCAL_RANK"]))
+    g = init_grid(*n, dims=dims, local_ranks=1, path=path)
     try:
         f32 = dtype == "f32"
         T, T2, Ci = app.alloc_fields(g, dtype=torch.float32 if f32 else None)
@@ -173,9 +182,8 @@ def full_size_case(path, dtype, nt=3):
         T0 = T[0].clone()
         d = app.spacing(g)
         if f32:   # dt of the float fields as the binary32 bench takes it: global max(Ci) on the device
-            mx = Ci[0].max().double()
-            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            dt = min(x * x for x in d) / 1.0 / float(mx) / 6.1
+            mx = g.global_max(float(Ci[0].max().double()))
+            dt = min(x * x for x in d) / 1.0 / mx / 6.1
         else:
             dt = app.stable_dt(g, Ci, *d)
         if f32:
@@ -216,12 +224,47 @@ def full_size_case(path, dtype, nt=3):
     log("full-size OK", dtype, path, dims)
 
 
+def boot_cases(world):
+    """One process per GPU with the host bootstrap instead of an NCCL communicator: the fused
+    stencil+NVLink-put kernel (default), the split pack/flag/unpack path, staggered update_halo, the
+    acoustic step, binary32, gather and global_max through the bootstrap -- bit-exact vs the oracle."""
+    dims = DIMS[world]
+    n = (40, 36, 34)
+    sizes = [n, (41, 36, 34), (40, 37, 34), (40, 36, 35)]
+    path = "p2p"
+    heat_case(path, (130, 36, 34), dims, (0, 0, 0), 1, (16, 2, 2), nt=4)                 # fused, pipelined
+    heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=4)                 # + periodic, corners
+    heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=3, per_step=True)  # single drained steps
+    heat_case(path, n, dims, (0, 0, 0), 1, (16, 2, 2), nt=3, opts={P.OPT_FUSED: 0})     # split P2P path
+    heat_case(path, (130, 36, 34), dims, (1, 0, 1), 1, (16, 2, 2), nt=3, opts={P.OPT_FUSED: 0})
+    for d2 in {2: [(1, 2, 1), (1, 1, 2)], 4: [(1, 2, 2)]}.get(world, []):
+        heat_case(path, (130, 36, 34), d2, (1, 1, 1), 1, (16, 2, 2), nt=3)
+    halo_case(path, n, dims, (0, 0, 0), 1, sizes, seed=1)
+    halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
+    acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4), nt=3)
+    heat_f32_case(path, n, dims, (1, 0, 1), nt=3)
+    if 8 % world == 0 and world < 8:   # 2x2x2 as virtual ranks over the processes
+        heat_case(path, (24, 20, 18), (2, 2, 2), (0, 0, 0), 8 // world, (4, 2, 2), nt=3)
+    gather_case(path, (20, 18, 16), dims, (1, 0, 1), (20, 17, 16))
+
+
 def main():
-    local_rank = int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    global BOOT
+    BOOT = len(sys.argv) > 2 and sys.argv[2] == "boot"
+    torch.cuda.set_device(device())
+    if BOOT:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device()))
     world = dist.get_world_size()
     paths = sys.argv[1].split(",") if len(sys.argv) > 1 else ["nccl", "p2p"]
+    if BOOT:
+        boot_cases(world)
+        dist.barrier()
+        if dist.get_rank() == 0:
+            print("BOOTSTRAP PARITY OK", world, flush=True)
+        dist.destroy_process_group()
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "full":   # the bench configuration at full size
         for dtype in ("f64", "f32"):
             full_size_case(paths[0], dtype)

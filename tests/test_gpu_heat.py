@@ -371,3 +371,55 @@ def test_binary32_aligned_x_slabs():
             assert np.array_equal(T[r].cpu().numpy(), W), r
     finally:
         g.finalize()
+
+
+@pytest.mark.parametrize("per", [(1, 1, 0), (1, 0, 1)])
+def test_fused_self_wrap_full_size_512(per):
+    """The fused P2P kernel at the bench size (512^3, 64-plane chunks + 8-plane tail, x faces staged)
+    with periodic axes wrapping onto the one GPU, through igg_heat_run (pipelined steps, drain):
+    EVERY cell bit-exact vs the canonical oracle on the global grid."""
+    import torch
+    n, nt = (512, 512, 512), 3
+    N = tuple(OG.global_size(n[i], 2, 1, bool(per[i])) for i in range(3))
+    ref, dtr = oracle_global(N, per, nt)
+    g = P.init_global_grid(*n, periods=per, local_ranks=1, device=0, path=P.PATH_P2P)
+    try:
+        T, T2, Ci = app.alloc_fields(g)
+        app.init_random(g, T, T2, Ci)
+        d = app.spacing(g)
+        dt = app.stable_dt(g, Ci, *d)
+        assert dt == dtr
+        l0 = g.kernel_launches()
+        T, T2 = app.run(g, T, T2, Ci, nt, dt, d)
+        torch.cuda.synchronize()
+        g.check()
+        assert g.kernel_launches() - l0 == nt + 1          # one fused launch per step + the drain
+        assert_windows([T[0].cpu().numpy()], ref, (1, 1, 1), n, (2, 2, 2), per)
+    finally:
+        g.finalize()
+
+
+def test_reallocated_array_is_never_taken_for_the_cached_one():
+    """the fused path caches peer mappings per array.  An array freed and re-allocated at the
+    same address (torch caching allocator after empty_cache) must not reuse the old entry: heat_run
+    re-validates the cache (allocation identity = base, size, buffer id) and stays bit-exact."""
+    import torch
+    n, per, nt = (130, 36, 34), (1, 1, 1), 3
+    N = tuple(OG.global_size(n[i], 2, 1, bool(per[i])) for i in range(3))
+    ref, dtr = oracle_global(N, per, nt)
+    g = P.init_global_grid(*n, periods=per, local_ranks=1, device=0, path=P.PATH_P2P)
+    try:
+        for rep in range(2):
+            T, T2, Ci = app.alloc_fields(g)
+            app.init_random(g, T, T2, Ci)
+            d = app.spacing(g)
+            dt = app.stable_dt(g, Ci, *d)
+            T, T2 = app.run(g, T, T2, Ci, nt, dt, d)
+            torch.cuda.synchronize()
+            g.check()
+            assert_windows([T[0].cpu().numpy()], ref, (1, 1, 1), n, (2, 2, 2), per)
+            g.release_arrays()
+            del T, T2, Ci
+            torch.cuda.empty_cache()
+    finally:
+        g.finalize()

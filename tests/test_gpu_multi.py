@@ -54,3 +54,22 @@ def test_torchrun_full_size_bench_config():
     sys.stderr.write(r.stderr[-4000:])
     assert r.returncode == 0
     assert "MULTI-GPU FULL-SIZE OK" in r.stdout
+
+
+def test_torchrun_bootstrap_no_nccl():
+    """One process per GPU with igg_init_args.bootstrap (host collectives over a gloo group, NO NCCL
+    communicator): the P2P data planes and the collective utilities bit-exact vs the oracle
+    (tests/mp_worker.py boot_cases).  Ranks that share a GPU are covered on one GPU by
+    tests/test_gpu_virtual_p2p.py (emulated in one process: spinning kernels of different processes on
+    one GPU are not co-scheduled)."""
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_worker.py"),
+           "p2p", "boot"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    sys.stdout.write(r.stdout[-4000:])
+    sys.stderr.write(r.stderr[-4000:])
+    assert r.returncode == 0
+    assert "BOOTSTRAP PARITY OK" in r.stdout
