@@ -326,8 +326,12 @@ enum {
     IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */
     IGG_OPT_COOP_HALO = 11,      /* 1: update_halo without NCCL messages runs as one cooperative kernel
                                     (grid barriers between axes); 0 (default, measured faster): per-axis launches */
-    IGG_OPT_HALO_STREAM = 12     /* 0 (default): update_halo runs on the library's high-priority comm
+    IGG_OPT_HALO_STREAM = 12,    /* 0 (default): update_halo runs on the library's high-priority comm
                                     stream joined to the caller's; 1: directly on the caller's stream */
+    IGG_OPT_LOCAL_P2P = 13       /* 1: ranks hosted by this process exchange update_halo faces through the
+                                    P2P protocol (stores into the receiver's slot, release flag, acquire
+                                    wait) instead of stream-ordered copies -- the cross-process data
+                                    plane emulated on one GPU (results identical; tests) */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

@@ -113,6 +113,8 @@ void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap) {
         g->recv_arena = (char *)dev_alloc(g, 2 * recv_half);
         IGG_CUDA(cudaMemset(g->recv_arena, 0, 2 * recv_half));
         g->recv_half = recv_half;
+        g->peer_recv.assign(g->nproc_procs, nullptr);
+        g->peer_recv[g->proc] = g->recv_arena;   // (IGG_OPT_LOCAL_P2P: sibling ranks' slots)
         if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
             cudaIpcMemHandle_t h;
             IGG_CUDA(cudaIpcGetMemHandle(&h, g->recv_arena));
@@ -188,7 +190,13 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
         P[a].epoch = U[a].epoch = g->epoch;
         U[a].err = P[a].err = g->d_err;
         U[a].timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
-        for (const PlanMsg &m : plan.msgs[a]) {
+        for (const PlanMsg &pm : plan.msgs[a]) {
+            // IGG_OPT_LOCAL_P2P: ranks of this process exchange through the P2P protocol (store into the
+            // receiver's slot, release flag, acquire wait) instead of plain stream-ordered copies -- the
+            // cross-process data plane emulated on one GPU; packs precede the waits on the stream, so no
+            // wait depends on a concurrently running launch
+            PlanMsg m = pm;
+            if (g->local_p2p && m.transport == kLocal) m.transport = kP2P;
             CopyDesc d{};
             const igg_field &F = fields[m.lr * nf + m.field];
             d.field = F.ptr;
@@ -216,7 +224,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
                     }
                 } else {
                     d.buf = sendb + m.sbuf;
-                    sends[a].push_back(&m);
+                    sends[a].push_back(&pm);
                     any_nccl = true;
                 }
                 pd[a].push_back(d);
@@ -234,7 +242,7 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
                     }
                     d.flag_slot = w;
                 } else if (m.transport == kNccl) {
-                    recvs[a].push_back(&m);
+                    recvs[a].push_back(&pm);
                     any_nccl = true;
                 }
                 ud[a].push_back(d);
@@ -426,7 +434,7 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
     for (int a = 0; a < 3; ++a)
         for (int lr = 0; lr < g->nlocal; ++lr)
             if (g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0) exch[a] = any = true;
-    if (!any && !(g->fused == 2 && g->nlocal == 1)) {   // nothing to exchange or hide: one full-region launch
+    if (!any) {   // nothing to exchange or hide: one full-region launch
         launch_full(g, T2, T, Ci, k, s);
         return;
     }
@@ -457,9 +465,11 @@ void heat_step(igg_grid *g, double *const *T2, const double *const *T, const dou
     std::vector<igg_field> f(g->nlocal);
     for (int lr = 0; lr < g->nlocal; ++lr) f[lr] = igg_field{T2[lr], {g->n[0], g->n[1], g->n[2]}};
     if (!sequential_req && g->stencil_kernel == 0 && fused_eligible(g)) {
-        HeatRegion R = make_region(g, 0, T2, T, Ci, 1, g->n[0] - 1, 1, g->n[1] - 1, 1, g->n[2] - 1);
-        if (heat_box_vectorizable(R)) {   // one kernel: stencil + exchange in peer memory
-            fused_step(g, T2[0], T[0], Ci[0], k, s, wait_prev, drain);
+        bool vec = true;
+        for (int lr = 0; lr < g->nlocal; ++lr)
+            vec = vec && heat_box_vectorizable(make_region(g, lr, T2, T, Ci, 1, g->n[0] - 1, 1, g->n[1] - 1, 1, g->n[2] - 1));
+        if (vec) {   // one kernel: stencil + exchange into the receivers' memory
+            fused_step(g, T2, T, Ci, k, s, wait_prev, drain);
             return;
         }
     }
@@ -616,7 +626,7 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->d_gather, (void *)g->fused_xsync, (void *)g->fused_xstg, (void *)g->fused_tgt, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->d_gather, (void *)g->fused_xstg, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
@@ -1148,6 +1158,7 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
             break;
         case IGG_OPT_COOP_HALO: g->coop = value != 0; break;
         case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
+        case IGG_OPT_LOCAL_P2P: g->local_p2p = value != 0; break;
         case IGG_OPT_FUSED_COMM_CTAS:
             if (value < 1 || value > 128) fail(IGG_E_ARG, "igg_set_option: FUSED_COMM_CTAS must be in [1, 128]");
             g->fused_ncomm = (int)value;

@@ -124,65 +124,52 @@ struct HeatRegionList {
 
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
-constexpr int kMaxTail = 6144;       // tiles of the last chunks, re-ordered face tiles first
+constexpr int kMaxFusedRanks = 8;    // ranks hosted on one GPU that one fused launch covers
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
-    double *dst;                     // the receiver's T2 (peer-mapped); the face lands in its halo layer
-    unsigned long long *flag;        // receiver's flags of (axis, side): [kMaxChunks] (z faces: [0])
-    unsigned long long *xflag;       // receiver's flags of the rim/forwarded cells (pipelined schedule)
+    double *dst;                     // the receiver's T2 (a sibling's, or peer-mapped); lands in its halo layer
+    unsigned long long *flag;        // receiver's data flags of (axis, side): [kMaxChunks] (z faces: [0])
+    unsigned long long *xflag;       // receiver's flags of the rim/forwarded cells
     int layer;                       // my send layer along the axis
     int active;
 };
 struct FusedHalo {                   // one halo side I receive
-    const unsigned long long *flag;  // my flags [kMaxChunks]
-    const unsigned long long *xflag; // my rim/forwarded-cell flags [kMaxChunks] (pipelined schedule)
+    const unsigned long long *flag;  // my data flags [kMaxChunks]
+    const unsigned long long *xflag; // my rim/forwarded-cell flags [kMaxChunks]
     int layer;                       // halo layer (0 or s-1)
     int active;
 };
-struct FusedParams {
+struct FusedRank {                   // one hosted rank of a fused launch
     const double *T;
     const double *Ci;
     double *T2;
-    int s[3];
     FusedFace face[3][2];
     FusedHalo halo[3][2];
-    int nchunks;                     // z-chunks; chunk ids 0..nbig-1 have kc1 planes, then kc2
-    int nbig, kc1, kc2, cz;          // cz: chunk id holding plane s_z-2, visited second
+    // x faces: the sender's face tiles store their captured x layer into the receiver's compact staging
+    // buffer [epoch parity][halo side][y][z] (z fastest: whole sectors, not one 8-B value per sector of
+    // a T2 column); the receiver's first/last x-tiles read the previous epoch's values into shared
+    // memory, the forwarders read the current epoch's, the drain copies the last epoch's into T2
+    const double *xstg;              // mine
+    double *xstg_peer[2];            // the receivers' (indexed like face[0][rs])
+    unsigned int *ctr;               // [6][kMaxChunks] data-flag contribution counters (sender side)
+    unsigned int *ctr_x;             // [6][kMaxChunks] rim/forwarded-cell counters
+    unsigned int *rim_ticket;
+};
+struct FusedParams {
+    int s[3];
+    int nranks, per_rank;            // blocks per rank: [nrim | nfwd | nstencil]
+    int nrim, nfwd, nstencil;
+    int wait_prev;                   // tiles reading halos wait for the previous epoch's data flags
+    int nchunks;
+    int2 zr[kMaxChunks];             // z range of each chunk, in visit order (= chunk id)
+    int zchunk[2];                   // chunk holding the z send layer of face (2, rs); -1 if none
     int xtiles, ytiles;
-    int nostore;                     // timing experiment: face tiles count without storing
-    int bmain;                       // blocks in plain order; the rest decode tail[]
-    unsigned short tail[kMaxTail];   // (x-tile, y-tile, chunk - first tail chunk) of the tail blocks
-    int zchunk[2];                   // chunk holding z send layer of face (2, rs); -1 if none
-    unsigned int *ctr;               // [6][kMaxChunks] contribution counters (sender side)
-    const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk)
+    const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk) data flag
+    const unsigned int *tgt_x;       // ... an xflag (rim + forwarders)
     unsigned long long epoch;
     long long timeout_cycles;
     int *err;
     HeatCoef k;
-    // pipelined schedule (one launch per step on the caller's stream): blocks [0, nrim) send the rim,
-    // the next nfwd forward the edge lines, the rest are the stencil tiles; face tiles
-    // count on ctr/tgt (data flags), rim and forwarders on ctr_x/tgt_x (xflags)
-    int pipe;
-    int wait_prev;                   // tiles reading halos wait for the previous epoch's data flags
-    int nrim, nstencil, nfwd;
-    unsigned int *ctr_x;
-    const unsigned int *tgt_x;
-    unsigned int *rim_ticket;
-    // x faces staged (pipelined schedule): the sender's face tiles store their x layer into the
-    // receiver's compact staging buffer [epoch parity][halo side][y][z] (z fastest: whole 32-B
-    // sectors, not one 8-B value per sector of a T2 column); the receiver's first/last x-tiles copy
-    // the previous epoch's values into their T column before their sweep, the forwarders read the
-    // current epoch's, the drain copies the last epoch's into T2
-    int xstage;
-    double *xstg;                    // mine
-    double *xstg_peer[2];            // the receivers' (indexed like face[0][rs])
-    // dedicated x blocks (staged schedule, default): the face tiles only count their chunk as computed
-    // (xcomp -> xcompe); nxb sender blocks per x face copy the layer column into the receiver's
-    // staging and publish the data flag; nxb receiver blocks per x halo copy the staged column into
-    // my T2 and publish xready (local), which the next step's halo tiles await
-    int xblk, nxb;
-    int xhint;                       // x-face tiles store with an L2 evict_last hint (experiment)
-    unsigned int *xcnt;              // [4][kMaxChunks]: 0..1 face-tile counts, 2..3 receiver-block counts
-    unsigned long long *xev;         // [4][kMaxChunks]: 0..1 chunk computed (epoch), 2..3 halo ready (epoch)
+    FusedRank r[kMaxFusedRanks];
 };
 
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
@@ -340,9 +327,11 @@ struct igg_grid : igg::Geom {
     int fused_ncomm = 1;                                 // IGG_OPT_FUSED_COMM_CTAS
     bool coop = false;                                   // IGG_OPT_COOP_HALO
     bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
+    bool local_p2p = false;                              // IGG_OPT_LOCAL_P2P
     std::list<std::pair<std::vector<long long>, igg::Plan>> plan_cache;   // field-list shape -> plan
-    unsigned int *fused_ctr = nullptr, *fused_tgt = nullptr, *fused_tgt_x = nullptr, *fused_tgt_pipe = nullptr;
-    int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // nbig, kc1, kc2, cz, xtiles, ytiles
+    unsigned int *fused_ctr = nullptr, *fused_tgt_x = nullptr, *fused_tgt_pipe = nullptr;
+    int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // [4] xtiles, [5] ytiles
+    std::vector<int2> fused_zr;                          // z-chunks in visit order
     // peer mappings of arrays the fused path stores into (PeerMap: fused.cu)
     struct PeerMap {
         const void *ptr;                 // my array
@@ -351,16 +340,11 @@ struct igg_grid : igg::Geom {
         std::vector<double *> peers;     // per process: the same array of that process, mapped
     };
     std::vector<PeerMap> fused_peer_maps;
-    std::vector<unsigned short> fused_tail;                                       // tail tile order
-    int fused_bmain = 0;
     std::vector<std::pair<std::string, void *>> fused_opened;                     // IPC handle -> mapping
     int fused_ntiles = 0, fused_nchunks = 0, fused_key = -1;
     int fused_zchunk[2] = {-1, -1};
-    int fused_zafter = 1;
     int fused_nfwd = 0;                                  // in-kernel forwarders (pipelined)
-    int fused_nxb = 4;                                   // x sender/receiver blocks per face (pipelined)
     double *fused_xstg = nullptr;                        // x-face staging buffer (pipelined)
-    void *fused_xsync = nullptr;                         // x-block counters and epochs
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
@@ -387,8 +371,8 @@ void validate_peer_maps(igg_grid *g);
 void check_device_error(igg_grid *g, const char *who);
 // one fused step; pipelined schedule: wait_prev = the previous step of the same run was fused (its
 // halos are awaited tile by tile), drain = wait for every incoming face at the end (step complete)
-void fused_step(igg_grid *g, double *T2, const double *T, const double *Ci, const HeatCoef &k, cudaStream_t s,
-                bool wait_prev = false, bool drain = true);
+void fused_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, const HeatCoef &k,
+                cudaStream_t s, bool wait_prev = false, bool drain = true);
 void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
 void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step

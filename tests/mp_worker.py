@@ -286,13 +286,9 @@ def main():
                 heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), opts=o)
             heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=12)
             heat_case(path, (66, 40, 36), dims, (0, 1, 0), 1, (16, 2, 2), nt=9)
-            # single igg_heat_step calls (each drained) and the legacy multi-stream fused schedule
+            # single igg_heat_step calls (each drained)
             heat_case(path, (130, 36, 34), dims, (1, 1, 1), 1, (16, 2, 2), nt=5, per_step=True)
-            heat_case(path, (130, 36, 34), dims, (1, 0, 1), 1, (16, 2, 2), nt=5, opts={P.OPT_FUSED_MODE: 130})
-            heat_case(path, (130, 36, 34), dims, (1, 1, 0), 1, (16, 2, 2), nt=6, opts={P.OPT_FUSED_MODE: 258})
-            heat_case(path, (130, 36, 34), dims, (0, 1, 1), 1, (16, 2, 2), nt=6, opts={P.OPT_FUSED_MODE: 2050})
-            # the x send layer stored from inside the sweep (fused mode bit 1)
-            heat_case(path, (130, 36, 70), dims, (1, 1, 1), 1, (16, 2, 2), nt=5, opts={P.OPT_FUSED_MODE: 3})
+            heat_case(path, (130, 36, 70), dims, (1, 0, 1), 1, (16, 2, 2), nt=5, per_step=True)
             # the fused put path on every split axis (z faces, corner forwarding x->y->z)
             extra = {2: [(1, 2, 1), (1, 1, 2)], 4: [(2, 1, 2), (1, 2, 2), (4, 1, 1), (1, 1, 4)]}.get(world, [])
             for d2 in extra:
