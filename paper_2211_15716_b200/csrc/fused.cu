@@ -133,24 +133,35 @@ constexpr int kFKC = 64;   // longest z-chunk
 }  // namespace
 
 // The z sweep of one tile: cp.async ring of kFD planes of T and Ci, x neighbours by shuffle, z by a
-// register queue.  XH: hl = cell index (in the tile) of the x halo column read from xr[] (the staged
-// previous-epoch values, plane z at xr[z - zs]) instead of T; xsl = cell index of the x send layer,
-// captured into xs[z - zs] (-1: none).
+// register queue.  XH (CTA-uniform: the tile holds an x halo or x send column):
+//  * hrow (the lane holding the x halo cell, else NULL): the staged previous-epoch values of that cell,
+//    plane z at hrow[z]; the lane fetches its pair as two 8-B cp.async -- the halo element from hrow, the
+//    other from T -- so the ring (and c) carry the neighbour's value; T's halo column is never read or
+//    written (hcy: which element of the pair);
+//  * xs (the lane holding the x send cell, else NULL): the cell's result of plane z goes to xs[z - zs]
+//    (shared memory; it leaves z-contiguous after the sweep) (scy: which element).
+__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+
 template <bool XH>
-__device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
-                                            double2 (*sC)[32 * kFTY], const double *xr, double *xs, int zs, int ze,
-                                            int y, int p, bool pair_in, bool w0, bool w1, int hl, int xsl) {
-    const double *__restrict__ T = R.T;
-    const double *__restrict__ Ci = R.Ci;
-    double *__restrict__ T2 = R.T2;
+__device__ __forceinline__ void fused_sweep(const HeatCoef &k, const double *__restrict__ T,
+                                            const double *__restrict__ Ci, double *__restrict__ T2,
+                                            double2 (*sT)[32 * kFTY], double2 (*sC)[32 * kFTY], int sx, long long sxy,
+                                            int zs, int ze, long long i, bool pair_in, bool w0, bool w1,
+                                            const double *hrow, bool hcy, double *xs, bool scy) {
     const int tid = threadIdx.x, lane = tid & 31;
-    const int sx = F.s[0];
-    const long long sxy = (long long)sx * F.s[1];
-    long long i = (long long)zs * sxy + (long long)y * sx + p;
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
-            cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
+            if (XH && hrow && zs + q + 1 < ze) {   // plane zs+q+1: halo element from the staging row
+                double *d = reinterpret_cast<double *>(&sT[q][tid]);
+                cp_async8f(d + (hcy ? 1 : 0), hrow + zs + q + 1);
+                cp_async8f(d + (hcy ? 0 : 1), T + i + (q + 1) * sxy + (hcy ? 0 : 1));
+            } else {
+                cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
+            }
             cp_async16f(&sC[q][tid], Ci + i + q * sxy);
         }
         cp_commit();
@@ -158,18 +169,15 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
+    if (XH && hrow) {
+        const double h = __ldcg(hrow + zs);
+        if (hcy) c.y = h; else c.x = h;
+    }
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
-    // XH: this lane holds the halo / send cell as element .x (0) or .y (1) of its pair
-    const bool hc = XH && hl >= 0 && (hl >> 1) == lane, hcy = hl & 1;
-    const bool sc = XH && xsl >= 0 && (xsl >> 1) == lane, scy = xsl & 1;
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
-        if (XH && hc) {   // the x halo cell of this plane: the neighbour's staged value
-            const double h = xr[z - zs];
-            if (hcy) c.y = h; else c.x = h;
-        }
         double2 ym = zero2, yp = zero2;
         if (pair_in) {
             ym = ldg2f(T + i - sx);
@@ -181,19 +189,25 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
         if (lo_edge) xm = __ldg(T + i - 1);
         if (hi_edge) xp = __ldg(T + i + 2);
-        const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
-        const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
+        const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, k);
+        const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, k);
         if (w0 && w1) {
             *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
         } else {
             if (w0) T2[i] = r0;
             if (w1) T2[i + 1] = r1;
         }
-        if (XH && sc) xs[z - zs] = scy ? r1 : r0;
+        if (XH && xs) xs[z - zs] = scy ? r1 : r0;
         zm = c;
         c = zp;
         if (pair_in && z + kFD < ze) {
-            cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
+            if (XH && hrow && z + kFD + 1 < ze) {
+                double *d = reinterpret_cast<double *>(&sT[slot][tid]);
+                cp_async8f(d + (hcy ? 1 : 0), hrow + z + kFD + 1);
+                cp_async8f(d + (hcy ? 0 : 1), T + i + (kFD + 1) * sxy + (hcy ? 0 : 1));
+            } else {
+                cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
+            }
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
         }
         cp_commit();
@@ -206,12 +220,13 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
 
 // One launch over all tiles of all hosted ranks, the 1-GPU loop unchanged.  Block b of rank r:
 // [0, nrim) rim, [nrim, nrim+nfwd) forwarders (last step of a run only), then the stencil tiles.
+// MR: more than one hosted rank (the rank's parameters are indexed at run time).
+template <bool MR>
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
     __shared__ double sXs[kFTY][kFKC];   // my x send-layer cell of each row, plane by plane (this sweep)
-    __shared__ double sXr[kFTY][kFKC];   // my x halo cell of each row, plane by plane (previous epoch)
-    const int rank = blockIdx.x / F.per_rank;
+    const int rank = MR ? blockIdx.x / F.per_rank : 0;
     int b = blockIdx.x - rank * F.per_rank;
     const FusedRank &R = F.r[rank];
     if (b < F.nrim + F.nfwd) {   // CTA-uniform
@@ -243,7 +258,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     for (int rs = 0; rs < 2; ++rs)
         if (R.face[0][rs].active && R.face[0][rs].layer >= xlo && R.face[0][rs].layer < xhi) xrs = rs;
     const int xsl = xrs >= 0 ? R.face[0][xrs].layer - tx * 64 : -1;   // its cell index in the tile
-    // the x halo column this tile reads (first x-tile: x = 0, last: x = sx-1), from the staging buffer
+    // the x halo column this tile reads (first x-tile: x = 0, last: x = sx-1): from the staging buffer
     // when the previous step of the run stored it there (first step of a run: T holds it)
     int hside = -1;
     if (F.wait_prev) {
@@ -264,23 +279,23 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             if (zu) spin_geq(F, R.halo[2][1].flag, prev);
         }
         __syncthreads();
-        if (hside >= 0) {   // my rows' staged halo cells of this chunk -> sXr (rows are z-contiguous)
-            for (int t = tid; t < kFTY * nz; t += 32 * kFTY) {
-                const int w = t / nz, z = zs + t % nz;
-                if (ty0 + w < sy - 1) sXr[w][z - zs] = __ldcg(R.xstg + xstg_at(F, F.epoch - 1, hside, ty0 + w, z));
-            }
-            __syncthreads();
-        }
     }
 
-    // ---- the z sweep; tiles that hold an x halo or x send column take the variant that patches /
+    // ---- the z sweep; tiles that hold an x halo or x send column take the variant that redirects /
     // captures it (CTA-uniform; the plain variant keeps the 1-GPU kernel's register budget)
-    if (hl >= 0 || xsl >= 0)
-        fused_sweep<true>(F, R, sT, sC, sXr[warp], sXs[warp], zs, ze, y, p, pair_in, w0, w1, hl, rowv ? xsl : -1);
-    else
-        fused_sweep<false>(F, R, sT, sC, sXr[warp], sXs[warp], zs, ze, y, p, pair_in, w0, w1, -1, -1);
+    const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
+    if (hl >= 0 || xsl >= 0) {
+        const bool hlane = hl >= 0 && (hl >> 1) == lane && rowv;
+        const bool slane = xsl >= 0 && (xsl >> 1) == lane && rowv;
+        const double *hrow = hlane ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
+        fused_sweep<true>(F.k, R.T, R.Ci, R.T2, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, hrow, hl & 1,
+                          slane ? sXs[warp] : nullptr, xsl & 1);
+    } else {
+        fused_sweep<false>(F.k, R.T, R.Ci, R.T2, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr, false,
+                           nullptr, false);
+    }
 
-    // ---- faces held by this tile -> the receivers
+// ---- faces held by this tile -> the receivers
     unsigned did = xrs >= 0 ? 1u << xrs : 0u;   // bit f: this tile holds part of face f = 2a + rs
 #pragma unroll
     for (int rs = 0; rs < 2; ++rs) {
@@ -518,7 +533,7 @@ static void build_layout(igg_grid *g, const bool act[3][2], bool zex) {
     const int ytiles = (n1 - 2 + kFTY - 1) / kFTY;
     const int wz = n2 - 2;
     if (g_fused_occ < 0) {
-        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel, 32 * kFTY, 0));
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false>, 32 * kFTY, 0));
         IGG_CUDA(cudaDeviceGetAttribute(&g_fused_nsm, cudaDevAttrMultiProcessorCount, g->device));
     }
     const int kc1 = kFKC, kc2 = g->fused_kc2 > 0 ? g->fused_kc2 : 8;
@@ -787,7 +802,10 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.per_rank = F.nrim + F.nfwd + F.nstencil;
     const long long blocks = (long long)F.per_rank * L;
     prof_begin(g, s);
-    heat_fused_kernel<<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
+    if (L > 1)
+        heat_fused_kernel<true><<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
+    else
+        heat_fused_kernel<false><<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
     IGG_CUDA(cudaGetLastError());
     g->launches++;
     prof_end(g, s, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2) * L);
