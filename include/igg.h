@@ -328,10 +328,14 @@ enum {
                                     (grid barriers between axes); 0 (default, measured faster): per-axis launches */
     IGG_OPT_HALO_STREAM = 12,    /* 0 (default): update_halo runs on the library's high-priority comm
                                     stream joined to the caller's; 1: directly on the caller's stream */
-    IGG_OPT_LOCAL_P2P = 13       /* 1: ranks hosted by this process exchange update_halo faces through the
-                                    P2P protocol (stores into the receiver's slot, release flag, acquire
-                                    wait) instead of stream-ordered copies -- the cross-process data
-                                    plane emulated on one GPU (results identical; tests) */
+    IGG_OPT_LOCAL_P2P = 13,      /* 1: update_halo runs the dimension-sequential P2P protocol (per axis: pack
+                                    into the receiver's slot, release flag, acquire wait, unpack) also
+                                    between the ranks hosted by this process (the cross-process protocol
+                                    emulated on one GPU; results identical; tests) */
+    IGG_OPT_HALO26 = 14          /* 1 (default): update_halo without NCCL messages is ONE kernel that stores
+                                    every halo region (faces, edges, corners) straight from its owner into
+                                    the receiver (26-neighbour single phase, bit-identical to the
+                                    dimension-sequential result); 0: the per-axis pack/flag/unpack kernels */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libigg.so")
-SOURCES = ["topology.cpp", "plan.cpp", "grid.cpp", "kernels.cu", "fused.cu", "acoustic.cu"]
+SOURCES = ["topology.cpp", "plan.cpp", "grid.cpp", "kernels.cu", "fused.cu", "halo26.cu", "acoustic.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -37,9 +37,12 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str = None, extra=()) -> str:
+    """out / extra: another build of the same sources (e.g. an A/B variant with -D flags, loaded with
+    IGG_LIBRARY=<out>); the default is the product library in-tree."""
+    if out is None and not force and not needs_build():
         return OUT
+    target = out or OUT
     nr = nccl_root()
     inc = os.path.join(nr, "include")
     lib = os.path.join(nr, "lib")
@@ -47,8 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
               "-I", inc, "-I", os.path.join(HERE, "..", "include")]
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
-        cmd = [nvcc()] + ARCH + common + ["-fmad=false", "-Xptxas", "-v" if verbose else "-O3",
+        obj = os.path.join(CSRC, src + (".%d.o" % os.getpid()))
+        cmd = [nvcc()] + ARCH + common + list(extra) + ["-fmad=false", "-Xptxas", "-v" if verbose else "-O3",
                                           "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -57,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
         objs.append(obj)
-    link = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs + [
+    link = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", target] + objs + [
         "-L", lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
@@ -65,8 +68,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("link of libigg.so failed")
     for o in objs:
         os.remove(o)
-    return OUT
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH -DFLAG ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    extra = [x for x in args if x.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, extra=extra))

@@ -145,12 +145,17 @@ __device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
 
+#ifndef FUSED_STCS
+#define FUSED_STCS 1
+#endif
 template <bool XH>
-__device__ __forceinline__ void fused_sweep(const HeatCoef &k, const double *__restrict__ T,
-                                            const double *__restrict__ Ci, double *__restrict__ T2,
-                                            double2 (*sT)[32 * kFTY], double2 (*sC)[32 * kFTY], int sx, long long sxy,
-                                            int zs, int ze, long long i, bool pair_in, bool w0, bool w1,
+__device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
+                                            double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
+                                            long long i, bool pair_in, bool w0, bool w1, bool cs,
                                             const double *hrow, bool hcy, double *xs, bool scy) {
+    const double *__restrict__ T = R.T;
+    const double *__restrict__ Ci = R.Ci;
+    double *__restrict__ T2 = R.T2;
     const int tid = threadIdx.x, lane = tid & 31;
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
@@ -189,10 +194,13 @@ __device__ __forceinline__ void fused_sweep(const HeatCoef &k, const double *__r
         double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
         if (lo_edge) xm = __ldg(T + i - 1);
         if (hi_edge) xp = __ldg(T + i + 2);
-        const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, k);
-        const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, k);
+        const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
+        const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
         if (w0 && w1) {
-            *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
+            if (FUSED_STCS && cs)   // (CTA-uniform) a tile without faces: T2 is not re-read this step
+                __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+            else
+                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
         } else {
             if (w0) T2[i] = r0;
             if (w1) T2[i + 1] = r1;
@@ -226,7 +234,9 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
     __shared__ double sXs[kFTY][kFKC];   // my x send-layer cell of each row, plane by plane (this sweep)
-    const int rank = MR ? blockIdx.x / F.per_rank : 0;
+    // (the rank index stays a run-time value even for one rank: the parameters are then read through
+    // uniform registers instead of being re-materialised from the constant bank in the sweep)
+    const int rank = blockIdx.x / F.per_rank;
     int b = blockIdx.x - rank * F.per_rank;
     const FusedRank &R = F.r[rank];
     if (b < F.nrim + F.nfwd) {   // CTA-uniform
@@ -284,15 +294,21 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     // ---- the z sweep; tiles that hold an x halo or x send column take the variant that redirects /
     // captures it (CTA-uniform; the plain variant keeps the 1-GPU kernel's register budget)
     const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
+    bool yzface = false;   // the tile re-reads its T2 for a y or z face after the sweep
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+        yzface = yzface || (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi);
+        yzface = yzface || (R.face[2][rs].active && F.zchunk[rs] == pos);
+    }
     if (hl >= 0 || xsl >= 0) {
         const bool hlane = hl >= 0 && (hl >> 1) == lane && rowv;
         const bool slane = xsl >= 0 && (xsl >> 1) == lane && rowv;
         const double *hrow = hlane ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
-        fused_sweep<true>(F.k, R.T, R.Ci, R.T2, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, hrow, hl & 1,
+        fused_sweep<true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, hrow, hl & 1,
                           slane ? sXs[warp] : nullptr, xsl & 1);
     } else {
-        fused_sweep<false>(F.k, R.T, R.Ci, R.T2, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr, false,
-                           nullptr, false);
+        fused_sweep<false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, nullptr, false, nullptr,
+                           false);
     }
 
 // ---- faces held by this tile -> the receivers
@@ -702,6 +718,8 @@ static const std::vector<double *> &peer_arrays(igg_grid *g, double *T2) {
     g->fused_peer_maps.push_back(e);
     return g->fused_peer_maps.back().peers;
 }
+
+const std::vector<double *> &peer_arrays_pub(igg_grid *g, double *arr) { return peer_arrays(g, arr); }
 
 // One step of every hosted rank: T2[lr] = step!(T[lr]) plus the faces into the receivers.
 // wait_prev: the previous step of the same run was fused (its faces are awaited tile by tile);

@@ -102,6 +102,7 @@ void ensure_arena(igg_grid *g, size_t recv_half, size_t send_cap) {
     const bool grow_send = send_cap > g->send_cap;
     if (!grow_recv && !grow_send) return;
     process_barrier(g);   // nobody may still be writing into the old arenas
+    release_h26(g);       // cached 26-neighbour plans point into the arenas
     if (grow_send) {
         if (g->send_arena) IGG_CUDA(cudaFree(g->send_arena));
         g->send_arena = (char *)dev_alloc(g, send_cap);
@@ -176,6 +177,10 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
 
     g->epoch++;
     if (g->skip_comm) return;
+    if (!plan.any_nccl && g->halo26 && !g->local_p2p) {   // no NCCL message: the one-kernel 26-neighbour exchange
+        exchange26(g, fields, nf, plan, st);
+        return;
+    }
     const int parity = (int)(g->epoch & 1);
     double *recv = reinterpret_cast<double *>(g->recv_arena + parity * g->recv_half);
     double *sendb = reinterpret_cast<double *>(g->send_arena);
@@ -568,7 +573,9 @@ IGG_API igg_status igg_init_global_grid(const igg_init_args *A, igg_grid **grid_
         }
         // receive flags (P2P), last-block tickets, error word, reduction scratch
         // [data | rim+forwarded] x nlocal x 6 faces x kMaxChunks
-        const size_t flag_bytes = 2 * sizeof(unsigned long long) * g->nlocal * 6 * igg::kMaxChunks;
+        // + the 26-neighbour exchange's data / ready flags (halo26.cu)
+        const size_t flag_bytes =
+            (2 * 6 * igg::kMaxChunks + igg::kH26Flags) * sizeof(unsigned long long) * g->nlocal;
         g->flags = (unsigned long long *)igg::dev_alloc(g, flag_bytes);
         IGG_CUDA(cudaMemset(g->flags, 0, flag_bytes));
         g->tickets = (unsigned int *)igg::dev_alloc(g, sizeof(unsigned int) * 4);
@@ -620,13 +627,14 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
     for (auto &o : g->fused_opened) cudaIpcCloseMemHandle(o.second);
     g->fused_opened.clear();
     g->fused_peer_maps.clear();
+    igg::release_h26(g);
     if (g->path == IGG_PATH_P2P && g->nproc_procs > 1) {
         igg::unmap_peers(g, g->peer_recv);
         for (int p = 0; p < g->nproc_procs; ++p)
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->d_gather, (void *)g->fused_xstg, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->h26_ctr, (void *)g->d_gather, (void *)g->fused_xstg, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);
@@ -1159,6 +1167,7 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_COOP_HALO: g->coop = value != 0; break;
         case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
         case IGG_OPT_LOCAL_P2P: g->local_p2p = value != 0; break;
+        case IGG_OPT_HALO26: g->halo26 = value != 0 ? 1 : 0; break;
         case IGG_OPT_FUSED_COMM_CTAS:
             if (value < 1 || value > 128) fail(IGG_E_ARG, "igg_set_option: FUSED_COMM_CTAS must be in [1, 128]");
             g->fused_ncomm = (int)value;
@@ -1215,6 +1224,7 @@ IGG_API igg_status igg_release_arrays(igg_grid *g) {
     IGG_TRY
     igg::check_live(g, "igg_release_arrays");
     igg::release_peer_maps(g);
+    igg::release_h26(g);
     IGG_CATCH
 }
 

@@ -262,6 +262,7 @@ struct PlanMsg {
 struct Plan {
     long long block = 0;                                   // doubles per rank in the receive arena half
     std::vector<std::array<long long, 3>> sz;
+    std::vector<std::array<std::array<long long, 2>, 3>> off;   // word offset of slot (field, axis, side)
     std::vector<PlanMsg> msgs[3];                          // per axis: all packs, then all unpacks
     bool any_nccl = false;
 };
@@ -328,6 +329,14 @@ struct igg_grid : igg::Geom {
     bool coop = false;                                   // IGG_OPT_COOP_HALO
     bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
     bool local_p2p = false;                              // IGG_OPT_LOCAL_P2P
+    int halo26 = 1;                                      // IGG_OPT_HALO26: P2P update_halo as one 26-neighbour kernel
+    unsigned int *h26_ctr = nullptr;                     // [claim, stores done]
+    struct H26Cache {
+        std::vector<long long> key;                      // field pointers, sizes, element sizes, arena
+        void *dplan = nullptr;                           // device plan
+        long long nchunks = 0;
+    };
+    std::vector<H26Cache> h26_cache;
     std::list<std::pair<std::vector<long long>, igg::Plan>> plan_cache;   // field-list shape -> plan
     unsigned int *fused_ctr = nullptr, *fused_tgt_x = nullptr, *fused_tgt_pipe = nullptr;
     int fused_geo[6] = {0, 0, 0, 0, 0, 0};               // [4] xtiles, [5] ytiles
@@ -351,6 +360,12 @@ struct igg_grid : igg::Geom {
 
 namespace igg {
 void exchange(igg_grid *g, const igg_field *fields, int nfields, cudaStream_t st, bool allow_coop = false);
+// update_halo on the P2P path (halo26.cu): ONE kernel per call, every halo region -- faces, edges,
+// corners -- stored straight from its owner into the receiver (26-neighbour single phase)
+void exchange26(igg_grid *g, const igg_field *fields, int nfields, const Plan &plan, cudaStream_t st);
+void release_h26(igg_grid *g);   // drop the cached device plans (they hold peer mappings)
+const std::vector<double *> &peer_arrays_pub(igg_grid *g, double *arr);
+constexpr int kH26Flags = 64;    // per hosted rank: data flags [0, 27), ready flags [32, 59) by direction
 void check_live(const igg_grid *g, const char *what);
 void heat_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci,
                double lam, double dt, double dx, double dy, double dz, const int bw[3],

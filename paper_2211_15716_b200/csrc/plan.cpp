@@ -112,6 +112,7 @@ Plan build_plan(const Geom &G, const long long *sizes, int nf, const int *esz) {
             }
         }
     P.block = block;
+    P.off = off;
     for (int a = 0; a < 3; ++a) {   // x -> y -> z
         std::vector<PlanMsg> packs, unpacks;
         for (int lr = 0; lr < L; ++lr)

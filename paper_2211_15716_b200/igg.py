@@ -36,6 +36,7 @@ OPT_FUSED_COMM_CTAS = 10
 OPT_COOP_HALO = 11
 OPT_HALO_STREAM = 12
 OPT_LOCAL_P2P = 13
+OPT_HALO26 = 14
 
 STATUS = {0: "IGG_OK", 1: "IGG_E_ARG", 2: "IGG_E_STATE", 3: "IGG_E_STAGGER", 4: "IGG_E_WIDTH",
           5: "IGG_E_CUDA", 6: "IGG_E_NCCL", 7: "IGG_E_TIMEOUT", 8: "IGG_E_UNSUPPORTED", 9: "IGG_E_BOOTSTRAP"}
