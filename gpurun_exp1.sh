@@ -1,7 +1,7 @@
-cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp3}
-timeout 900 python -m pytest tests -q -m gpu -x -k "halo or virtual_p2p or fused or hide_comm or acoustic" > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
-for lib in paper_2211_15716_b200/libigg.so ablation/libigg_nostcs.so; do
-for per in 0,0,0 1,0,0 0,1,0 1,1,1; do
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp4}
+timeout 900 python -m pytest tests -q -m gpu -x -k "virtual_p2p or fused" > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
+for lib in paper_2211_15716_b200/libigg.so; do
+for per in 0,0,0 1,0,0 0,1,0 0,0,1 1,1,1; do
   echo "== $lib $per" >> gpurun_out/${T}.txt
   IGG_LIBRARY=$lib timeout 300 python bench.py --periodic $per --no-e2e --no-cpu --no-stats --steps 100 2>&1 | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['exposed_halo'], d['roofline']['avg_launch_ms'])" >> gpurun_out/${T}.txt 2>&1

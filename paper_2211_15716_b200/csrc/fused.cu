@@ -133,26 +133,23 @@ constexpr int kFKC = 64;   // longest z-chunk
 }  // namespace
 
 // The z sweep of one tile: cp.async ring of kFD planes of T and Ci, x neighbours by shuffle, z by a
-// register queue.  XH (CTA-uniform: the tile holds an x halo or x send column):
-//  * hrow (the lane holding the x halo cell, else NULL): the staged previous-epoch values of that cell,
-//    plane z at hrow[z]; the lane fetches its pair as two 8-B cp.async -- the halo element from hrow, the
-//    other from T -- so the ring (and c) carry the neighbour's value; T's halo column is never read or
-//    written (hcy: which element of the pair);
-//  * xs (the lane holding the x send cell, else NULL): the cell's result of plane z goes to xs[z - zs]
-//    (shared memory; it leaves z-contiguous after the sweep) (scy: which element).
-__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-
+// register queue.  XH (CTA-uniform: the tile holds an x halo and/or an x send column), both handled with
+// warp shuffles so the loop keeps its shape (no extra memory instructions per plane):
+//  * hl >= 0: cell hl (tile index) is the x halo column; its previous-epoch values of this chunk's planes
+//    (hrow[z], z-contiguous in the staging buffer) are loaded once, two planes per lane, and each plane's
+//    value is shuffled to the lane holding the cell, which substitutes it for T's (never read or written)
+//    halo value;
+//  * sl >= 0: cell sl is the x send layer; each plane's result is shuffled from the lane computing it to
+//    lane (z - zs) % 32 (two planes per lane), and after the sweep every lane stores its two values
+//    z-contiguous into the receiver's staging row sdst[z] (whole sectors over NVLink).
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
 template <bool XH>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
                                             double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
-                                            long long i, bool pair_in, bool w0, bool w1, bool cs,
-                                            const double *hrow, bool hcy, double *xs, bool scy) {
+                                            long long i, bool pair_in, bool w0, bool w1, bool cs, int hl,
+                                            const double *hrow, int sl, double *sdst) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
@@ -160,13 +157,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
-            if (XH && hrow && zs + q + 1 < ze) {   // plane zs+q+1: halo element from the staging row
-                double *d = reinterpret_cast<double *>(&sT[q][tid]);
-                cp_async8f(d + (hcy ? 1 : 0), hrow + zs + q + 1);
-                cp_async8f(d + (hcy ? 0 : 1), T + i + (q + 1) * sxy + (hcy ? 0 : 1));
-            } else {
-                cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
-            }
+            cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
             cp_async16f(&sC[q][tid], Ci + i + q * sxy);
         }
         cp_commit();
@@ -174,9 +165,16 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
-    if (XH && hrow) {
-        const double h = __ldcg(hrow + zs);
-        if (hcy) c.y = h; else c.x = h;
+    double h0 = 0.0, h1 = 0.0, s0 = 0.0, s1 = 0.0;
+    const int hlane = hl >> 1, slane = sl >> 1;
+    const bool hhi = hl & 1, shi = sl & 1;
+    if (XH && hl >= 0) {   // this chunk's staged halo values, planes zs+lane and zs+32+lane
+        if (hrow && zs + lane < ze) h0 = __ldcg(hrow + zs + lane);
+        if (hrow && zs + 32 + lane < ze) h1 = __ldcg(hrow + zs + 32 + lane);
+        const double v = __shfl_sync(0xffffffffu, h0, 0);
+        if (hrow && lane == hlane) {
+            if (hhi) c.y = v; else c.x = v;
+        }
     }
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
@@ -205,23 +203,36 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
             if (w0) T2[i] = r0;
             if (w1) T2[i + 1] = r1;
         }
-        if (XH && xs) xs[z - zs] = scy ? r1 : r0;
         zm = c;
         c = zp;
-        if (pair_in && z + kFD < ze) {
-            if (XH && hrow && z + kFD + 1 < ze) {
-                double *d = reinterpret_cast<double *>(&sT[slot][tid]);
-                cp_async8f(d + (hcy ? 1 : 0), hrow + z + kFD + 1);
-                cp_async8f(d + (hcy ? 0 : 1), T + i + (kFD + 1) * sxy + (hcy ? 0 : 1));
-            } else {
-                cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
+        if (XH) {
+            const int k = z - zs;
+            if (sl >= 0) {   // plane z's send-layer value -> lane k % 32
+                const double v = __shfl_sync(0xffffffffu, shi ? r1 : r0, slane);
+                if (lane == (k & 31)) {
+                    if (k < 32) s0 = v; else s1 = v;
+                }
             }
+            if (hl >= 0) {   // plane z+1's halo value -> the halo lane (c now holds plane z+1)
+                const int k1 = k + 1;
+                const double v = __shfl_sync(0xffffffffu, k1 < 32 ? h0 : h1, k1 & 31);
+                if (hrow && lane == hlane && z + 1 < ze) {
+                    if (hhi) c.y = v; else c.x = v;
+                }
+            }
+        }
+        if (pair_in && z + kFD < ze) {
+            cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
         }
         cp_commit();
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
+    if (XH && sl >= 0 && sdst) {   // my two planes of the row's send layer, z-contiguous
+        if (zs + lane < ze) sdst[zs + lane] = s0;
+        if (zs + 32 + lane < ze) sdst[zs + 32 + lane] = s1;
+    }
 }
 
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b);
@@ -233,7 +244,6 @@ template <bool MR>
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
-    __shared__ double sXs[kFTY][kFKC];   // my x send-layer cell of each row, plane by plane (this sweep)
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
     const int rank = blockIdx.x / F.per_rank;
@@ -246,7 +256,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     b -= F.nrim + F.nfwd;
     const int tx = b % F.xtiles, rr = b / F.xtiles, ty = rr % F.ytiles, pos = rr / F.ytiles;
     const int2 zr = F.zr[pos];
-    const int zs = zr.x, ze = zr.y, nz = ze - zs;
+    const int zs = zr.x, ze = zr.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sx = F.s[0], sy = F.s[1];
     const int ty0 = 1 + ty * kFTY;
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const int yhi = min(ty0 + kFTY, sy - 1);
 
     // the x send layer in this tile (rs: 0 = my upper layer -> upper neighbour's halo 0, 1 = layer 1 ->
-    // lower neighbour's halo s-1): its value is captured into sXs during the sweep and leaves
+    // lower neighbour's halo s-1): its value is gathered by shuffles during the sweep and leaves
     // z-contiguous after it
     int xrs = -1;
 #pragma unroll
@@ -300,15 +310,12 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         yzface = yzface || (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi);
         yzface = yzface || (R.face[2][rs].active && F.zchunk[rs] == pos);
     }
-    if (hl >= 0 || xsl >= 0) {
-        const bool hlane = hl >= 0 && (hl >> 1) == lane && rowv;
-        const bool slane = xsl >= 0 && (xsl >> 1) == lane && rowv;
-        const double *hrow = hlane ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
-        fused_sweep<true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, hrow, hl & 1,
-                          slane ? sXs[warp] : nullptr, xsl & 1);
+    if (hl >= 0 || xsl >= 0) {   // (the row pointers are NULL on rows past the grid: warp-uniform)
+        const double *hrow = hl >= 0 && rowv ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
+        double *sdst = xsl >= 0 && rowv ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;
+        fused_sweep<true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, hl, hrow, xsl, sdst);
     } else {
-        fused_sweep<false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, nullptr, false, nullptr,
-                           false);
+        fused_sweep<false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, -1, nullptr, -1, nullptr);
     }
 
 // ---- faces held by this tile -> the receivers
@@ -320,13 +327,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     }
     if (!did) return;   // CTA-uniform
     double *__restrict__ T2 = R.T2;
-    __syncthreads();    // the CTA's T2 stores (and sXs) are visible to the CTA
-    if (xrs >= 0) {     // x face: my rows' captured layer cells, z-contiguous, into the staging
-        if (rowv) {
-            double *dst = R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, zs);
-            for (int zz = lane; zz < nz; zz += 32) dst[zz] = sXs[warp][zz];
-        }
-    }
+    __syncthreads();    // the CTA's T2 stores (and x staging stores) are visible to the CTA
 #pragma unroll
     for (int rs = 0; rs < 2; ++rs) {
         // y face: the layer row over the chunk's planes -> the receiver's halo row; the warps take planes
