@@ -240,8 +240,26 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
 // One launch over all tiles of all hosted ranks, the 1-GPU loop unchanged.  Block b of rank r:
 // [0, nrim) rim, [nrim, nrim+nfwd) forwarders (last step of a run only), then the stencil tiles.
 // MR: more than one hosted rank (the rank's parameters are indexed at run time).
+#ifndef FUSED_TRACE
+#define FUSED_TRACE 0   // diagnostics build only: per-block %globaltimer stamps into g_fused_trace
+#endif
+#if FUSED_TRACE
+__device__ unsigned long long g_fused_trace[65536 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ unsigned long long g_trace_epoch;
+#define TRACE_AT(k) \
+    if (threadIdx.x == 0 && blockIdx.x < 65536 && F.epoch == g_trace_epoch) g_fused_trace[blockIdx.x * 4 + (k)] = gtimer()
+#else
+#define TRACE_AT(k)
+#endif
+
 template <bool MR>
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
+    TRACE_AT(0);
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
@@ -251,6 +269,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const FusedRank &R = F.r[rank];
     if (b < F.nrim + F.nfwd) {   // CTA-uniform
         fused_extra(F, R, b);
+        TRACE_AT(3);
         return;
     }
     b -= F.nrim + F.nfwd;
@@ -325,7 +344,11 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         if (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi) did |= 4u << rs;
         if (R.face[2][rs].active && F.zchunk[rs] == pos) did |= 16u << rs;
     }
-    if (!did) return;   // CTA-uniform
+    TRACE_AT(1);
+    if (!did) {   // CTA-uniform
+        TRACE_AT(3);
+        return;
+    }
     double *__restrict__ T2 = R.T2;
     __syncthreads();    // the CTA's T2 stores (and x staging stores) are visible to the CTA
 #pragma unroll
@@ -381,6 +404,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         for (int f = 0; f < 6; ++f)
             if (did & (1u << f)) contribute(F, R, f >> 1, f & 1, f < 4 ? pos : 0);
     }
+    TRACE_AT(3);
 }
 
 // forward my fresh halo line (axis b, side) x (face a, rs) over the third axis range [lo, hi)
@@ -721,6 +745,27 @@ static const std::vector<double *> &peer_arrays(igg_grid *g, double *T2) {
 }
 
 const std::vector<double *> &peer_arrays_pub(igg_grid *g, double *arr) { return peer_arrays(g, arr); }
+
+}  // namespace igg
+
+#if FUSED_TRACE
+// diagnostics build only: the per-block stamps (start, sweep end, -, end; ns) of the last fused launch
+// record the launch of epoch (current + offset)
+IGG_API igg_status igg_debug_trace_epoch(igg_grid *g, long long offset) {
+    IGG_TRY
+    const unsigned long long e = g->epoch + offset;
+    IGG_CUDA(cudaMemcpyToSymbol(igg::g_trace_epoch, &e, sizeof e));
+    IGG_CATCH
+}
+IGG_API igg_status igg_debug_fused_trace(unsigned long long *host, int nblocks) {
+    IGG_TRY
+    IGG_CUDA(cudaDeviceSynchronize());
+    IGG_CUDA(cudaMemcpyFromSymbol(host, igg::g_fused_trace, sizeof(unsigned long long) * 4 * std::min(nblocks, 65536)));
+    IGG_CATCH
+}
+#endif
+
+namespace igg {
 
 // One step of every hosted rank: T2[lr] = step!(T[lr]) plus the faces into the receivers.
 // wait_prev: the previous step of the same run was fused (its faces are awaited tile by tile);

@@ -1,7 +1,9 @@
-"""update_halo bandwidth sweep (config B:11 analogue): one periodic field of n^3
-per GPU, dims 2x1x1 / 2x2x1 (/2x2x2), NCCL vs P2P; time per call (max over
-ranks, CUDA events) and GB/s of halo payload each GPU sends per call."""
-import json, os, sys
+"""update_halo bandwidth sweep (config B:11 analogue): one periodic field of n^3 per GPU, dims by world
+size (2: 2x1x1, 4: 2x2x1, 8: 2x2x2), transports: NCCL (per-axis grouped send/recv), P2P per-axis
+pack/flag/unpack, and P2P 26-neighbour single kernel (default).  20 samples of 100 calls each (median),
+CUDA events on the calling stream, max over ranks; GB/s per GPU = bytes this GPU sends to OTHER GPUs per
+call / t; 'payload' also counts the faces a rank stores into itself (periodic self-wrap axes)."""
+import json, os, statistics, sys
 sys.path.insert(0, ".")
 import torch
 import torch.distributed as dist
@@ -12,31 +14,38 @@ torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 world = dist.get_world_size()
 dims = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}[world]
+sizes = [int(x) for x in os.environ.get("HALO_SIZES", "64,96,128,192,256,384,512,640,768").split(",")]
 out = []
-variants = [("nccl", 0, 1), ("p2p", 0, 1), ("p2p", 1, 1), ("p2p", 1, 0)]   # (path, caller stream, coop)
-for path, on_caller, coop in variants:
-    for n in (64, 96, 128, 192, 256, 384, 512, 640, 768):
+variants = [("nccl", 0), ("p2p", 0), ("p2p", 1)]   # (path, halo26)
+for path, h26 in variants:
+    for n in sizes:
         g = P.init_global_grid(n, n, n, dims=dims, periods=(1, 1, 1), path=path, device=local)
-        g.set_option(P.igg.OPT_HALO_STREAM, on_caller)
-        g.set_option(P.igg.OPT_COOP_HALO, coop)
+        g.set_option(P.OPT_HALO26, h26)
+        g.set_option(P.OPT_HALO_STREAM, 1)   # on the caller's stream (no event joins)
         A = torch.rand((n, n, n), dtype=torch.float64, device="cuda")
         for _ in range(10):
             g.update_halo(A)
         torch.cuda.synchronize(); dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(40_000_000)   # keep the GPU busy while the host enqueues: GPU time only
-        e0.record()
-        for _ in range(100):
-            g.update_halo(A)
-        e1.record()
-        torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / 100], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        xs = []
+        for rep in range(20):
+            dist.barrier(); torch.cuda.synchronize()
+            torch.cuda._sleep(20_000_000)   # keep the GPU busy while the host enqueues: GPU time only
+            e0.record()
+            for _ in range(100):
+                g.update_halo(A)
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / 100], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            xs.append(float(t.item()))
+        g.check()
+        ms = statistics.median(xs)
         remote_axes = sum(1 for d in dims if d > 1)
-        sent = remote_axes * 2 * n * n * 8   # bytes this GPU sends to other GPUs per call
-        out.append({"path": path, "caller_stream": on_caller, "coop": coop, "n": n, "dims": dims, "ms_per_call": ms, "remote_bytes": sent,
-                    "GBps_per_gpu": sent / (ms * 1e-3) / 1e9})
+        sent = remote_axes * 2 * n * n * 8   # face bytes this GPU sends to other GPUs per call
+        out.append({"path": path, "halo26": h26, "n": n, "dims": dims, "ms_per_call_median": ms,
+                    "ms_min": min(xs), "remote_bytes": sent, "GBps_per_gpu": sent / (ms * 1e-3) / 1e9,
+                    "payload_GBps": 6 * n * n * 8 / (ms * 1e-3) / 1e9})
         g.finalize()
         del A
         torch.cuda.empty_cache()
