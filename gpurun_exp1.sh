@@ -1,9 +1,10 @@
-cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp4}
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp5}
 timeout 900 python -m pytest tests -q -m gpu -x -k "virtual_p2p or fused" > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
-for lib in paper_2211_15716_b200/libigg.so; do
 for per in 0,0,0 1,0,0 0,1,0 0,0,1 1,1,1; do
-  echo "== $lib $per" >> gpurun_out/${T}.txt
-  IGG_LIBRARY=$lib timeout 300 python bench.py --periodic $per --no-e2e --no-cpu --no-stats --steps 100 2>&1 | tail -1 | python -c "
+  echo "== $per" >> gpurun_out/${T}.txt
+  timeout 300 python bench.py --periodic $per --no-e2e --no-cpu --no-stats --steps 100 2>&1 | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['exposed_halo'], d['roofline']['avg_launch_ms'])" >> gpurun_out/${T}.txt 2>&1
-done; done
+done
+mkdir -p gpurun_out/$T; cd gpurun_out/$T && ln -s ../../scripts . && ln -s ../../ablation . && ln -s ../../paper_2211_15716_b200 . && ln -s ../../synthetic_inputs.py . ; cd $GRAFT_REPO_ROOT
+timeout 600 python scripts/fused_trace.py > gpurun_out/${T}_trace.txt 2>&1; mkdir -p gpurun_out/${T}_npz; mv gpurun_out/trace_*.npz gpurun_out/${T}_npz/
 echo done

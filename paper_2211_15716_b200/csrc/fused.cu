@@ -133,23 +133,26 @@ constexpr int kFKC = 64;   // longest z-chunk
 }  // namespace
 
 // The z sweep of one tile: cp.async ring of kFD planes of T and Ci, x neighbours by shuffle, z by a
-// register queue.  XH (CTA-uniform: the tile holds an x halo and/or an x send column), both handled with
-// warp shuffles so the loop keeps its shape (no extra memory instructions per plane):
-//  * hl >= 0: cell hl (tile index) is the x halo column; its previous-epoch values of this chunk's planes
-//    (hrow[z], z-contiguous in the staging buffer) are loaded once, two planes per lane, and each plane's
-//    value is shuffled to the lane holding the cell, which substitutes it for T's (never read or written)
-//    halo value;
-//  * sl >= 0: cell sl is the x send layer; each plane's result is shuffled from the lane computing it to
-//    lane (z - zs) % 32 (two planes per lane), and after the sweep every lane stores its two values
-//    z-contiguous into the receiver's staging row sdst[z] (whole sectors over NVLink).
+// register queue.  The y and z faces leave from inside the sweep: the warp whose row is a y send layer
+// stores its results also into the receiver's halo row (ydst), and on the plane that is a z send layer
+// every warp stores its row also into the receiver's halo plane (zdst) -- the same 16-B stores as T2's,
+// one extra per plane for those warps / that plane, no re-read after the sweep.
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
-template <bool XH>
+__device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r0, double r1) {
+    if (w0 && w1) {
+        *reinterpret_cast<double2 *>(d) = make_double2(r0, r1);
+    } else {
+        if (w0) d[0] = r0;
+        if (w1) d[1] = r1;
+    }
+}
+
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
                                             double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
-                                            long long i, bool pair_in, bool w0, bool w1, bool cs, int hl,
-                                            const double *hrow, int sl, double *sdst) {
+                                            long long i, bool pair_in, bool w0, bool w1, bool cs, double *ydst,
+                                            int zlay, double *zdst) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
@@ -165,18 +168,8 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
-    double h0 = 0.0, h1 = 0.0, s0 = 0.0, s1 = 0.0;
-    const int hlane = hl >> 1, slane = sl >> 1;
-    const bool hhi = hl & 1, shi = sl & 1;
-    if (XH && hl >= 0) {   // this chunk's staged halo values, planes zs+lane and zs+32+lane
-        if (hrow && zs + lane < ze) h0 = __ldcg(hrow + zs + lane);
-        if (hrow && zs + 32 + lane < ze) h1 = __ldcg(hrow + zs + 32 + lane);
-        const double v = __shfl_sync(0xffffffffu, h0, 0);
-        if (hrow && lane == hlane) {
-            if (hhi) c.y = v; else c.x = v;
-        }
-    }
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
+    const long long yoff = ydst ? i : 0;   // (ydst: my row's cell of plane z at ydst + i, i advancing)
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
@@ -194,33 +187,14 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (hi_edge) xp = __ldg(T + i + 2);
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (w0 && w1) {
-            if (FUSED_STCS && cs)   // (CTA-uniform) a tile without faces: T2 is not re-read this step
-                __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
-            else
-                *reinterpret_cast<double2 *>(T2 + i) = make_double2(r0, r1);
-        } else {
-            if (w0) T2[i] = r0;
-            if (w1) T2[i + 1] = r1;
-        }
+        if (FUSED_STCS && cs && w0 && w1)   // (CTA-uniform cs) a tile without faces: T2 is not re-read
+            __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+        else
+            store_pair(T2 + i, w0, w1, r0, r1);
+        if (ydst) store_pair(ydst + (i - yoff), w0, w1, r0, r1);   // (warp-uniform) y face row
+        if (z == zlay) store_pair(zdst + (i - (long long)z * sxy), w0, w1, r0, r1);   // z face plane
         zm = c;
         c = zp;
-        if (XH) {
-            const int k = z - zs;
-            if (sl >= 0) {   // plane z's send-layer value -> lane k % 32
-                const double v = __shfl_sync(0xffffffffu, shi ? r1 : r0, slane);
-                if (lane == (k & 31)) {
-                    if (k < 32) s0 = v; else s1 = v;
-                }
-            }
-            if (hl >= 0) {   // plane z+1's halo value -> the halo lane (c now holds plane z+1)
-                const int k1 = k + 1;
-                const double v = __shfl_sync(0xffffffffu, k1 < 32 ? h0 : h1, k1 & 31);
-                if (hrow && lane == hlane && z + 1 < ze) {
-                    if (hhi) c.y = v; else c.x = v;
-                }
-            }
-        }
         if (pair_in && z + kFD < ze) {
             cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
@@ -229,34 +203,30 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
-    if (XH && sl >= 0 && sdst) {   // my two planes of the row's send layer, z-contiguous
-        if (zs + lane < ze) sdst[zs + lane] = s0;
-        if (zs + 32 + lane < ze) sdst[zs + 32 + lane] = s1;
-    }
 }
 
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b);
 
-// One launch over all tiles of all hosted ranks, the 1-GPU loop unchanged.  Block b of rank r:
-// [0, nrim) rim, [nrim, nrim+nfwd) forwarders (last step of a run only), then the stencil tiles.
-// MR: more than one hosted rank (the rank's parameters are indexed at run time).
 #ifndef FUSED_TRACE
 #define FUSED_TRACE 0   // diagnostics build only: per-block %globaltimer stamps into g_fused_trace
 #endif
 #if FUSED_TRACE
 __device__ unsigned long long g_fused_trace[65536 * 4];
+__device__ unsigned long long g_trace_epoch;
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ unsigned long long g_trace_epoch;
 #define TRACE_AT(k) \
     if (threadIdx.x == 0 && blockIdx.x < 65536 && F.epoch == g_trace_epoch) g_fused_trace[blockIdx.x * 4 + (k)] = gtimer()
 #else
 #define TRACE_AT(k)
 #endif
 
+// One launch over all tiles of all hosted ranks, the 1-GPU loop unchanged.  Block b of rank r:
+// [0, nrim) rim, [nrim, nrim+nfwd) forwarders (last step of a run only), then the stencil tiles.
+// MR: more than one hosted rank (the rank's parameters are indexed at run time).
 template <bool MR>
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     TRACE_AT(0);
@@ -289,29 +259,32 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const int xlo = max(tx * 64, 1), xhi = min(tx * 64 + 64, sx - 1);   // inner x of this tile
     const int yhi = min(ty0 + kFTY, sy - 1);
 
-    // the x send layer in this tile (rs: 0 = my upper layer -> upper neighbour's halo 0, 1 = layer 1 ->
-    // lower neighbour's halo s-1): its value is gathered by shuffles during the sweep and leaves
-    // z-contiguous after it
+    // faces this tile holds (bit f = 2a + rs; rs 0: my upper send layer -> the upper neighbour's halo 0,
+    // rs 1: my layer 1 -> the lower neighbour's halo s-1)
+    unsigned did = 0u;
     int xrs = -1;
 #pragma unroll
-    for (int rs = 0; rs < 2; ++rs)
-        if (R.face[0][rs].active && R.face[0][rs].layer >= xlo && R.face[0][rs].layer < xhi) xrs = rs;
-    const int xsl = xrs >= 0 ? R.face[0][xrs].layer - tx * 64 : -1;   // its cell index in the tile
-    // the x halo column this tile reads (first x-tile: x = 0, last: x = sx-1): from the staging buffer
-    // when the previous step of the run stored it there (first step of a run: T holds it)
-    int hside = -1;
-    if (F.wait_prev) {
-        if (tx == 0 && R.halo[0][0].active) hside = 0;
-        if (tx == F.xtiles - 1 && R.halo[0][1].active) hside = 1;
+    for (int rs = 0; rs < 2; ++rs) {
+        if (R.face[0][rs].active && R.face[0][rs].layer >= xlo && R.face[0][rs].layer < xhi) {
+            did |= 1u << rs;
+            xrs = rs;
+        }
+        if (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi) did |= 4u << rs;
+        if (R.face[2][rs].active && F.zchunk[rs] == pos) did |= 16u << rs;
     }
-    const int hl = hside < 0 ? -1 : (hside == 0 ? 0 : sx - 1 - tx * 64);   // its cell index in the tile
+    // the x halo column beside the x send layer: staged by the neighbour in the previous step of the run
+    // (first step of a run: T holds it)
+    const int hside = xrs < 0 ? -1 : (xrs == 0 ? 1 : 0);   // send layer s-2 sits beside halo s-1, 1 beside 0
+    const bool hstaged = xrs >= 0 && F.wait_prev && R.halo[0][hside].active;
 
     if (F.wait_prev) {   // CTA-uniform: this step's halo cells are the previous epoch's faces
+        const bool xh0 = R.halo[0][0].active && tx == 0, xh1 = R.halo[0][1].active && tx == F.xtiles - 1;
         const bool yl = R.halo[1][0].active && ty == 0, yu = R.halo[1][1].active && ty == F.ytiles - 1;
         const bool zl = R.halo[2][0].active && zs == 1, zu = R.halo[2][1].active && ze == F.s[2] - 1;
         if (tid == 0) {
             const unsigned long long prev = F.epoch - 1;
-            if (hside >= 0) spin_geq(F, R.halo[0][hside].flag + pos, prev);
+            if (xh0) spin_geq(F, R.halo[0][0].flag + pos, prev);
+            if (xh1) spin_geq(F, R.halo[0][1].flag + pos, prev);
             if (yl) spin_geq(F, R.halo[1][0].flag + pos, prev);
             if (yu) spin_geq(F, R.halo[1][1].flag + pos, prev);
             if (zl) spin_geq(F, R.halo[2][0].flag, prev);
@@ -320,79 +293,69 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         __syncthreads();
     }
 
-    // ---- the z sweep; tiles that hold an x halo or x send column take the variant that redirects /
-    // captures it (CTA-uniform; the plain variant keeps the 1-GPU kernel's register budget)
-    const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
-    bool yzface = false;   // the tile re-reads its T2 for a y or z face after the sweep
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        yzface = yzface || (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi);
-        yzface = yzface || (R.face[2][rs].active && F.zchunk[rs] == pos);
-    }
-    if (hl >= 0 || xsl >= 0) {   // (the row pointers are NULL on rows past the grid: warp-uniform)
-        const double *hrow = hl >= 0 && rowv ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
-        double *sdst = xsl >= 0 && rowv ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;
-        fused_sweep<true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, hl, hrow, xsl, sdst);
-    } else {
-        fused_sweep<false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, !yzface, -1, nullptr, -1, nullptr);
-    }
-
-// ---- faces held by this tile -> the receivers
-    unsigned did = xrs >= 0 ? 1u << xrs : 0u;   // bit f: this tile holds part of face f = 2a + rs
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        if (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi) did |= 4u << rs;
-        if (R.face[2][rs].active && F.zchunk[rs] == pos) did |= 16u << rs;
+    // ---- the z sweep, with the y / z faces stored from inside it
+    {
+        double *ydst = nullptr;
+        if (did & 12u) {
+            const int rs = (did & 4u) ? 0 : 1;
+            if (rowv && y == R.face[1][rs].layer)   // (warp-uniform) my row is the y send layer
+                ydst = R.face[1][rs].dst + (long long)(rs == 0 ? 0 : sy - 1) * sx - (long long)y * sx;
+        }
+        int zlay = -1;
+        double *zdst = nullptr;
+        if (did & 48u) {
+            const int rs = (did & 16u) ? 0 : 1;
+            zlay = R.face[2][rs].layer;
+            zdst = R.face[2][rs].dst + (long long)(rs == 0 ? 0 : F.s[2] - 1) * sxy;
+        }
+        const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
+        fused_sweep(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, did == 0u, ydst, zlay, zdst);
     }
     TRACE_AT(1);
     if (!did) {   // CTA-uniform
         TRACE_AT(3);
         return;
     }
-    double *__restrict__ T2 = R.T2;
-    __syncthreads();    // the CTA's T2 stores (and x staging stores) are visible to the CTA
-#pragma unroll
-    for (int rs = 0; rs < 2; ++rs) {
-        // y face: the layer row over the chunk's planes -> the receiver's halo row; the warps take planes
-        // round-robin, lanes the row segment as 16-B pairs (the cells were just written: L2 hits)
-        const FusedFace &fy = R.face[1][rs];
-        if (did & (4u << rs)) {
-            const int hy = rs == 0 ? 0 : sy - 1;
-            constexpr int U = 4;
-            for (int zb = zs + warp; zb < ze; zb += kFTY * U) {
-                double2 v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int zz = zb + kFTY * u;
-                    v[u] = (zz < ze && p < sx)
-                               ? *reinterpret_cast<const double2 *>(T2 + (long long)zz * sxy + (long long)fy.layer * sx + p)
-                               : make_double2(0.0, 0.0);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int zz = zb + kFTY * u;
-                    if (zz >= ze) continue;
-                    double *d = fy.dst + (long long)zz * sxy + (long long)hy * sx + p;
-                    if (p >= xlo && p + 1 < xhi) {
-                        *reinterpret_cast<double2 *>(d) = v[u];
-                    } else {
-                        if (p >= xlo && p < xhi) d[0] = v[u].x;
-                        if (p + 1 >= xlo && p + 1 < xhi) d[1] = v[u].y;
-                    }
-                }
+    __syncthreads();   // the CTA's T2 stores are visible to the CTA
+    if (xrs >= 0) {
+        // ---- the x send layer xf (beside the x halo column): the sweep took T's halo value; recompute the
+        // column with the neighbour's staged values (lanes along z, loads mostly L2 hits of the rows and
+        // planes just streamed), overwrite its T2 cells and store them z-contiguous into the receiver's
+        // staging row.  Same operations in the same order as the sweep: bit-identical cells.
+        const int xf = R.face[0][xrs].layer, xh = hside == 0 ? 0 : sx - 1;
+        const double *__restrict__ T = R.T;
+        const double *__restrict__ Ci = R.Ci;
+        double *__restrict__ T2 = R.T2;
+        if (rowv) {
+            const double *hrow = R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0);
+            double *sdst = R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0);
+            for (int z = zs + lane; z < ze; z += 32) {
+                const long long c0 = (long long)z * sxy + (long long)y * sx + xf;
+                const double c = __ldcg(T + c0);
+                const double h = hstaged ? __ldcg(hrow + z) : __ldcg(T + c0 + (xh - xf));
+                const double o = __ldcg(T + c0 - (xh - xf));   // the other x neighbour
+                const double xm = xh < xf ? h : o, xp = xh < xf ? o : h;
+                const double r = cell(c, xm, xp, __ldcg(T + c0 - sx), __ldcg(T + c0 + sx), __ldcg(T + c0 - sxy),
+                                      __ldcg(T + c0 + sxy), __ldcg(Ci + c0), F.k);
+                T2[c0] = r;
+                sdst[z] = r;
             }
         }
-        // z face: my row of the layer plane -> the receiver's z halo plane
-        const FusedFace &fz = R.face[2][rs];
-        if ((did & (16u << rs)) && rowv && p < sx) {
-            const int hz = rs == 0 ? 0 : F.s[2] - 1;
-            const double2 v = *reinterpret_cast<const double2 *>(T2 + (long long)fz.layer * sxy + (long long)y * sx + p);
-            double *d = fz.dst + (long long)hz * sxy + (long long)y * sx + p;
-            if (p >= xlo && p + 1 < xhi) {
-                *reinterpret_cast<double2 *>(d) = v;
-            } else {
-                if (p >= xlo && p < xhi) d[0] = v.x;
-                if (p + 1 >= xlo && p + 1 < xhi) d[1] = v.y;
+    }
+    // (the y / z face rows of the x send column hold the sweep's value there; the fix-up above corrects
+    // T2 but the receiver's y/z halo copies of that cell are written below, after the correction)
+    if ((did & 60u) && xrs >= 0 && rowv) {   // (each lane re-sends cells it recomputed itself)
+        const int xf = R.face[0][xrs].layer;
+        for (int rs = 0; rs < 2; ++rs) {
+            if ((did & (4u << rs)) && y == R.face[1][rs].layer)
+                for (int z = zs + lane; z < ze; z += 32) {
+                    const long long c0 = (long long)z * sxy + (long long)y * sx + xf;
+                    R.face[1][rs].dst[c0 + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx] = R.T2[c0];
+                }
+            const int zl = R.face[2][rs].layer;
+            if ((did & (16u << rs)) && zl >= zs && zl < ze && ((zl - zs) & 31) == lane) {
+                const long long c0 = (long long)zl * sxy + (long long)y * sx + xf;
+                R.face[2][rs].dst[c0 + (long long)((rs == 0 ? 0 : F.s[2] - 1) - zl) * sxy] = R.T2[c0];
             }
         }
     }

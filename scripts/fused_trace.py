@@ -43,6 +43,7 @@ for per in [(1, 0, 0), (0, 1, 0), (0, 0, 1)]:
         xt = 8
         idx = np.nonzero(used)[0]
         tx = idx % xt
+        np.savez_compressed(f"gpurun_out/trace_{''.join(map(str, per))}_{skip}.npz", a=a, idx=idx)
         rec = {"periods": per, "skip_comm": skip, "blocks": int(nbk), "span_us": float(en.max() / 1e3),
                "median_block_us": float(np.median(dur) / 1e3),
                "tx0_us": float(np.median(dur[tx == 0]) / 1e3), "tx7_us": float(np.median(dur[tx == 7]) / 1e3),
