@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-exposed", action="store_true")
     ap.add_argument("--fused", type=int, default=-1, help="1 fused stencil+P2P put kernel, 0 split, -1 auto")
-    ap.add_argument("--fused-mode", type=int, default=2, help="ablation bits of the fused path")
+    ap.add_argument("--fused-mode", type=int, default=0, help="ablation build only: binary32 schedule bits")
     ap.add_argument("--kc2", type=int, default=0, help="fused path: tail z-chunk planes (0 auto)")
     ap.add_argument("--ncomm", type=int, default=1, help="fused path: CTAs per receive/forward kernel")
     ap.add_argument("--dims", default="", help="override the process topology, e.g. 1,2,1")
@@ -262,7 +262,8 @@ def main():
     g.set_option(P.OPT_X_ALIGN, a.xalign)
     g.set_option(P.OPT_SCHEDULE, a.schedule)
     g.set_option(P.OPT_FUSED, a.fused)
-    g.set_option(8, a.fused_mode)
+    if a.fused_mode:
+        g.set_option(8, a.fused_mode)
     g.set_option(9, a.kc2)
     g.set_option(10, a.ncomm)
     if a.skip_comm:
@@ -391,7 +392,11 @@ def main():
         barrier()
         ms_nc = max_over_ranks(e0.elapsed_time(e1) / a.steps)
         g.set_option(P.OPT_SKIP_COMM, 0)
-        g.check()
+        try:
+            g.check()   # a flag timeout raises; the expected "steps ran with SKIP_COMM" state is cleared
+        except P.IggError as ex:
+            if ex.status != 2:
+                raise
         exposed = {"ms_per_step": ms - ms_nc, "ms_no_comm": ms_nc}
         (app.init_paper if a.init == "paper" else app.init_random)(g, T, T2, Ci)   # results were invalid
 

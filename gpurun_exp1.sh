@@ -5,6 +5,5 @@ for per in 0,0,0 1,0,0 0,1,0 0,0,1 1,1,1; do
   timeout 300 python bench.py --periodic $per --no-e2e --no-cpu --no-stats --steps 100 2>&1 | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['exposed_halo'], d['roofline']['avg_launch_ms'])" >> gpurun_out/${T}.txt 2>&1
 done
-mkdir -p gpurun_out/$T; cd gpurun_out/$T && ln -s ../../scripts . && ln -s ../../ablation . && ln -s ../../paper_2211_15716_b200 . && ln -s ../../synthetic_inputs.py . ; cd $GRAFT_REPO_ROOT
 timeout 600 python scripts/fused_trace.py > gpurun_out/${T}_trace.txt 2>&1; mkdir -p gpurun_out/${T}_npz; mv gpurun_out/trace_*.npz gpurun_out/${T}_npz/
 echo done

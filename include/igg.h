@@ -295,9 +295,14 @@ igg_status igg_gather(igg_grid *grid, const igg_field *fields, int root_proc, do
 
 /* ------------------------------------------------------------------ control */
 enum {
-    IGG_OPT_SKIP_COMM = 1,       /* timing-only: skip pack/exchange/unpack (results INVALID) */
+    IGG_OPT_SKIP_COMM = 1,       /* timing only (SURVEY.md 8(d) "comm disabled"): the exchange is skipped
+                                    so exposed halo time = t(overlap) - t(overlap, comm disabled) can be
+                                    measured; halo results are INVALID while it is on, and igg_check
+                                    reports IGG_E_STATE for the steps taken with it */
     IGG_OPT_SPIN_TIMEOUT_MS = 2, /* P2P flag wait bound (default 20000) */
-    IGG_OPT_STENCIL_KERNEL = 3,  /* 0 = auto, 1 = generic region kernel only (ablation) */
+    IGG_OPT_STENCIL_KERNEL = 3,  /* 0 = auto, 1 = the generic scalar region kernel for every region (a
+                                    reference kernel; same cells); other values: the tuning variants of the
+                                    ablation build only (IGG_E_UNSUPPORTED in the product library) */
     IGG_OPT_PROFILE = 4,         /* 1 = bracket every main stencil launch (the full-region or
                                     inner-box kernel) with CUDA events on its own stream;
                                     2 = also record the overlap timeline (igg_profile_timeline) */
@@ -309,23 +314,11 @@ enum {
                                     send layers straight into the neighbours' halos over NVLink, chunk
                                     by chunk; 0 = boundary/inner kernels + pack/exchange/unpack;
                                     -1 (default) = fused whenever eligible */
-    IGG_OPT_FUSED_MODE = 8,      /* ablation bits of the fused path: 1 = the x send layer is stored to the
-                                    neighbour from inside the z sweep, 2 = stencil on the low-priority inner
-                                    stream (default), 4/8/16 = timing experiments (INVALID halos: no
-                                    receive side / no face stores / stores to own T2), 32 = no tail
-                                    re-order table, 64 = visit the upper z-face chunk second,
-                                    128 = legacy multi-stream schedule (rim / receive kernels on
-                                    comm streams joined by events) instead of the pipelined one,
-                                    256 = x faces stored straight into the receiver's T2 column
-                                    instead of its staging buffer, 512 = no forwarders (timing,
-                                    INVALID edge cells), 1024 = single forwarding steps stay on the
-                                    pipelined schedule, 2048 = dedicated x sender/receiver blocks
-                                    move the staged x columns (ablation, measured slower) */
-    IGG_OPT_FUSED_KC2 = 9,       /* planes per tail z-chunk of the fused stencil (0 = auto: 8; 16 on the
-                                    legacy schedule with more than one exchanging axis) */
-    IGG_OPT_FUSED_COMM_CTAS = 10,/* CTAs of each fused receive/forward kernel (default 1) */
-    IGG_OPT_COOP_HALO = 11,      /* 1: update_halo without NCCL messages runs as one cooperative kernel
-                                    (grid barriers between axes); 0 (default, measured faster): per-axis launches */
+    IGG_OPT_FUSED_MODE = 8,      /* ablation build only (ablation/libigg_ablation.so): binary32 schedule bits
+                                    8192 / 16384; the product library answers IGG_E_UNSUPPORTED */
+    IGG_OPT_FUSED_KC2 = 9,       /* planes per short (end) z-chunk of the fused stencil (0 = auto: 8) */
+    IGG_OPT_FUSED_COMM_CTAS = 10,/* forwarder blocks per rank in the last step of a fused run (default 1) */
+    /* 11: retired (the cooperative per-axis update_halo, superseded by IGG_OPT_HALO26) */
     IGG_OPT_HALO_STREAM = 12,    /* 0 (default): update_halo runs on the library's high-priority comm
                                     stream joined to the caller's; 1: directly on the caller's stream */
     IGG_OPT_LOCAL_P2P = 13,      /* 1: update_halo runs the dimension-sequential P2P protocol (per axis: pack

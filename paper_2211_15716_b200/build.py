@@ -43,6 +43,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, extra=())
     if out is None and not force and not needs_build():
         return OUT
     target = out or OUT
+    os.makedirs(os.path.dirname(os.path.abspath(target)), exist_ok=True)
     nr = nccl_root()
     inc = os.path.join(nr, "include")
     lib = os.path.join(nr, "lib")

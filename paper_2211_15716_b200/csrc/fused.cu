@@ -149,6 +149,7 @@ __device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r
     }
 }
 
+template <bool FACES>   // FACES: the tile stores a y or z face from the sweep (CTA-uniform)
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
                                             double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
                                             long long i, bool pair_in, bool w0, bool w1, bool cs, double *ydst,
@@ -169,7 +170,6 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
-    const long long yoff = ydst ? i : 0;   // (ydst: my row's cell of plane z at ydst + i, i advancing)
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
@@ -187,12 +187,14 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (hi_edge) xp = __ldg(T + i + 2);
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (FUSED_STCS && cs && w0 && w1)   // (CTA-uniform cs) a tile without faces: T2 is not re-read
+        if (!FACES && FUSED_STCS && cs && w0 && w1)   // a tile without faces: T2 is not re-read
             __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
         else
             store_pair(T2 + i, w0, w1, r0, r1);
-        if (ydst) store_pair(ydst + (i - yoff), w0, w1, r0, r1);   // (warp-uniform) y face row
-        if (z == zlay) store_pair(zdst + (i - (long long)z * sxy), w0, w1, r0, r1);   // z face plane
+        if (FACES) {
+            if (ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
+            if (z == zlay) store_pair(zdst + (i - (long long)z * sxy), w0, w1, r0, r1);   // z face plane
+        }
         zm = c;
         c = zp;
         if (pair_in && z + kFD < ze) {
@@ -298,8 +300,9 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         double *ydst = nullptr;
         if (did & 12u) {
             const int rs = (did & 4u) ? 0 : 1;
-            if (rowv && y == R.face[1][rs].layer)   // (warp-uniform) my row is the y send layer
-                ydst = R.face[1][rs].dst + (long long)(rs == 0 ? 0 : sy - 1) * sx - (long long)y * sx;
+            if (rowv && y == R.face[1][rs].layer)   // (warp-uniform) my row is the y send layer: cell i of
+                                                    // my row lands at ydst + i in the receiver's halo row
+                ydst = R.face[1][rs].dst + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx;
         }
         int zlay = -1;
         double *zdst = nullptr;
@@ -309,7 +312,10 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             zdst = R.face[2][rs].dst + (long long)(rs == 0 ? 0 : F.s[2] - 1) * sxy;
         }
         const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
-        fused_sweep(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, did == 0u, ydst, zlay, zdst);
+        if (did & 60u)
+            fused_sweep<true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, ydst, zlay, zdst);
+        else
+            fused_sweep<false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, did == 0u, nullptr, -1, nullptr);
     }
     TRACE_AT(1);
     if (!did) {   // CTA-uniform

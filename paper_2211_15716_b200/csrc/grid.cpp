@@ -12,6 +12,10 @@
 
 #include "igg_internal.h"
 
+#ifndef IGG_ABLATION
+#define IGG_ABLATION 0   // the ablation build (-DIGG_ABLATION=1): tuning variants and schedule bits
+#endif
+
 namespace igg {
 
 int proc_of(const igg_grid *g, int r) { return r / g->nlocal; }
@@ -253,33 +257,6 @@ void exchange(igg_grid *g, const igg_field *fields, int nf, cudaStream_t st, boo
                 ud[a].push_back(d);
             }
         }
-    }
-    size_t ndesc = 0;
-    for (int a = 0; a < 3; ++a) ndesc += pd[a].size() + ud[a].size();
-    if (allow_coop && !any_nccl && ndesc <= (size_t)kCoopMax && g->coop) {
-        // one cooperative launch for the whole call
-        CoopPlan C{};
-        int j = 0;
-        for (int a = 0; a < 3; ++a) {
-            C.pk0[a] = j;
-            for (const CopyDesc &d : pd[a]) C.d[j++] = d;
-            C.pk1[a] = C.up0[a] = j;
-            for (CopyDesc d : ud[a]) {
-                d.flag_slot = -1;
-                C.d[j++] = d;
-            }
-            C.up1[a] = j;
-            C.nsignal[a] = P[a].nsignal;
-            for (int q = 0; q < P[a].nsignal; ++q) C.signal[a][q] = P[a].signal[q];
-            C.nwait[a] = U[a].nsignal;
-            for (int q = 0; q < U[a].nsignal; ++q) C.wait[a][q] = U[a].wait[q];
-        }
-        C.epoch = g->epoch;
-        C.timeout_cycles = U[0].timeout_cycles;
-        C.err = g->d_err;
-        launch_halo_coop(C, st);
-        g->launches++;
-        return;
     }
     for (int a = 0; a < 3; ++a) {
         if (plan.msgs[a].empty()) continue;
@@ -1153,18 +1130,24 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
     IGG_TRY
     igg::check_live(g, "igg_set_option");
     switch (key) {
-        case IGG_OPT_SKIP_COMM: g->skip_comm = value != 0; break;
+        case IGG_OPT_SKIP_COMM:
+            g->skip_comm = value != 0;
+            g->skipped = g->skipped || g->skip_comm;
+            break;
         case IGG_OPT_SPIN_TIMEOUT_MS: g->spin_timeout_ms = value; break;
-        case IGG_OPT_STENCIL_KERNEL: g->stencil_kernel = (int)value; break;
+        case IGG_OPT_STENCIL_KERNEL:
+            if (!IGG_ABLATION && value != 0 && value != 1)
+                fail(IGG_E_UNSUPPORTED, "igg_set_option: stencil variants are in the ablation build only");
+            g->stencil_kernel = (int)value;
+            break;
         case IGG_OPT_PROFILE: g->profile = (int)value; break;
         case IGG_OPT_X_ALIGN: g->x_align = (int)(value < 1 ? 1 : value); break;
         case IGG_OPT_SCHEDULE: g->schedule = (int)value; break;
         case IGG_OPT_FUSED: g->fused = (int)value; break;
         case IGG_OPT_FUSED_MODE:
+            if (!IGG_ABLATION) fail(IGG_E_UNSUPPORTED, "igg_set_option: FUSED_MODE is in the ablation build only");
             g->fused_mode = (int)value;
-            g->fused_key = -1;   // bits 32/64 change the tile layout
             break;
-        case IGG_OPT_COOP_HALO: g->coop = value != 0; break;
         case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
         case IGG_OPT_LOCAL_P2P: g->local_p2p = value != 0; break;
         case IGG_OPT_HALO26: g->halo26 = value != 0 ? 1 : 0; break;
@@ -1232,6 +1215,10 @@ IGG_API igg_status igg_check(igg_grid *g) {
     IGG_TRY
     igg::check_live(g, "igg_check");
     igg::check_device_error(g, "igg_check");
+    if (g->skipped) {   // steps were taken with the exchange skipped (timing only): halos are invalid
+        g->skipped = g->skip_comm;
+        fail(IGG_E_STATE, "igg_check: steps ran with IGG_OPT_SKIP_COMM (timing only): halo values are invalid");
+    }
     if (g->comm) {
         ncclResult_t r = ncclSuccess;
         IGG_NCCL(ncclCommGetAsyncError(g->comm, &r));

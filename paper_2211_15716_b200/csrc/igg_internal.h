@@ -173,21 +173,6 @@ struct FusedParams {
 };
 
 // ---------------------------------------------------------------- kernel launchers (kernels.cu)
-// the whole update_halo of a call in ONE cooperative launch (P2P / local transports):
-// per axis pack -> grid sync -> publish flags -> wait peers' flags -> unpack -> grid sync
-constexpr int kCoopMax = 96;
-struct CoopPlan {
-    CopyDesc d[kCoopMax];
-    int pk0[3], pk1[3], up0[3], up1[3];     // descriptor ranges of each axis
-    unsigned long long *signal[3][kMaxSignal];
-    int nsignal[3];
-    const unsigned long long *wait[3][kMaxSignal];
-    int nwait[3];
-    unsigned long long epoch;
-    long long timeout_cycles;
-    int *err;
-};
-void launch_halo_coop(const CoopPlan &C, cudaStream_t s);
 
 // pack (op 0) or unpack (op 1) of any number of faces: chunks of kMaxCopy
 // descriptors per launch; `proto` carries signals/waits/epoch; returns launches
@@ -318,6 +303,7 @@ struct igg_grid : igg::Geom {
 
     // options
     bool skip_comm = false;
+    bool skipped = false;                                // a step ran with skip_comm since the last check
     long long spin_timeout_ms = 20000;
     int stencil_kernel = 0;
     int x_align = 64;
@@ -326,7 +312,6 @@ struct igg_grid : igg::Geom {
     int fused_mode = 2;                                  // IGG_OPT_FUSED_MODE (ablation bits)
     int fused_kc2 = 0;                                   // IGG_OPT_FUSED_KC2: tail chunk planes (0 auto)
     int fused_ncomm = 1;                                 // IGG_OPT_FUSED_COMM_CTAS
-    bool coop = false;                                   // IGG_OPT_COOP_HALO
     bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
     bool local_p2p = false;                              // IGG_OPT_LOCAL_P2P
     int halo26 = 1;                                      // IGG_OPT_HALO26: P2P update_halo as one 26-neighbour kernel

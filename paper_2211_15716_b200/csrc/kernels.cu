@@ -5,12 +5,17 @@
 //
 // Fp64 throughout ("@init_parallel_stencil(CUDA, Float64, 3)").
 // No tensor cores: the 7-point stencil is not a contraction.
-#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstdio>
 
 #include "igg_internal.h"
+
+// IGG_ABLATION (a separate build, ablation/libigg_ablation.so): the tuning variants measured in profiles/
+// (IGG_OPT_STENCIL_KERNEL 2..56 binary64, 100..126 binary32); the product library has only the defaults
+#ifndef IGG_ABLATION
+#define IGG_ABLATION 0
+#endif
 
 namespace igg {
 
@@ -290,6 +295,7 @@ void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3],
     const bool aligned = n[0] % 4 == 0 && (((uintptr_t)T | (uintptr_t)T2 | (uintptr_t)Ci) & 15) == 0;
     if (n[0] > 1 && n[1] > 1 && n[2] > 1 && aligned && wx >= 64 && variant != 1) {
         switch (variant) {
+#if IGG_ABLATION
             case 101: launch_f32_async<8, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
             case 102: launch_f32_async<4, 4, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
             case 103: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;
@@ -317,6 +323,7 @@ void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3],
             case 125: launch_f32_async<4, 2, 4, false>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
             case 126: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;
             case 100: launch_f32_async<4, 3, 4, true>(T2, T, Ci, n, lo, hi, k, s, 64, 8); break;   // = f64 default
+#endif
             default: launch_f32_async<4, 2, 4, true>(T2, T, Ci, n, lo, hi, k, s, 48, 8); break;   // 0 = 115
         }
         return;
@@ -483,6 +490,7 @@ void launch_heat_slabs(HeatRegionList &L, cudaStream_t s) {
 // 24 B/cell algorithmic.
 __device__ __forceinline__ double2 ldg2(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
 
+#if IGG_ABLATION
 // TY rows per CTA (one warp per row), KC planes per z-sweep.  With PF the
 // loads of plane z+1 (T[z+2], T[z+1] rows y+-1, Ci[z+1]) are issued before
 // plane z is computed, so every thread keeps two planes of DRAM reads in
@@ -572,6 +580,8 @@ static void launch_box_variant(const HeatRegion &r, const HeatCoef &k, cudaStrea
                                                                       r.wx, r.wy, r.wz, ax0, xtiles, ytiles, k);
     IGG_CUDA(cudaGetLastError());
 }
+
+#endif  // IGG_ABLATION
 
 bool heat_box_vectorizable(const HeatRegion &r) {
     return (r.sx % 2 == 0) && ((reinterpret_cast<uintptr_t>(r.T) | reinterpret_cast<uintptr_t>(r.Ci) |
@@ -713,6 +723,7 @@ static void launch_box_async(const HeatRegion &r, const HeatCoef &k, cudaStream_
     IGG_CUDA(cudaGetLastError());
 }
 
+#if IGG_ABLATION
 // ------------------------------------------------------------- wide tiles (ablation)
 // heat_box_async_kernel with WX warps side by side along x (tile (64*WX) x TY):
 // a CTA streams whole 4-KB rows when WX = 8 (DRAM page locality experiment).
@@ -928,6 +939,8 @@ static void launch_box_rows(const HeatRegion &r, const HeatCoef &k, cudaStream_t
     IGG_CUDA(cudaGetLastError());
 }
 
+#endif  // IGG_ABLATION
+
 // ------------------------------------------------------------- the production kernel
 // heat_box_async_kernel's sweep over a LIST of box regions (one launch for all
 // local ranks, or for all six boundary slabs).  TY=4 rows per CTA, D=3 planes
@@ -1023,7 +1036,12 @@ void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant) {
         for (int &o : occs) o = -1;
         init = true;
     }
+#if IGG_ABLATION
     const int vi = variant >= 30 && variant < 40 ? variant - 30 : 0;
+#else
+    const int vi = 0;
+    (void)variant;
+#endif
     const size_t extra = (size_t)vi * 4096;   // 0, 4 KB, 8 KB, ...
     auto kern = heat_box_list_kernel<1>;
     int &occ = occs[vi];
@@ -1076,6 +1094,7 @@ void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant) {
 void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant) {
     if (r.wx <= 0 || r.wy <= 0 || r.wz <= 0) return;
     switch (variant) {
+#if IGG_ABLATION
         case 2: launch_box_variant<8, 32, false>(r, k, s); break;
         case 4: launch_box_variant<8, 64, true>(r, k, s); break;
         case 5: launch_box_variant<16, 32, true>(r, k, s); break;
@@ -1111,6 +1130,7 @@ void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int
         case 55: launch_box_wide<2, 1, 3>(r, k, s, 64, 8); break;
         case 56: launch_box_wide<1, 4, 3>(r, k, s, 64, 8); break;
         case 3: launch_box_variant<8, 32, true>(r, k, s); break;
+#endif
         default: launch_box_async<4, 3, true>(r, k, s, 64, 8); break;   // 0 = 20: the measured best
     }
 }
@@ -1316,91 +1336,6 @@ int launch_copies(int op, const std::vector<CopyDesc> &descs, const CopyList &pr
                                               : launch_copies_n<kMaxCopy>(op, descs, proto, s);
 }
 
-// ============================================================== cooperative update_halo
-// One launch per update_halo call when no NCCL message is involved: all CTAs are
-// co-resident (cooperative launch), so the axis phases are separated by grid
-// barriers instead of kernel boundaries, and the peer flags are published and
-// awaited inside the kernel (removes ~6 dependent launches per call).
-template <bool PACK, typename E>
-__device__ __forceinline__ void copy_face_grid_t(const CopyDesc &d) {
-    E *field = reinterpret_cast<E *>(d.field);
-    E *buf = reinterpret_cast<E *>(d.buf);
-    const long long nthreads = (long long)gridDim.x * blockDim.x;
-    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (long long base = 0; base < d.count; base += nthreads * kCopyILP) {
-        E v[kCopyILP];
-#pragma unroll
-        for (int u = 0; u < kCopyILP; ++u) {
-            const long long i = base + u * nthreads + gtid;
-            if (i < d.count) v[u] = PACK ? __ldcg(field + face_index(d, i)) : __ldcg(buf + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kCopyILP; ++u) {
-            const long long i = base + u * nthreads + gtid;
-            if (i < d.count) {
-                if (PACK)
-                    buf[i] = v[u];
-                else
-                    field[face_index(d, i)] = v[u];
-            }
-        }
-    }
-}
-template <bool PACK>
-__device__ __forceinline__ void copy_face_grid(const CopyDesc &d) {
-    if (d.esz == 4)
-        copy_face_grid_t<PACK, float>(d);
-    else
-        copy_face_grid_t<PACK, double>(d);
-}
-
-__global__ void __launch_bounds__(kCopyThreads) halo_coop_kernel(const __grid_constant__ CoopPlan C) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    for (int a = 0; a < 3; ++a) {
-        if (C.pk0[a] == C.pk1[a] && C.up0[a] == C.up1[a]) continue;   // uniform
-        for (int j = C.pk0[a]; j < C.pk1[a]; ++j) copy_face_grid<true>(C.d[j]);
-        if (C.nsignal[a] > 0) __threadfence_system();   // my peer stores, before the barrier
-        grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x < C.nsignal[a]) {
-            __threadfence_system();
-            st_release_sys(C.signal[a][threadIdx.x], C.epoch);
-        }
-        if (C.nwait[a] > 0) {
-            if (blockIdx.x == 0 && threadIdx.x < C.nwait[a]) {
-                const unsigned long long *f = C.wait[a][threadIdx.x];
-                const long long t0 = clock64();
-                while (ld_acquire_sys(f) < C.epoch) {
-                    if (clock64() - t0 > C.timeout_cycles) {
-                        atomicExch(C.err, 1);
-                        break;
-                    }
-                    __nanosleep(32);
-                }
-            }
-            grid.sync();
-        }
-        for (int j = C.up0[a]; j < C.up1[a]; ++j) copy_face_grid<false>(C.d[j]);
-        grid.sync();   // the next axis packs the halos written here (edges and corners)
-    }
-}
-
-void launch_halo_coop(const CoopPlan &C, cudaStream_t s) {
-    static int occ = -1, nsm = 0;
-    if (occ < 0) {
-        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, halo_coop_kernel, kCopyThreads, 0));
-        int dev = 0;
-        IGG_CUDA(cudaGetDevice(&dev));
-        IGG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    }
-    long long mx = 1;
-    for (int a = 0; a < 3; ++a)
-        for (int j = C.pk0[a]; j < C.up1[a]; ++j) mx = std::max(mx, C.d[j].count);
-    long long want = (mx + (long long)kCopyThreads * kCopyILP - 1) / ((long long)kCopyThreads * kCopyILP);
-    const int grid = (int)std::max(1LL, std::min<long long>(want, (long long)occ * nsm));
-    void *args[] = {(void *)&C};
-    IGG_CUDA(cudaLaunchCooperativeKernel((const void *)halo_coop_kernel, dim3(grid), dim3(kCopyThreads), args, 0, s));
-}
 
 // ============================================================== box pack (gather)
 // Copies the sub-box [b0, b1) of a (sx, sy, sz) field into a contiguous buffer, x fastest.

@@ -33,7 +33,6 @@ OPT_FUSED = 7
 OPT_FUSED_MODE = 8
 OPT_FUSED_KC2 = 9
 OPT_FUSED_COMM_CTAS = 10
-OPT_COOP_HALO = 11
 OPT_HALO_STREAM = 12
 OPT_LOCAL_P2P = 13
 OPT_HALO26 = 14

@@ -10,6 +10,18 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run through gpurun)")
     config.addinivalue_line("markers", "slow: long-running (full-size) case")
+    config.addinivalue_line("markers", "ablation: needs the ablation build (IGG_LIBRARY=ablation/libigg_ablation.so); "
+                                       "run by tests/test_gpu_ablation.py in a subprocess")
+
+
+def pytest_collection_modifyitems(config, items):
+    import pytest
+    if "ablation" in os.environ.get("IGG_LIBRARY", ""):
+        return
+    skip = pytest.mark.skip(reason="ablation build only (tests/test_gpu_ablation.py runs these with it)")
+    for it in items:
+        if "ablation" in it.keywords:
+            it.add_marker(skip)
 
 
 def pytest_sessionstart(session):

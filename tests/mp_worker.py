@@ -298,7 +298,6 @@ def main():
         acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4))
         heat_f32_case(path, n, dims, (1, 0, 1))
         heat_f32_case(path, (520, 20, 34), dims, (0, 0, 0), bw=(16, 2, 2))   # hide_communication, float4 kernel
-        heat_f32_case(path, (520, 20, 34), dims, (0, 1, 0), bw=(16, 2, 2), opts={P.OPT_FUSED_MODE: 2 | 16384})
         heat_f32_case(path, (264, 36, 34), dims, (1, 1, 0), bw=(0, 0, 0))
         acoustic_case(path, n, dims, (1, 0, 1), 1, (4, 4, 4))
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
