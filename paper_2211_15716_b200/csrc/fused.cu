@@ -133,10 +133,16 @@ constexpr int kFKC = 64;   // longest z-chunk
 }  // namespace
 
 // The z sweep of one tile: cp.async ring of kFD planes of T and Ci, x neighbours by shuffle, z by a
-// register queue.  The y and z faces leave from inside the sweep: the warp whose row is a y send layer
-// stores its results also into the receiver's halo row (ydst), and on the plane that is a z send layer
-// every warp stores its row also into the receiver's halo plane (zdst) -- the same 16-B stores as T2's,
-// one extra per plane for those warps / that plane, no re-read after the sweep.
+// register queue.  Faces leave from inside the sweep (no re-read of T2 afterwards):
+//  * YF (CTA-uniform): the warp whose row is a y send layer stores its results also into the receiver's
+//    halo row (ydst + i) -- the same 16-B stores as T2's (the z send layer, the first or last plane of an
+//    end chunk, is copied after the sweep: one row per warp, just written);
+//  * XF (CTA-uniform: the tile holds the x send layer and the x halo column beside it): the lane holding
+//    the send cell stores its value of every plane into the receiver's staging row (sdst[z]: z-contiguous,
+//    the stores of consecutive planes fill whole sectors), and the lane holding the halo cell fetches the
+//    neighbour's staged value of every plane (hrow[z]) with one 8-B cp.async into a small ring sH beside
+//    the plane's T and Ci, and substitutes it for T's halo value (T's halo column is never read for a
+//    kept result, and never written).  Predicated instructions only: no divergence in the loop.
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
@@ -148,27 +154,36 @@ __device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r
         if (w1) d[1] = r1;
     }
 }
+__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
 
-template <bool FACES>   // FACES: the tile stores a y or z face from the sweep (CTA-uniform)
+template <bool YF, bool XF>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
-                                            double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
-                                            long long i, bool pair_in, bool w0, bool w1, bool cs, double *ydst,
-                                            int zlay, double *zdst) {
+                                            double2 (*sC)[32 * kFTY], double (*sH)[kFTY], int sx, long long sxy,
+                                            int zs, int ze, long long i, bool pair_in, bool w0, bool w1, bool cs,
+                                            double *ydst, const double *hrow, bool hhi, double *sdst, bool shi) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
             cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
             cp_async16f(&sC[q][tid], Ci + i + q * sxy);
         }
+        if (XF && hrow && zs + q + 1 < ze) cp_async8f(&sH[q][warp], hrow + zs + q + 1);
         cp_commit();
     }
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
+    if (XF && hrow) {
+        const double h = __ldcg(hrow + zs);
+        if (hhi) c.y = h; else c.x = h;
+    }
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
 #pragma unroll 2
@@ -187,20 +202,23 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (hi_edge) xp = __ldg(T + i + 2);
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (!FACES && FUSED_STCS && cs && w0 && w1)   // a tile without faces: T2 is not re-read
+        if (!YF && !XF && FUSED_STCS && cs && w0 && w1)   // a tile without faces: T2 is not re-read
             __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
         else
             store_pair(T2 + i, w0, w1, r0, r1);
-        if (FACES) {
-            if (ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
-            if (z == zlay) store_pair(zdst + (i - (long long)z * sxy), w0, w1, r0, r1);   // z face plane
-        }
+        if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
+        if (XF && sdst) sdst[z] = shi ? r1 : r0;   // (one lane) the x send cell -> the receiver's staging
         zm = c;
         c = zp;
+        if (XF && hrow && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
+            const double h = sH[slot][warp];
+            if (hhi) c.y = h; else c.x = h;
+        }
         if (pair_in && z + kFD < ze) {
             cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
         }
+        if (XF && hrow && z + kFD + 1 < ze) cp_async8f(&sH[slot][warp], hrow + z + kFD + 1);
         cp_commit();
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
@@ -234,6 +252,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     TRACE_AT(0);
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
+    __shared__ double sH[kFD][kFTY];   // the x halo lanes' staged values, a ring like sT's
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
     const int rank = blockIdx.x / F.per_rank;
@@ -295,7 +314,8 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         __syncthreads();
     }
 
-    // ---- the z sweep, with the y / z faces stored from inside it
+    // ---- the z sweep, with the x and y faces stored from inside it
+    const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
     {
         double *ydst = nullptr;
         if (did & 12u) {
@@ -304,66 +324,38 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                                                     // my row lands at ydst + i in the receiver's halo row
                 ydst = R.face[1][rs].dst + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx;
         }
-        int zlay = -1;
-        double *zdst = nullptr;
-        if (did & 48u) {
-            const int rs = (did & 16u) ? 0 : 1;
-            zlay = R.face[2][rs].layer;
-            zdst = R.face[2][rs].dst + (long long)(rs == 0 ? 0 : F.s[2] - 1) * sxy;
+        if (xrs >= 0) {
+            const int xf = R.face[0][xrs].layer - tx * 64, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
+            const double *hrow = (hstaged && rowv && (xh >> 1) == lane)
+                                     ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
+            double *sdst = (rowv && (xf >> 1) == lane) ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;
+            if (did & 12u)
+                fused_sweep<true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, ydst, hrow,
+                                        xh & 1, sdst, xf & 1);
+            else
+                fused_sweep<false, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, nullptr,
+                                         hrow, xh & 1, sdst, xf & 1);
+        } else if (did & 12u) {
+            fused_sweep<true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, ydst, nullptr,
+                                     false, nullptr, false);
+        } else {
+            fused_sweep<false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, did == 0u, nullptr,
+                                      nullptr, false, nullptr, false);
         }
-        const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
-        if (did & 60u)
-            fused_sweep<true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, ydst, zlay, zdst);
-        else
-            fused_sweep<false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, did == 0u, nullptr, -1, nullptr);
+    }
+    if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver
+        const int rs = (did & 16u) ? 0 : 1;
+        const FusedFace &fz = R.face[2][rs];
+        if (rowv && p < sx) {
+            const long long o = (long long)fz.layer * sxy + (long long)y * sx + p;
+            const double2 v = *reinterpret_cast<const double2 *>(R.T2 + o);
+            store_pair(fz.dst + o + (long long)((rs == 0 ? 0 : F.s[2] - 1) - fz.layer) * sxy, w0, w1, v.x, v.y);
+        }
     }
     TRACE_AT(1);
     if (!did) {   // CTA-uniform
         TRACE_AT(3);
         return;
-    }
-    __syncthreads();   // the CTA's T2 stores are visible to the CTA
-    if (xrs >= 0) {
-        // ---- the x send layer xf (beside the x halo column): the sweep took T's halo value; recompute the
-        // column with the neighbour's staged values (lanes along z, loads mostly L2 hits of the rows and
-        // planes just streamed), overwrite its T2 cells and store them z-contiguous into the receiver's
-        // staging row.  Same operations in the same order as the sweep: bit-identical cells.
-        const int xf = R.face[0][xrs].layer, xh = hside == 0 ? 0 : sx - 1;
-        const double *__restrict__ T = R.T;
-        const double *__restrict__ Ci = R.Ci;
-        double *__restrict__ T2 = R.T2;
-        if (rowv) {
-            const double *hrow = R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0);
-            double *sdst = R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0);
-            for (int z = zs + lane; z < ze; z += 32) {
-                const long long c0 = (long long)z * sxy + (long long)y * sx + xf;
-                const double c = __ldcg(T + c0);
-                const double h = hstaged ? __ldcg(hrow + z) : __ldcg(T + c0 + (xh - xf));
-                const double o = __ldcg(T + c0 - (xh - xf));   // the other x neighbour
-                const double xm = xh < xf ? h : o, xp = xh < xf ? o : h;
-                const double r = cell(c, xm, xp, __ldcg(T + c0 - sx), __ldcg(T + c0 + sx), __ldcg(T + c0 - sxy),
-                                      __ldcg(T + c0 + sxy), __ldcg(Ci + c0), F.k);
-                T2[c0] = r;
-                sdst[z] = r;
-            }
-        }
-    }
-    // (the y / z face rows of the x send column hold the sweep's value there; the fix-up above corrects
-    // T2 but the receiver's y/z halo copies of that cell are written below, after the correction)
-    if ((did & 60u) && xrs >= 0 && rowv) {   // (each lane re-sends cells it recomputed itself)
-        const int xf = R.face[0][xrs].layer;
-        for (int rs = 0; rs < 2; ++rs) {
-            if ((did & (4u << rs)) && y == R.face[1][rs].layer)
-                for (int z = zs + lane; z < ze; z += 32) {
-                    const long long c0 = (long long)z * sxy + (long long)y * sx + xf;
-                    R.face[1][rs].dst[c0 + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx] = R.T2[c0];
-                }
-            const int zl = R.face[2][rs].layer;
-            if ((did & (16u << rs)) && zl >= zs && zl < ze && ((zl - zs) & 31) == lane) {
-                const long long c0 = (long long)zl * sxy + (long long)y * sx + xf;
-                R.face[2][rs].dst[c0 + (long long)((rs == 0 ? 0 : F.s[2] - 1) - zl) * sxy] = R.T2[c0];
-            }
-        }
     }
     // one system-scope release for the CTA: the barrier orders every warp's face stores before thread
     // 0's fence, which is cumulative (PTX memory model), then the counters
