@@ -202,7 +202,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (hi_edge) xp = __ldg(T + i + 2);
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (!YF && !XF && FUSED_STCS && cs && w0 && w1)   // a tile without faces: T2 is not re-read
+        if (FUSED_STCS && cs && w0 && w1)   // T2 is not re-read in this step (evict-first keeps L2 for T)
             __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
         else
             store_pair(T2 + i, w0, w1, r0, r1);
@@ -264,10 +264,40 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         return;
     }
     b -= F.nrim + F.nfwd;
-    const int tx = b % F.xtiles, rr = b / F.xtiles, ty = rr % F.ytiles, pos = rr / F.ytiles;
+    // tile of this block: chunks in visit order; within a chunk, when x or y faces exist, the border
+    // tiles (rows ty = 0 and ytiles-1, then columns tx = 0 and xtiles-1) first -- they carry the faces and
+    // take longer, so they start early instead of trailing their chunk -- then the interior, row-major
+    const int nt = F.xtiles * F.ytiles, pos = b / nt;
+    int tx, ty;
+    {
+        const int t = b - pos * nt, xt = F.xtiles, yt = F.ytiles;
+        const int nrow = xt * min(yt, 2), nborder = nrow + 2 * max(yt - 2, 0);
+        if (!F.border_first) {
+            tx = t % xt;
+            ty = t / xt;
+        } else if (t < xt) {
+            tx = t;
+            ty = 0;
+        } else if (t < nrow) {
+            tx = t - xt;
+            ty = yt - 1;
+        } else if (t < nborder) {
+            const int u = t - nrow;
+            ty = 1 + (u >> 1);
+            tx = (u & 1) ? xt - 1 : 0;
+        } else {
+            const int v = t - nborder;
+            tx = 1 + v % (xt - 2);
+            ty = 1 + v / (xt - 2);
+        }
+    }
     const int2 zr = F.zr[pos];
     const int zs = zr.x, ze = zr.y;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if FUSED_TRACE
+    if (tid == 0 && blockIdx.x < 65536 && F.epoch == g_trace_epoch)
+        g_fused_trace[blockIdx.x * 4 + 2] = (unsigned long long)tx | ((unsigned long long)ty << 8) | ((unsigned long long)pos << 20);
+#endif
     const int sx = F.s[0], sy = F.s[1];
     const int ty0 = 1 + ty * kFTY;
     const int y = ty0 + warp;
@@ -329,17 +359,23 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             const double *hrow = (hstaged && rowv && (xh >> 1) == lane)
                                      ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
             double *sdst = (rowv && (xf >> 1) == lane) ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;
+#ifdef FUSED_DIAG_NOHALO   // diagnostics builds only (timing; INVALID halos)
+            hrow = nullptr;
+#endif
+#ifdef FUSED_DIAG_NOSEND
+            sdst = nullptr;
+#endif
             if (did & 12u)
-                fused_sweep<true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, ydst, hrow,
+                fused_sweep<true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst, hrow,
                                         xh & 1, sdst, xf & 1);
             else
-                fused_sweep<false, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, nullptr,
+                fused_sweep<false, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
                                          hrow, xh & 1, sdst, xf & 1);
         } else if (did & 12u) {
-            fused_sweep<true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, false, ydst, nullptr,
+            fused_sweep<true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst, nullptr,
                                      false, nullptr, false);
         } else {
-            fused_sweep<false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, did == 0u, nullptr,
+            fused_sweep<false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
                                       nullptr, false, nullptr, false);
         }
     }
@@ -815,6 +851,9 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.zchunk[1] = g->fused_zchunk[1];
     F.tgt = g->fused_tgt_pipe;
     F.tgt_x = g->fused_tgt_x;
+#ifndef FUSED_DIAG_NATURAL_ORDER
+    F.border_first = (act[0][0] || act[0][1] || act[1][0] || act[1][1]) ? 1 : 0;
+#endif
     // ONE launch on the caller's stream and, when the step must be complete on return, a drain.  The rim
     // cells and the forwarded edge lines are never read by the stencil, so only the step that completes a
     // run sends them (rim blocks + forwarders in its launch); the steps before it move only the faces the

@@ -163,6 +163,7 @@ struct FusedParams {
     int2 zr[kMaxChunks];             // z range of each chunk, in visit order (= chunk id)
     int zchunk[2];                   // chunk holding the z send layer of face (2, rs); -1 if none
     int xtiles, ytiles;
+    int border_first;                // within a chunk: the border tiles (faces) first
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk) data flag
     const unsigned int *tgt_x;       // ... an xflag (rim + forwarders)
     unsigned long long epoch;
