@@ -452,7 +452,7 @@ def main():
         d2h = cells * 8
         e2e = {"value": world * BYTES_PER_CELL * cells * nt / (t_call * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": h2d / nt, "d2h_bytes_per_step": d2h / nt,
-               "call": "igg_heat_run_host: H2D T,Ci from pinned host + T2=copy(T) + nt=100 heat steps + D2H T",
+               "call": "igg_heat_run_host: H2D T,Ci from pinned host + T2 outer layers = T + nt=100 heat steps + D2H T",
                "nt_per_call": nt, "h2d_bytes_per_call": h2d, "d2h_bytes_per_call": d2h,
                "ms_per_call": t_call}
 

@@ -944,13 +944,14 @@ IGG_API igg_status igg_heat_run_host(igg_grid *g, double *T_host, const double *
     }
     IGG_CUDA(cudaMemcpyAsync(g->run_T, T_host, bytes, cudaMemcpyHostToDevice, s));
     IGG_CUDA(cudaMemcpyAsync(g->run_Ci, Ci_host, bytes, cudaMemcpyHostToDevice, s));
-    IGG_CUDA(cudaMemcpyAsync(g->run_T2, g->run_T, bytes, cudaMemcpyDeviceToDevice, s));   // T2 = copy(T)
     std::vector<double *> a(g->nlocal), b(g->nlocal);
     std::vector<const double *> c(g->nlocal);
     for (int lr = 0; lr < g->nlocal; ++lr) {
         a[lr] = g->run_T + lr * cells;
         b[lr] = g->run_T2 + lr * cells;
         c[lr] = g->run_Ci + lr * cells;
+        igg::launch_copy_outer(b[lr], a[lr], g->n, s);   // T2 = copy(T) on the cells no step writes first
+        g->launches++;
     }
     for (int it = 0; it < nt; ++it) {
         std::vector<const double *> ac(a.begin(), a.end());

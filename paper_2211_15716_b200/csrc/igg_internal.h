@@ -198,6 +198,8 @@ void launch_heat_lowdim(double *T2, const double *T, const double *Ci, const int
 // vectorised z-sweep kernel for one box region of an even-sx, 16-B aligned field
 bool heat_box_vectorizable(const HeatRegion &r);
 void launch_heat_box(const HeatRegion &r, const HeatCoef &k, cudaStream_t s, int variant);
+// T2's six outer layers = T's (the cells of T2 = copy(T), that no step or exchange writes first)
+void launch_copy_outer(double *T2, const double *T, const int n[3], cudaStream_t s);
 // sub-box [b0, b1) of a field -> contiguous buffer (x fastest)
 void launch_box_pack(const double *f, double *out, long long sx, long long sy, const int b0[3], const int b1[3],
                      cudaStream_t s);

@@ -1364,6 +1364,43 @@ void launch_box_pack(const double *f, double *out, long long sx, long long sy, c
     IGG_CUDA(cudaGetLastError());
 }
 
+// ============================================================== outer layers (T2 = copy(T) where it matters)
+// PAPER.md:69 T2 = copy(T): the step writes every inner cell of T2 and update_halo! every halo cell, so only
+// the six outer layers (the global-boundary values of Dirichlet-by-initialisation, reading 10, and the
+// halo layers before their first exchange) need T's values -- 6 n^2 cells instead of the n^3 copy.
+__global__ void __launch_bounds__(256) copy_outer_kernel(double *__restrict__ T2, const double *__restrict__ T, int nx,
+                                                         int ny, int nz) {
+    const long long fz = (long long)nx * ny, fy = (long long)nx * nz, fx = (long long)ny * nz;
+    const long long total = 2 * (fz + fy + fx);
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long x, y, z, r = t;
+        if (r < 2 * fz) {   // planes z = 0, nz-1 (contiguous)
+            z = r < fz ? 0 : nz - 1;
+            r %= fz;
+            x = r % nx;
+            y = r / nx;
+        } else if ((r -= 2 * fz) < 2 * fy) {   // rows y = 0, ny-1
+            y = r < fy ? 0 : ny - 1;
+            r %= fy;
+            x = r % nx;
+            z = r / nx;
+        } else {   // columns x = 0, nx-1
+            r -= 2 * fy;
+            x = r < fx ? 0 : nx - 1;
+            r %= fx;
+            y = r % ny;
+            z = r / ny;
+        }
+        const long long i = (z * ny + y) * nx + x;
+        T2[i] = T[i];
+    }
+}
+void launch_copy_outer(double *T2, const double *T, const int n[3], cudaStream_t s) {
+    copy_outer_kernel<<<148 * 4, 256, 0, s>>>(T2, T, n[0], n[1], n[2]);
+    IGG_CUDA(cudaGetLastError());
+}
+
 // ============================================================== max reduction
 constexpr int kMaxThreads = 256;
 constexpr int kMaxPartials = 1184;   // 148 SMs x 8

@@ -12,6 +12,8 @@
 #     launches     plain bench, then ncu launch list        -> gpurun_out/<tag>_launches.csv
 #     ncu:<regex>  plain bench, then ncu --set full of the first 3 matching launches -> <tag>_prof.ncu-rep
 #     halo2/4      update_halo sweep (scripts/halo_sweep.py) -> gpurun_out/<tag>_halo_n2.txt
+#     san:<tool>   compute-sanitizer --tool <tool> (memcheck | racecheck | synccheck; ONE per call) of
+#                  scripts/sanitize_small.py, after a plain run of it -> gpurun_out/<tag>_san_<tool>.log
 # Extra bench.py arguments: BENCH_ARGS="..." (plain runs and the ncu runs).
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
@@ -41,6 +43,11 @@ for step in "$@"; do
              -o gpurun_out/${tag}_prof $B > gpurun_out/${tag}_ncu_full.log 2>&1 ;;
     halo2) timeout 600 $TR --nproc-per-node 2 scripts/halo_sweep.py > gpurun_out/${tag}_halo_n2.txt 2>&1 ;;
     halo4) timeout 600 $TR --nproc-per-node 4 scripts/halo_sweep.py > gpurun_out/${tag}_halo_n4.txt 2>&1 ;;
+    san:*) tool=${step#san:}
+           timeout 300 python scripts/sanitize_small.py > gpurun_out/${tag}_san_plain.log 2>&1 && \
+           timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 python scripts/sanitize_small.py \
+             > gpurun_out/${tag}_san_${tool}.log 2>&1
+           echo "rc=$?" >> gpurun_out/${tag}_san_${tool}.log ;;
     *) echo "unknown step $step" ;;
   esac
 done
