@@ -23,9 +23,10 @@
 //   * unpack: x-face unpack chunks acquire the sender's data flag first;
 //   * end:    the last block to leave acquires every incoming data flag, so the halos are complete for any
 //             later work on the stream.
-// Work is claimed chunk by chunk from a counter, store chunks first: a block only ever waits for (a) other
-// GPUs, or (b) store chunks already claimed by running blocks, which never wait on this launch -- so the
-// launch cannot deadlock whatever the block residency (DESIGN.md §6 "forward progress").
+// Work is claimed in batches of chunks from a counter, store chunks first: a block only ever waits for (a)
+// other GPUs, or (b) store chunks already claimed by running blocks, which never wait on this launch and
+// count themselves before their block claims again -- so the launch cannot deadlock whatever the block
+// residency (DESIGN.md §6 "forward progress").
 #include <algorithm>
 #include <cstring>
 
@@ -104,53 +105,77 @@ __device__ __forceinline__ void copy_chunk(const H26Item &it, long long c) {
 
 }  // namespace
 
+constexpr int kH26Batch = 4;   // chunks per claim (one counter update and one item search per batch)
+
 __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restrict__ base, unsigned long long epoch,
                                                              unsigned int *ctr, long long timeout, int *err) {
     const H26Plan &P = *reinterpret_cast<const H26Plan *>(base);
     const H26Item *items = reinterpret_cast<const H26Item *>(base + P.o_items);
     __shared__ long long s_c;
+    __shared__ int s_it, s_waited;
     if (blockIdx.x == 0 && threadIdx.x < P.nready) {   // my remote senders may store into me
         unsigned long long *const *ready = reinterpret_cast<unsigned long long *const *>(base + P.o_ready);
         st_rel_sys(ready[threadIdx.x], epoch);
     }
-    long long c;
-    for (;;) {
-        if (threadIdx.x == 0) s_c = (long long)atomicAdd(ctr, 1u);
+    const long long nbatch = (P.nchunks + kH26Batch - 1) / kH26Batch;
+    unsigned mydone = 0;   // store chunks this block finished and has not counted yet
+    // count my finished store chunks (after a system fence); the count completing all store chunks
+    // publishes every data flag (release)
+    auto flush = [&]() {
         __syncthreads();
-        c = s_c;
-        __syncthreads();
-        if (c >= P.nchunks) break;
-        int lo = 0, hi = P.nitems - 1;   // the item holding chunk c
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (items[mid].chunk0 <= c) lo = mid; else hi = mid - 1;
-        }
-        const H26Item &it = items[lo];
-        if (it.wait >= 0) {
-            if (threadIdx.x == 0) {
-                const unsigned long long *const *wp =
-                    reinterpret_cast<const unsigned long long *const *>(base + P.o_waitp);
-                spin(wp[it.wait], epoch, timeout, err);
-            }
-            __syncthreads();
-        }
-        if (it.esz == 4)
-            copy_chunk<float>(it, c - it.chunk0);
-        else
-            copy_chunk<double>(it, c - it.chunk0);
-        if (c < P.nstore_chunks) {   // count the store chunk; the last one publishes every data flag
-            __syncthreads();
-            if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && mydone) {
+            __threadfence_system();
+            if (atomicAdd(ctr + 1, mydone) + mydone == (unsigned)P.nstore_chunks) {
                 __threadfence_system();
-                if (atomicAdd(ctr + 1, 1u) == (unsigned)P.nstore_chunks - 1) {
-                    __threadfence_system();
-                    unsigned long long *const *sig = reinterpret_cast<unsigned long long *const *>(base + P.o_signal);
-                    for (int q = 0; q < P.nsignal; ++q) st_rel_sys(sig[q], epoch);
-                }
+                unsigned long long *const *sig = reinterpret_cast<unsigned long long *const *>(base + P.o_signal);
+                for (int q = 0; q < P.nsignal; ++q) st_rel_sys(sig[q], epoch);
             }
         }
+        mydone = 0;
+    };
+    long long bt;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            s_c = (long long)atomicAdd(ctr, 1u);
+            const long long c0 = s_c * kH26Batch;
+            int lo = 0, hi = P.nitems - 1;   // the item holding the batch's first chunk
+            if (c0 < P.nchunks)
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (items[mid].chunk0 <= c0) lo = mid; else hi = mid - 1;
+                }
+            s_it = lo;
+            s_waited = -1;
+        }
+        __syncthreads();
+        bt = s_c;
+        int iti = s_it;
+        if (bt >= nbatch) break;
+        const long long c0 = bt * kH26Batch, c1 = min(c0 + kH26Batch, P.nchunks);
+        if (c0 >= P.nstore_chunks && mydone) flush();   // (claims are monotonic: no store work follows)
+        for (long long c = c0; c < c1; ++c) {
+            while (iti + 1 < P.nitems && items[iti + 1].chunk0 <= c) ++iti;
+            const H26Item &it = items[iti];
+            if (it.wait >= 0 && s_waited != it.wait) {   // (block-uniform)
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    const unsigned long long *const *wp =
+                        reinterpret_cast<const unsigned long long *const *>(base + P.o_waitp);
+                    spin(wp[it.wait], epoch, timeout, err);
+                    s_waited = it.wait;
+                }
+                __syncthreads();
+            }
+            if (it.esz == 4)
+                copy_chunk<float>(it, c - it.chunk0);
+            else
+                copy_chunk<double>(it, c - it.chunk0);
+            if (c < P.nstore_chunks) ++mydone;
+        }
+        __syncthreads();   // (s_c / s_it / s_waited are rewritten by the next claim)
     }
-    if (c == P.nchunks + gridDim.x - 1) {   // the last block to leave: every incoming face, then reset
+    flush();
+    if (bt == nbatch + gridDim.x - 1) {   // the last block to leave: every incoming face, then reset
         const unsigned long long *const *we = reinterpret_cast<const unsigned long long *const *>(base + P.o_wait_end);
         for (int q = threadIdx.x; q < P.nwait_end; q += blockDim.x) spin(we[q], epoch, timeout, err);
         if (threadIdx.x == 0) {
@@ -277,8 +302,10 @@ void exchange26(igg_grid *g, const igg_field *fields, int nf, const Plan &plan, 
                         it.dsz = (long long)ext[0] * ext[1];
                     } else {
                         const long long dsy = s[0], dsz = s[0] * s[1];   // same field shape on the receiver
+                        // the receiver's array: a sibling's, or process mp's array of ITS rank mlr (the
+                                        // mapping of position (mlr, f) of the collective exchange)
                         char *dbase = ml >= 0 ? reinterpret_cast<char *>(fields[ml * nf + f].ptr)
-                                              : reinterpret_cast<char *>(pmap[lr * nf + f][mp]);
+                                              : reinterpret_cast<char *>(pmap[mlr * nf + f][mp]);
                         it.dst = dbase + ((long long)d0[2] * dsz + (long long)d0[1] * dsy + d0[0]) * esz;
                         it.dsy = dsy;
                         it.dsz = dsz;
@@ -403,7 +430,7 @@ void exchange26(igg_grid *g, const igg_field *fields, int nf, const Plan &plan, 
         g->allocs++;
     }
     // every process launches (a rank with nothing to send still publishes ready and awaits its halos)
-    const long long grid = std::max(1LL, std::min<long long>(hit->nchunks, 2LL * g->sm_count));
+    const long long grid = std::max(1LL, std::min<long long>((hit->nchunks + kH26Batch - 1) / kH26Batch, 2LL * g->sm_count));
     halo26_kernel<<<(unsigned)grid, kH26Threads, 0, st>>>(static_cast<const char *>(hit->dplan), g->epoch, g->h26_ctr,
                                                           (long long)(g->spin_timeout_ms * g->clock_khz), g->d_err);
     IGG_CUDA(cudaGetLastError());

@@ -604,11 +604,13 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-#ifndef BOX_MINB
-#define BOX_MINB 1   // (ablation builds: minimum resident blocks per SM, i.e. a register cap)
+#ifdef BOX_MINB   // (ablation builds: minimum resident blocks per SM, i.e. a register cap)
+#define BOX_BOUNDS(t) __launch_bounds__(t, BOX_MINB)
+#else
+#define BOX_BOUNDS(t) __launch_bounds__(t)
 #endif
 template <int TY, int D, bool ST>
-__global__ void __launch_bounds__(32 * TY, BOX_MINB)
+__global__ void BOX_BOUNDS(32 * TY)
     heat_box_async_kernel(const double *__restrict__ T, const double *__restrict__ Ci, double *__restrict__ T2,
                           int sx, int sy, int x0, int y0, int z0, int wx, int wy, int wz, int ax0, int xtiles,
                           int ytiles, int kc1, int nbig, int kc2, const HeatCoef k) {

@@ -35,7 +35,7 @@ for per in ((0, 0, 0), (1, 1, 1)):
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
-            torch.cuda._sleep(20_000_000)
+            torch.cuda._sleep(100_000_000)
             e0.record()
             for _ in range(20):
                 g.update_halo(*F)

@@ -3,7 +3,7 @@ size (2: 2x1x1, 4: 2x2x1, 8: 2x2x2), transports: NCCL (per-axis grouped send/rec
 pack/flag/unpack, and P2P 26-neighbour single kernel (default).  20 samples of 100 calls each (median),
 CUDA events on the calling stream, max over ranks; GB/s per GPU = bytes this GPU sends to OTHER GPUs per
 call / t; 'payload' also counts the faces a rank stores into itself (periodic self-wrap axes)."""
-import json, os, statistics, sys
+import json, os, statistics, sys, time
 sys.path.insert(0, ".")
 import torch
 import torch.distributed as dist
@@ -27,14 +27,16 @@ for path, h26 in variants:
             g.update_halo(A)
         torch.cuda.synchronize(); dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        xs = []
+        xs, host_us = [], []
         for rep in range(20):
             dist.barrier(); torch.cuda.synchronize()
-            torch.cuda._sleep(20_000_000)   # keep the GPU busy while the host enqueues: GPU time only
+            torch.cuda._sleep(200_000_000)   # the GPU stays busy while the host enqueues: GPU time only
+            h0 = time.perf_counter()
             e0.record()
             for _ in range(100):
                 g.update_halo(A)
             e1.record()
+            host_us.append((time.perf_counter() - h0) * 1e4)
             torch.cuda.synchronize()
             t = torch.tensor([e0.elapsed_time(e1) / 100], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -45,7 +47,8 @@ for path, h26 in variants:
         sent = remote_axes * 2 * n * n * 8   # face bytes this GPU sends to other GPUs per call
         out.append({"path": path, "halo26": h26, "n": n, "dims": dims, "ms_per_call_median": ms,
                     "ms_min": min(xs), "remote_bytes": sent, "GBps_per_gpu": sent / (ms * 1e-3) / 1e9,
-                    "payload_GBps": 6 * n * n * 8 / (ms * 1e-3) / 1e9})
+                    "payload_GBps": 6 * n * n * 8 / (ms * 1e-3) / 1e9,
+                    "host_enqueue_us_per_call": statistics.median(host_us)})
         g.finalize()
         del A
         torch.cuda.empty_cache()
