@@ -89,7 +89,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.draw,clocks.mem")
 
     def __init__(self, device: int):
         self.device = device
@@ -109,7 +109,7 @@ class ClockSampler:
         time.sleep(0.25)
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw, mem = [], None, set(), [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
@@ -118,13 +118,17 @@ class ClockSampler:
             try:
                 sm.append(float(f[0]))
                 mx = float(f[1])
+                if len(f) >= 9:
+                    pw.append(float(f[7]))
+                    mem.append(float(f[8]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_median": statistics.median(pw) if pw else None,
+                "mem_mhz_median": statistics.median(mem) if mem else None}
 
 
 def cpu_oracle_baseline(n: int, target_s: float = 12.0, f32: bool = False):
@@ -339,11 +343,23 @@ def main():
 
     stats = None
     if not a.no_stats:
+        sclk = ClockSampler(local) if rank == 0 else None
+        if sclk:
+            sclk.start()
+            time.sleep(0.4)
         stats = sampled(a.samples, 100)
+        if sclk:
+            stats["clocks"] = sclk.stop()
         stats["t_eff_per_gpu_gbs_median"] = bpc_(f32) * n ** 3 / (stats["median_ms"] * 1e-3) / 1e9
         if a.init == "paper":   # B:8 (ii): the same timing on non-trivial (random) data
             (app.init_random)(g, T, T2, Ci)
+            rclk = ClockSampler(local) if rank == 0 else None
+            if rclk:
+                rclk.start()
+                time.sleep(0.4)
             stats["random_init"] = sampled(a.samples, 100)
+            if rclk:
+                stats["random_init"]["clocks"] = rclk.stop()
             app.init_paper(g, T, T2, Ci)
         g.check()
     # roofline pass (not timed above): CUDA events around the main stencil launches on their stream

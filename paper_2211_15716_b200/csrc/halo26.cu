@@ -152,8 +152,10 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
         int iti = s_it;
         if (bt >= nbatch) break;
         const long long c0 = bt * kH26Batch, c1 = min(c0 + kH26Batch, P.nchunks);
-        if (c0 >= P.nstore_chunks && mydone) flush();   // (claims are monotonic: no store work follows)
         for (long long c = c0; c < c1; ++c) {
+            // before the first unpack chunk (the only ones that wait on this launch), count my store
+            // chunks: claims are monotonic, so no store work follows (block-uniform)
+            if (c >= P.nstore_chunks && mydone) flush();
             while (iti + 1 < P.nitems && items[iti + 1].chunk0 <= c) ++iti;
             const H26Item &it = items[iti];
             if (it.wait >= 0 && s_waited != it.wait) {   // (block-uniform)
