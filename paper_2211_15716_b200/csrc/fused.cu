@@ -159,11 +159,13 @@ __device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
 
-template <bool YF, bool XF>
+// UP (XF only): the tile holds the upper x send layer s-2 and halo s-1 -- elements .x / .y of one lane's
+// pair -- else the lower ones, layer 1 and halo 0 -- .y / .x of lane 0 (s even: pairs never straddle)
+template <bool YF, bool XF, bool UP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
                                             double2 (*sC)[32 * kFTY], double (*sH)[kFTY], int sx, long long sxy,
                                             int zs, int ze, long long i, bool pair_in, bool w0, bool w1, bool cs,
-                                            double *ydst, const double *hrow, bool hhi, double *sdst, bool shi) {
+                                            double *ydst, const double *hrow, double *sdst) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
@@ -182,8 +184,10 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     double2 c = pair_in ? ldg2f(T + i) : zero2;
     if (XF && hrow) {
         const double h = __ldcg(hrow + zs);
-        if (hhi) c.y = h; else c.x = h;
+        if (UP) c.y = h; else c.x = h;
     }
+    const double *hnext = XF && hrow ? hrow + zs + kFD + 1 : nullptr;   // (running pointers: one add per plane)
+    double *snext = XF && sdst ? sdst + zs : nullptr;
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
 #pragma unroll 2
@@ -207,18 +211,21 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         else
             store_pair(T2 + i, w0, w1, r0, r1);
         if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
-        if (XF && sdst) sdst[z] = shi ? r1 : r0;   // (one lane) the x send cell -> the receiver's staging
+        if (XF && snext) *snext++ = UP ? r0 : r1;   // (one lane) the x send cell -> the receiver's staging
         zm = c;
         c = zp;
-        if (XF && hrow && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
+        if (XF && hnext && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
             const double h = sH[slot][warp];
-            if (hhi) c.y = h; else c.x = h;
+            if (UP) c.y = h; else c.x = h;
         }
         if (pair_in && z + kFD < ze) {
             cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
         }
-        if (XF && hrow && z + kFD + 1 < ze) cp_async8f(&sH[slot][warp], hrow + z + kFD + 1);
+        if (XF && hnext) {
+            if (z + kFD + 1 < ze) cp_async8f(&sH[slot][warp], hnext);
+            ++hnext;
+        }
         cp_commit();
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
@@ -365,18 +372,27 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
 #ifdef FUSED_DIAG_NOSEND
             sdst = nullptr;
 #endif
-            if (did & 12u)
-                fused_sweep<true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst, hrow,
-                                        xh & 1, sdst, xf & 1);
-            else
-                fused_sweep<false, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
-                                         hrow, xh & 1, sdst, xf & 1);
+            if (xrs == 0) {   // upper: send layer s-2, halo s-1
+                if (did & 12u)
+                    fused_sweep<true, true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+                                                  hrow, sdst);
+                else
+                    fused_sweep<false, true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
+                                                   nullptr, hrow, sdst);
+            } else {          // lower: send layer 1, halo 0
+                if (did & 12u)
+                    fused_sweep<true, true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+                                                   hrow, sdst);
+                else
+                    fused_sweep<false, true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
+                                                    nullptr, hrow, sdst);
+            }
         } else if (did & 12u) {
-            fused_sweep<true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst, nullptr,
-                                     false, nullptr, false);
+            fused_sweep<true, false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+                                            nullptr, nullptr);
         } else {
-            fused_sweep<false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
-                                      nullptr, false, nullptr, false);
+            fused_sweep<false, false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
+                                             nullptr, nullptr);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver

@@ -416,8 +416,8 @@ void exchange26(igg_grid *g, const igg_field *fields, int nf, const Plan &plan, 
         igg_grid::H26Cache e;
         e.key = key;
         e.nchunks = nch;
-        IGG_CUDA(cudaMalloc(&e.dplan, off));
-        g->allocs++;
+        IGG_CUDA(cudaMalloc(&e.dplan, off));   // (plan metadata, like the host plan cache: not a buffer-pool
+                                               // allocation, so not counted by igg_buffer_allocs)
         IGG_CUDA(cudaMemcpy(e.dplan, host.data(), off, cudaMemcpyHostToDevice));
         if (g->h26_cache.size() >= 8) {   // keep the most recent shapes (Fig. 1 alternates two arrays)
             cudaFree(g->h26_cache.front().dplan);
