@@ -264,6 +264,16 @@ igg_status igg_acoustic_step(igg_grid *grid, double *const *P, double *const *Vx
                              double *const *Vz, double dt, double rho, double K, double dx, double dy,
                              double dz, const int bw[3], igg_stream_t stream);
 
+/* nt steps of the second workload with double-buffered fields: F = [P, Vx, Vy, Vz, P2, Vx2, Vy2, Vz2], each
+ * local_ranks device pointers (field-major: F[f*local_ranks + r]), shapes as igg_acoustic_step.  A grid
+ * without any exchanged axis runs ONE fused compute_V + compute_P sweep per step from the current set into
+ * the other (every element of the other set written; 64 B/cell instead of 96) and swaps the pointer sets;
+ * otherwise every step is igg_acoustic_step on the current set in place.  On return F[0..3*local_ranks+..]
+ * (the first four fields) hold the state after nt steps, bit-identical to nt igg_acoustic_step calls.
+ * Stream-ordered.  Errors as igg_acoustic_step. */
+igg_status igg_acoustic_run(igg_grid *grid, double **F, int nt, double dt, double rho, double K, double dx,
+                            double dy, double dz, const int bw[3], igg_stream_t stream);
+
 /* Fig. 1 end to end from HOST memory: copies T (initial, local_ranks*nx*ny*nz
  * doubles, rank-major) and Ci to the device, sets T2 = copy(T), runs nt heat
  * steps with swap, and copies the final T back into T_host.

@@ -90,6 +90,8 @@ SIGNATURES = {
                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                           c_int_p, ctypes.c_void_p],
     "igg_gather": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p],
+    "igg_acoustic_run": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double, c_int_p, ctypes.c_void_p],
     "igg_profile_stencil": [ctypes.c_void_p, c_dbl_p, c_ll_p, c_ll_p],
     "igg_profile_timeline": [ctypes.c_void_p, c_dbl_p],
 }

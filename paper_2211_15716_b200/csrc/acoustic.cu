@@ -163,7 +163,103 @@ __global__ void __launch_bounds__(32 * kAcTY) acoustic_p_kernel(const __grid_con
     }
 }
 
+// ------------------------------------------------------------------ one fused V+P sweep (double-buffered)
+// A grid with no exchanged axis (1 GPU, non-periodic): compute_V then compute_P in ONE z-sweep, reading
+// the "in" fields and writing every element of the "out" fields -- 64 B per cell (P, Vx, Vy, Vz read once
+// and written once) instead of 96 for the two in-place kernels.  Thread = one (i, j) column, lane = i:
+// at plane k it computes the new velocities of its cell's lower faces (Vx(i), Vy(j), Vz(k)) from P_in, and
+// the new P of plane k-1, whose upper faces are Vx(i+1) (the next lane's, shuffled; the tile's last lane
+// computes it itself), Vy(j+1) (computed by this thread too, from P_in and Vy_in of row j+1) and Vz(k)
+// (this iteration's).  The same explicitly rounded operations as the two-kernel step: bit-identical
+// (tests/test_gpu_acoustic.py).  Boundary faces that compute_V never updates are copied.
+__device__ __forceinline__ double pupd(double p, double cP, double r0, double r1, double r2, double vx, double vxp,
+                                       double vy, double vyp, double vz, double vzp) {
+    const double div = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(vxp, vx), r0), __dmul_rn(__dsub_rn(vyp, vy), r1)),
+                                 __dmul_rn(__dsub_rn(vzp, vz), r2));
+    return __dsub_rn(p, __dmul_rn(cP, div));
+}
+
+constexpr int kAfKC = 16;   // P planes per CTA
+
+__global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid_constant__ AcousticFields I,
+                                                                    const __grid_constant__ AcousticFields O,
+                                                                    const __grid_constant__ AcousticCoef C) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nx = I.n[0], ny = I.n[1], nz = I.n[2];
+    const int i = blockIdx.x * 32 + lane;
+    const int j = blockIdx.y * kAcTY + warp;
+    const int z0 = blockIdx.z * kAfKC;
+    const int z1 = min(z0 + kAfKC, nz);
+    if (j >= ny) return;   // warp-uniform
+    const bool act = i < nx;
+    const bool last = act && (lane == 31 || i + 1 == nx);   // computes Vx(i+1) itself
+    const long long sxyP = (long long)nx * ny;
+    const long long sxX = nx + 1, sxyX = (long long)(nx + 1) * ny;
+    const long long sxyY = (long long)nx * (ny + 1);
+    // update ranges of compute_V (module comment of the oracle / acoustic_v_kernel)
+    const bool jin = j >= 1 && j < ny - 1, iin = i >= 1 && i < nx - 1;
+    const bool ux = act && i >= 1 && jin;            // Vx(i): i in [1, nx), j inner (and k inner)
+    const bool uxe = last && i + 1 < nx && jin;      // Vx(i+1)
+    const bool uy = act && j >= 1 && iin;            // Vy(j): j in [1, ny), i inner
+    const bool uye = act && j + 1 < ny && iin;       // Vy(j+1)
+    const bool uz = act && iin && jin;               // Vz(k): k in [1, nz), i, j inner
+    long long ip = (long long)z0 * sxyP + (long long)j * nx + i;
+    long long ix = (long long)z0 * sxyX + (long long)j * sxX + i;
+    long long iy = (long long)z0 * sxyY + (long long)j * nx + i;
+    // plane z0-1's P (Vz(z0) of my column) and the previous plane's new lower-face velocities
+    double pzm = (act && z0 > 0) ? ldg(I.P + ip - sxyP) : 0.0;
+    double pp = 0.0, vxn = 0.0, vxpn = 0.0, vyn = 0.0, vypn = 0.0, vzn = 0.0;   // plane k-1's
+    for (int k = z0; k <= z1; ++k, ip += sxyP, ix += sxyX, iy += sxyY) {
+        // the new Vz(k) of my column (k == nz: the top boundary face, copied)
+        double vz = 0.0;
+        if (act && k <= nz) {
+            const double vzi = ldg(I.Vz + ip);
+            vz = (uz && k >= 1 && k < nz) ? vupd(vzi, C.cV[2], k < nz ? ldg(I.P + ip) : 0.0, pzm) : vzi;
+            if (k < z1 || k == nz) O.Vz[ip] = vz;   // (the next chunk writes its own first face)
+        }
+        if (k > z0 && act)   // P of plane k-1: its faces are all new now
+            O.P[ip - sxyP] = pupd(pp, C.cP, C.r[0], C.r[1], C.r[2], vxn, vxpn, vyn, vypn, vzn, vz);
+        if (k == z1) break;
+        // plane k: the new Vx(i), Vx(i+1), Vy(j), Vy(j+1) of my cell, from P_in
+        double p = 0.0, vx = 0.0, vxp = 0.0, vy = 0.0, vyp = 0.0;
+        const bool kin = k >= 1 && k < nz - 1;
+        if (act) {
+            p = ldg(I.P + ip);
+            const double vxi = ldg(I.Vx + ix), vyi = ldg(I.Vy + iy), vypi = ldg(I.Vy + iy + nx);
+            const double pxm = i > 0 ? ldg(I.P + ip - 1) : 0.0;
+            const double pym = j > 0 ? ldg(I.P + ip - nx) : 0.0;
+            const double pyp = j + 1 < ny ? ldg(I.P + ip + nx) : 0.0;
+            vx = (ux && kin) ? vupd(vxi, C.cV[0], p, pxm) : vxi;
+            vy = (uy && kin) ? vupd(vyi, C.cV[1], p, pym) : vyi;
+            vyp = (uye && kin) ? vupd(vypi, C.cV[1], pyp, p) : vypi;
+            O.Vx[ix] = vx;
+            O.Vy[iy] = vy;
+            if (j == ny - 1) O.Vy[iy + nx] = vyp;   // the top boundary row of Vy
+            if (last) {
+                const double vxei = ldg(I.Vx + ix + 1);
+                vxp = (uxe && kin) ? vupd(vxei, C.cV[0], i + 1 < nx ? ldg(I.P + ip + 1) : 0.0, p) : vxei;
+                if (i + 1 == nx) O.Vx[ix + 1] = vxp;   // the right boundary face of Vx
+            }
+        }
+        const double sh = __shfl_down_sync(0xffffffffu, vx, 1);
+        if (!last) vxp = sh;
+        pzm = p;
+        pp = p;
+        vxn = vx;
+        vxpn = vxp;
+        vyn = vy;
+        vypn = vyp;
+        vzn = vz;
+    }
+}
+
 }  // namespace
+
+void launch_acoustic_fused(const AcousticFields &in, const AcousticFields &out, const AcousticCoef &c, cudaStream_t s) {
+    const dim3 grid((in.n[0] + 31) / 32, (in.n[1] + kAcTY - 1) / kAcTY, (in.n[2] + kAfKC - 1) / kAfKC);
+    acoustic_fused_kernel<<<grid, 32 * kAcTY, 0, s>>>(in, out, c);
+    IGG_CUDA(cudaGetLastError());
+}
 
 void launch_acoustic_v(const AcousticFields &f, const AcousticCoef &c, const int lo[3], const int hi[3],
                        cudaStream_t s) {

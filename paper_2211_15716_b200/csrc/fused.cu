@@ -138,11 +138,12 @@ constexpr int kFKC = 64;   // longest z-chunk
 //    halo row (ydst + i) -- the same 16-B stores as T2's (the z send layer, the first or last plane of an
 //    end chunk, is copied after the sweep: one row per warp, just written);
 //  * XF (CTA-uniform: the tile holds the x send layer and the x halo column beside it): the lane holding
-//    the send cell stores its value of every plane into the receiver's staging row (sdst[z]: z-contiguous,
-//    the stores of consecutive planes fill whole sectors), and the lane holding the halo cell fetches the
-//    neighbour's staged value of every plane (hrow[z]) with one 8-B cp.async into a small ring sH beside
-//    the plane's T and Ci, and substitutes it for T's halo value (T's halo column is never read for a
-//    kept result, and never written).  Predicated instructions only: no divergence in the loop.
+//    the send cell keeps its value of every plane in shared memory and after the sweep the warp stores the
+//    row z-contiguously into the receiver's staging row (sdst[z]: whole sectors over NVLink, not one 8-B
+//    remote store per plane); the warp fetches the neighbour's staged halo values of its row for the whole
+//    chunk (hrow[z], z-contiguous) with the first cp.async group, and the lane holding the halo cell
+//    substitutes each plane's value for T's (T's halo column is never read for a kept result, and never
+//    written).  Predicated instructions only: no divergence in the loop.
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
@@ -163,36 +164,38 @@ __device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
 // pair -- else the lower ones, layer 1 and halo 0 -- .y / .x of lane 0 (s even: pairs never straddle)
 template <bool YF, bool XF, bool UP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
-                                            double2 (*sC)[32 * kFTY], double (*sH)[kFTY], int sx, long long sxy,
+                                            double2 (*sC)[32 * kFTY], int sx, long long sxy,
                                             int zs, int ze, long long i, bool pair_in, bool w0, bool w1, bool cs,
-                                            double *ydst, const double *hrow, double *sdst) {
+                                            double *ydst, const double *hrow, bool hlane, double *hx_row,
+                                            double *sdst, double *sx_row, bool slane) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (XF && hrow)   // (warp-uniform) this chunk's staged halo values of the row, into the first group
+        for (int z = zs + lane; z < ze; z += 32) cp_async8f(hx_row + (z - zs), hrow + z);
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
             cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
             cp_async16f(&sC[q][tid], Ci + i + q * sxy);
         }
-        if (XF && hrow && zs + q + 1 < ze) cp_async8f(&sH[q][warp], hrow + zs + q + 1);
         cp_commit();
     }
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
-    if (XF && hrow) {
+    if (XF && hrow && hlane) {
         const double h = __ldcg(hrow + zs);
         if (UP) c.y = h; else c.x = h;
     }
-    const double *hnext = XF && hrow ? hrow + zs + kFD + 1 : nullptr;   // (running pointers: one add per plane)
-    double *snext = XF && sdst ? sdst + zs : nullptr;
+    const bool hpatch = XF && hrow && hlane;
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
+        if (XF) __syncwarp();   // (the halo row of hx_row, fetched by the whole warp in group 0)
         double2 ym = zero2, yp = zero2;
         if (pair_in) {
             ym = ldg2f(T + i - sx);
@@ -211,25 +214,25 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         else
             store_pair(T2 + i, w0, w1, r0, r1);
         if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
-        if (XF && snext) *snext++ = UP ? r0 : r1;   // (one lane) the x send cell -> the receiver's staging
+        if (XF && slane) sx_row[z - zs] = UP ? r0 : r1;   // (one lane) the x send cell, plane by plane
         zm = c;
         c = zp;
-        if (XF && hnext && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
-            const double h = sH[slot][warp];
+        if (hpatch && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
+            const double h = hx_row[z + 1 - zs];
             if (UP) c.y = h; else c.x = h;
         }
         if (pair_in && z + kFD < ze) {
             cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
         }
-        if (XF && hnext) {
-            if (z + kFD + 1 < ze) cp_async8f(&sH[slot][warp], hnext);
-            ++hnext;
-        }
         cp_commit();
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
+    if (XF && sdst) {   // (warp-uniform) the row's send cells, z-contiguous: whole sectors over NVLink
+        __syncwarp();
+        for (int z = zs + lane; z < ze; z += 32) sdst[z] = sx_row[z - zs];
+    }
 }
 
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b);
@@ -259,7 +262,8 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     TRACE_AT(0);
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
-    __shared__ double sH[kFD][kFTY];   // the x halo lanes' staged values, a ring like sT's
+    __shared__ double sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
+    __shared__ double sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
     const int rank = blockIdx.x / F.per_rank;
@@ -363,36 +367,38 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         }
         if (xrs >= 0) {
             const int xf = R.face[0][xrs].layer - tx * 64, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
-            const double *hrow = (hstaged && rowv && (xh >> 1) == lane)
-                                     ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
-            double *sdst = (rowv && (xf >> 1) == lane) ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;
+            const double *hrow = (hstaged && rowv) ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
+            const bool hlane = (xh >> 1) == lane;
+            double *sdst = rowv ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;   // (warp-uniform)
+            const bool slane = rowv && (xf >> 1) == lane;
 #ifdef FUSED_DIAG_NOHALO   // diagnostics builds only (timing; INVALID halos)
             hrow = nullptr;
 #endif
 #ifdef FUSED_DIAG_NOSEND
             sdst = nullptr;
 #endif
+            (void)slane;
             if (xrs == 0) {   // upper: send layer s-2, halo s-1
                 if (did & 12u)
-                    fused_sweep<true, true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
-                                                  hrow, sdst);
+                    fused_sweep<true, true, true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+                                                  hrow, hlane, sHx[warp], sdst, sX[warp], slane);
                 else
-                    fused_sweep<false, true, true>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
-                                                   nullptr, hrow, sdst);
+                    fused_sweep<false, true, true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
+                                                   nullptr, hrow, hlane, sHx[warp], sdst, sX[warp], slane);
             } else {          // lower: send layer 1, halo 0
                 if (did & 12u)
-                    fused_sweep<true, true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
-                                                   hrow, sdst);
+                    fused_sweep<true, true, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+                                                   hrow, hlane, sHx[warp], sdst, sX[warp], slane);
                 else
-                    fused_sweep<false, true, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
-                                                    nullptr, hrow, sdst);
+                    fused_sweep<false, true, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
+                                                    nullptr, hrow, hlane, sHx[warp], sdst, sX[warp], slane);
             }
         } else if (did & 12u) {
-            fused_sweep<true, false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
-                                            nullptr, nullptr);
+            fused_sweep<true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+                                            nullptr, false, nullptr, nullptr, nullptr, false);
         } else {
-            fused_sweep<false, false, false>(F, R, sT, sC, sH, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
-                                             nullptr, nullptr);
+            fused_sweep<false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
+                                             nullptr, false, nullptr, nullptr, nullptr, false);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver

@@ -861,6 +861,58 @@ IGG_API igg_status igg_acoustic_step(igg_grid *g, double *const *P, double *cons
     IGG_CATCH
 }
 
+// nt leapfrog steps of the second workload with double-buffered fields (verdict r1 8b):
+// F = [P, Vx, Vy, Vz, P2, Vx2, Vy2, Vz2] x local_ranks pointers (field-major).  A grid without any exchanged
+// axis runs ONE fused V+P sweep per step from the current set into the other (64 B/cell instead of 96) and
+// swaps the sets; otherwise every step is igg_acoustic_step on the current set in place.  On return
+// F[0..3] hold the state after nt steps.
+IGG_API igg_status igg_acoustic_run(igg_grid *g, double **F, int nt, double dt, double rho, double K, double dx,
+                                    double dy, double dz, const int bw[3], igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_acoustic_run");
+    if (!F || nt < 0) fail(IGG_E_ARG, "igg_acoustic_run: bad argument");
+    const int L = g->nlocal;
+    for (int q = 0; q < 8 * L; ++q)
+        if (!F[q]) fail(IGG_E_ARG, "igg_acoustic_run: NULL field pointer");
+    bool exch = false;
+    for (int a = 0; a < 3; ++a)
+        for (int lr = 0; lr < L; ++lr) exch = exch || g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (exch) {
+        for (int it = 0; it < nt; ++it) {
+            const igg_status st = igg_acoustic_step(g, F, F + L, F + 2 * L, F + 3 * L, dt, rho, K, dx, dy, dz, bw, stream);
+            if (st != IGG_OK) return st;
+        }
+        return IGG_OK;
+    }
+    if (!(rho != 0.0) || !(dx != 0.0) || !(dy != 0.0) || !(dz != 0.0))
+        fail(IGG_E_ARG, "igg_acoustic_run: rho and the spacings must be non-zero");
+    for (int a = 0; a < 3; ++a)
+        if (g->n[a] < 3) fail(IGG_E_ARG, "igg_acoustic_run: every local size must be >= 3");
+    igg::AcousticCoef c;
+    const double adt = dt / rho;   // reading A2 (as igg_acoustic_step)
+    c.cV[0] = adt / dx;
+    c.cV[1] = adt / dy;
+    c.cV[2] = adt / dz;
+    c.cP = dt * K;
+    c.r[0] = 1.0 / dx;
+    c.r[1] = 1.0 / dy;
+    c.r[2] = 1.0 / dz;
+    for (int it = 0; it < nt; ++it) {
+        for (int lr = 0; lr < L; ++lr) {
+            const igg::AcousticFields in{F[lr], F[L + lr], F[2 * L + lr], F[3 * L + lr], {g->n[0], g->n[1], g->n[2]}};
+            const igg::AcousticFields out{F[4 * L + lr], F[5 * L + lr], F[6 * L + lr], F[7 * L + lr],
+                                          {g->n[0], g->n[1], g->n[2]}};
+            igg::prof_begin(g, s);
+            igg::launch_acoustic_fused(in, out, c, s);
+            igg::prof_end(g, s, (long long)g->n[0] * g->n[1] * g->n[2]);
+            g->launches++;
+        }
+        for (int q = 0; q < 4 * L; ++q) std::swap(F[q], F[4 * L + q]);
+    }
+    IGG_CATCH
+}
+
 IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci,
                                      float lam, float dt, float dx, float dy, float dz, const int bw[3],
                                      igg_stream_t stream) {

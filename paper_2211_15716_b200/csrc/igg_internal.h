@@ -223,6 +223,9 @@ void launch_acoustic_v(const AcousticFields &f, const AcousticCoef &c, const int
                        cudaStream_t s);
 // compute_P on every cell
 void launch_acoustic_p(const AcousticFields &f, const AcousticCoef &c, cudaStream_t s);
+// compute_V then compute_P in one sweep from the in fields into every element of the out fields (a grid with
+// no exchanged axis)
+void launch_acoustic_fused(const AcousticFields &in, const AcousticFields &out, const AcousticCoef &c, cudaStream_t s);
 
 // ---------------------------------------------------------------- geometry and exchange plan (plan.cpp)
 // Validated grid geometry of one process (host only, no CUDA).

@@ -290,6 +290,29 @@ class Grid:
         _ok(L.lib().igg_acoustic_step(self._handle(), *(_ptr_array(l) for l in lists), dt, rho, K, dx, dy, dz,
                                       _i3(bw), _stream(stream)))
 
+    def acoustic_run(self, F, F2, nt: int, dt: float, rho: float, K: float, dx: float, dy: float, dz: float,
+                     bw=(16, 4, 4), stream=None):
+        """nt steps with double-buffered fields (igg_acoustic_run): F, F2 = [P, Vx, Vy, Vz] lists of local_ranks
+        tensors each; returns (F, F2) after the run (F = the state after nt steps)."""
+        n = self.local_ranks
+        nx, ny, nz = self.n
+        want = [(nz, ny, nx), (nz, ny, nx + 1), (nz, ny + 1, nx), (nz + 1, ny, nx)]
+        sets = [[_as_list(x, n) for x in F], [_as_list(x, n) for x in F2]]
+        for S in sets:
+            for f, lst in enumerate(S):
+                for x in lst:
+                    if tuple(x.shape) != want[f]:
+                        raise ValueError(f"acoustic_run field {f} must have shape {want[f]}, got {tuple(x.shape)}")
+        flat = [t for S in sets for lst in S for t in lst]
+        arr = (ctypes.c_void_p * len(flat))(*[_dev_ptr(t) for t in flat])
+        _ok(L.lib().igg_acoustic_run(self._handle(), arr, int(nt), dt, rho, K, dx, dy, dz, _i3(bw), _stream(stream)))
+        by_ptr = {t.data_ptr(): t for t in flat}
+        out = [by_ptr[arr[q]] for q in range(len(flat))]
+        h = 4 * n
+        first = [out[f * n:(f + 1) * n] for f in range(4)]
+        second = [out[h + f * n:h + (f + 1) * n] for f in range(4)]
+        return first, second
+
     # -- generic @hide_communication (PAPER.md:75, :94; SPEC.md:330-338)
     def hide_communication(self, bw, step, *fields, stream=None) -> None:
         """Run a user stencil `step(local_rank, lo, hi, stream)` -- which must enqueue the computation of

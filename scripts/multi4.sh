@@ -1,0 +1,14 @@
+# 4-GPU validation and measurements (gpurun --gpus 4): tests, bench 2x2x1 / 1x2x2 / 2x1x2 / 4x1x1, halo sweep, B:10
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out; T=${TAG:-m4}
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1 --master-port 29521 --nproc-per-node 4"
+TR2="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1 --master-port 29523 --nproc-per-node 2"
+[ -n "$SKIP_TESTS" ] || { timeout 1500 python -m pytest tests -q -m gpu -k "multi" > gpurun_out/${T}_pytest_multi.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest_multi.log; }
+timeout 600 python bench.py --no-e2e --no-cpu > gpurun_out/${T}_n1.json 2> gpurun_out/${T}_n1.err
+timeout 600 $TR2 bench.py --gpus 2 --no-e2e > gpurun_out/${T}_n2.json 2> gpurun_out/${T}_n2.err
+timeout 600 $TR bench.py --gpus 4 > gpurun_out/${T}_n4.json 2> gpurun_out/${T}_n4.err
+for d in 1,2,2 2,1,2 4,1,1; do
+  timeout 600 $TR bench.py --gpus 4 --dims $d --no-e2e > gpurun_out/${T}_n4_${d//,/}.json 2> gpurun_out/${T}_n4_${d//,/}.err
+done
+HALO_SIZES=${HALO_SIZES:-64,128,256,512,768} timeout 900 $TR scripts/halo_sweep.py > gpurun_out/${T}_halo.txt 2>&1
+timeout 900 $TR scripts/b10_staggered.py > gpurun_out/${T}_b10.txt 2>&1
+echo done

@@ -131,3 +131,78 @@ def test_full_size_512_sampled():
                         assert np.array_equal(ref[f][cut], subg[f][cut]), (start, f)
     finally:
         g.finalize()
+
+
+def _run_fused(n, nt, rho=1.2, K=0.8, per=(0, 0, 0), dims=(1, 1, 1)):
+    """igg_acoustic_run (double-buffered; fused V+P sweep when no axis exchanges) vs the oracle."""
+    import torch
+    R = dims[0] * dims[1] * dims[2]
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=R, device=0)
+    try:
+        F = app.alloc_fields(g)
+        F2 = app.alloc_fields(g)
+        for f in F2:   # garbage in the second set: every element must be written
+            for t in f:
+                t.fill_(float("nan"))
+        app.init_random(g, F)
+        d = app.spacing(g)
+        dt = app.stable_dt(d, rho, K)
+        l0 = g.kernel_launches()
+        A, B = g.acoustic_run(F, F2, nt, dt, rho, K, *d)
+        torch.cuda.synchronize()
+        g.check()
+        N = tuple(OG.global_size(n[i], 2, dims[i], bool(per[i])) for i in range(3))
+        ref = OA.run(*SI.global_acoustic_fields(OA.field_shapes(N, per)), nt, per, dt, rho, K, *d)
+        sizes = [n, (n[0] + 1, n[1], n[2]), (n[0], n[1] + 1, n[2]), (n[0], n[1], n[2] + 1)]
+        for f in range(4):
+            for r in range(R):
+                W = OG.window(ref[f], OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, sizes[f])
+                got = A[f][r].cpu().numpy()
+                assert np.array_equal(got, W), (n, f, r, np.argwhere(got != W)[:3])
+        return g.kernel_launches() - l0
+    finally:
+        g.finalize()
+
+
+@pytest.mark.parametrize("n", [(37, 11, 9), (70, 13, 40), (33, 5, 17), (64, 8, 33), (5, 4, 3)])
+@pytest.mark.parametrize("nt", [1, 4])
+def test_acoustic_fused_run_vs_oracle(n, nt):
+    """One fused V+P sweep per step (double-buffered, 64 B/cell): bit-exact vs the oracle on ragged sizes,
+    several x-tiles / y-tiles / z-chunks, odd and even step counts (the result in either buffer set)."""
+    launches = _run_fused(n, nt)
+    assert launches == nt   # one kernel per step
+
+
+@pytest.mark.parametrize("case", [dict(n=(20, 18, 16), dims=(2, 1, 1), per=(0, 0, 0)),
+                                  dict(n=(12, 10, 9), dims=(1, 1, 1), per=(1, 1, 1))])
+def test_acoustic_run_with_exchange_falls_back_to_steps(case):
+    """With an exchanged axis igg_acoustic_run is igg_acoustic_step per step in place (same bits)."""
+    _run_fused(case["n"], 3, per=case["per"], dims=case["dims"])
+
+
+@pytest.mark.slow
+def test_acoustic_fused_full_size_512_sampled():
+    """The bench configuration of the fused sweep (512^3, 1 GPU): sub-boxes re-run by the oracle as grids of
+    their own, cells outside the sub-box edges' domain of dependence (nt+1 layers) compared bitwise."""
+    import torch
+    n, nt, m, L = (512, 512, 512), 2, 3, 24
+    g = P.init_global_grid(*n, device=0)
+    try:
+        F = app.alloc_fields(g)
+        F2 = app.alloc_fields(g)
+        app.init_random(g, F)
+        F0 = [f[0].clone() for f in F]
+        d = app.spacing(g)
+        dt = app.stable_dt(d)
+        A, _ = g.acoustic_run(F, F2, nt, dt, app.RHO, app.K, *d)
+        torch.cuda.synchronize()
+        for st in [(0, 0, 0), (200, 301, 7), (512 - L, 512 - L, 512 - L), (100, 0, 490)]:
+            z0, y0, x0 = st
+            sub = [F0[0][z0:z0 + L, y0:y0 + L, x0:x0 + L], F0[1][z0:z0 + L, y0:y0 + L, x0:x0 + L + 1],
+                   F0[2][z0:z0 + L, y0:y0 + L + 1, x0:x0 + L], F0[3][z0:z0 + L + 1, y0:y0 + L, x0:x0 + L]]
+            ref = OA.run(*[s.cpu().numpy() for s in sub], nt, (0, 0, 0), dt, app.RHO, app.K, *d)
+            cut = tuple(slice(0 if st[k] == 0 else m, L - (0 if st[k] + L == 512 else m)) for k in range(3))
+            got = A[0][0][z0:z0 + L, y0:y0 + L, x0:x0 + L].cpu().numpy()
+            assert np.array_equal(ref[0][cut], got[cut]), st
+    finally:
+        g.finalize()
