@@ -181,6 +181,31 @@ __device__ __forceinline__ double pupd(double p, double cP, double r0, double r1
 
 constexpr int kAfKC = 16;   // P planes per CTA
 
+// the in-field values one thread needs at plane k (loaded one plane ahead)
+struct AfPlane {
+    double p, pxm, pym, pyp, vx, vy, vyp, vz, vxe, pxp;
+};
+
+__device__ __forceinline__ void af_load(AfPlane &v, const AcousticFields &I, bool act, bool last, int i, int j, int k,
+                                        long long ip, long long ix, long long iy) {
+    const int nx = I.n[0], ny = I.n[1], nz = I.n[2];
+    v = AfPlane{};
+    if (!act) return;
+    v.vz = ldg(I.Vz + ip);   // (k <= nz: Vz has nz+1 planes)
+    if (k >= nz) return;
+    v.p = ldg(I.P + ip);
+    v.vx = ldg(I.Vx + ix);
+    v.vy = ldg(I.Vy + iy);
+    v.vyp = ldg(I.Vy + iy + nx);
+    if ((threadIdx.x & 31) == 0 && i > 0) v.pxm = ldg(I.P + ip - 1);
+    if (j > 0) v.pym = ldg(I.P + ip - nx);
+    if (j + 1 < ny) v.pyp = ldg(I.P + ip + nx);
+    if (last) {
+        v.vxe = ldg(I.Vx + ix + 1);
+        if (i + 1 < nx) v.pxp = ldg(I.P + ip + 1);
+    }
+}
+
 __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid_constant__ AcousticFields I,
                                                                     const __grid_constant__ AcousticFields O,
                                                                     const __grid_constant__ AcousticCoef C) {
@@ -196,7 +221,7 @@ __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid
     const long long sxyP = (long long)nx * ny;
     const long long sxX = nx + 1, sxyX = (long long)(nx + 1) * ny;
     const long long sxyY = (long long)nx * (ny + 1);
-    // update ranges of compute_V (module comment of the oracle / acoustic_v_kernel)
+    // update ranges of compute_V (oracle/acoustic3d.py, acoustic_v_kernel)
     const bool jin = j >= 1 && j < ny - 1, iin = i >= 1 && i < nx - 1;
     const bool ux = act && i >= 1 && jin;            // Vx(i): i in [1, nx), j inner (and k inner)
     const bool uxe = last && i + 1 < nx && jin;      // Vx(i+1)
@@ -206,50 +231,41 @@ __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid
     long long ip = (long long)z0 * sxyP + (long long)j * nx + i;
     long long ix = (long long)z0 * sxyX + (long long)j * sxX + i;
     long long iy = (long long)z0 * sxyY + (long long)j * nx + i;
-    // plane z0-1's P (Vz(z0) of my column) and the previous plane's new lower-face velocities
-    double pzm = (act && z0 > 0) ? ldg(I.P + ip - sxyP) : 0.0;
-    double pp = 0.0, vxn = 0.0, vxpn = 0.0, vyn = 0.0, vypn = 0.0, vzn = 0.0;   // plane k-1's
+    double pzm = (act && z0 > 0) ? ldg(I.P + ip - sxyP) : 0.0;   // P_in of plane k-1
+    double pp = 0.0, vxn = 0.0, vxpn = 0.0, vyn = 0.0, vypn = 0.0, vzn = 0.0;   // plane k-1's new values
+    AfPlane cur, nxt;
+    af_load(cur, I, act, last, i, j, z0, ip, ix, iy);
     for (int k = z0; k <= z1; ++k, ip += sxyP, ix += sxyX, iy += sxyY) {
+        if (k < z1) af_load(nxt, I, act, last, i, j, k + 1, ip + sxyP, ix + sxyX, iy + sxyY);   // one plane ahead
         // the new Vz(k) of my column (k == nz: the top boundary face, copied)
-        double vz = 0.0;
-        if (act && k <= nz) {
-            const double vzi = ldg(I.Vz + ip);
-            vz = (uz && k >= 1 && k < nz) ? vupd(vzi, C.cV[2], k < nz ? ldg(I.P + ip) : 0.0, pzm) : vzi;
-            if (k < z1 || k == nz) O.Vz[ip] = vz;   // (the next chunk writes its own first face)
-        }
+        const double vz = (uz && k >= 1 && k < nz) ? vupd(cur.vz, C.cV[2], cur.p, pzm) : cur.vz;
+        if (act && (k < z1 || k == nz)) O.Vz[ip] = vz;   // (the next chunk writes its own first face)
         if (k > z0 && act)   // P of plane k-1: its faces are all new now
             O.P[ip - sxyP] = pupd(pp, C.cP, C.r[0], C.r[1], C.r[2], vxn, vxpn, vyn, vypn, vzn, vz);
         if (k == z1) break;
-        // plane k: the new Vx(i), Vx(i+1), Vy(j), Vy(j+1) of my cell, from P_in
-        double p = 0.0, vx = 0.0, vxp = 0.0, vy = 0.0, vyp = 0.0;
+        // plane k: the new Vx(i), Vx(i+1), Vy(j), Vy(j+1) of my cell
         const bool kin = k >= 1 && k < nz - 1;
+        double xm = __shfl_up_sync(0xffffffffu, cur.p, 1);
+        if (lane == 0) xm = cur.pxm;
+        const double vx = (ux && kin) ? vupd(cur.vx, C.cV[0], cur.p, xm) : cur.vx;
+        const double vy = (uy && kin) ? vupd(cur.vy, C.cV[1], cur.p, cur.pym) : cur.vy;
+        const double vyp = (uye && kin) ? vupd(cur.vyp, C.cV[1], cur.pyp, cur.p) : cur.vyp;
+        double vxp = __shfl_down_sync(0xffffffffu, vx, 1);
+        if (last) vxp = (uxe && kin) ? vupd(cur.vxe, C.cV[0], cur.pxp, cur.p) : cur.vxe;
         if (act) {
-            p = ldg(I.P + ip);
-            const double vxi = ldg(I.Vx + ix), vyi = ldg(I.Vy + iy), vypi = ldg(I.Vy + iy + nx);
-            const double pxm = i > 0 ? ldg(I.P + ip - 1) : 0.0;
-            const double pym = j > 0 ? ldg(I.P + ip - nx) : 0.0;
-            const double pyp = j + 1 < ny ? ldg(I.P + ip + nx) : 0.0;
-            vx = (ux && kin) ? vupd(vxi, C.cV[0], p, pxm) : vxi;
-            vy = (uy && kin) ? vupd(vyi, C.cV[1], p, pym) : vyi;
-            vyp = (uye && kin) ? vupd(vypi, C.cV[1], pyp, p) : vypi;
             O.Vx[ix] = vx;
             O.Vy[iy] = vy;
-            if (j == ny - 1) O.Vy[iy + nx] = vyp;   // the top boundary row of Vy
-            if (last) {
-                const double vxei = ldg(I.Vx + ix + 1);
-                vxp = (uxe && kin) ? vupd(vxei, C.cV[0], i + 1 < nx ? ldg(I.P + ip + 1) : 0.0, p) : vxei;
-                if (i + 1 == nx) O.Vx[ix + 1] = vxp;   // the right boundary face of Vx
-            }
+            if (j == ny - 1) O.Vy[iy + nx] = vyp;        // the top boundary row of Vy
+            if (last && i + 1 == nx) O.Vx[ix + 1] = vxp;   // the right boundary face of Vx
         }
-        const double sh = __shfl_down_sync(0xffffffffu, vx, 1);
-        if (!last) vxp = sh;
-        pzm = p;
-        pp = p;
+        pzm = cur.p;
+        pp = cur.p;
         vxn = vx;
         vxpn = vxp;
         vyn = vy;
         vypn = vyp;
         vzn = vz;
+        cur = nxt;
     }
 }
 
