@@ -162,16 +162,17 @@ __device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
 
 // UP (XF only): the tile holds the upper x send layer s-2 and halo s-1 -- elements .x / .y of one lane's
 // pair -- else the lower ones, layer 1 and halo 0 -- .y / .x of lane 0 (s even: pairs never straddle)
-template <bool YF, bool XF, bool UP>
+template <bool YF, int XM, bool UP>   // XM: 0 no x face, 1 staged x faces, 2 direct x faces
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
                                             double2 (*sC)[32 * kFTY], int sx, long long sxy,
                                             int zs, int ze, long long i, bool pair_in, bool w0, bool w1, bool cs,
                                             double *ydst, const double *hrow, bool hlane, double *hx_row,
                                             double *sdst, double *sx_row, bool slane) {
+    constexpr bool XF = XM == 1;   // (staged: the receive side and the post-sweep send below)
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     if (XF && hrow)   // (warp-uniform) this chunk's staged halo values of the row, into the first group
         for (int z = zs + lane; z < ze; z += 32) cp_async8f(hx_row + (z - zs), hrow + z);
 #pragma unroll
@@ -190,6 +191,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (UP) c.y = h; else c.x = h;
     }
     const bool hpatch = XF && hrow && hlane;
+    (void)hx_row;
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
 #pragma unroll 2
@@ -215,6 +217,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
             store_pair(T2 + i, w0, w1, r0, r1);
         if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
         if (XF && slane) sx_row[z - zs] = UP ? r0 : r1;   // (one lane) the x send cell, plane by plane
+        if (XM == 2 && slane) sdst[(long long)z * sxy] = UP ? r0 : r1;   // direct: into the receiver's T2 column
         zm = c;
         c = zp;
         if (hpatch && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
@@ -337,7 +340,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     // the x halo column beside the x send layer: staged by the neighbour in the previous step of the run
     // (first step of a run: T holds it)
     const int hside = xrs < 0 ? -1 : (xrs == 0 ? 1 : 0);   // send layer s-2 sits beside halo s-1, 1 beside 0
-    const bool hstaged = xrs >= 0 && F.wait_prev && R.halo[0][hside].active;
+    const bool hstaged = xrs >= 0 && F.wait_prev && R.halo[0][hside].active && !F.xdirect;
 
     if (F.wait_prev) {   // CTA-uniform: this step's halo cells are the previous epoch's faces
         const bool xh0 = R.halo[0][0].active && tx == 0, xh1 = R.halo[0][1].active && tx == F.xtiles - 1;
@@ -367,37 +370,35 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         }
         if (xrs >= 0) {
             const int xf = R.face[0][xrs].layer - tx * 64, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
-            const double *hrow = (hstaged && rowv) ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
-            const bool hlane = (xh >> 1) == lane;
-            double *sdst = rowv ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;   // (warp-uniform)
             const bool slane = rowv && (xf >> 1) == lane;
-#ifdef FUSED_DIAG_NOHALO   // diagnostics builds only (timing; INVALID halos)
-            hrow = nullptr;
-#endif
-#ifdef FUSED_DIAG_NOSEND
-            sdst = nullptr;
-#endif
-            (void)slane;
-            if (xrs == 0) {   // upper: send layer s-2, halo s-1
-                if (did & 12u)
-                    fused_sweep<true, true, true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
-                                                  hrow, hlane, sHx[warp], sdst, sX[warp], slane);
-                else
-                    fused_sweep<false, true, true>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
-                                                   nullptr, hrow, hlane, sHx[warp], sdst, sX[warp], slane);
-            } else {          // lower: send layer 1, halo 0
-                if (did & 12u)
-                    fused_sweep<true, true, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
-                                                   hrow, hlane, sHx[warp], sdst, sX[warp], slane);
-                else
-                    fused_sweep<false, true, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true,
-                                                    nullptr, hrow, hlane, sHx[warp], sdst, sX[warp], slane);
+            if (F.xdirect) {   // x face straight into the receiver's T2 column; T holds my x halo
+                double *xcol = rowv ? R.face[0][xrs].dst + (long long)y * sx + (xrs == 0 ? 0 : sx - 1) : nullptr;
+#define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, 2, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, YD, \
+                                                       nullptr, false, nullptr, xcol, nullptr, slane)
+                if (xrs == 0) {
+                    if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
+                } else {
+                    if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
+                }
+#undef XSWEEP
+            } else {   // staged
+                const double *hrow = (hstaged && rowv) ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
+                const bool hlane = (xh >> 1) == lane;
+                double *sdst = rowv ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;   // (warp-uniform)
+#define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, 1, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, YD, \
+                                                       hrow, hlane, sHx[warp], sdst, sX[warp], slane)
+                if (xrs == 0) {
+                    if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
+                } else {
+                    if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
+                }
+#undef XSWEEP
             }
         } else if (did & 12u) {
-            fused_sweep<true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
+            fused_sweep<true, 0, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
                                             nullptr, false, nullptr, nullptr, nullptr, false);
         } else {
-            fused_sweep<false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
+            fused_sweep<false, 0, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
                                              nullptr, false, nullptr, nullptr, nullptr, false);
         }
     }
@@ -440,7 +441,7 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
         c[third] = t;
         if (forward_phase(F, R, a, c) != b || later_halo(F, R, a, c)) continue;
         double v;
-        if (b == 0 && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1)
+        if (b == 0 && !F.xdirect && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1)
             v = __ldcg(R.xstg + xstg_at(F, F.epoch, side, c[1], c[2]));   // staged, not yet in T2
         else
             v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
@@ -549,10 +550,11 @@ __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
         const int a = f / (2 * F.nchunks), rs = (f / F.nchunks) & 1, ch = f % F.nchunks;
         const FusedHalo &h = R.halo[a][rs];
         if (!h.active || (a == 2 && ch > 0)) continue;
-        if (blockIdx.x == 0 || a == 0) spin_geq(F, h.flag + ch, F.epoch);   // (x data: every block copies)
+        if (blockIdx.x == 0 || (a == 0 && !F.xdirect)) spin_geq(F, h.flag + ch, F.epoch);   // (staged x: every block copies)
         if (blockIdx.x == 0) spin_geq(F, h.xflag + ch, F.epoch);
     }
     __syncthreads();
+    if (F.xdirect) return;   // (direct x faces: already in T2)
     const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
     const long long sxy = (long long)sx * sy, ncell = (long long)(sy - 2) * (sz - 2);
     for (int side = 0; side < 2; ++side) {
@@ -799,7 +801,11 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         g->allocs++;
     }
     const bool comm = !g->skip_comm;
-    const bool xst = comm && (g->dims[0] > 1 || g->periods[0]);   // x halos exist: staging buffers
+#ifndef FUSED_XDIRECT
+#define FUSED_XDIRECT 0
+#endif
+    const bool xdirect = FUSED_XDIRECT != 0;
+    const bool xst = comm && !xdirect && (g->dims[0] > 1 || g->periods[0]);   // x halos exist: staging buffers
     const size_t stg_words = 4 * (size_t)g->n[1] * g->n[2];       // [parity][side][y][z] per rank
     if (xst && !g->fused_xstg) {
         IGG_CUDA(cudaMalloc(&g->fused_xstg, sizeof(double) * stg_words * L));
@@ -813,6 +819,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.err = g->d_err;
     F.k = k;
     F.nranks = L;
+    F.xdirect = xdirect ? 1 : 0;
     bool act[3][2] = {{false, false}, {false, false}, {false, false}};
     bool zex = false;
     // flags of hosted rank lr: data (lr*6 + a*2 + rs) * kMaxChunks, rim/forwarded (L*6 + lr*6 + a*2 + rs)
@@ -842,13 +849,13 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
                         f.dst = T2[li];
                         f.flag = g->flags + (li * 6 + a * 2 + rs) * kMaxChunks;
                         f.xflag = g->flags + (L * 6 + li * 6 + a * 2 + rs) * kMaxChunks;
-                        if (a == 0) R.xstg_peer[rs] = g->fused_xstg + li * stg_words;
+                        if (a == 0 && xst) R.xstg_peer[rs] = g->fused_xstg + li * stg_words;
                     } else {         // another process (one rank each): its arrays mapped over NVLink
                         const int pp = proc_of(g, nb);
                         f.dst = peer_arrays(g, T2[lr])[pp];
                         f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
                         f.xflag = g->peer_flags[pp] + (6 + a * 2 + rs) * kMaxChunks;
-                        if (a == 0) R.xstg_peer[rs] = peer_arrays(g, g->fused_xstg)[pp];
+                        if (a == 0 && xst) R.xstg_peer[rs] = peer_arrays(g, g->fused_xstg)[pp];
                     }
                 }
                 FusedHalo &h = R.halo[a][rs];   // my halo side rs is filled by my neighbour on side rs

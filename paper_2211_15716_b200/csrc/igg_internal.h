@@ -164,6 +164,7 @@ struct FusedParams {
     int zchunk[2];                   // chunk holding the z send layer of face (2, rs); -1 if none
     int xtiles, ytiles;
     int border_first;                // within a chunk: the border tiles (faces) first
+    int xdirect;                     // x faces stored straight into the receiver's T2 column (no staging)
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk) data flag
     const unsigned int *tgt_x;       // ... an xflag (rim + forwarders)
     unsigned long long epoch;
