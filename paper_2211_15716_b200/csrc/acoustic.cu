@@ -180,42 +180,43 @@ __device__ __forceinline__ double pupd(double p, double cP, double r0, double r1
 }
 
 constexpr int kAfKC = 16;   // P planes per CTA
+constexpr int kAfD = 3;     // planes in flight per thread (cp.async ring)
+constexpr int kAfS = 7;     // ring streams: P, Vx, Vy, Vz of my cell; P(j-1), P(j+1), Vy(j+1) of the rows beside
 
-// the in-field values one thread needs at plane k (loaded one plane ahead)
-struct AfPlane {
-    double p, pxm, pym, pyp, vx, vy, vyp, vz, vxe, pxp;
-};
+__device__ __forceinline__ void cp8(double *smem, const double *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cpcommit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpwait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__device__ __forceinline__ void af_load(AfPlane &v, const AcousticFields &I, bool act, bool last, int i, int j, int k,
-                                        long long ip, long long ix, long long iy) {
+// the ring entry of plane k: issue the cp.asyncs of my cell's in-field values (nothing past the fields)
+__device__ __forceinline__ void af_issue(double (*r)[kAfS], const AcousticFields &I, bool act, int j, int k,
+                                         long long ip, long long ix, long long iy) {
     const int nx = I.n[0], ny = I.n[1], nz = I.n[2];
-    v = AfPlane{};
     if (!act) return;
-    v.vz = ldg(I.Vz + ip);   // (k <= nz: Vz has nz+1 planes)
+    cp8(&r[0][3], I.Vz + ip);   // (k <= nz: Vz has nz+1 planes)
     if (k >= nz) return;
-    v.p = ldg(I.P + ip);
-    v.vx = ldg(I.Vx + ix);
-    v.vy = ldg(I.Vy + iy);
-    v.vyp = ldg(I.Vy + iy + nx);
-    if ((threadIdx.x & 31) == 0 && i > 0) v.pxm = ldg(I.P + ip - 1);
-    if (j > 0) v.pym = ldg(I.P + ip - nx);
-    if (j + 1 < ny) v.pyp = ldg(I.P + ip + nx);
-    if (last) {
-        v.vxe = ldg(I.Vx + ix + 1);
-        if (i + 1 < nx) v.pxp = ldg(I.P + ip + 1);
-    }
+    cp8(&r[0][0], I.P + ip);
+    cp8(&r[0][1], I.Vx + ix);
+    cp8(&r[0][2], I.Vy + iy);
+    cp8(&r[0][6], I.Vy + iy + nx);
+    if (j > 0) cp8(&r[0][4], I.P + ip - nx);
+    if (j + 1 < ny) cp8(&r[0][5], I.P + ip + nx);
 }
 
 __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid_constant__ AcousticFields I,
                                                                     const __grid_constant__ AcousticFields O,
                                                                     const __grid_constant__ AcousticCoef C) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ double ring[kAfD][32 * kAcTY][kAfS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
     const int nx = I.n[0], ny = I.n[1], nz = I.n[2];
     const int i = blockIdx.x * 32 + lane;
     const int j = blockIdx.y * kAcTY + warp;
     const int z0 = blockIdx.z * kAfKC;
     const int z1 = min(z0 + kAfKC, nz);
-    if (j >= ny) return;   // warp-uniform
+    if (j >= ny) return;   // warp-uniform (no CTA barrier is used)
     const bool act = i < nx;
     const bool last = act && (lane == 31 || i + 1 == nx);   // computes Vx(i+1) itself
     const long long sxyP = (long long)nx * ny;
@@ -231,42 +232,61 @@ __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid
     long long ip = (long long)z0 * sxyP + (long long)j * nx + i;
     long long ix = (long long)z0 * sxyX + (long long)j * sxX + i;
     long long iy = (long long)z0 * sxyY + (long long)j * nx + i;
+#pragma unroll
+    for (int q = 0; q < kAfD; ++q) {   // planes z0 .. z0+kAfD-1 (the loop covers z0 .. z1)
+        if (z0 + q <= z1) af_issue(&ring[q][tid], I, act, j, z0 + q, ip + q * sxyP, ix + q * sxyX, iy + q * sxyY);
+        cpcommit();
+    }
     double pzm = (act && z0 > 0) ? ldg(I.P + ip - sxyP) : 0.0;   // P_in of plane k-1
     double pp = 0.0, vxn = 0.0, vxpn = 0.0, vyn = 0.0, vypn = 0.0, vzn = 0.0;   // plane k-1's new values
-    AfPlane cur, nxt;
-    af_load(cur, I, act, last, i, j, z0, ip, ix, iy);
+    int slot = 0;
     for (int k = z0; k <= z1; ++k, ip += sxyP, ix += sxyX, iy += sxyY) {
-        if (k < z1) af_load(nxt, I, act, last, i, j, k + 1, ip + sxyP, ix + sxyX, iy + sxyY);   // one plane ahead
+        cpwait<kAfD - 1>();
+        const double *e = ring[slot][tid];
+        const double cp = e[0], cvx = e[1], cvy = e[2], cvz = e[3], cpym = e[4], cpyp = e[5], cvyp = e[6];
+        double cpxm = 0.0, cvxe = 0.0, cpxp = 0.0;   // (rarely needed: plain loads)
+        if (act && k < nz) {
+            if (lane == 0 && i > 0) cpxm = ldg(I.P + ip - 1);
+            if (last) {
+                cvxe = ldg(I.Vx + ix + 1);
+                if (i + 1 < nx) cpxp = ldg(I.P + ip + 1);
+            }
+        }
+        // refill this slot with plane k+kAfD
+        if (k + kAfD <= z1)
+            af_issue(&ring[slot][tid], I, act, j, k + kAfD, ip + kAfD * sxyP, ix + kAfD * sxyX, iy + kAfD * sxyY);
+        cpcommit();
+        slot = slot + 1 == kAfD ? 0 : slot + 1;
         // the new Vz(k) of my column (k == nz: the top boundary face, copied)
-        const double vz = (uz && k >= 1 && k < nz) ? vupd(cur.vz, C.cV[2], cur.p, pzm) : cur.vz;
+        const double vz = (uz && k >= 1 && k < nz) ? vupd(cvz, C.cV[2], cp, pzm) : cvz;
         if (act && (k < z1 || k == nz)) O.Vz[ip] = vz;   // (the next chunk writes its own first face)
         if (k > z0 && act)   // P of plane k-1: its faces are all new now
             O.P[ip - sxyP] = pupd(pp, C.cP, C.r[0], C.r[1], C.r[2], vxn, vxpn, vyn, vypn, vzn, vz);
         if (k == z1) break;
         // plane k: the new Vx(i), Vx(i+1), Vy(j), Vy(j+1) of my cell
         const bool kin = k >= 1 && k < nz - 1;
-        double xm = __shfl_up_sync(0xffffffffu, cur.p, 1);
-        if (lane == 0) xm = cur.pxm;
-        const double vx = (ux && kin) ? vupd(cur.vx, C.cV[0], cur.p, xm) : cur.vx;
-        const double vy = (uy && kin) ? vupd(cur.vy, C.cV[1], cur.p, cur.pym) : cur.vy;
-        const double vyp = (uye && kin) ? vupd(cur.vyp, C.cV[1], cur.pyp, cur.p) : cur.vyp;
+        double xm = __shfl_up_sync(0xffffffffu, cp, 1);
+        if (lane == 0) xm = cpxm;
+        const double vx = (ux && kin) ? vupd(cvx, C.cV[0], cp, xm) : cvx;
+        const double vy = (uy && kin) ? vupd(cvy, C.cV[1], cp, cpym) : cvy;
+        const double vyp = (uye && kin) ? vupd(cvyp, C.cV[1], cpyp, cp) : cvyp;
         double vxp = __shfl_down_sync(0xffffffffu, vx, 1);
-        if (last) vxp = (uxe && kin) ? vupd(cur.vxe, C.cV[0], cur.pxp, cur.p) : cur.vxe;
+        if (last) vxp = (uxe && kin) ? vupd(cvxe, C.cV[0], cpxp, cp) : cvxe;
         if (act) {
             O.Vx[ix] = vx;
             O.Vy[iy] = vy;
             if (j == ny - 1) O.Vy[iy + nx] = vyp;        // the top boundary row of Vy
             if (last && i + 1 == nx) O.Vx[ix + 1] = vxp;   // the right boundary face of Vx
         }
-        pzm = cur.p;
-        pp = cur.p;
+        pzm = cp;
+        pp = cp;
         vxn = vx;
         vxpn = vxp;
         vyn = vy;
         vypn = vyp;
         vzn = vz;
-        cur = nxt;
     }
+    cpwait<0>();
 }
 
 }  // namespace
