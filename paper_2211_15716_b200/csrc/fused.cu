@@ -65,11 +65,16 @@ __device__ __forceinline__ double cell(double c, double xm, double xp, double ym
     return __dadd_rn(c, __dmul_rn(k.dt, __dmul_rn(__dmul_rn(k.lam, ci), lap)));
 }
 
+// release / acquire fence at system scope: the PTX release and acquire patterns (fence.acq_rel + relaxed
+// write / relaxed read + fence.acq_rel) are all the flag protocol needs; __threadfence_system is the
+// heavier sequentially consistent fence.sc (measured ~6 us per face tile with NVLink stores outstanding)
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 // one contribution to the data flag of (face a/rs, chunk c) of rank R; the last one publishes the epoch
 __device__ __forceinline__ void contribute(const FusedParams &F, const FusedRank &R, int a, int rs, int c) {
     const int i = (a * 2 + rs) * kMaxChunks + c;
     if (atomicAdd(R.ctr + i, 1u) == F.tgt[i] - 1) {
-        __threadfence_system();
+        fence_acq_rel_sys();   // (acquire side of the other contributors' release, then the flag's release)
         st_rel_sys(R.face[a][rs].flag + c, F.epoch);
         atomicExch(R.ctr + i, 0u);
     }
@@ -78,7 +83,7 @@ __device__ __forceinline__ void contribute(const FusedParams &F, const FusedRank
 __device__ __forceinline__ void contribute_x(const FusedParams &F, const FusedRank &R, int a, int rs, int c) {
     const int i = (a * 2 + rs) * kMaxChunks + c;
     if (atomicAdd(R.ctr_x + i, 1u) == F.tgt_x[i] - 1) {
-        __threadfence_system();
+        fence_acq_rel_sys();
         st_rel_sys(R.face[a][rs].xflag + c, F.epoch);
         atomicExch(R.ctr_x + i, 0u);
     }
@@ -417,10 +422,16 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         return;
     }
     // one system-scope release for the CTA: the barrier orders every warp's face stores before thread
-    // 0's fence, which is cumulative (PTX memory model), then the counters
+    // 0's fence.acq_rel, which is cumulative (PTX memory model), then the relaxed counters
     __syncthreads();
     if (tid == 0) {
+#ifndef FUSED_DIAG_NOFENCE   // (diagnostics build: timing without the release, INVALID ordering)
+#ifdef FUSED_DIAG_SCFENCE
         __threadfence_system();
+#else
+        fence_acq_rel_sys();
+#endif
+#endif
         for (int f = 0; f < 6; ++f)
             if (did & (1u << f)) contribute(F, R, f >> 1, f & 1, f < 4 ? pos : 0);
     }
@@ -488,11 +499,11 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
                 c[a] = rs == 0 ? 0 : F.s[a] - 1;
                 fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = val;
             }
-            __threadfence_system();
+            fence_acq_rel_sys();
         }
         __syncthreads();
         if (threadIdx.x == 0 && atomicAdd(R.rim_ticket, 1u) == (unsigned)F.nrim - 1) {
-            __threadfence_system();
+            fence_acq_rel_sys();
             for (int g = 0; g < 6; ++g) {
                 const int ga = g >> 1, grs = g & 1;
                 if (!R.face[ga][grs].active) continue;
@@ -525,7 +536,7 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
                     if (R.face[2][rs].layer >= zr.x && R.face[2][rs].layer < zr.y)
                         fwd |= forward_line(F, R, hb, side, 2, rs, 0, F.s[hb == 0 ? 1 : 0], q, F.nfwd);
                 }
-            if (__syncthreads_or(fwd)) __threadfence_system();
+            if (__syncthreads_or(fwd)) fence_acq_rel_sys();
             __syncthreads();
             if (threadIdx.x == 0)
                 for (int a = hb + 1; a < 3; ++a)
