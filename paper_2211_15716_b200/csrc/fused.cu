@@ -69,6 +69,12 @@ __device__ __forceinline__ double cell(double c, double xm, double xp, double ym
 // write / relaxed read + fence.acq_rel) are all the flag protocol needs; __threadfence_system is the
 // heavier sequentially consistent fence.sc (measured ~6 us per face tile with NVLink stores outstanding)
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acq_gpu_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // one contribution to the data flag of (face a/rs, chunk c) of rank R; the last one publishes the epoch
 __device__ __forceinline__ void contribute(const FusedParams &F, const FusedRank &R, int a, int rs, int c) {
@@ -119,10 +125,6 @@ __device__ __forceinline__ bool later_halo(const FusedParams &F, const FusedRank
     return false;
 }
 
-// staging buffer offset of (epoch parity, halo side, y, z): z fastest
-__device__ __forceinline__ long long xstg_at(const FusedParams &F, unsigned long long epoch, int side, int y, int z) {
-    return ((long long)((int)(epoch & 1) * 2 + side) * F.s[1] + y) * F.s[2] + z;
-}
 // z range a chunk covers on the x- and y-faces (the rim planes 0 and s-1 go with the end chunks)
 __device__ __forceinline__ int2 ext_range(const FusedParams &F, int c) {
     int2 r = F.zr[c];
@@ -142,13 +144,11 @@ constexpr int kFKC = 64;   // longest z-chunk
 //  * YF (CTA-uniform): the warp whose row is a y send layer stores its results also into the receiver's
 //    halo row (ydst + i) -- the same 16-B stores as T2's (the z send layer, the first or last plane of an
 //    end chunk, is copied after the sweep: one row per warp, just written);
-//  * XF (CTA-uniform: the tile holds the x send layer and the x halo column beside it): the lane holding
-//    the send cell keeps its value of every plane in shared memory and after the sweep the warp stores the
-//    row z-contiguously into the receiver's staging row (sdst[z]: whole sectors over NVLink, not one 8-B
-//    remote store per plane); the warp fetches the neighbour's staged halo values of its row for the whole
-//    chunk (hrow[z], z-contiguous) with the first cp.async group, and the lane holding the halo cell
-//    substitutes each plane's value for T's (T's halo column is never read for a kept result, and never
-//    written).  Predicated instructions only: no divergence in the loop.
+//  * XS (CTA-uniform: the tile holds an x send layer): the lane holding the send cell keeps its value of
+//    every plane in shared memory, and after the sweep the warp stores the row z-contiguously into this
+//    rank's LOCAL x staging buffer, from which the x sender blocks move it into the receiver's T2 column
+//    (one system-scope release per chunk and sender instead of one per face tile).  The receiver needs
+//    nothing: its next step reads the x halo from T like any other cell.
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
@@ -160,26 +160,18 @@ __device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r
         if (w1) d[1] = r1;
     }
 }
-__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
 
-// UP (XF only): the tile holds the upper x send layer s-2 and halo s-1 -- elements .x / .y of one lane's
-// pair -- else the lower ones, layer 1 and halo 0 -- .y / .x of lane 0 (s even: pairs never straddle)
-template <bool YF, int XM, bool UP>   // XM: 0 no x face, 1 staged x faces, 2 direct x faces
+// UP (XS only): the tile holds the upper x send layer s-2 -- element .x of its lane's pair -- else the
+// lower one, layer 1 -- element .y of lane 0 (s even: pairs never straddle)
+template <bool YF, bool XS, bool UP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
-                                            double2 (*sC)[32 * kFTY], int sx, long long sxy,
-                                            int zs, int ze, long long i, bool pair_in, bool w0, bool w1, bool cs,
-                                            double *ydst, const double *hrow, bool hlane, double *hx_row,
-                                            double *sdst, double *sx_row, bool slane) {
-    constexpr bool XF = XM == 1;   // (staged: the receive side and the post-sweep send below)
+                                            double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
+                                            long long i, bool pair_in, bool w0, bool w1, double *ydst,
+                                            double *sx_row, bool slane, double *xloc_row) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
     const int tid = threadIdx.x, lane = tid & 31;
-    if (XF && hrow)   // (warp-uniform) this chunk's staged halo values of the row, into the first group
-        for (int z = zs + lane; z < ze; z += 32) cp_async8f(hx_row + (z - zs), hrow + z);
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
@@ -191,18 +183,11 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
-    if (XF && hrow && hlane) {
-        const double h = __ldcg(hrow + zs);
-        if (UP) c.y = h; else c.x = h;
-    }
-    const bool hpatch = XF && hrow && hlane;
-    (void)hx_row;
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
-        if (XF) __syncwarp();   // (the halo row of hx_row, fetched by the whole warp in group 0)
         double2 ym = zero2, yp = zero2;
         if (pair_in) {
             ym = ldg2f(T + i - sx);
@@ -216,19 +201,14 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (hi_edge) xp = __ldg(T + i + 2);
         const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
         const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
-        if (FUSED_STCS && cs && w0 && w1)   // T2 is not re-read in this step (evict-first keeps L2 for T)
+        if (FUSED_STCS && w0 && w1)   // T2 is not re-read in this step (evict-first keeps L2 for T)
             __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
         else
             store_pair(T2 + i, w0, w1, r0, r1);
         if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
-        if (XF && slane) sx_row[z - zs] = UP ? r0 : r1;   // (one lane) the x send cell, plane by plane
-        if (XM == 2 && slane) sdst[(long long)z * sxy] = UP ? r0 : r1;   // direct: into the receiver's T2 column
+        if (XS && slane) sx_row[z - zs] = UP ? r0 : r1;          // (one lane) the x send cell, plane by plane
         zm = c;
         c = zp;
-        if (hpatch && z + 1 < ze) {   // (one lane) plane z+1's x halo cell: the neighbour's value
-            const double h = hx_row[z + 1 - zs];
-            if (UP) c.y = h; else c.x = h;
-        }
         if (pair_in && z + kFD < ze) {
             cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
@@ -237,9 +217,9 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
-    if (XF && sdst) {   // (warp-uniform) the row's send cells, z-contiguous: whole sectors over NVLink
+    if (XS && xloc_row) {   // (warp-uniform) the row's send cells, z-contiguous, into the local staging
         __syncwarp();
-        for (int z = zs + lane; z < ze; z += 32) sdst[z] = sx_row[z - zs];
+        for (int z = zs + lane; z < ze; z += 32) xloc_row[z] = sx_row[z - zs];
     }
 }
 
@@ -270,19 +250,18 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     TRACE_AT(0);
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
-    __shared__ double sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
     __shared__ double sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
     const int rank = blockIdx.x / F.per_rank;
     int b = blockIdx.x - rank * F.per_rank;
     const FusedRank &R = F.r[rank];
-    if (b < F.nrim + F.nfwd) {   // CTA-uniform
+    if (b < F.nrim + F.nfwd + 2 * F.nxs) {   // CTA-uniform
         fused_extra(F, R, b);
         TRACE_AT(3);
         return;
     }
-    b -= F.nrim + F.nfwd;
+    b -= F.nrim + F.nfwd + 2 * F.nxs;
     // tile of this block: chunks in visit order; within a chunk, when x or y faces exist, the border
     // tiles (rows ty = 0 and ytiles-1, then columns tx = 0 and xtiles-1) first -- they carry the faces and
     // take longer, so they start early instead of trailing their chunk -- then the interior, row-major
@@ -342,11 +321,6 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         if (R.face[1][rs].active && R.face[1][rs].layer >= ty0 && R.face[1][rs].layer < yhi) did |= 4u << rs;
         if (R.face[2][rs].active && F.zchunk[rs] == pos) did |= 16u << rs;
     }
-    // the x halo column beside the x send layer: staged by the neighbour in the previous step of the run
-    // (first step of a run: T holds it)
-    const int hside = xrs < 0 ? -1 : (xrs == 0 ? 1 : 0);   // send layer s-2 sits beside halo s-1, 1 beside 0
-    const bool hstaged = xrs >= 0 && F.wait_prev && R.halo[0][hside].active && !F.xdirect;
-
     if (F.wait_prev) {   // CTA-uniform: this step's halo cells are the previous epoch's faces
         const bool xh0 = R.halo[0][0].active && tx == 0, xh1 = R.halo[0][1].active && tx == F.xtiles - 1;
         const bool yl = R.halo[1][0].active && ty == 0, yu = R.halo[1][1].active && ty == F.ytiles - 1;
@@ -374,37 +348,23 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                 ydst = R.face[1][rs].dst + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx;
         }
         if (xrs >= 0) {
-            const int xf = R.face[0][xrs].layer - tx * 64, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
+            const int xf = R.face[0][xrs].layer - tx * 64;
             const bool slane = rowv && (xf >> 1) == lane;
-            if (F.xdirect) {   // x face straight into the receiver's T2 column; T holds my x halo
-                double *xcol = rowv ? R.face[0][xrs].dst + (long long)y * sx + (xrs == 0 ? 0 : sx - 1) : nullptr;
-#define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, 2, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, YD, \
-                                                       nullptr, false, nullptr, xcol, nullptr, slane)
-                if (xrs == 0) {
-                    if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
-                } else {
-                    if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
-                }
-#undef XSWEEP
-            } else {   // staged
-                const double *hrow = (hstaged && rowv) ? R.xstg + xstg_at(F, F.epoch - 1, hside, y, 0) : nullptr;
-                const bool hlane = (xh >> 1) == lane;
-                double *sdst = rowv ? R.xstg_peer[xrs] + xstg_at(F, F.epoch, xrs, y, 0) : nullptr;   // (warp-uniform)
-#define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, 1, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, YD, \
-                                                       hrow, hlane, sHx[warp], sdst, sX[warp], slane)
-                if (xrs == 0) {
-                    if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
-                } else {
-                    if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
-                }
-#undef XSWEEP
+            double *xloc_row = rowv ? R.xloc + ((long long)xrs * sy + y) * F.s[2] : nullptr;   // (warp-uniform)
+#define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, YD, \
+                                                          sX[warp], slane, xloc_row)
+            if (xrs == 0) {   // upper: send layer s-2
+                if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
+            } else {          // lower: send layer 1
+                if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
             }
+#undef XSWEEP
         } else if (did & 12u) {
-            fused_sweep<true, 0, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, ydst,
-                                            nullptr, false, nullptr, nullptr, nullptr, false);
+            fused_sweep<true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, ydst, nullptr,
+                                            false, nullptr);
         } else {
-            fused_sweep<false, 0, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, true, nullptr,
-                                             nullptr, false, nullptr, nullptr, nullptr, false);
+            fused_sweep<false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr, nullptr,
+                                             false, nullptr);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver
@@ -425,15 +385,21 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     // 0's fence.acq_rel, which is cumulative (PTX memory model), then the relaxed counters
     __syncthreads();
     if (tid == 0) {
+        if (did & 60u) {   // y / z faces: their stores went to the receiver: system-scope release
 #ifndef FUSED_DIAG_NOFENCE   // (diagnostics build: timing without the release, INVALID ordering)
 #ifdef FUSED_DIAG_SCFENCE
-        __threadfence_system();
+            __threadfence_system();
 #else
-        fence_acq_rel_sys();
+            fence_acq_rel_sys();
 #endif
 #endif
-        for (int f = 0; f < 6; ++f)
-            if (did & (1u << f)) contribute(F, R, f >> 1, f & 1, f < 4 ? pos : 0);
+            for (int f = 2; f < 6; ++f)
+                if (did & (1u << f)) contribute(F, R, f >> 1, f & 1, f < 4 ? pos : 0);
+        }
+        if (did & 3u) {    // x face: the local staging rows, GPU-scope release, then the senders' count
+            fence_acq_rel_gpu();
+            atomicAdd(R.xcnt + xrs * kMaxChunks + pos, 1u);
+        }
     }
     TRACE_AT(3);
 }
@@ -451,11 +417,7 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
         c[a] = fc.layer;
         c[third] = t;
         if (forward_phase(F, R, a, c) != b || later_halo(F, R, a, c)) continue;
-        double v;
-        if (b == 0 && !F.xdirect && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1)
-            v = __ldcg(R.xstg + xstg_at(F, F.epoch, side, c[1], c[2]));   // staged, not yet in T2
-        else
-            v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
+        const double v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
         c[a] = rs == 0 ? 0 : F.s[a] - 1;
         fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v;
         any = true;
@@ -516,6 +478,52 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
         }
         return;
     }
+    if (b >= F.nrim + F.nfwd) {   // x sender: role rs, part of nxs
+        const int e = b - F.nrim - F.nfwd, rs = e / F.nxs, part = e % F.nxs;
+        const FusedFace &fx = R.face[0][rs];
+        if (!fx.active) return;
+        const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
+        const long long sxy = (long long)sx * sy;
+        const int hx = rs == 0 ? 0 : sx - 1;   // the receiver's halo column
+        const double *loc = R.xloc + (long long)rs * sy * sz;
+        for (int pos = 0; pos < F.nchunks; ++pos) {
+            if (threadIdx.x == 0) {   // every face tile of the chunk has staged its rows (GPU-scope acquire)
+                const long long t0 = clock64();
+                while (ld_acq_gpu_u32(R.xcnt + rs * kMaxChunks + pos) < F.xtarget) {
+                    if (clock64() - t0 > F.timeout_cycles) {
+                        atomicExch(F.err, 1);
+                        break;
+                    }
+                    __nanosleep(200);
+                }
+            }
+            __syncthreads();
+            const int2 zr = F.zr[pos];
+            const int nz = zr.y - zr.x;
+            const long long ncell = (long long)(sy - 2) * nz;
+            constexpr int U = 4;
+            for (long long t0 = ((long long)part * blockDim.x + threadIdx.x) * U; t0 < ncell;
+                 t0 += (long long)F.nxs * blockDim.x * U) {
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {   // z-contiguous reads of the local rows
+                    const long long t = t0 + u;
+                    v[u] = t < ncell ? __ldcg(loc + (1 + t / nz) * sz + zr.x + t % nz) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const long long t = t0 + u;
+                    if (t < ncell) fx.dst[(long long)(zr.x + t % nz) * sxy + (long long)(1 + t / nz) * sx + hx] = v[u];
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                fence_acq_rel_sys();
+                contribute(F, R, 0, rs, pos);
+            }
+        }
+        return;
+    }
     const int q = b - F.nrim;   // forwarder q of nfwd: chunk by chunk, each edge line leaves as soon as
                                 // its halo has arrived
     for (int ch = 0; ch < F.nchunks; ++ch) {
@@ -552,30 +560,16 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
 }
 
 // After the last step of a run: every incoming face (data and rim/forwarded cells) of the epoch has
-// arrived -- the step is complete for any later work on the stream -- and the last epoch's staged x halo
-// columns (inner rows and planes) are copied into T2.  blockIdx.y = hosted rank.  (Waits only for flags
-// of the launch before it on the stream.)
+// arrived -- the step is complete for any later work on the stream.  blockIdx.x = hosted rank.  (Waits
+// only for flags of the launch before it on the stream.)
 __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
-    const FusedRank &R = F.r[blockIdx.y];
+    const FusedRank &R = F.r[blockIdx.x];
     for (int f = threadIdx.x; f < 6 * F.nchunks; f += blockDim.x) {
         const int a = f / (2 * F.nchunks), rs = (f / F.nchunks) & 1, ch = f % F.nchunks;
         const FusedHalo &h = R.halo[a][rs];
         if (!h.active || (a == 2 && ch > 0)) continue;
-        if (blockIdx.x == 0 || (a == 0 && !F.xdirect)) spin_geq(F, h.flag + ch, F.epoch);   // (staged x: every block copies)
-        if (blockIdx.x == 0) spin_geq(F, h.xflag + ch, F.epoch);
-    }
-    __syncthreads();
-    if (F.xdirect) return;   // (direct x faces: already in T2)
-    const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
-    const long long sxy = (long long)sx * sy, ncell = (long long)(sy - 2) * (sz - 2);
-    for (int side = 0; side < 2; ++side) {
-        if (!R.halo[0][side].active) continue;
-        const int hx = side == 0 ? 0 : sx - 1;
-        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
-             t += (long long)gridDim.x * blockDim.x) {
-            const int z = 1 + (int)(t % (sz - 2)), y = 1 + (int)(t / (sz - 2));
-            R.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(R.xstg + xstg_at(F, F.epoch, side, y, z));
-        }
+        spin_geq(F, h.flag + ch, F.epoch);
+        spin_geq(F, h.xflag + ch, F.epoch);
     }
 }
 
@@ -644,7 +638,7 @@ static void build_layout(igg_grid *g, const bool act[3][2], bool zex) {
     std::vector<unsigned> tgt_d(6 * kMaxChunks, 0u), tgt_x(6 * kMaxChunks, 0u);
     for (int rs = 0; rs < 2; ++rs) {
         for (int c = 0; c < nch; ++c) {
-            tgt_d[(0 * 2 + rs) * kMaxChunks + c] = ytiles;
+            tgt_d[(0 * 2 + rs) * kMaxChunks + c] = kFusedXSenders;   // (the x senders publish x faces)
             tgt_x[(0 * 2 + rs) * kMaxChunks + c] = 1;
             tgt_d[(1 * 2 + rs) * kMaxChunks + c] = xtiles;
             tgt_x[(1 * 2 + rs) * kMaxChunks + c] = 1 + (xh ? nf : 0);
@@ -812,15 +806,14 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         g->allocs++;
     }
     const bool comm = !g->skip_comm;
-#ifndef FUSED_XDIRECT
-#define FUSED_XDIRECT 0
-#endif
-    const bool xdirect = FUSED_XDIRECT != 0;
-    const bool xst = comm && !xdirect && (g->dims[0] > 1 || g->periods[0]);   // x halos exist: staging buffers
-    const size_t stg_words = 4 * (size_t)g->n[1] * g->n[2];       // [parity][side][y][z] per rank
-    if (xst && !g->fused_xstg) {
-        IGG_CUDA(cudaMalloc(&g->fused_xstg, sizeof(double) * stg_words * L));
-        g->allocs++;
+    const bool xex = comm && (g->dims[0] > 1 || g->periods[0]);   // x faces exist: local staging rows
+    const size_t stg_words = 2 * (size_t)g->n[1] * g->n[2];       // [side][y][z] per rank
+    if (xex && !g->fused_xloc) {
+        IGG_CUDA(cudaMalloc(&g->fused_xloc, sizeof(double) * stg_words * L));
+        IGG_CUDA(cudaMalloc(&g->fused_xcnt, sizeof(unsigned) * 2 * kMaxChunks * L));
+        IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
+        g->fused_xsteps = 0;
+        g->allocs += 2;
     }
     g->epoch++;
     FusedParams F{};
@@ -830,7 +823,6 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.err = g->d_err;
     F.k = k;
     F.nranks = L;
-    F.xdirect = xdirect ? 1 : 0;
     bool act[3][2] = {{false, false}, {false, false}, {false, false}};
     bool zex = false;
     // flags of hosted rank lr: data (lr*6 + a*2 + rs) * kMaxChunks, rim/forwarded (L*6 + lr*6 + a*2 + rs)
@@ -843,7 +835,8 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         R.ctr = g->fused_ctr + lr * ctr_words;
         R.ctr_x = R.ctr + 6 * kMaxChunks;
         R.rim_ticket = R.ctr + 12 * kMaxChunks;
-        R.xstg = xst ? g->fused_xstg + lr * stg_words : nullptr;
+        R.xloc = xex ? g->fused_xloc + lr * stg_words : nullptr;
+        R.xcnt = xex ? g->fused_xcnt + lr * 2 * kMaxChunks : nullptr;
         for (int a = 0; a < 3; ++a)
             for (int rs = 0; rs < 2; ++rs) {
                 // rs = receiver side: 0 <- my layer n-2 into my upper neighbour's layer 0,
@@ -860,13 +853,11 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
                         f.dst = T2[li];
                         f.flag = g->flags + (li * 6 + a * 2 + rs) * kMaxChunks;
                         f.xflag = g->flags + (L * 6 + li * 6 + a * 2 + rs) * kMaxChunks;
-                        if (a == 0 && xst) R.xstg_peer[rs] = g->fused_xstg + li * stg_words;
                     } else {         // another process (one rank each): its arrays mapped over NVLink
                         const int pp = proc_of(g, nb);
                         f.dst = peer_arrays(g, T2[lr])[pp];
                         f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
                         f.xflag = g->peer_flags[pp] + (6 + a * 2 + rs) * kMaxChunks;
-                        if (a == 0 && xst) R.xstg_peer[rs] = peer_arrays(g, g->fused_xstg)[pp];
                     }
                 }
                 FusedHalo &h = R.halo[a][rs];   // my halo side rs is filled by my neighbour on side rs
@@ -882,7 +873,15 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     if (g->fused_key != key) {
         build_layout(g, act, zex);
         g->fused_key = key;
+        if (g->fused_xcnt) {   // the x senders' cumulative counters restart with the layout
+            IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
+            g->fused_xsteps = 0;
+        }
     }
+    const bool xface = act[0][0] || act[0][1];
+    if (xface) ++g->fused_xsteps;   // launches whose x-face tiles count on the cumulative counters
+    F.xtarget = (unsigned)((unsigned long long)g->fused_geo[5] * g->fused_xsteps);
+    F.nxs = xface ? kFusedXSenders : 0;
     F.nchunks = g->fused_nchunks;
     for (int c = 0; c < F.nchunks; ++c) F.zr[c] = g->fused_zr[c];
     F.xtiles = g->fused_geo[4];
@@ -903,7 +902,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.nrim = (comm && drain) ? 48 : 0;
     F.nfwd = (comm && drain) ? g->fused_nfwd : 0;
     F.nstencil = g->fused_ntiles;
-    F.per_rank = F.nrim + F.nfwd + F.nstencil;
+    F.per_rank = F.nrim + F.nfwd + 2 * F.nxs + F.nstencil;
     const long long blocks = (long long)F.per_rank * L;
     prof_begin(g, s);
     if (L > 1)
@@ -914,7 +913,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     g->launches++;
     prof_end(g, s, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2) * L);
     if (drain && comm) {
-        fused_drain_kernel<<<dim3(xst ? 2 * g->sm_count / L + 1 : 1, L), 128, 0, s>>>(F);
+        fused_drain_kernel<<<L, 128, 0, s>>>(F);
         IGG_CUDA(cudaGetLastError());
         g->launches++;
     }

@@ -68,6 +68,9 @@ __device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long lon
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// the PTX release / acquire patterns (fence.acq_rel + relaxed RMW / relaxed RMW + fence.acq_rel) are all the
+// protocol needs; __threadfence_system would be the heavier sequentially consistent fence.sc
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void spin(const unsigned long long *f, unsigned long long v, long long timeout, int *err) {
     const long long t0 = clock64();
     while (ld_acq_sys(f) < v) {
@@ -124,9 +127,9 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
     auto flush = [&]() {
         __syncthreads();
         if (threadIdx.x == 0 && mydone) {
-            __threadfence_system();
+            fence_acq_rel_sys();   // (release: the block's stores, ordered before thread 0 by the barrier)
             if (atomicAdd(ctr + 1, mydone) + mydone == (unsigned)P.nstore_chunks) {
-                __threadfence_system();
+                fence_acq_rel_sys();   // (acquire: every other block's release; then the flags' release)
                 unsigned long long *const *sig = reinterpret_cast<unsigned long long *const *>(base + P.o_signal);
                 for (int q = 0; q < P.nsignal; ++q) st_rel_sys(sig[q], epoch);
             }

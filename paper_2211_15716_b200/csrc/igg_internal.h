@@ -125,6 +125,7 @@ struct HeatRegionList {
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
 constexpr int kMaxFusedRanks = 8;    // ranks hosted on one GPU that one fused launch covers
+constexpr int kFusedXSenders = 4;    // x sender blocks per x face and rank
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // the receiver's T2 (a sibling's, or peer-mapped); lands in its halo layer
     unsigned long long *flag;        // receiver's data flags of (axis, side): [kMaxChunks] (z faces: [0])
@@ -144,12 +145,11 @@ struct FusedRank {                   // one hosted rank of a fused launch
     double *T2;
     FusedFace face[3][2];
     FusedHalo halo[3][2];
-    // x faces: the sender's face tiles store their captured x layer into the receiver's compact staging
-    // buffer [epoch parity][halo side][y][z] (z fastest: whole sectors, not one 8-B value per sector of
-    // a T2 column); the receiver's first/last x-tiles read the previous epoch's values into shared
-    // memory, the forwarders read the current epoch's, the drain copies the last epoch's into T2
-    const double *xstg;              // mine
-    double *xstg_peer[2];            // the receivers' (indexed like face[0][rs])
+    // x faces: the face tiles store their x send column z-contiguously into the local staging rows
+    // xloc [side rs][y][z] and count on xcnt [rs][chunk] (GPU scope); the x sender blocks move each
+    // completed chunk into the receiver's T2 halo column and publish its flag
+    double *xloc;
+    unsigned int *xcnt;
     unsigned int *ctr;               // [6][kMaxChunks] data-flag contribution counters (sender side)
     unsigned int *ctr_x;             // [6][kMaxChunks] rim/forwarded-cell counters
     unsigned int *rim_ticket;
@@ -164,7 +164,8 @@ struct FusedParams {
     int zchunk[2];                   // chunk holding the z send layer of face (2, rs); -1 if none
     int xtiles, ytiles;
     int border_first;                // within a chunk: the border tiles (faces) first
-    int xdirect;                     // x faces stored straight into the receiver's T2 column (no staging)
+    int nxs;                         // x sender blocks per x face (0: no x faces)
+    unsigned xtarget;                // x-face tile count of a chunk after this launch (cumulative)
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk) data flag
     const unsigned int *tgt_x;       // ... an xflag (rim + forwarders)
     unsigned long long epoch;
@@ -345,7 +346,9 @@ struct igg_grid : igg::Geom {
     int fused_ntiles = 0, fused_nchunks = 0, fused_key = -1;
     int fused_zchunk[2] = {-1, -1};
     int fused_nfwd = 0;                                  // in-kernel forwarders (pipelined)
-    double *fused_xstg = nullptr;                        // x-face staging buffer (pipelined)
+    double *fused_xloc = nullptr;                        // x-face local staging rows (fused path)
+    unsigned int *fused_xcnt = nullptr;                  // x-face tile counters (cumulative)
+    unsigned long long fused_xsteps = 0;                 // launches with x faces since the counters' reset
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
