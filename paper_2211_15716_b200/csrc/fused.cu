@@ -70,6 +70,25 @@ __device__ __forceinline__ double cell(double c, double xm, double xp, double ym
 // heavier sequentially consistent fence.sc (measured ~6 us per face tile with NVLink stores outstanding)
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_rel_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acq_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// the calling thread spins (bounded) until the LOCAL *fl >= v (GPU scope)
+__device__ __forceinline__ void spin_geq_gpu(const FusedParams &F, const unsigned long long *fl, unsigned long long v) {
+    const long long t0 = clock64();
+    while (ld_acq_gpu(fl) < v) {
+        if (clock64() - t0 > F.timeout_cycles) {
+            atomicExch(F.err, 1);
+            break;
+        }
+        __nanosleep(200);
+    }
+}
 __device__ __forceinline__ unsigned ld_acq_gpu_u32(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -256,12 +275,12 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const int rank = blockIdx.x / F.per_rank;
     int b = blockIdx.x - rank * F.per_rank;
     const FusedRank &R = F.r[rank];
-    if (b < F.nrim + F.nfwd + 2 * F.nxs) {   // CTA-uniform
+    if (b < F.nrim + F.nfwd + 4 * F.nxs) {   // CTA-uniform
         fused_extra(F, R, b);
         TRACE_AT(3);
         return;
     }
-    b -= F.nrim + F.nfwd + 2 * F.nxs;
+    b -= F.nrim + F.nfwd + 4 * F.nxs;
     // tile of this block: chunks in visit order; within a chunk, when x or y faces exist, the border
     // tiles (rows ty = 0 and ytiles-1, then columns tx = 0 and xtiles-1) first -- they carry the faces and
     // take longer, so they start early instead of trailing their chunk -- then the interior, row-major
@@ -327,8 +346,8 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         const bool zl = R.halo[2][0].active && zs == 1, zu = R.halo[2][1].active && ze == F.s[2] - 1;
         if (tid == 0) {
             const unsigned long long prev = F.epoch - 1;
-            if (xh0) spin_geq(F, R.halo[0][0].flag + pos, prev);
-            if (xh1) spin_geq(F, R.halo[0][1].flag + pos, prev);
+            if (xh0) spin_geq_gpu(F, R.xrdy + pos, prev);                // (my unpackers wrote the column)
+            if (xh1) spin_geq_gpu(F, R.xrdy + kMaxChunks + pos, prev);
             if (yl) spin_geq(F, R.halo[1][0].flag + pos, prev);
             if (yu) spin_geq(F, R.halo[1][1].flag + pos, prev);
             if (zl) spin_geq(F, R.halo[2][0].flag, prev);
@@ -478,14 +497,55 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
         }
         return;
     }
+    if (b >= F.nrim + F.nfwd + 2 * F.nxs) {   // x unpacker of my halo side hs: staged rows -> my T2 column
+        const int e = b - F.nrim - F.nfwd - 2 * F.nxs, hs = e / F.nxs, part = e % F.nxs;
+        if (!R.halo[0][hs].active) return;
+        const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
+        const long long sxy = (long long)sx * sy;
+        const int hx = hs == 0 ? 0 : sx - 1;
+        const double *stg = R.xrem + ((long long)(F.epoch & 1) * 2 + hs) * sy * sz;
+        for (int pos = 0; pos < F.nchunks; ++pos) {
+            if (threadIdx.x == 0) spin_geq(F, R.halo[0][hs].flag + pos, F.epoch);   // the sender's rows arrived
+            __syncthreads();
+            const int2 zr = F.zr[pos];
+            const int nz = zr.y - zr.x;
+            const long long ncell = (long long)(sy - 2) * nz;
+            constexpr int U = 4;
+            for (long long t0 = ((long long)part * blockDim.x + threadIdx.x) * U; t0 < ncell;
+                 t0 += (long long)F.nxs * blockDim.x * U) {
+                double v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const long long t = t0 + u;
+                    v[u] = t < ncell ? __ldcg(stg + (1 + t / nz) * sz + zr.x + t % nz) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const long long t = t0 + u;
+                    if (t < ncell) R.T2[(long long)(zr.x + t % nz) * sxy + (long long)(1 + t / nz) * sx + hx] = v[u];
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {   // the last unpacker of the chunk publishes "x halo of chunk pos ready"
+                fence_acq_rel_gpu();
+                const int ci = hs * kMaxChunks + pos;
+                if (atomicAdd(R.xucnt + ci, 1u) == (unsigned)F.nxs - 1) {
+                    atomicExch(R.xucnt + ci, 0u);
+                    fence_acq_rel_gpu();
+                    st_rel_gpu(R.xrdy + ci, F.epoch);
+                }
+            }
+        }
+        return;
+    }
     if (b >= F.nrim + F.nfwd) {   // x sender: role rs, part of nxs
         const int e = b - F.nrim - F.nfwd, rs = e / F.nxs, part = e % F.nxs;
         const FusedFace &fx = R.face[0][rs];
         if (!fx.active) return;
-        const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
-        const long long sxy = (long long)sx * sy;
-        const int hx = rs == 0 ? 0 : sx - 1;   // the receiver's halo column
+        const int sy = F.s[1], sz = F.s[2];
         const double *loc = R.xloc + (long long)rs * sy * sz;
+        // the receiver's staging rows of its halo side rs, this epoch's parity (z-contiguous)
+        double *dst = R.xrem_peer[rs] + ((long long)(F.epoch & 1) * 2 + rs) * sy * sz;
         for (int pos = 0; pos < F.nchunks; ++pos) {
             if (threadIdx.x == 0) {   // every face tile of the chunk has staged its rows (GPU-scope acquire)
                 const long long t0 = clock64();
@@ -513,7 +573,7 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const long long t = t0 + u;
-                    if (t < ncell) fx.dst[(long long)(zr.x + t % nz) * sxy + (long long)(1 + t / nz) * sx + hx] = v[u];
+                    if (t < ncell) dst[(1 + t / nz) * sz + zr.x + t % nz] = v[u];
                 }
             }
             __syncthreads();
@@ -533,7 +593,10 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
             if (threadIdx.x == 0)
                 for (int side = 0; side < 2; ++side)
                     if (R.halo[hb][side].active) {
-                        spin_geq(F, R.halo[hb][side].flag + ch, F.epoch);
+                        if (hb == 0)   // x halo: in T2 once my unpackers finished the chunk
+                            spin_geq_gpu(F, R.xrdy + side * kMaxChunks + ch, F.epoch);
+                        else
+                            spin_geq(F, R.halo[hb][side].flag + ch, F.epoch);
                         spin_geq(F, R.halo[hb][side].xflag + ch, F.epoch);
                     }
             __syncthreads();
@@ -568,7 +631,10 @@ __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
         const int a = f / (2 * F.nchunks), rs = (f / F.nchunks) & 1, ch = f % F.nchunks;
         const FusedHalo &h = R.halo[a][rs];
         if (!h.active || (a == 2 && ch > 0)) continue;
-        spin_geq(F, h.flag + ch, F.epoch);
+        if (a == 0)
+            spin_geq_gpu(F, R.xrdy + rs * kMaxChunks + ch, F.epoch);   // (unpacked into T2)
+        else
+            spin_geq(F, h.flag + ch, F.epoch);
         spin_geq(F, h.xflag + ch, F.epoch);
     }
 }
@@ -810,10 +876,13 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     const size_t stg_words = 2 * (size_t)g->n[1] * g->n[2];       // [side][y][z] per rank
     if (xex && !g->fused_xloc) {
         IGG_CUDA(cudaMalloc(&g->fused_xloc, sizeof(double) * stg_words * L));
-        IGG_CUDA(cudaMalloc(&g->fused_xcnt, sizeof(unsigned) * 2 * kMaxChunks * L));
-        IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
+        IGG_CUDA(cudaMalloc(&g->fused_xrem, sizeof(double) * 2 * stg_words * L));   // [parity][side][y][z]
+        IGG_CUDA(cudaMalloc(&g->fused_xcnt, sizeof(unsigned) * 4 * kMaxChunks * L));  // [send 2 | unpack 2]
+        IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 4 * kMaxChunks * L));
+        IGG_CUDA(cudaMalloc(&g->fused_xrdy, sizeof(unsigned long long) * 2 * kMaxChunks * L));
+        IGG_CUDA(cudaMemset(g->fused_xrdy, 0, sizeof(unsigned long long) * 2 * kMaxChunks * L));
         g->fused_xsteps = 0;
-        g->allocs += 2;
+        g->allocs += 4;
     }
     g->epoch++;
     FusedParams F{};
@@ -836,7 +905,10 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         R.ctr_x = R.ctr + 6 * kMaxChunks;
         R.rim_ticket = R.ctr + 12 * kMaxChunks;
         R.xloc = xex ? g->fused_xloc + lr * stg_words : nullptr;
-        R.xcnt = xex ? g->fused_xcnt + lr * 2 * kMaxChunks : nullptr;
+        R.xrem = xex ? g->fused_xrem + lr * 2 * stg_words : nullptr;
+        R.xcnt = xex ? g->fused_xcnt + lr * 4 * kMaxChunks : nullptr;
+        R.xucnt = xex ? R.xcnt + 2 * kMaxChunks : nullptr;
+        R.xrdy = xex ? g->fused_xrdy + lr * 2 * kMaxChunks : nullptr;
         for (int a = 0; a < 3; ++a)
             for (int rs = 0; rs < 2; ++rs) {
                 // rs = receiver side: 0 <- my layer n-2 into my upper neighbour's layer 0,
@@ -853,11 +925,13 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
                         f.dst = T2[li];
                         f.flag = g->flags + (li * 6 + a * 2 + rs) * kMaxChunks;
                         f.xflag = g->flags + (L * 6 + li * 6 + a * 2 + rs) * kMaxChunks;
+                        if (a == 0) R.xrem_peer[rs] = g->fused_xrem + li * 2 * stg_words;
                     } else {         // another process (one rank each): its arrays mapped over NVLink
                         const int pp = proc_of(g, nb);
                         f.dst = peer_arrays(g, T2[lr])[pp];
                         f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
                         f.xflag = g->peer_flags[pp] + (6 + a * 2 + rs) * kMaxChunks;
+                        if (a == 0) R.xrem_peer[rs] = peer_arrays(g, g->fused_xrem)[pp];
                     }
                 }
                 FusedHalo &h = R.halo[a][rs];   // my halo side rs is filled by my neighbour on side rs
@@ -874,7 +948,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         build_layout(g, act, zex);
         g->fused_key = key;
         if (g->fused_xcnt) {   // the x senders' cumulative counters restart with the layout
-            IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
+            IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 4 * kMaxChunks * L));
             g->fused_xsteps = 0;
         }
     }
@@ -902,7 +976,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.nrim = (comm && drain) ? 48 : 0;
     F.nfwd = (comm && drain) ? g->fused_nfwd : 0;
     F.nstencil = g->fused_ntiles;
-    F.per_rank = F.nrim + F.nfwd + 2 * F.nxs + F.nstencil;
+    F.per_rank = F.nrim + F.nfwd + 4 * F.nxs + F.nstencil;   // (x senders + x unpackers)
     const long long blocks = (long long)F.per_rank * L;
     prof_begin(g, s);
     if (L > 1)

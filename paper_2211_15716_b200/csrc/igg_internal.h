@@ -150,6 +150,13 @@ struct FusedRank {                   // one hosted rank of a fused launch
     // completed chunk into the receiver's T2 halo column and publish its flag
     double *xloc;
     unsigned int *xcnt;
+    // ... into the receiver's staging rows xrem [parity][side][y][z] (contiguous: whole sectors over NVLink,
+    // no scattered remote stores); the receiver's x unpacker blocks copy each chunk into its T2 halo column
+    // and publish xrdy [side][chunk] (GPU scope) for its next step's halo tiles, forwarders and drain
+    double *xrem;                    // mine (written by my neighbours' senders)
+    double *xrem_peer[2];            // the receivers' (indexed like face[0][rs])
+    unsigned int *xucnt;             // [2][kMaxChunks] unpacker counters
+    unsigned long long *xrdy;        // [2][kMaxChunks] epoch whose x halo column of the chunk is in T2
     unsigned int *ctr;               // [6][kMaxChunks] data-flag contribution counters (sender side)
     unsigned int *ctr_x;             // [6][kMaxChunks] rim/forwarded-cell counters
     unsigned int *rim_ticket;
@@ -164,7 +171,7 @@ struct FusedParams {
     int zchunk[2];                   // chunk holding the z send layer of face (2, rs); -1 if none
     int xtiles, ytiles;
     int border_first;                // within a chunk: the border tiles (faces) first
-    int nxs;                         // x sender blocks per x face (0: no x faces)
+    int nxs;                         // x sender (and x unpacker) blocks per x face / halo side (0: none)
     unsigned xtarget;                // x-face tile count of a chunk after this launch (cumulative)
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk) data flag
     const unsigned int *tgt_x;       // ... an xflag (rim + forwarders)
@@ -347,7 +354,9 @@ struct igg_grid : igg::Geom {
     int fused_zchunk[2] = {-1, -1};
     int fused_nfwd = 0;                                  // in-kernel forwarders (pipelined)
     double *fused_xloc = nullptr;                        // x-face local staging rows (fused path)
-    unsigned int *fused_xcnt = nullptr;                  // x-face tile counters (cumulative)
+    unsigned int *fused_xcnt = nullptr;                  // x-face tile counters (cumulative) + unpackers
+    double *fused_xrem = nullptr;                        // x-face receive staging (IPC-mapped by the senders)
+    unsigned long long *fused_xrdy = nullptr;            // x halo column unpacked (epoch per side and chunk)
     unsigned long long fused_xsteps = 0;                 // launches with x faces since the counters' reset
     int sm_count = 148;
     double clock_khz = 1.9e6;
