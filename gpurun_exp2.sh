@@ -1,4 +1,4 @@
-cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp18}
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp19}
 TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1 --master-port 29525 --nproc-per-node 2"
 timeout 600 python -m pytest tests -q -m gpu -x -k "virtual_p2p or fused or smoke" > gpurun_out/${T}_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest.log
 timeout 300 python bench.py --periodic 1,0,0 --no-e2e --no-cpu --no-stats > gpurun_out/${T}_p100.json 2>&1

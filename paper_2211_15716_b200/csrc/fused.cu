@@ -70,25 +70,6 @@ __device__ __forceinline__ double cell(double c, double xm, double xp, double ym
 // heavier sequentially consistent fence.sc (measured ~6 us per face tile with NVLink stores outstanding)
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void st_rel_gpu(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acq_gpu(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// the calling thread spins (bounded) until the LOCAL *fl >= v (GPU scope)
-__device__ __forceinline__ void spin_geq_gpu(const FusedParams &F, const unsigned long long *fl, unsigned long long v) {
-    const long long t0 = clock64();
-    while (ld_acq_gpu(fl) < v) {
-        if (clock64() - t0 > F.timeout_cycles) {
-            atomicExch(F.err, 1);
-            break;
-        }
-        __nanosleep(200);
-    }
-}
 __device__ __forceinline__ unsigned ld_acq_gpu_u32(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -171,6 +152,10 @@ constexpr int kFKC = 64;   // longest z-chunk
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
+__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r0, double r1) {
     if (w0 && w1) {
         *reinterpret_cast<double2 *>(d) = make_double2(r0, r1);
@@ -186,7 +171,8 @@ template <bool YF, bool XS, bool UP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
                                             double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
                                             long long i, bool pair_in, bool w0, bool w1, double *ydst,
-                                            double *sx_row, bool slane, double *xloc_row) {
+                                            double *sx_row, bool slane, bool hpatch, double h0,
+                                            const double *hx_row) {
     const double *__restrict__ T = R.T;
     const double *__restrict__ Ci = R.Ci;
     double *__restrict__ T2 = R.T2;
@@ -202,11 +188,15 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     const double2 zero2 = make_double2(0.0, 0.0);
     double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
     double2 c = pair_in ? ldg2f(T + i) : zero2;
+    if (XS && hpatch) {   // (one lane) substitutes the staged x halo values for T's, plane zs first
+        if (UP) c.y = h0; else c.x = h0;
+    }
     const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
+        if (XS) __syncwarp();   // (the halo row in hx_row, fetched by the whole warp in group 0)
         double2 ym = zero2, yp = zero2;
         if (pair_in) {
             ym = ldg2f(T + i - sx);
@@ -228,6 +218,10 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         if (XS && slane) sx_row[z - zs] = UP ? r0 : r1;          // (one lane) the x send cell, plane by plane
         zm = c;
         c = zp;
+        if (XS && hpatch && z + 1 < ze) {   // plane z+1's x halo cell: the neighbour's staged value
+            const double h = hx_row[z + 1 - zs];
+            if (UP) c.y = h; else c.x = h;
+        }
         if (pair_in && z + kFD < ze) {
             cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
             cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
@@ -236,10 +230,6 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         slot = slot + 1 == kFD ? 0 : slot + 1;
     }
     cp_wait<0>();
-    if (XS && xloc_row) {   // (warp-uniform) the row's send cells, z-contiguous, into the local staging
-        __syncwarp();
-        for (int z = zs + lane; z < ze; z += 32) xloc_row[z] = sx_row[z - zs];
-    }
 }
 
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b);
@@ -270,17 +260,18 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     __shared__ double2 sT[kFD][32 * kFTY];
     __shared__ double2 sC[kFD][32 * kFTY];
     __shared__ double sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
+    __shared__ double sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
     const int rank = blockIdx.x / F.per_rank;
     int b = blockIdx.x - rank * F.per_rank;
     const FusedRank &R = F.r[rank];
-    if (b < F.nrim + F.nfwd + 4 * F.nxs) {   // CTA-uniform
+    if (b < F.nrim + F.nfwd + 2 * F.nxs) {   // CTA-uniform
         fused_extra(F, R, b);
         TRACE_AT(3);
         return;
     }
-    b -= F.nrim + F.nfwd + 4 * F.nxs;
+    b -= F.nrim + F.nfwd + 2 * F.nxs;
     // tile of this block: chunks in visit order; within a chunk, when x or y faces exist, the border
     // tiles (rows ty = 0 and ytiles-1, then columns tx = 0 and xtiles-1) first -- they carry the faces and
     // take longer, so they start early instead of trailing their chunk -- then the interior, row-major
@@ -346,8 +337,8 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         const bool zl = R.halo[2][0].active && zs == 1, zu = R.halo[2][1].active && ze == F.s[2] - 1;
         if (tid == 0) {
             const unsigned long long prev = F.epoch - 1;
-            if (xh0) spin_geq_gpu(F, R.xrdy + pos, prev);                // (my unpackers wrote the column)
-            if (xh1) spin_geq_gpu(F, R.xrdy + kMaxChunks + pos, prev);
+            if (xh0) spin_geq(F, R.halo[0][0].flag + pos, prev);   // (the neighbour's senders staged it)
+            if (xh1) spin_geq(F, R.halo[0][1].flag + pos, prev);
             if (yl) spin_geq(F, R.halo[1][0].flag + pos, prev);
             if (yu) spin_geq(F, R.halo[1][1].flag + pos, prev);
             if (zl) spin_geq(F, R.halo[2][0].flag, prev);
@@ -370,20 +361,36 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
             const int xf = R.face[0][xrs].layer - tx * 64;
             const bool slane = rowv && (xf >> 1) == lane;
             double *xloc_row = rowv ? R.xloc + ((long long)xrs * sy + y) * F.s[2] : nullptr;   // (warp-uniform)
+            // the x halo column beside the send layer: the neighbour's previous-epoch values, staged in my
+            // receive rows by its senders (first step of a run: T holds it)
+            const int hside = xrs == 0 ? 1 : 0, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
+            const double *hrow = (F.wait_prev && R.halo[0][hside].active && rowv)
+                                     ? R.xrem + (((long long)((F.epoch - 1) & 1) * 2 + hside) * sy + y) * F.s[2]
+                                     : nullptr;
+            const bool hpatch = hrow && (xh >> 1) == lane;
+            double h0 = 0.0;
+            if (hrow) {   // (warp-uniform) this chunk's staged halo values of the row, into the first group
+                for (int z = zs + lane; z < ze; z += 32) cp_async8f(&sHx[warp][z - zs], hrow + z);
+                if (hpatch) h0 = __ldcg(hrow + zs);
+            }
 #define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, YD, \
-                                                          sX[warp], slane, xloc_row)
+                                                          sX[warp], slane, hpatch, h0, sHx[warp])
             if (xrs == 0) {   // upper: send layer s-2
                 if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
             } else {          // lower: send layer 1
                 if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
             }
 #undef XSWEEP
+            if (xloc_row) {   // (warp-uniform) the row's send cells, z-contiguous, into the local staging
+                __syncwarp();
+                for (int z = zs + lane; z < ze; z += 32) xloc_row[z] = sX[warp][z - zs];
+            }
         } else if (did & 12u) {
             fused_sweep<true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, ydst, nullptr,
-                                            false, nullptr);
+                                            false, false, 0.0, nullptr);
         } else {
             fused_sweep<false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr, nullptr,
-                                             false, nullptr);
+                                             false, false, 0.0, nullptr);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver
@@ -436,7 +443,11 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
         c[a] = fc.layer;
         c[third] = t;
         if (forward_phase(F, R, a, c) != b || later_halo(F, R, a, c)) continue;
-        const double v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
+        double v;
+        if (b == 0 && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1)   // staged, not in T2
+            v = __ldcg(R.xrem + (((long long)(F.epoch & 1) * 2 + side) * F.s[1] + c[1]) * F.s[2] + c[2]);
+        else
+            v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
         c[a] = rs == 0 ? 0 : F.s[a] - 1;
         fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v;
         any = true;
@@ -497,47 +508,6 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
         }
         return;
     }
-    if (b >= F.nrim + F.nfwd + 2 * F.nxs) {   // x unpacker of my halo side hs: staged rows -> my T2 column
-        const int e = b - F.nrim - F.nfwd - 2 * F.nxs, hs = e / F.nxs, part = e % F.nxs;
-        if (!R.halo[0][hs].active) return;
-        const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
-        const long long sxy = (long long)sx * sy;
-        const int hx = hs == 0 ? 0 : sx - 1;
-        const double *stg = R.xrem + ((long long)(F.epoch & 1) * 2 + hs) * sy * sz;
-        for (int pos = 0; pos < F.nchunks; ++pos) {
-            if (threadIdx.x == 0) spin_geq(F, R.halo[0][hs].flag + pos, F.epoch);   // the sender's rows arrived
-            __syncthreads();
-            const int2 zr = F.zr[pos];
-            const int nz = zr.y - zr.x;
-            const long long ncell = (long long)(sy - 2) * nz;
-            constexpr int U = 4;
-            for (long long t0 = ((long long)part * blockDim.x + threadIdx.x) * U; t0 < ncell;
-                 t0 += (long long)F.nxs * blockDim.x * U) {
-                double v[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const long long t = t0 + u;
-                    v[u] = t < ncell ? __ldcg(stg + (1 + t / nz) * sz + zr.x + t % nz) : 0.0;
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const long long t = t0 + u;
-                    if (t < ncell) R.T2[(long long)(zr.x + t % nz) * sxy + (long long)(1 + t / nz) * sx + hx] = v[u];
-                }
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {   // the last unpacker of the chunk publishes "x halo of chunk pos ready"
-                fence_acq_rel_gpu();
-                const int ci = hs * kMaxChunks + pos;
-                if (atomicAdd(R.xucnt + ci, 1u) == (unsigned)F.nxs - 1) {
-                    atomicExch(R.xucnt + ci, 0u);
-                    fence_acq_rel_gpu();
-                    st_rel_gpu(R.xrdy + ci, F.epoch);
-                }
-            }
-        }
-        return;
-    }
     if (b >= F.nrim + F.nfwd) {   // x sender: role rs, part of nxs
         const int e = b - F.nrim - F.nfwd, rs = e / F.nxs, part = e % F.nxs;
         const FusedFace &fx = R.face[0][rs];
@@ -593,10 +563,7 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
             if (threadIdx.x == 0)
                 for (int side = 0; side < 2; ++side)
                     if (R.halo[hb][side].active) {
-                        if (hb == 0)   // x halo: in T2 once my unpackers finished the chunk
-                            spin_geq_gpu(F, R.xrdy + side * kMaxChunks + ch, F.epoch);
-                        else
-                            spin_geq(F, R.halo[hb][side].flag + ch, F.epoch);
+                        spin_geq(F, R.halo[hb][side].flag + ch, F.epoch);
                         spin_geq(F, R.halo[hb][side].xflag + ch, F.epoch);
                     }
             __syncthreads();
@@ -623,19 +590,30 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
 }
 
 // After the last step of a run: every incoming face (data and rim/forwarded cells) of the epoch has
-// arrived -- the step is complete for any later work on the stream.  blockIdx.x = hosted rank.  (Waits
-// only for flags of the launch before it on the stream.)
+// arrived -- the step is complete for any later work on the stream -- and the last epoch's staged x halo
+// columns (inner rows and planes) are copied into T2.  blockIdx.y = hosted rank.  (Waits only for flags
+// of the launch before it on the stream.)
 __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
-    const FusedRank &R = F.r[blockIdx.x];
+    const FusedRank &R = F.r[blockIdx.y];
     for (int f = threadIdx.x; f < 6 * F.nchunks; f += blockDim.x) {
         const int a = f / (2 * F.nchunks), rs = (f / F.nchunks) & 1, ch = f % F.nchunks;
         const FusedHalo &h = R.halo[a][rs];
         if (!h.active || (a == 2 && ch > 0)) continue;
-        if (a == 0)
-            spin_geq_gpu(F, R.xrdy + rs * kMaxChunks + ch, F.epoch);   // (unpacked into T2)
-        else
-            spin_geq(F, h.flag + ch, F.epoch);
-        spin_geq(F, h.xflag + ch, F.epoch);
+        if (blockIdx.x == 0 || a == 0) spin_geq(F, h.flag + ch, F.epoch);   // (x data: every block copies)
+        if (blockIdx.x == 0) spin_geq(F, h.xflag + ch, F.epoch);
+    }
+    __syncthreads();
+    const int sx = F.s[0], sy = F.s[1], sz = F.s[2];
+    const long long sxy = (long long)sx * sy, ncell = (long long)(sy - 2) * (sz - 2);
+    for (int side = 0; side < 2; ++side) {
+        if (!R.halo[0][side].active) continue;
+        const int hx = side == 0 ? 0 : sx - 1;
+        const double *stg = R.xrem + ((long long)(F.epoch & 1) * 2 + side) * sy * sz;
+        for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
+             t += (long long)gridDim.x * blockDim.x) {
+            const int z = 1 + (int)(t % (sz - 2)), y = 1 + (int)(t / (sz - 2));
+            R.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(stg + (long long)y * sz + z);
+        }
     }
 }
 
@@ -877,12 +855,10 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     if (xex && !g->fused_xloc) {
         IGG_CUDA(cudaMalloc(&g->fused_xloc, sizeof(double) * stg_words * L));
         IGG_CUDA(cudaMalloc(&g->fused_xrem, sizeof(double) * 2 * stg_words * L));   // [parity][side][y][z]
-        IGG_CUDA(cudaMalloc(&g->fused_xcnt, sizeof(unsigned) * 4 * kMaxChunks * L));  // [send 2 | unpack 2]
-        IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 4 * kMaxChunks * L));
-        IGG_CUDA(cudaMalloc(&g->fused_xrdy, sizeof(unsigned long long) * 2 * kMaxChunks * L));
-        IGG_CUDA(cudaMemset(g->fused_xrdy, 0, sizeof(unsigned long long) * 2 * kMaxChunks * L));
+        IGG_CUDA(cudaMalloc(&g->fused_xcnt, sizeof(unsigned) * 2 * kMaxChunks * L));
+        IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
         g->fused_xsteps = 0;
-        g->allocs += 4;
+        g->allocs += 3;
     }
     g->epoch++;
     FusedParams F{};
@@ -906,9 +882,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         R.rim_ticket = R.ctr + 12 * kMaxChunks;
         R.xloc = xex ? g->fused_xloc + lr * stg_words : nullptr;
         R.xrem = xex ? g->fused_xrem + lr * 2 * stg_words : nullptr;
-        R.xcnt = xex ? g->fused_xcnt + lr * 4 * kMaxChunks : nullptr;
-        R.xucnt = xex ? R.xcnt + 2 * kMaxChunks : nullptr;
-        R.xrdy = xex ? g->fused_xrdy + lr * 2 * kMaxChunks : nullptr;
+        R.xcnt = xex ? g->fused_xcnt + lr * 2 * kMaxChunks : nullptr;
         for (int a = 0; a < 3; ++a)
             for (int rs = 0; rs < 2; ++rs) {
                 // rs = receiver side: 0 <- my layer n-2 into my upper neighbour's layer 0,
@@ -948,7 +922,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         build_layout(g, act, zex);
         g->fused_key = key;
         if (g->fused_xcnt) {   // the x senders' cumulative counters restart with the layout
-            IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 4 * kMaxChunks * L));
+            IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
             g->fused_xsteps = 0;
         }
     }
@@ -976,7 +950,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.nrim = (comm && drain) ? 48 : 0;
     F.nfwd = (comm && drain) ? g->fused_nfwd : 0;
     F.nstencil = g->fused_ntiles;
-    F.per_rank = F.nrim + F.nfwd + 4 * F.nxs + F.nstencil;   // (x senders + x unpackers)
+    F.per_rank = F.nrim + F.nfwd + 2 * F.nxs + F.nstencil;   // (rim, forwarders, x senders, tiles)
     const long long blocks = (long long)F.per_rank * L;
     prof_begin(g, s);
     if (L > 1)
@@ -987,7 +961,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     g->launches++;
     prof_end(g, s, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2) * L);
     if (drain && comm) {
-        fused_drain_kernel<<<L, 128, 0, s>>>(F);
+        fused_drain_kernel<<<dim3(xex ? 2 * g->sm_count / L + 1 : 1, L), 128, 0, s>>>(F);
         IGG_CUDA(cudaGetLastError());
         g->launches++;
     }

@@ -611,7 +611,7 @@ IGG_API igg_status igg_finalize_global_grid(igg_grid *g) {
             if (p != g->proc && g->peer_flags[p]) cudaIpcCloseMemHandle(g->peer_flags[p]);
     }
     igg::process_barrier(g);
-    for (void *p : {(void *)g->h26_ctr, (void *)g->d_gather, (void *)g->fused_xloc, (void *)g->fused_xcnt, (void *)g->fused_xrem, (void *)g->fused_xrdy, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
+    for (void *p : {(void *)g->h26_ctr, (void *)g->d_gather, (void *)g->fused_xloc, (void *)g->fused_xcnt, (void *)g->fused_xrem, (void *)g->fused_tgt_x, (void *)g->fused_tgt_pipe, (void *)g->fused_ctr, (void *)g->recv_arena, (void *)g->send_arena, (void *)g->flags, (void *)g->tickets,
                     (void *)g->d_err, (void *)g->d_scratch, (void *)g->run_T, (void *)g->run_T2, (void *)g->run_Ci})
         if (p) cudaFree(p);
     if (g->d_pinned_out) cudaFreeHost(g->d_pinned_out);

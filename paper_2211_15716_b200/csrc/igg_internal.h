@@ -151,12 +151,10 @@ struct FusedRank {                   // one hosted rank of a fused launch
     double *xloc;
     unsigned int *xcnt;
     // ... into the receiver's staging rows xrem [parity][side][y][z] (contiguous: whole sectors over NVLink,
-    // no scattered remote stores); the receiver's x unpacker blocks copy each chunk into its T2 halo column
-    // and publish xrdy [side][chunk] (GPU scope) for its next step's halo tiles, forwarders and drain
+    // no scattered remote stores); the receiver's halo tiles substitute them for T's halo column in their
+    // sweep (no column is ever written), the forwarders read them, the drain copies the last into T2
     double *xrem;                    // mine (written by my neighbours' senders)
     double *xrem_peer[2];            // the receivers' (indexed like face[0][rs])
-    unsigned int *xucnt;             // [2][kMaxChunks] unpacker counters
-    unsigned long long *xrdy;        // [2][kMaxChunks] epoch whose x halo column of the chunk is in T2
     unsigned int *ctr;               // [6][kMaxChunks] data-flag contribution counters (sender side)
     unsigned int *ctr_x;             // [6][kMaxChunks] rim/forwarded-cell counters
     unsigned int *rim_ticket;
@@ -354,9 +352,8 @@ struct igg_grid : igg::Geom {
     int fused_zchunk[2] = {-1, -1};
     int fused_nfwd = 0;                                  // in-kernel forwarders (pipelined)
     double *fused_xloc = nullptr;                        // x-face local staging rows (fused path)
-    unsigned int *fused_xcnt = nullptr;                  // x-face tile counters (cumulative) + unpackers
+    unsigned int *fused_xcnt = nullptr;                  // x-face tile counters (cumulative)
     double *fused_xrem = nullptr;                        // x-face receive staging (IPC-mapped by the senders)
-    unsigned long long *fused_xrdy = nullptr;            // x halo column unpacked (epoch per side and chunk)
     unsigned long long fused_xsteps = 0;                 // launches with x faces since the counters' reset
     int sm_count = 148;
     double clock_khz = 1.9e6;
