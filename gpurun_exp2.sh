@@ -6,5 +6,6 @@ for d in 2,1,1 1,1,2 1,2,1; do
   timeout 600 $TR bench.py --gpus 2 --dims $d --no-e2e --no-stats > gpurun_out/${T}_n2_${d//,/}.json 2>&1
 done
 IGG_LIBRARY=ablation/libigg_trace.so timeout 300 $TR scripts/fused_trace2.py > gpurun_out/${T}_trace.txt 2>&1; mkdir -p gpurun_out/${T}_trace; mv gpurun_out/trace2_*.npz gpurun_out/${T}_trace/
-timeout 900 python -m pytest tests -q -m gpu -k "multi" > gpurun_out/${T}_pytest_multi.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest_multi.log
+TRACE_DIMS=1,2,1 IGG_LIBRARY=ablation/libigg_trace.so timeout 300 $TR scripts/fused_trace2.py > gpurun_out/${T}_trace_y.txt 2>&1; mkdir -p gpurun_out/${T}_trace_y; mv gpurun_out/trace2_*.npz gpurun_out/${T}_trace_y/
+[ -n "$MULTI" ] && timeout 900 python -m pytest tests -q -m gpu -k "multi" > gpurun_out/${T}_pytest_multi.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_pytest_multi.log
 echo done

@@ -274,13 +274,16 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     b -= F.nrim + F.nfwd + 2 * F.nxs;
     // tile of this block: chunks in visit order; within a chunk, when x or y faces exist, the border
     // tiles (rows ty = 0 and ytiles-1, then columns tx = 0 and xtiles-1) first -- they carry the faces and
-    // take longer, so they start early instead of trailing their chunk -- then the interior, row-major
+    // take longer, so they start early instead of trailing their chunk -- then the interior, row-major.
+    // (Border tiles of chunk c+1 placed before the interior of chunk c measured slower: 2x1x1 exposed
+    // halo 35 us instead of 25.)
     const int nt = F.xtiles * F.ytiles, pos = b / nt;
     int tx, ty;
     {
-        const int t = b - pos * nt, xt = F.xtiles, yt = F.ytiles;
-        const int nrow = xt * min(yt, 2), nborder = nrow + 2 * max(yt - 2, 0);
-        if (!F.border_first) {
+        const int xt = F.xtiles, yt = F.ytiles, t = b - pos * nt;
+        const bool ring = xt > 2 && yt > 2;   // (else every tile is a border tile, row-major)
+        const int nrow = xt * 2, nborder = nrow + 2 * (yt - 2);
+        if (!F.border_first || !ring) {
             tx = t % xt;
             ty = t / xt;
         } else if (t < xt) {
@@ -360,18 +363,18 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         if (xrs >= 0) {
             const int xf = R.face[0][xrs].layer - tx * 64;
             const bool slane = rowv && (xf >> 1) == lane;
-            double *xloc_row = rowv ? R.xloc + ((long long)xrs * sy + y) * F.s[2] : nullptr;   // (warp-uniform)
+            double *xloc = R.xloc + (long long)xrs * sy * F.s[2];   // (staging rows: [z][y])
             // the x halo column beside the send layer: the neighbour's previous-epoch values, staged in my
             // receive rows by its senders (first step of a run: T holds it)
             const int hside = xrs == 0 ? 1 : 0, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
             const double *hrow = (F.wait_prev && R.halo[0][hside].active && rowv)
-                                     ? R.xrem + (((long long)((F.epoch - 1) & 1) * 2 + hside) * sy + y) * F.s[2]
-                                     : nullptr;
+                                     ? R.xrem + ((long long)((F.epoch - 1) & 1) * 2 + hside) * sy * F.s[2] + y
+                                     : nullptr;   // (cell z of the row at hrow[z sy])
             const bool hpatch = hrow && (xh >> 1) == lane;
             double h0 = 0.0;
             if (hrow) {   // (warp-uniform) this chunk's staged halo values of the row, into the first group
-                for (int z = zs + lane; z < ze; z += 32) cp_async8f(&sHx[warp][z - zs], hrow + z);
-                if (hpatch) h0 = __ldcg(hrow + zs);
+                for (int z = zs + lane; z < ze; z += 32) cp_async8f(&sHx[warp][z - zs], hrow + (long long)z * sy);
+                if (hpatch) h0 = __ldcg(hrow + (long long)zs * sy);
             }
 #define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, YD, \
                                                           sX[warp], slane, hpatch, h0, sHx[warp])
@@ -381,9 +384,12 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                 if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
             }
 #undef XSWEEP
-            if (xloc_row) {   // (warp-uniform) the row's send cells, z-contiguous, into the local staging
-                __syncwarp();
-                for (int z = zs + lane; z < ze; z += 32) xloc_row[z] = sX[warp][z - zs];
+            // the tile's send cells into the local staging, plane by plane (the kFTY rows of a plane adjacent)
+            __syncthreads();
+            const int nr = min(kFTY, sy - 1 - ty0);
+            for (int t = tid; t < (ze - zs) * kFTY; t += blockDim.x) {
+                const int r = t % kFTY, z = zs + t / kFTY;
+                if (r < nr) xloc[(long long)z * sy + ty0 + r] = sX[r][z - zs];
             }
         } else if (did & 12u) {
             fused_sweep<true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, ydst, nullptr,
@@ -445,7 +451,7 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
         if (forward_phase(F, R, a, c) != b || later_halo(F, R, a, c)) continue;
         double v;
         if (b == 0 && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1)   // staged, not in T2
-            v = __ldcg(R.xrem + (((long long)(F.epoch & 1) * 2 + side) * F.s[1] + c[1]) * F.s[2] + c[2]);
+            v = __ldcg(R.xrem + ((long long)(F.epoch & 1) * 2 + side) * F.s[1] * F.s[2] + (long long)c[2] * F.s[1] + c[1]);
         else
             v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
         c[a] = rs == 0 ? 0 : F.s[a] - 1;
@@ -514,9 +520,9 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
         if (!fx.active) return;
         const int sy = F.s[1], sz = F.s[2];
         const double *loc = R.xloc + (long long)rs * sy * sz;
-        // the receiver's staging rows of its halo side rs, this epoch's parity (z-contiguous)
+        // the receiver's staging of its halo side rs ([z][y]), this epoch's parity
         double *dst = R.xrem_peer[rs] + ((long long)(F.epoch & 1) * 2 + rs) * sy * sz;
-        for (int pos = 0; pos < F.nchunks; ++pos) {
+        for (int pos = part; pos < F.nchunks; pos += F.nxs) {   // sender part owns chunks part + k nxs
             if (threadIdx.x == 0) {   // every face tile of the chunk has staged its rows (GPU-scope acquire)
                 const long long t0 = clock64();
                 while (ld_acq_gpu_u32(R.xcnt + rs * kMaxChunks + pos) < F.xtarget) {
@@ -528,25 +534,38 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
                 }
             }
             __syncthreads();
+            TRACE_AT(1);
+            // the chunk's planes are one contiguous block of the [z][y] staging: a flat copy, 16-B vectors
+            // when aligned, U vectors in flight per thread.  One sender per chunk: a chunk's copy then
+            // overlaps the next chunks' tiles.  (All senders copying a slice of every chunk measured
+            // slower -- each sender pays one system fence per chunk in sequence -- and one SM's NVLink
+            // stores drain at only a few GB/s, so the copy is not made wider.)
             const int2 zr = F.zr[pos];
-            const int nz = zr.y - zr.x;
-            const long long ncell = (long long)(sy - 2) * nz;
+            const long long a0 = (long long)zr.x * sy, a1 = (long long)zr.y * sy;
             constexpr int U = 4;
-            for (long long t0 = ((long long)part * blockDim.x + threadIdx.x) * U; t0 < ncell;
-                 t0 += (long long)F.nxs * blockDim.x * U) {
-                double v[U];
+            if (a0 < a1 && !(a0 & 1)) {
+                const double2 *s2 = reinterpret_cast<const double2 *>(loc + a0);
+                double2 *d2 = reinterpret_cast<double2 *>(dst + a0);
+                const long long n2 = (a1 - a0) >> 1;
+                for (long long t0 = threadIdx.x; t0 < n2; t0 += (long long)blockDim.x * U) {
+                    double2 v[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {   // z-contiguous reads of the local rows
-                    const long long t = t0 + u;
-                    v[u] = t < ncell ? __ldcg(loc + (1 + t / nz) * sz + zr.x + t % nz) : 0.0;
-                }
+                    for (int u = 0; u < U; ++u) {
+                        const long long t = t0 + (long long)u * blockDim.x;
+                        if (t < n2) v[u] = __ldcg(s2 + t);
+                    }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const long long t = t0 + u;
-                    if (t < ncell) dst[(1 + t / nz) * sz + zr.x + t % nz] = v[u];
+                    for (int u = 0; u < U; ++u) {
+                        const long long t = t0 + (long long)u * blockDim.x;
+                        if (t < n2) d2[t] = v[u];
+                    }
                 }
+                if (((a1 - a0) & 1) && threadIdx.x == 0) dst[a1 - 1] = __ldcg(loc + a1 - 1);
+            } else {
+                for (long long t = a0 + threadIdx.x; t < a1; t += blockDim.x) dst[t] = __ldcg(loc + t);
             }
             __syncthreads();
+            TRACE_AT(2);
             if (threadIdx.x == 0) {
                 fence_acq_rel_sys();
                 contribute(F, R, 0, rs, pos);
@@ -611,8 +630,8 @@ __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
         const double *stg = R.xrem + ((long long)(F.epoch & 1) * 2 + side) * sy * sz;
         for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
              t += (long long)gridDim.x * blockDim.x) {
-            const int z = 1 + (int)(t % (sz - 2)), y = 1 + (int)(t / (sz - 2));
-            R.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(stg + (long long)y * sz + z);
+            const int y = 1 + (int)(t % (sy - 2)), z = 1 + (int)(t / (sy - 2));
+            R.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(stg + (long long)z * sy + y);
         }
     }
 }
@@ -682,7 +701,7 @@ static void build_layout(igg_grid *g, const bool act[3][2], bool zex) {
     std::vector<unsigned> tgt_d(6 * kMaxChunks, 0u), tgt_x(6 * kMaxChunks, 0u);
     for (int rs = 0; rs < 2; ++rs) {
         for (int c = 0; c < nch; ++c) {
-            tgt_d[(0 * 2 + rs) * kMaxChunks + c] = kFusedXSenders;   // (the x senders publish x faces)
+            tgt_d[(0 * 2 + rs) * kMaxChunks + c] = 1;   // (the chunk's x sender publishes its x face)
             tgt_x[(0 * 2 + rs) * kMaxChunks + c] = 1;
             tgt_d[(1 * 2 + rs) * kMaxChunks + c] = xtiles;
             tgt_x[(1 * 2 + rs) * kMaxChunks + c] = 1 + (xh ? nf : 0);
@@ -929,7 +948,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     const bool xface = act[0][0] || act[0][1];
     if (xface) ++g->fused_xsteps;   // launches whose x-face tiles count on the cumulative counters
     F.xtarget = (unsigned)((unsigned long long)g->fused_geo[5] * g->fused_xsteps);
-    F.nxs = xface ? kFusedXSenders : 0;
+    F.nxs = xface ? std::min(kFusedXSenders, g->fused_nchunks) : 0;
     F.nchunks = g->fused_nchunks;
     for (int c = 0; c < F.nchunks; ++c) F.zr[c] = g->fused_zr[c];
     F.xtiles = g->fused_geo[4];

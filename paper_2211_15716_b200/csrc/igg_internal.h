@@ -125,7 +125,7 @@ struct HeatRegionList {
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
 constexpr int kMaxFusedRanks = 8;    // ranks hosted on one GPU that one fused launch covers
-constexpr int kFusedXSenders = 4;    // x sender blocks per x face and rank
+constexpr int kFusedXSenders = 16;   // x sender blocks per x face and rank (at most one per chunk)
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // the receiver's T2 (a sibling's, or peer-mapped); lands in its halo layer
     unsigned long long *flag;        // receiver's data flags of (axis, side): [kMaxChunks] (z faces: [0])

@@ -61,6 +61,8 @@ CASES = [
     ((130, 20, 22), (2, 2, 2), (1, 0, 1)),
     ((68, 18, 20), (4, 1, 1), (1, 0, 0)),     # interior ranks: both x sides
     ((130, 20, 22), (1, 2, 4), (0, 1, 1)),
+    ((66, 36, 34), (2, 2, 1), (0, 1, 0)),     # two x tiles: every tile a border tile
+    ((130, 6, 34), (2, 1, 2), (0, 0, 0)),     # one y tile
 ]
 
 
