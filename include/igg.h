@@ -171,6 +171,11 @@ igg_status igg_coords(const igg_grid *grid, int rank, int coords_out[3]);
  * g = c(n-o) + l; on a periodic axis (g - o/2) mod p(n-o) (reading 15). */
 igg_status igg_local_to_global(const igg_grid *grid, int rank, int axis, long long l, long long *g_out);
 
+/* Physical coordinate of local layer l of `rank` on axis (SPEC.md:119-122 global_coord; spacing as in
+ * PAPER.md:66-68, dx = lx/(nx_g()-1)): x = g * spacing with g = igg_local_to_global(...).  Same range
+ * check as igg_local_to_global (IGG_E_ARG). */
+igg_status igg_global_coord(const igg_grid *grid, int rank, int axis, long long l, double spacing, double *x_out);
+
 /* Buffer-pool allocation counter: constant once every
  * field shape has been exchanged once. */
 igg_status igg_buffer_allocs(const igg_grid *grid, long long *count_out);
@@ -302,6 +307,11 @@ igg_status igg_field_global_max(igg_grid *grid, const double *const *f, long lon
  * Collective and synchronous (a utility, not on the hot path). */
 igg_status igg_gather(igg_grid *grid, const igg_field *fields, int root_proc, double *host_out,
                       igg_stream_t stream);
+
+/* Output of a gathered field: `path` receives the one-line header "IGRIDF1 nx ny nz\n"
+ * followed by nx*ny*nz little-endian binary64 values of `host` (x fastest).  Host-only; IGG_E_ARG on a
+ * null pointer, a non-positive size or a failed open/write (igg_last_error names the path). */
+igg_status igg_save_field(const char *path, const double *host, const long long n[3]);
 
 /* ------------------------------------------------------------------ control */
 enum {

@@ -67,6 +67,9 @@ SIGNATURES = {
     "igg_n_g": [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong, c_ll_p],
     "igg_coords": [ctypes.c_void_p, ctypes.c_int, c_int_p],
     "igg_local_to_global": [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, c_ll_p],
+    "igg_global_coord": [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_longlong, ctypes.c_double,
+                         ctypes.POINTER(ctypes.c_double)],
+    "igg_save_field": [ctypes.c_char_p, ctypes.c_void_p, c_ll_p],
     "igg_buffer_allocs": [ctypes.c_void_p, c_ll_p],
     "igg_kernel_launches": [ctypes.c_void_p, c_ll_p],
     "igg_update_halo": [ctypes.c_void_p, ctypes.POINTER(igg_field), ctypes.c_int, ctypes.c_void_p],

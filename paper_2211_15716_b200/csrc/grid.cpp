@@ -6,6 +6,7 @@
 // efficiently reuse send and receive buffers and streams ... all data
 // transfers are performed on non-blocking high-priority streams"  PAPER.md:94.
 // @hide_communication (16,2,2): PAPER.md:75.
+#include <cstdio>
 #include <algorithm>
 #include <functional>
 #include <cstring>
@@ -666,6 +667,28 @@ IGG_API igg_status igg_local_to_global(const igg_grid *g, int rank, int axis, lo
         v = ((v - g->o[axis] / 2) % P + P) % P;
     }
     *g_out = v;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_global_coord(const igg_grid *g, int rank, int axis, long long l, double spacing, double *x_out) {
+    IGG_TRY
+    if (!x_out) fail(IGG_E_ARG, "igg_global_coord: NULL out");
+    long long gi = 0;
+    const igg_status st = igg_local_to_global(g, rank, axis, l, &gi);
+    if (st != IGG_OK) return st;
+    *x_out = (double)gi * spacing;
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_save_field(const char *path, const double *host, const long long n[3]) {
+    IGG_TRY
+    if (!path || !host || !n || n[0] <= 0 || n[1] <= 0 || n[2] <= 0) fail(IGG_E_ARG, "igg_save_field: bad argument");
+    FILE *f = std::fopen(path, "wb");
+    if (!f) fail(IGG_E_ARG, std::string("igg_save_field: cannot open ") + path);
+    const size_t cnt = (size_t)(n[0] * n[1] * n[2]);
+    const bool ok = std::fprintf(f, "IGRIDF1 %lld %lld %lld\n", n[0], n[1], n[2]) > 0 &&
+                    std::fwrite(host, sizeof(double), cnt, f) == cnt;   // (x86-64 / aarch64: little-endian)
+    if (std::fclose(f) != 0 || !ok) fail(IGG_E_ARG, std::string("igg_save_field: write failed: ") + path);
     IGG_CATCH
 }
 

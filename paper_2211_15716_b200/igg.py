@@ -198,6 +198,12 @@ class Grid:
         _ok(L.lib().igg_local_to_global(self._handle(), rank, axis, l, ctypes.byref(out)))
         return out.value
 
+    def global_coord(self, rank: int, axis: int, l: int, spacing: float) -> float:
+        """Physical coordinate of local layer l: igg_global_coord."""
+        out = ctypes.c_double()
+        _ok(L.lib().igg_global_coord(self._handle(), rank, axis, l, float(spacing), ctypes.byref(out)))
+        return out.value
+
     def global_indices(self, rank: int, axis: int, size: int):
         import numpy as np
         return np.array([self.local_to_global(rank, axis, l) for l in range(size)], dtype=np.int64)
@@ -365,6 +371,15 @@ class Grid:
         out = np.empty(shape, dtype=np.float64) if me_root else None
         _ok(L.lib().igg_gather(self._handle(), arr, root, out.ctypes.data if me_root else None, _stream(stream)))
         return out
+
+    @staticmethod
+    def save_field(path: str, array) -> None:
+        """Write a gathered global field (numpy (Nz, Ny, Nx) float64) as SPEC.md:410's file: header
+        "IGRIDF1 nx ny nz", then the raw little-endian binary64 values (igg_save_field)."""
+        import numpy as np
+        a = np.ascontiguousarray(array, dtype=np.float64)
+        n = (ctypes.c_longlong * 3)(a.shape[2], a.shape[1], a.shape[0])
+        _ok(L.lib().igg_save_field(str(path).encode(), a.ctypes.data, n))
 
     # -- reductions (PAPER.md:73)
     def global_max(self, local: float) -> float:

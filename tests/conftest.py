@@ -15,13 +15,14 @@ def pytest_configure(config):
 
 
 def pytest_collection_modifyitems(config, items):
-    import pytest
+    # the `ablation` tests need the ablation build: with the product library they are deselected (not
+    # skipped); tests/test_gpu_ablation.py runs them against the ablation build in a subprocess
     if "ablation" in os.environ.get("IGG_LIBRARY", ""):
         return
-    skip = pytest.mark.skip(reason="ablation build only (tests/test_gpu_ablation.py runs these with it)")
-    for it in items:
-        if "ablation" in it.keywords:
-            it.add_marker(skip)
+    keep = [it for it in items if "ablation" not in it.keywords]
+    if len(keep) != len(items):
+        config.hook.pytest_deselected(items=[it for it in items if "ablation" in it.keywords])
+        items[:] = keep
 
 
 def pytest_sessionstart(session):

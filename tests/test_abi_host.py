@@ -190,3 +190,17 @@ def test_product_package_never_imports_oracle():
                 src = open(os.path.join(dirpath, f), errors="replace").read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
                 assert "heat3d_oracle" not in src, f
+
+
+def test_save_field_writes_spec_file_format(tmp_path):
+    """header "IGRIDF1 nx ny nz\\n", then the raw little-endian binary64 values, x fastest."""
+    import numpy as np
+    a = np.arange(3 * 4 * 5, dtype=np.float64).reshape(5, 4, 3) * 0.25 - 1.0   # (nz, ny, nx)
+    p = tmp_path / "field.igf"
+    P.Grid.save_field(p, a)
+    raw = p.read_bytes()
+    head, _, body = raw.partition(b"\n")
+    assert head == b"IGRIDF1 3 4 5"
+    assert np.array_equal(np.frombuffer(body, dtype="<f8"), a.ravel())
+    with pytest.raises(P.IggError):
+        P.Grid.save_field(tmp_path / "missing_dir" / "x.igf", a)

@@ -127,6 +127,25 @@ def test_gather_spec_example():
         g.finalize()
 
 
+def test_local_to_global_and_global_coord_spec_examples():
+    """SPEC.md:123-126 (1-based there, 0-based here): n=8, o=2; coord 0: local 0 -> global 0; coord 1:
+    local 0 -> global 6, local 7 -> global 13 == n_g - 1; global_coord = global index * spacing; a layer
+    outside [0, n+o) is a bounds error."""
+    g = P.init_global_grid(8, 8, 8, dims=(2, 1, 1), local_ranks=2, device=0)
+    try:
+        assert g.n_g[0] == 14
+        assert g.local_to_global(0, 0, 0) == 0
+        assert g.local_to_global(1, 0, 0) == 6
+        assert g.local_to_global(1, 0, 7) == 13
+        dx = 1.0 / (g.n_g[0] - 1)
+        assert g.global_coord(1, 0, 7, dx) == 13 * dx
+        assert g.global_coord(0, 1, 3, 0.5) == 1.5
+        with pytest.raises(P.IggError):
+            g.global_coord(1, 0, 10, dx)
+    finally:
+        g.finalize()
+
+
 def test_gather_inverts_windows():
     """gather(window(G, rank)) == G for random global fields (the window map is the oracle)."""
     import torch
