@@ -2,7 +2,7 @@
 every kernel family of the single-process paths on virtual ranks -- the fused stencil + peer-store
 kernel over several ranks in one launch (flags, staging, forwarders, drain), the 26-neighbour
 update_halo kernel, the per-axis P2P protocol (IGG_OPT_LOCAL_P2P), the split schedule's box-list / slab /
-generic region kernels, the acoustic kernels, the binary32 kernels, the max reduction."""
+generic region kernels, the acoustic kernels (split step and fused run), the binary32 kernels, the max reduction."""
 import sys
 sys.path.insert(0, ".")
 import torch
@@ -58,6 +58,15 @@ F = ac.alloc_fields(g)
 ac.init_random(g, F)
 d = ac.spacing(g)
 ac.run(g, F, 2, ac.stable_dt(d), d, bw=(4, 4, 4))
+torch.cuda.synchronize()
+g.check()
+g.finalize()
+# acoustic run on one rank: the fused V+P sweep (double-buffered)
+g = P.init_global_grid(70, 20, 37, device=0)
+F, F2 = ac.alloc_fields(g), ac.alloc_fields(g)
+ac.init_random(g, F)
+d = ac.spacing(g)
+g.acoustic_run(F, F2, 3, ac.stable_dt(d), ac.RHO, ac.K, *d)
 torch.cuda.synchronize()
 g.check()
 g.finalize()
