@@ -37,8 +37,9 @@ namespace igg {
 
 namespace {
 
-__device__ __forceinline__ void st_rel_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// (after a fence.acq_rel: fence + relaxed store is the PTX release pattern; st.release would fence again)
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long *p) {
     unsigned long long v;
@@ -81,7 +82,7 @@ __device__ __forceinline__ void contribute(const FusedParams &F, const FusedRank
     const int i = (a * 2 + rs) * kMaxChunks + c;
     if (atomicAdd(R.ctr + i, 1u) == F.tgt[i] - 1) {
         fence_acq_rel_sys();   // (acquire side of the other contributors' release, then the flag's release)
-        st_rel_sys(R.face[a][rs].flag + c, F.epoch);
+        st_relaxed_sys(R.face[a][rs].flag + c, F.epoch);
         atomicExch(R.ctr + i, 0u);
     }
 }
@@ -90,7 +91,7 @@ __device__ __forceinline__ void contribute_x(const FusedParams &F, const FusedRa
     const int i = (a * 2 + rs) * kMaxChunks + c;
     if (atomicAdd(R.ctr_x + i, 1u) == F.tgt_x[i] - 1) {
         fence_acq_rel_sys();
-        st_rel_sys(R.face[a][rs].xflag + c, F.epoch);
+        st_relaxed_sys(R.face[a][rs].xflag + c, F.epoch);
         atomicExch(R.ctr_x + i, 0u);
     }
 }

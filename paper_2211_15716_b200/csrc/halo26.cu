@@ -37,7 +37,7 @@ namespace igg {
 namespace {
 
 constexpr int kH26Threads = 256;
-constexpr int kH26ILP = 8;
+constexpr int kH26ILP = 4;
 constexpr int kH26Chunk = kH26Threads * kH26ILP;   // elements per work chunk
 
 struct H26Item {
@@ -48,7 +48,7 @@ struct H26Item {
     int bx, by, bz;       // box extent
     int esz;              // bytes per element (8 or 4)
     int wait;             // index into waitp (-1: none): flag that must reach the epoch first
-    int pad;
+    int remote;           // 1: the destination is another GPU's memory (system-scope release)
     long long chunk0;     // first chunk of this item
     long long cells;
 };
@@ -63,6 +63,10 @@ struct H26Plan {
 __device__ __forceinline__ void st_rel_sys(unsigned long long *p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// (after a fence.acq_rel: the release pattern without a fence per store)
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -71,6 +75,7 @@ __device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long lon
 // the PTX release / acquire patterns (fence.acq_rel + relaxed RMW / relaxed RMW + fence.acq_rel) are all the
 // protocol needs; __threadfence_system would be the heavier sequentially consistent fence.sc
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void spin(const unsigned long long *f, unsigned long long v, long long timeout, int *err) {
     const long long t0 = clock64();
     while (ld_acq_sys(f) < v) {
@@ -108,33 +113,68 @@ __device__ __forceinline__ void copy_chunk(const H26Item &it, long long c) {
 
 }  // namespace
 
-constexpr int kH26Batch = 4;   // chunks per claim (one counter update and one item search per batch)
+constexpr int kH26Batch = 1;   // chunks per claim (small chunks, one per claim: latency, not bandwidth, rules
+                               // small halos; a trace of n = 64 showed 2.9 us per chunk in few blocks)
+constexpr int kH26SmemItems = 512;   // item starts cached in shared memory (the claim's search)
+
+#ifndef H26_TRACE
+#define H26_TRACE 0   // diagnostics build only: per-block %globaltimer stamps of the last launch
+#endif
+#if H26_TRACE
+__device__ unsigned long long g_h26_trace[4096 * 8];
+__device__ __forceinline__ unsigned long long h26_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define H26_AT(k) \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_h26_trace[blockIdx.x * 8 + (k)] = h26_gtimer()
+#define H26_VAL(k, v) \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_h26_trace[blockIdx.x * 8 + (k)] = (v)
+#else
+#define H26_AT(k)
+#define H26_VAL(k, v)
+#endif
 
 __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restrict__ base, unsigned long long epoch,
                                                              unsigned int *ctr, long long timeout, int *err) {
+    H26_AT(0);
     const H26Plan &P = *reinterpret_cast<const H26Plan *>(base);
     const H26Item *items = reinterpret_cast<const H26Item *>(base + P.o_items);
     __shared__ long long s_c;
     __shared__ int s_it, s_waited;
+    __shared__ long long s_chunk0[kH26SmemItems];
+    const bool cached = P.nitems <= kH26SmemItems;
+    if (cached)
+        for (int q = threadIdx.x; q < P.nitems; q += blockDim.x) s_chunk0[q] = items[q].chunk0;
+    __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x < P.nready) {   // my remote senders may store into me
         unsigned long long *const *ready = reinterpret_cast<unsigned long long *const *>(base + P.o_ready);
         st_rel_sys(ready[threadIdx.x], epoch);
     }
     const long long nbatch = (P.nchunks + kH26Batch - 1) / kH26Batch;
     unsigned mydone = 0;   // store chunks this block finished and has not counted yet
+    bool myremote = false;   // some of them went to another GPU: system-scope release, else GPU scope
     // count my finished store chunks (after a system fence); the count completing all store chunks
     // publishes every data flag (release)
     auto flush = [&]() {
         __syncthreads();
         if (threadIdx.x == 0 && mydone) {
-            fence_acq_rel_sys();   // (release: the block's stores, ordered before thread 0 by the barrier)
+            // (release: the block's stores, ordered before thread 0 by the barrier; GPU scope suffices when
+            // they all stayed on this GPU -- the completing block's system-scope fence and flag release
+            // extend the chain to any receiver)
+            if (myremote) fence_acq_rel_sys(); else fence_acq_rel_gpu();
             if (atomicAdd(ctr + 1, mydone) + mydone == (unsigned)P.nstore_chunks) {
-                fence_acq_rel_sys();   // (acquire: every other block's release; then the flags' release)
+                // acquire every other block's release, then ONE release for all the flags: fence.acq_rel +
+                // relaxed stores is the PTX release pattern (a st.release per flag would fence per flag:
+                // a trace showed ~1.5 us each, 40 us for the 26 flags of a periodic rank)
+                fence_acq_rel_sys();
                 unsigned long long *const *sig = reinterpret_cast<unsigned long long *const *>(base + P.o_signal);
-                for (int q = 0; q < P.nsignal; ++q) st_rel_sys(sig[q], epoch);
+                for (int q = 0; q < P.nsignal; ++q) st_relaxed_sys(sig[q], epoch);
             }
         }
         mydone = 0;
+        myremote = false;
     };
     long long bt;
     for (;;) {
@@ -145,7 +185,7 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
             if (c0 < P.nchunks)
                 while (lo < hi) {
                     const int mid = (lo + hi + 1) >> 1;
-                    if (items[mid].chunk0 <= c0) lo = mid; else hi = mid - 1;
+                    if ((cached ? s_chunk0[mid] : items[mid].chunk0) <= c0) lo = mid; else hi = mid - 1;
                 }
             s_it = lo;
             s_waited = -1;
@@ -159,14 +199,16 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
             // before the first unpack chunk (the only ones that wait on this launch), count my store
             // chunks: claims are monotonic, so no store work follows (block-uniform)
             if (c >= P.nstore_chunks && mydone) flush();
-            while (iti + 1 < P.nitems && items[iti + 1].chunk0 <= c) ++iti;
+            while (iti + 1 < P.nitems && (cached ? s_chunk0[iti + 1] : items[iti + 1].chunk0) <= c) ++iti;
             const H26Item &it = items[iti];
             if (it.wait >= 0 && s_waited != it.wait) {   // (block-uniform)
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     const unsigned long long *const *wp =
                         reinterpret_cast<const unsigned long long *const *>(base + P.o_waitp);
+                    H26_AT(5);
                     spin(wp[it.wait], epoch, timeout, err);
+                    H26_AT(6);
                     s_waited = it.wait;
                 }
                 __syncthreads();
@@ -175,11 +217,17 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
                 copy_chunk<float>(it, c - it.chunk0);
             else
                 copy_chunk<double>(it, c - it.chunk0);
-            if (c < P.nstore_chunks) ++mydone;
+            if (c < P.nstore_chunks) {
+                ++mydone;
+                myremote = myremote || it.remote;
+            }
         }
         __syncthreads();   // (s_c / s_it / s_waited are rewritten by the next claim)
+        H26_AT(1);
     }
+    H26_AT(2);
     flush();
+    H26_AT(3);
     if (bt == nbatch + gridDim.x - 1) {   // the last block to leave: every incoming face, then reset
         const unsigned long long *const *we = reinterpret_cast<const unsigned long long *const *>(base + P.o_wait_end);
         for (int q = threadIdx.x; q < P.nwait_end; q += blockDim.x) spin(we[q], epoch, timeout, err);
@@ -188,7 +236,21 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
             ctr[1] = 0u;
         }
     }
+    H26_AT(4);
+    H26_VAL(7, (unsigned long long)P.nchunks | ((unsigned long long)P.nstore_chunks << 20) |
+                   ((unsigned long long)P.nitems << 40));
 }
+
+#if H26_TRACE
+}  // namespace igg
+IGG_API igg_status igg_debug_h26_trace(unsigned long long *host, int nblocks) {
+    IGG_TRY
+    IGG_CUDA(cudaDeviceSynchronize());
+    IGG_CUDA(cudaMemcpyFromSymbol(host, igg::g_h26_trace, sizeof(unsigned long long) * 8 * std::min(nblocks, 4096)));
+    IGG_CATCH
+}
+namespace igg {
+#endif
 
 // ------------------------------------------------------------------ host side
 static int dir_index(int ex, int ey, int ez) { return (ex + 1) * 9 + (ey + 1) * 3 + (ez + 1); }
@@ -315,8 +377,10 @@ void exchange26(igg_grid *g, const igg_field *fields, int nf, const Plan &plan, 
                         it.dsy = dsy;
                         it.dsz = dsz;
                     }
-                    if (ml < 0)   // remote receiver: wait until it released its halos of the last epoch
+                    if (ml < 0) {   // remote receiver: wait until it released its halos of the last epoch
                         it.wait = waitp_index(h26_flag(g->flags, L, lr, 32 + e));
+                        it.remote = 1;
+                    }
                     store.push_back(it);
                     // the receiver's data flag of the direction pointing back at me
                     add_unique(signal, h26_flag(mflags, L, mlr, dir_index(-ev[0], -ev[1], -ev[2])));
@@ -435,7 +499,7 @@ void exchange26(igg_grid *g, const igg_field *fields, int nf, const Plan &plan, 
         g->allocs++;
     }
     // every process launches (a rank with nothing to send still publishes ready and awaits its halos)
-    const long long grid = std::max(1LL, std::min<long long>((hit->nchunks + kH26Batch - 1) / kH26Batch, 2LL * g->sm_count));
+    const long long grid = std::max(1LL, std::min<long long>((hit->nchunks + kH26Batch - 1) / kH26Batch, 4LL * g->sm_count));
     halo26_kernel<<<(unsigned)grid, kH26Threads, 0, st>>>(static_cast<const char *>(hit->dplan), g->epoch, g->h26_ctr,
                                                           (long long)(g->spin_timeout_ms * g->clock_khz), g->d_err);
     IGG_CUDA(cudaGetLastError());

@@ -1158,9 +1158,10 @@ __device__ __forceinline__ long long face_index(const CopyDesc &d, long long i) 
     return ((d.lo + zl) * d.sy + y) * d.sx + x;
 }
 
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void fence_acq_rel_sys_k() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1208,21 +1209,22 @@ __device__ __forceinline__ void copy_face(const CopyDesc &d) {
 
 // pack: field slab -> buffer (own send buffer, a local rank's receive slot, or a
 // peer GPU's receive slot over NVLink).  If the list carries signals, the last
-// CTA to finish publishes the epoch to the peers' receive flags: every thread
-// fences its stores (system scope) before the CTA barrier, the elected CTA
-// acquires through the ticket and release-stores each flag.
+// CTA to finish publishes the epoch to the peers' receive flags: the CTA barrier
+// orders every thread's stores before thread 0's fence.acq_rel.sys (cumulative),
+// the ticket counts the CTA; the last CTA acquires with one more fence and
+// stores the flags relaxed (fence + relaxed stores = one release for them all).
 template <int N>
 __global__ void __launch_bounds__(kCopyThreads) pack_kernel(const __grid_constant__ CopyListT<N> L) {
     const CopyDesc &d = L.d[blockIdx.y];
     copy_face<true>(d);
     if (L.nsignal > 0) {
-        __threadfence_system();
         __syncthreads();
         if (threadIdx.x == 0) {
+            fence_acq_rel_sys_k();
             const unsigned t = atomicAdd(L.ticket, 1u);
             if (t == L.ticket_total - 1) {
-                __threadfence_system();
-                for (int s = 0; s < L.nsignal; ++s) st_release_sys(L.signal[s], L.epoch);
+                fence_acq_rel_sys_k();
+                for (int s = 0; s < L.nsignal; ++s) st_relaxed_sys(L.signal[s], L.epoch);
                 atomicExch(L.ticket, 0u);
             }
         }

@@ -9,9 +9,9 @@ import paper_2211_15716_b200 as P
 dims = tuple(int(x) for x in os.environ.get("HL_DIMS", "2,1,1").split(","))
 R = dims[0] * dims[1] * dims[2]
 reps = int(os.environ.get("HL_REPS", "100"))
-for h26, lp in ((1, 0), (0, 1)):
+for h26, lp in ((1, 0), (0, 1)) if not os.environ.get("HL_ONLY26") else ((1, 0),):
     for n in [int(x) for x in os.environ.get("HL_SIZES", "64,128,256,512,768").split(",")]:
-        g = P.init_global_grid(n, n, n, dims=dims, periods=(1, 1, 1), path="p2p", local_ranks=R, device=0)
+        g = P.init_global_grid(n, n, n, dims=dims, periods=tuple(int(x) for x in os.environ.get("HL_PER", "1,1,1").split(",")), path="p2p", local_ranks=R, device=0)
         g.set_option(P.OPT_HALO26, h26)
         g.set_option(P.OPT_LOCAL_P2P, lp)
         g.set_option(P.OPT_HALO_STREAM, 1)

@@ -37,6 +37,25 @@ __global__ void add_v4(const double *__restrict__ a, const double *__restrict__ 
     }
 }
 
+// the acoustic step's pattern: 4 streams read, 4 written (P, Vx, Vy, Vz in; out fields), 8-B per thread
+__global__ void rw44(const double *__restrict__ a, const double *__restrict__ b, const double *__restrict__ c,
+                     const double *__restrict__ d, double *__restrict__ e, double *__restrict__ f,
+                     double *__restrict__ g, double *__restrict__ h, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double x = __ldg(a + i), y = __ldg(b + i), z = __ldg(c + i), w = __ldg(d + i);
+        e[i] = x + y; f[i] = y + z; g[i] = z + w; h[i] = w + x;
+    }
+}
+__global__ void rw44v2(const double2 *__restrict__ a, const double2 *__restrict__ b, const double2 *__restrict__ c,
+                       const double2 *__restrict__ d, double2 *__restrict__ e, double2 *__restrict__ f,
+                       double2 *__restrict__ g, double2 *__restrict__ h, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double2 x = __ldg(a + i), y = __ldg(b + i), z = __ldg(c + i), w = __ldg(d + i);
+        e[i] = make_double2(x.x + y.x, x.y + y.y); f[i] = make_double2(y.x + z.x, y.y + z.y);
+        g[i] = make_double2(z.x + w.x, z.y + w.y); h[i] = make_double2(w.x + x.x, w.y + x.y);
+    }
+}
+
 // TMA bulk: tiles of kT doubles of a and b per stage
 constexpr int kT = 2048, kS = 3;
 __global__ void __launch_bounds__(256, 1) add_bulk(const double *a, const double *b, double *c, long long ntiles) {
@@ -115,6 +134,19 @@ int main() {
     const int smem = 2 * kS * kT * 8 + kS * 8;
     CK(cudaFuncSetAttribute(add_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     timeit("bulk 1x256 (TMA, 3 stages)", bytes, [&] { add_bulk<<<sms, 256, smem>>>(a, b, c, n / kT); });
+    {   // 4R4W over 8 arrays of 512^3 doubles (the acoustic step's 64 B per cell)
+        const long long m = 1LL << 27;
+        double *q[8];
+        for (int t = 0; t < 8; ++t) { CK(cudaMalloc(&q[t], m * 8)); CK(cudaMemset(q[t], 0, m * 8)); }
+        for (int k : {4, 8, 16}) {
+            char nm[64]; snprintf(nm, 64, "4R4W 8-B %dx256", k);
+            timeit(nm, 64.0 * m, [&] { rw44<<<sms * k, 256>>>(q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], m); });
+            snprintf(nm, 64, "4R4W 16-B %dx256", k);
+            timeit(nm, 64.0 * m, [&] { rw44v2<<<sms * k, 256>>>((double2 *)q[0], (double2 *)q[1], (double2 *)q[2], (double2 *)q[3],
+                                                             (double2 *)q[4], (double2 *)q[5], (double2 *)q[6], (double2 *)q[7], m / 2); });
+        }
+        for (int t = 0; t < 8; ++t) CK(cudaFree(q[t]));
+    }
     cudaMemcpy(c, a, n * 8, cudaMemcpyDeviceToDevice);
     timeit("cudaMemcpy D2D (2 x 8 B)", 2.0 * 8 * n, [&] { cudaMemcpyAsync(c, a, n * 8, cudaMemcpyDeviceToDevice); });
     printf("sms %d\n", sms);
