@@ -185,6 +185,10 @@ __device__ __forceinline__ double pupd(double p, double cP, double r0, double r1
 #ifndef AF_D
 #define AF_D 2
 #endif
+#ifndef AF_TY
+#define AF_TY 4
+#endif
+constexpr int kAfTY = AF_TY;   // rows per CTA (one warp each)
 constexpr int kAfKC = AF_KC;   // P planes per CTA
 constexpr int kAfD = AF_D;     // planes in flight per thread (cp.async ring)
 constexpr int kAfS = 7;     // ring streams: P, Vx, Vy, Vz of my cell; P(j-1), P(j+1), Vy(j+1) of the rows beside
@@ -223,7 +227,7 @@ __device__ __forceinline__ void af_issue(double (*r)[kAfS], const AcousticFields
 #define AF_ST(p, v) (*(p) = (v))
 #endif
 __device__ __forceinline__ void af_sweep(const AcousticFields &I, const AcousticFields &O, const AcousticCoef &C,
-                                         double (*ring)[32 * kAcTY][kAfS], int lane, int tid, int i, int j, int z0,
+                                         double (*ring)[32 * kAfTY][kAfS], int lane, int tid, int i, int j, int z0,
                                          int z1) {
     const int nx = I.n[0], ny = I.n[1], nz = I.n[2];
     const bool act = i < nx;
@@ -308,10 +312,10 @@ __device__ __forceinline__ void af_sweep(const AcousticFields &I, const Acoustic
     cpwait<0>();
 }
 
-__global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid_constant__ AcousticFields I,
+__global__ void __launch_bounds__(32 * kAfTY) acoustic_fused_kernel(const __grid_constant__ AcousticFields I,
                                                                     const __grid_constant__ AcousticFields O,
                                                                     const __grid_constant__ AcousticCoef C) {
-    __shared__ double ring[kAfD][32 * kAcTY][kAfS];
+    __shared__ double ring[kAfD][32 * kAfTY][kAfS];
 #ifdef AF_PAD   // (ablation: fewer CTAs per SM)
     __shared__ char pad[AF_PAD];
     if (threadIdx.x == 1023) pad[blockIdx.x & 7] = 0;
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
     const int nx = I.n[0], ny = I.n[1], nz = I.n[2];
     const int i = blockIdx.x * 32 + lane;
-    const int j = blockIdx.y * kAcTY + warp;
+    const int j = blockIdx.y * kAfTY + warp;
     const int z0 = blockIdx.z * kAfKC;
     const int z1 = min(z0 + kAfKC, nz);
     if (j >= ny) return;   // warp-uniform (no CTA barrier is used)
@@ -329,8 +333,8 @@ __global__ void __launch_bounds__(32 * kAcTY) acoustic_fused_kernel(const __grid
 }  // namespace
 
 void launch_acoustic_fused(const AcousticFields &in, const AcousticFields &out, const AcousticCoef &c, cudaStream_t s) {
-    const dim3 grid((in.n[0] + 31) / 32, (in.n[1] + kAcTY - 1) / kAcTY, (in.n[2] + kAfKC - 1) / kAfKC);
-    acoustic_fused_kernel<<<grid, 32 * kAcTY, 0, s>>>(in, out, c);
+    const dim3 grid((in.n[0] + 31) / 32, (in.n[1] + kAfTY - 1) / kAfTY, (in.n[2] + kAfKC - 1) / kAfKC);
+    acoustic_fused_kernel<<<grid, 32 * kAfTY, 0, s>>>(in, out, c);
     IGG_CUDA(cudaGetLastError());
 }
 

@@ -78,12 +78,24 @@ __device__ __forceinline__ unsigned ld_acq_gpu_u32(const unsigned *p) {
 }
 
 // one contribution to the data flag of (face a/rs, chunk c) of rank R; the last one publishes the epoch
-__device__ __forceinline__ void contribute(const FusedParams &F, const FusedRank &R, int a, int rs, int c) {
+__device__ __forceinline__ void contribute(const FusedParams &F, const FusedRank &R, int a, int rs, int c,
+                                           unsigned long long ep) {
     const int i = (a * 2 + rs) * kMaxChunks + c;
     if (atomicAdd(R.ctr + i, 1u) == F.tgt[i] - 1) {
         fence_acq_rel_sys();   // (acquire side of the other contributors' release, then the flag's release)
-        st_relaxed_sys(R.face[a][rs].flag + c, F.epoch);
+        st_relaxed_sys(R.face[a][rs].flag + c, ep);
         atomicExch(R.ctr + i, 0u);
+    }
+}
+// one x piece of (x face rs, chunk c) for epoch ep: counters by epoch parity (module comment at the
+// deferral, fused_step), the chunk's count completing publishes ep
+__device__ __forceinline__ void contribute_xp(const FusedParams &F, const FusedRank &R, int rs, int c,
+                                              unsigned long long ep) {
+    const int i = ((int)(ep & 1) * 2 + rs) * kMaxChunks + c;
+    if (atomicAdd(R.xpc + i, 1u) == F.tgt[rs * kMaxChunks + c] - 1) {
+        fence_acq_rel_sys();
+        st_relaxed_sys(R.face[0][rs].flag + c, ep);
+        atomicExch(R.xpc + i, 0u);
     }
 }
 // rim / forwarded cells of (face, chunk): their own counters and flags
@@ -364,7 +376,9 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         if (xrs >= 0) {
             const int xf = R.face[0][xrs].layer - tx * 64;
             const bool slane = rowv && (xf >> 1) == lane;
-            double *xloc = R.xloc + (long long)xrs * sy * F.s[2];   // (staging rows: [z][y])
+            // (local staging [parity][side][z][y]: the next launch's senders may still copy this epoch's
+            // deferred chunks while its own tiles stage theirs)
+            double *xloc = R.xloc + ((long long)(F.epoch & 1) * 2 + xrs) * sy * F.s[2];
             // the x halo column beside the send layer: the neighbour's previous-epoch values, staged in my
             // receive rows by its senders (first step of a run: T holds it)
             const int hside = xrs == 0 ? 1 : 0, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
@@ -427,7 +441,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
 #endif
 #endif
             for (int f = 2; f < 6; ++f)
-                if (did & (1u << f)) contribute(F, R, f >> 1, f & 1, f < 4 ? pos : 0);
+                if (did & (1u << f)) contribute(F, R, f >> 1, f & 1, f < 4 ? pos : 0, F.epoch);
         }
         if (did & 3u) {    // x face: the local staging rows, GPU-scope release, then the senders' count
             fence_acq_rel_gpu();
@@ -469,6 +483,38 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
 // halo of the chunk -- its data and its rim/forwarded cells -- forward the edge lines later faces take
 // from it, and count on those faces' xflags.  Only these few blocks wait on blocks of the same launch
 // (the sibling ranks' or the peers' tiles): DESIGN.md §6 "forward progress".
+// planes [za, zb) of the [z][y] x staging -- one contiguous block -- from my local staging to the
+// receiver's: a flat copy, 16-B vectors when aligned, U vectors in flight per thread.  The senders take
+// pieces of <= kFusedXPiece planes round-robin in chunk order, so a chunk's pieces move in parallel on
+// several SMs (one SM drains NVLink stores at only ~6 GB/s: a 64-plane chunk took 45 us in one block)
+// while each sender's pieces lie in different chunks.  (All senders copying a slice of every chunk
+// measured slower: each pays a system fence per chunk in sequence.)
+__device__ __forceinline__ void x_piece_copy(const double *loc, double *dst, int za, int zb, int sy) {
+    const long long a0 = (long long)za * sy, a1 = (long long)zb * sy;
+    constexpr int U = 4;
+    if (a0 < a1 && !(a0 & 1)) {
+        const double2 *s2 = reinterpret_cast<const double2 *>(loc + a0);
+        double2 *d2 = reinterpret_cast<double2 *>(dst + a0);
+        const long long n2 = (a1 - a0) >> 1;
+        for (long long t0 = threadIdx.x; t0 < n2; t0 += (long long)blockDim.x * U) {
+            double2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long t = t0 + (long long)u * blockDim.x;
+                if (t < n2) v[u] = __ldcg(s2 + t);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long t = t0 + (long long)u * blockDim.x;
+                if (t < n2) d2[t] = v[u];
+            }
+        }
+        if (((a1 - a0) & 1) && threadIdx.x == 0) dst[a1 - 1] = __ldcg(loc + a1 - 1);
+    } else {
+        for (long long t = a0 + threadIdx.x; t < a1; t += blockDim.x) dst[t] = __ldcg(loc + t);
+    }
+}
+
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b) {
     if (b < F.nrim) {
         const int per = F.nrim / 6;
@@ -520,56 +566,40 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
         const FusedFace &fx = R.face[0][rs];
         if (!fx.active) return;
         const int sy = F.s[1], sz = F.s[2];
-        const double *loc = R.xloc + (long long)rs * sy * sz;
-        // the receiver's staging of its halo side rs ([z][y]), this epoch's parity
-        double *dst = R.xrem_peer[rs] + ((long long)(F.epoch & 1) * 2 + rs) * sy * sz;
-        for (int pos = part; pos < F.nchunks; pos += F.nxs) {   // sender part owns chunks part + k nxs
-            if (threadIdx.x == 0) {   // every face tile of the chunk has staged its rows (GPU-scope acquire)
-                const long long t0 = clock64();
-                while (ld_acq_gpu_u32(R.xcnt + rs * kMaxChunks + pos) < F.xtarget) {
-                    if (clock64() - t0 > F.timeout_cycles) {
-                        atomicExch(F.err, 1);
-                        break;
-                    }
-                    __nanosleep(200);
-                }
-            }
-            __syncthreads();
-            TRACE_AT(1);
-            // the chunk's planes are one contiguous block of the [z][y] staging: a flat copy, 16-B vectors
-            // when aligned, U vectors in flight per thread.  One sender per chunk: a chunk's copy then
-            // overlaps the next chunks' tiles.  (All senders copying a slice of every chunk measured
-            // slower -- each sender pays one system fence per chunk in sequence -- and one SM's NVLink
-            // stores drain at only a few GB/s, so the copy is not made wider.)
-            const int2 zr = F.zr[pos];
-            const long long a0 = (long long)zr.x * sy, a1 = (long long)zr.y * sy;
-            constexpr int U = 4;
-            if (a0 < a1 && !(a0 & 1)) {
-                const double2 *s2 = reinterpret_cast<const double2 *>(loc + a0);
-                double2 *d2 = reinterpret_cast<double2 *>(dst + a0);
-                const long long n2 = (a1 - a0) >> 1;
-                for (long long t0 = threadIdx.x; t0 < n2; t0 += (long long)blockDim.x * U) {
-                    double2 v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const long long t = t0 + (long long)u * blockDim.x;
-                        if (t < n2) v[u] = __ldcg(s2 + t);
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const long long t = t0 + (long long)u * blockDim.x;
-                        if (t < n2) d2[t] = v[u];
+        // pass 0: the previous epoch's deferred chunks (its tiles staged them in the other parity; the
+        // previous launch is complete, so their count is in); pass 1: this epoch's chunks before defer_from
+        for (int pass = 0; pass < 2; ++pass) {
+            const unsigned long long ep = pass ? F.epoch : F.epoch - 1;
+            const int c0 = pass ? 0 : F.undefer_from, c1 = pass ? F.defer_from : F.nchunks;
+            const unsigned target = pass ? F.xtarget : F.xtarget_prev;
+            const double *loc = R.xloc + ((long long)(ep & 1) * 2 + rs) * sy * sz;
+            // the receiver's staging of its halo side rs ([z][y]), the epoch's parity
+            double *dst = R.xrem_peer[rs] + ((long long)(ep & 1) * 2 + rs) * sy * sz;
+            int u = 0;   // piece index, in chunk order
+            for (int pos = 0; pos < c1; ++pos) {
+              const int2 zr = F.zr[pos];
+              for (int za = zr.x; za < zr.y; za += kFusedXPiece, ++u) {
+                if (pos < c0 || u % F.nxs != part) continue;
+                if (threadIdx.x == 0) {   // every face tile of the chunk has staged its rows (GPU-scope acquire)
+                    const long long t0 = clock64();
+                    while (ld_acq_gpu_u32(R.xcnt + rs * kMaxChunks + pos) < target) {
+                        if (clock64() - t0 > F.timeout_cycles) {
+                            atomicExch(F.err, 1);
+                            break;
+                        }
+                        __nanosleep(200);
                     }
                 }
-                if (((a1 - a0) & 1) && threadIdx.x == 0) dst[a1 - 1] = __ldcg(loc + a1 - 1);
-            } else {
-                for (long long t = a0 + threadIdx.x; t < a1; t += blockDim.x) dst[t] = __ldcg(loc + t);
-            }
-            __syncthreads();
-            TRACE_AT(2);
-            if (threadIdx.x == 0) {
-                fence_acq_rel_sys();
-                contribute(F, R, 0, rs, pos);
+                __syncthreads();
+                TRACE_AT(1);
+                x_piece_copy(loc, dst, za, min(za + kFusedXPiece, zr.y), sy);
+                __syncthreads();
+                TRACE_AT(2);
+                if (threadIdx.x == 0) {
+                    fence_acq_rel_sys();
+                    contribute_xp(F, R, rs, pos, ep);   // (the chunk's last piece publishes it)
+                }
+              }
             }
         }
         return;
@@ -702,7 +732,8 @@ static void build_layout(igg_grid *g, const bool act[3][2], bool zex) {
     std::vector<unsigned> tgt_d(6 * kMaxChunks, 0u), tgt_x(6 * kMaxChunks, 0u);
     for (int rs = 0; rs < 2; ++rs) {
         for (int c = 0; c < nch; ++c) {
-            tgt_d[(0 * 2 + rs) * kMaxChunks + c] = 1;   // (the chunk's x sender publishes its x face)
+            // (the x senders' pieces of the chunk publish its x face)
+            tgt_d[(0 * 2 + rs) * kMaxChunks + c] = (zc[c].y - zc[c].x + kFusedXPiece - 1) / kFusedXPiece;
             tgt_x[(0 * 2 + rs) * kMaxChunks + c] = 1;
             tgt_d[(1 * 2 + rs) * kMaxChunks + c] = xtiles;
             tgt_x[(1 * 2 + rs) * kMaxChunks + c] = 1 + (xh ? nf : 0);
@@ -863,7 +894,8 @@ namespace igg {
 void fused_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, const HeatCoef &k,
                 cudaStream_t s, bool wait_prev, bool drain) {
     const int L = g->nlocal;
-    const size_t ctr_words = 12 * kMaxChunks + 8;   // [data ctr | rim/forward ctr] x 6 x kMaxChunks, ticket
+    // [data ctr | rim/forward ctr] x 6 x kMaxChunks, ticket (8), x-piece ctr [parity][2] x kMaxChunks
+    const size_t ctr_words = 16 * kMaxChunks + 8;
     if (!g->fused_ctr) {
         IGG_CUDA(cudaMalloc(&g->fused_ctr, L * ctr_words * sizeof(unsigned int)));
         IGG_CUDA(cudaMemset(g->fused_ctr, 0, L * ctr_words * sizeof(unsigned int)));
@@ -873,7 +905,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     const bool xex = comm && (g->dims[0] > 1 || g->periods[0]);   // x faces exist: local staging rows
     const size_t stg_words = 2 * (size_t)g->n[1] * g->n[2];       // [side][y][z] per rank
     if (xex && !g->fused_xloc) {
-        IGG_CUDA(cudaMalloc(&g->fused_xloc, sizeof(double) * stg_words * L));
+        IGG_CUDA(cudaMalloc(&g->fused_xloc, sizeof(double) * 2 * stg_words * L));   // [parity][side][z][y]
         IGG_CUDA(cudaMalloc(&g->fused_xrem, sizeof(double) * 2 * stg_words * L));   // [parity][side][y][z]
         IGG_CUDA(cudaMalloc(&g->fused_xcnt, sizeof(unsigned) * 2 * kMaxChunks * L));
         IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));
@@ -900,7 +932,8 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
         R.ctr = g->fused_ctr + lr * ctr_words;
         R.ctr_x = R.ctr + 6 * kMaxChunks;
         R.rim_ticket = R.ctr + 12 * kMaxChunks;
-        R.xloc = xex ? g->fused_xloc + lr * stg_words : nullptr;
+        R.xpc = R.ctr + 12 * kMaxChunks + 8;
+        R.xloc = xex ? g->fused_xloc + lr * 2 * stg_words : nullptr;
         R.xrem = xex ? g->fused_xrem + lr * 2 * stg_words : nullptr;
         R.xcnt = xex ? g->fused_xcnt + lr * 2 * kMaxChunks : nullptr;
         for (int a = 0; a < 3; ++a)
@@ -939,6 +972,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     for (int a = 0; a < 3; ++a)
         for (int rs = 0; rs < 2; ++rs) key |= (act[a][rs] ? 1 : 0) << (a * 2 + rs);
     if (g->fused_key != key) {
+        if (g->fused_deferred >= 0) fail(IGG_E_STATE, "fused step: topology changed inside a run");
         build_layout(g, act, zex);
         g->fused_key = key;
         if (g->fused_xcnt) {   // the x senders' cumulative counters restart with the layout
@@ -949,7 +983,8 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     const bool xface = act[0][0] || act[0][1];
     if (xface) ++g->fused_xsteps;   // launches whose x-face tiles count on the cumulative counters
     F.xtarget = (unsigned)((unsigned long long)g->fused_geo[5] * g->fused_xsteps);
-    F.nxs = xface ? std::min(kFusedXSenders, g->fused_nchunks) : 0;
+    F.xtarget_prev = (unsigned)((unsigned long long)g->fused_geo[5] * (g->fused_xsteps - 1));
+    F.nxs = xface ? kFusedXSenders : 0;
     F.nchunks = g->fused_nchunks;
     for (int c = 0; c < F.nchunks; ++c) F.zr[c] = g->fused_zr[c];
     F.xtiles = g->fused_geo[4];
@@ -970,6 +1005,15 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.nrim = (comm && drain) ? 48 : 0;
     F.nfwd = (comm && drain) ? g->fused_nfwd : 0;
     F.nstencil = g->fused_ntiles;
+    // the x chunks visited last would trail the launch by one copy + one system fence (~8 us measured):
+    // a step that does not complete its run leaves them to the next launch's senders, which send them
+    // first -- the receiver reads them only at the end of its next step.  A draining step
+    // publishes such a chunk for two epochs: separate counters by parity; a piece of a chunk has the
+    // same sender in both passes, and every sender finishes pass 0 first, so the chunk's flag reaches
+    // epoch-1 before epoch (never backwards).
+    F.undefer_from = g->fused_deferred >= 0 ? g->fused_deferred : F.nchunks;
+    F.defer_from = (xface && !drain && F.nchunks > kFusedDefer) ? F.nchunks - kFusedDefer : F.nchunks;
+    g->fused_deferred = F.defer_from < F.nchunks ? F.defer_from : -1;
     F.per_rank = F.nrim + F.nfwd + 2 * F.nxs + F.nstencil;   // (rim, forwarders, x senders, tiles)
     const long long blocks = (long long)F.per_rank * L;
     prof_begin(g, s);

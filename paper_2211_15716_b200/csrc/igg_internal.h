@@ -125,7 +125,9 @@ struct HeatRegionList {
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
 constexpr int kMaxFusedRanks = 8;    // ranks hosted on one GPU that one fused launch covers
-constexpr int kFusedXSenders = 16;   // x sender blocks per x face and rank (at most one per chunk)
+constexpr int kFusedDefer = 3;       // x chunks a pipelined step leaves to the next launch's senders
+constexpr int kFusedXSenders = 16;   // x sender blocks per x face and rank
+constexpr int kFusedXPiece = 8;      // planes per x sender work piece
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // the receiver's T2 (a sibling's, or peer-mapped); lands in its halo layer
     unsigned long long *flag;        // receiver's data flags of (axis, side): [kMaxChunks] (z faces: [0])
@@ -158,6 +160,8 @@ struct FusedRank {                   // one hosted rank of a fused launch
     unsigned int *ctr;               // [6][kMaxChunks] data-flag contribution counters (sender side)
     unsigned int *ctr_x;             // [6][kMaxChunks] rim/forwarded-cell counters
     unsigned int *rim_ticket;
+    unsigned int *xpc;               // [parity][2][kMaxChunks] x-piece counters, by epoch parity: a launch
+                                     // may publish a chunk for two epochs (deferred and its own)
 };
 struct FusedParams {
     int s[3];
@@ -171,6 +175,11 @@ struct FusedParams {
     int border_first;                // within a chunk: the border tiles (faces) first
     int nxs;                         // x sender (and x unpacker) blocks per x face / halo side (0: none)
     unsigned xtarget;                // x-face tile count of a chunk after this launch (cumulative)
+    unsigned xtarget_prev;           // ... after the previous launch
+    int defer_from;                  // x chunks [defer_from, nchunks) of this epoch are sent by the NEXT
+                                     // launch's senders (nchunks: none deferred)
+    int undefer_from;                // x chunks [undefer_from, nchunks) of the previous epoch, deferred by
+                                     // the previous launch, are sent first by this launch's senders
     const unsigned int *tgt;         // [6][kMaxChunks] contributions completing a (face, chunk) data flag
     const unsigned int *tgt_x;       // ... an xflag (rim + forwarders)
     unsigned long long epoch;
@@ -355,6 +364,7 @@ struct igg_grid : igg::Geom {
     unsigned int *fused_xcnt = nullptr;                  // x-face tile counters (cumulative)
     double *fused_xrem = nullptr;                        // x-face receive staging (IPC-mapped by the senders)
     unsigned long long fused_xsteps = 0;                 // launches with x faces since the counters' reset
+    int fused_deferred = -1;                             // the last fused launch deferred x chunks from here (-1: none)
     int sm_count = 148;
     double clock_khz = 1.9e6;
 };
@@ -386,7 +396,8 @@ void validate_peer_maps(igg_grid *g);
 // synchronizes the grid's device work and fails with IGG_E_TIMEOUT if a flag wait timed out
 void check_device_error(igg_grid *g, const char *who);
 // one fused step; pipelined schedule: wait_prev = the previous step of the same run was fused (its
-// halos are awaited tile by tile), drain = wait for every incoming face at the end (step complete)
+// halos are awaited tile by tile), drain = wait for every incoming face at the end (step complete; a
+// step that does not drain leaves its last x chunks to the next launch's senders)
 void fused_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, const HeatCoef &k,
                 cudaStream_t s, bool wait_prev = false, bool drain = true);
 void prof_begin(igg_grid *g, cudaStream_t s);
