@@ -9,6 +9,9 @@ timeout 600 $TR bench.py --gpus 4 > gpurun_out/${T}_n4.json 2> gpurun_out/${T}_n
 for d in 1,2,2 2,1,2 4,1,1; do
   timeout 600 $TR bench.py --gpus 4 --dims $d --no-e2e > gpurun_out/${T}_n4_${d//,/}.json 2> gpurun_out/${T}_n4_${d//,/}.err
 done
+timeout 600 $TR2 bench.py --gpus 2 --dtype f32 --dims 2,1,1 --no-e2e > gpurun_out/${T}_f32_n2_211.json 2> gpurun_out/${T}_f32_n2_211.err
+timeout 600 $TR bench.py --gpus 4 --dtype f32 --no-e2e > gpurun_out/${T}_f32_n4.json 2> gpurun_out/${T}_f32_n4.err
+timeout 600 $TR bench.py --gpus 4 --workload acoustic --no-e2e > gpurun_out/${T}_ac_n4.json 2> gpurun_out/${T}_ac_n4.err
 HALO_SIZES=${HALO_SIZES:-64,128,256,512,768} timeout 900 $TR scripts/halo_sweep.py > gpurun_out/${T}_halo.txt 2>&1
 timeout 900 $TR scripts/b10_staggered.py > gpurun_out/${T}_b10.txt 2>&1
 echo done
