@@ -186,7 +186,7 @@ __device__ __forceinline__ double pupd(double p, double cP, double r0, double r1
 #define AF_D 2
 #endif
 #ifndef AF_TY
-#define AF_TY 4
+#define AF_TY 2
 #endif
 constexpr int kAfTY = AF_TY;   // rows per CTA (one warp each)
 constexpr int kAfKC = AF_KC;   // P planes per CTA

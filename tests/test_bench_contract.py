@@ -26,13 +26,18 @@ def test_reference_arm_json_line():
 
 def test_committed_traffic_summaries_match_the_algorithmic_bytes():
     """The ncu traffic files bench.py reads carry the algorithmic bytes of DESIGN.md's per-cell figures
-    (heat 24 B, binary32 heat 12 B per updated cell of the 510^3 interior; compute_V 56 B per cell of its
-    511^3 box) and a DRAM traffic within a few percent of them (no wasted re-reads)."""
-    want = {"traffic.json": 24 * 510 ** 3, "traffic_f32.json": 12 * 510 ** 3,
-            "traffic_acoustic.json": 56 * 511 ** 3}
-    for name, alg in want.items():
+    (heat 24 B, binary32 heat 12 B per updated cell of the 510^3 interior; the fused acoustic sweep 64 B
+    per cell of 512^3) and a DRAM traffic within a few percent of them (no wasted re-reads).  The fused
+    heat kernel (per rank of a two-rank launch, x data plane included) may exceed it by its short
+    z chunks' plane re-reads and the staging traffic: < 5 %."""
+    want = {"traffic.json": (24 * 510 ** 3, 1.03, [1, 1, 1]), "traffic_f32.json": (12 * 510 ** 3, 1.03, [1, 1, 1]),
+            "traffic_acoustic.json": (64 * 512 ** 3, 1.03, [1, 1, 1]),
+            "traffic_fused.json": (24 * 510 ** 3, 1.05, [2, 1, 1])}
+    for name, (alg, tol, dims) in want.items():
         d = json.load(open(os.path.join(ROOT, "profiles", name)))
-        assert d["n"] == 512 and d["dims"] == [1, 1, 1], name
+        assert d["n"] == 512 and d["dims"] == dims, name
         assert d["algorithmic_bytes_per_launch"] == alg, name
         assert abs(d["dram_read_bytes"] + d["dram_write_bytes"] - d["dram_bytes_per_launch"]) < 1e3, name
-        assert 1.0 <= d["dram_bytes_per_launch"] / alg < 1.03, name
+        assert 1.0 <= d["dram_bytes_per_launch"] / alg < tol, name
+
+
