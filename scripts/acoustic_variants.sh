@@ -1,3 +1,6 @@
+# acoustic_fused_kernel A/B (1 GPU): VARIANTS="cur ty2 ..." runs bench.py --workload acoustic twice per
+# variant, cur = the product library, <v> = ablation/libigg_ac_<v>.so (built with
+# python paper_2211_15716_b200/build.py --out ablation/libigg_ac_<v>.so -DIGG_ABLATION -DAF_TY=.. -DAF_KC=.. -DAF_D=..)
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out; T=${TAG:-exp}
 for v in ${VARIANTS:-cur}; do
   L=ablation/libigg_ac_$v.so; [ $v = cur ] && L=paper_2211_15716_b200/libigg.so
