@@ -79,6 +79,9 @@ SIGNATURES = {
                           ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, c_int_p, ctypes.c_void_p],
     "igg_heat_run": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, c_dbl_pp, ctypes.c_double, ctypes.c_double,
                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_int_p, ctypes.c_void_p],
+    "igg_heat_run_f32": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_float,
+                         ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_int, c_int_p,
+                         ctypes.c_void_p],
     "igg_heat_run_host": [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
                           ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, c_int_p,
                           ctypes.c_void_p],

@@ -53,18 +53,58 @@ __device__ __forceinline__ void cp_async16f(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ double2 ldg2f(const double *p) { return __ldg(reinterpret_cast<const double2 *>(p)); }
-
-// the cell of PAPER.md:46-49, same explicitly rounded operations as kernels.cu
-__device__ __forceinline__ double cell(double c, double xm, double xp, double ym, double yp, double zm, double zp,
-                                       double ci, const HeatCoef &k) {
-    const double d2x = __dsub_rn(__dsub_rn(xp, c), __dsub_rn(c, xm));
-    const double d2y = __dsub_rn(__dsub_rn(yp, c), __dsub_rn(c, ym));
-    const double d2z = __dsub_rn(__dsub_rn(zp, c), __dsub_rn(c, zm));
-    const double lap =
-        __dadd_rn(__dadd_rn(__dmul_rn(d2x, k.rdx2), __dmul_rn(d2y, k.rdy2)), __dmul_rn(d2z, k.rdz2));
-    return __dadd_rn(c, __dmul_rn(k.dt, __dmul_rn(__dmul_rn(k.lam, ci), lap)));
+__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
+
+// element type E of the sweep: binary64 (the paper's Float64) or binary32; a lane holds
+// a pair of x-adjacent cells (vec2<E>: 16 or 8 bytes) in both
+template <typename E> struct V2;
+template <> struct V2<double> { using t = double2; };
+template <> struct V2<float> { using t = float2; };
+template <typename E> using vec2 = typename V2<E>::t;
+template <typename E>
+__device__ __forceinline__ vec2<E> ldg2(const E *p) { return __ldg(reinterpret_cast<const vec2<E> *>(p)); }
+template <typename E>
+__device__ __forceinline__ vec2<E> mk2(E a, E b) {
+    vec2<E> r;
+    r.x = a;
+    r.y = b;
+    return r;
+}
+template <typename E>
+__device__ __forceinline__ void cp_pair(void *smem, const void *gmem) {   // one pair, L1-bypassing if 16 B
+    if constexpr (sizeof(E) == 8) cp_async16f(smem, gmem); else cp_async8f(smem, gmem);
+}
+template <typename E>
+__device__ __forceinline__ void cp_elem(void *smem, const void *gmem) {   // one element
+    if constexpr (sizeof(E) == 8) {
+        cp_async8f(smem, gmem);
+    } else {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+    }
+}
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+
+// the cell of PAPER.md:46-49, same explicitly rounded operations (and association) as kernels.cu's
+// binary64 and binary32 kernels
+template <typename E, typename K>
+__device__ __forceinline__ E cell(E c, E xm, E xp, E ym, E yp, E zm, E zp, E ci, const K &k) {
+    const E d2x = rsub(rsub(xp, c), rsub(c, xm));
+    const E d2y = rsub(rsub(yp, c), rsub(c, ym));
+    const E d2z = rsub(rsub(zp, c), rsub(c, zm));
+    const E lap = radd(radd(rmul(d2x, k.rdx2), rmul(d2y, k.rdy2)), rmul(d2z, k.rdz2));
+    return radd(c, rmul(k.dt, rmul(rmul(k.lam, ci), lap)));
+}
+__device__ __forceinline__ const HeatCoef &coef_of(const FusedParams &F, double) { return F.k; }
+__device__ __forceinline__ const HeatCoefF &coef_of(const FusedParams &F, float) { return F.kf; }
 
 // release / acquire fence at system scope: the PTX release and acquire patterns (fence.acq_rel + relaxed
 // write / relaxed read + fence.acq_rel) are all the flag protocol needs; __threadfence_system is the
@@ -165,13 +205,10 @@ constexpr int kFKC = 64;   // longest z-chunk
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
-__device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r0, double r1) {
+template <typename E>
+__device__ __forceinline__ void store_pair(E *d, bool w0, bool w1, E r0, E r1) {
     if (w0 && w1) {
-        *reinterpret_cast<double2 *>(d) = make_double2(r0, r1);
+        *reinterpret_cast<vec2<E> *>(d) = mk2<E>(r0, r1);
     } else {
         if (w0) d[0] = r0;
         if (w1) d[1] = r1;
@@ -180,27 +217,27 @@ __device__ __forceinline__ void store_pair(double *d, bool w0, bool w1, double r
 
 // UP (XS only): the tile holds the upper x send layer s-2 -- element .x of its lane's pair -- else the
 // lower one, layer 1 -- element .y of lane 0 (s even: pairs never straddle)
-template <bool YF, bool XS, bool UP>
-__device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, double2 (*sT)[32 * kFTY],
-                                            double2 (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
-                                            long long i, bool pair_in, bool w0, bool w1, double *ydst,
-                                            double *sx_row, bool slane, bool hpatch, double h0,
-                                            const double *hx_row) {
-    const double *__restrict__ T = R.T;
-    const double *__restrict__ Ci = R.Ci;
-    double *__restrict__ T2 = R.T2;
+template <typename E, bool YF, bool XS, bool UP>
+__device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, vec2<E> (*sT)[32 * kFTY],
+                                            vec2<E> (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
+                                            long long i, bool pair_in, bool w0, bool w1, E *ydst,
+                                            E *sx_row, bool slane, bool hpatch, E h0,
+                                            const E *hx_row) {
+    const E *__restrict__ T = reinterpret_cast<const E *>(R.T);
+    const E *__restrict__ Ci = reinterpret_cast<const E *>(R.Ci);
+    E *__restrict__ T2 = reinterpret_cast<E *>(R.T2);
     const int tid = threadIdx.x, lane = tid & 31;
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
         if (pair_in && zs + q < ze) {
-            cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
-            cp_async16f(&sC[q][tid], Ci + i + q * sxy);
+            cp_pair<E>(&sT[q][tid], T + i + (q + 1) * sxy);
+            cp_pair<E>(&sC[q][tid], Ci + i + q * sxy);
         }
         cp_commit();
     }
-    const double2 zero2 = make_double2(0.0, 0.0);
-    double2 zm = pair_in ? ldg2f(T + i - sxy) : zero2;
-    double2 c = pair_in ? ldg2f(T + i) : zero2;
+    const vec2<E> zero2 = mk2<E>(E(0), E(0));
+    vec2<E> zm = pair_in ? ldg2(T + i - sxy) : zero2;
+    vec2<E> c = pair_in ? ldg2(T + i) : zero2;
     if (XS && hpatch) {   // (one lane) substitutes the staged x halo values for T's, plane zs first
         if (UP) c.y = h0; else c.x = h0;
     }
@@ -210,21 +247,21 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
         if (XS) __syncwarp();   // (the halo row in hx_row, fetched by the whole warp in group 0)
-        double2 ym = zero2, yp = zero2;
+        vec2<E> ym = zero2, yp = zero2;
         if (pair_in) {
-            ym = ldg2f(T + i - sx);
-            yp = ldg2f(T + i + sx);
+            ym = ldg2(T + i - sx);
+            yp = ldg2(T + i + sx);
         }
-        const double2 zp = sT[slot][tid];
-        const double2 ci = sC[slot][tid];
-        double xm = __shfl_up_sync(0xffffffffu, c.y, 1);
-        double xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+        const vec2<E> zp = sT[slot][tid];
+        const vec2<E> ci = sC[slot][tid];
+        E xm = __shfl_up_sync(0xffffffffu, c.y, 1);
+        E xp = __shfl_down_sync(0xffffffffu, c.x, 1);
         if (lo_edge) xm = __ldg(T + i - 1);
         if (hi_edge) xp = __ldg(T + i + 2);
-        const double r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, F.k);
-        const double r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, F.k);
+        const E r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, coef_of(F, E()));
+        const E r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, coef_of(F, E()));
         if (FUSED_STCS && w0 && w1)   // T2 is not re-read in this step (evict-first keeps L2 for T)
-            __stcs(reinterpret_cast<double2 *>(T2 + i), make_double2(r0, r1));
+            __stcs(reinterpret_cast<vec2<E> *>(T2 + i), mk2<E>(r0, r1));
         else
             store_pair(T2 + i, w0, w1, r0, r1);
         if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
@@ -232,12 +269,12 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         zm = c;
         c = zp;
         if (XS && hpatch && z + 1 < ze) {   // plane z+1's x halo cell: the neighbour's staged value
-            const double h = hx_row[z + 1 - zs];
+            const E h = hx_row[z + 1 - zs];
             if (UP) c.y = h; else c.x = h;
         }
         if (pair_in && z + kFD < ze) {
-            cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
-            cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
+            cp_pair<E>(&sT[slot][tid], T + i + (kFD + 1) * sxy);
+            cp_pair<E>(&sC[slot][tid], Ci + i + kFD * sxy);
         }
         cp_commit();
         slot = slot + 1 == kFD ? 0 : slot + 1;
@@ -245,6 +282,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
     cp_wait<0>();
 }
 
+template <typename E>
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b);
 
 #ifndef FUSED_TRACE
@@ -267,20 +305,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // One launch over all tiles of all hosted ranks, the 1-GPU loop unchanged.  Block b of rank r:
 // [0, nrim) rim, [nrim, nrim+nfwd) forwarders (last step of a run only), then the stencil tiles.
 // MR: more than one hosted rank (the rank's parameters are indexed at run time).
-template <bool MR>
+template <bool MR, typename E>
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     TRACE_AT(0);
-    __shared__ double2 sT[kFD][32 * kFTY];
-    __shared__ double2 sC[kFD][32 * kFTY];
-    __shared__ double sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
-    __shared__ double sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
+    __shared__ vec2<E> sT[kFD][32 * kFTY];
+    __shared__ vec2<E> sC[kFD][32 * kFTY];
+    __shared__ E sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
+    __shared__ E sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
     const int rank = blockIdx.x / F.per_rank;
     int b = blockIdx.x - rank * F.per_rank;
     const FusedRank &R = F.r[rank];
     if (b < F.nrim + F.nfwd + 2 * F.nxs) {   // CTA-uniform
-        fused_extra(F, R, b);
+        fused_extra<E>(F, R, b);
         TRACE_AT(3);
         return;
     }
@@ -366,32 +404,33 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     // ---- the z sweep, with the x and y faces stored from inside it
     const long long i0 = (long long)zs * sxy + (long long)y * sx + p;
     {
-        double *ydst = nullptr;
+        E *ydst = nullptr;
         if (did & 12u) {
             const int rs = (did & 4u) ? 0 : 1;
             if (rowv && y == R.face[1][rs].layer)   // (warp-uniform) my row is the y send layer: cell i of
                                                     // my row lands at ydst + i in the receiver's halo row
-                ydst = R.face[1][rs].dst + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx;
+                ydst = reinterpret_cast<E *>(R.face[1][rs].dst) + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx;
         }
         if (xrs >= 0) {
             const int xf = R.face[0][xrs].layer - tx * 64;
             const bool slane = rowv && (xf >> 1) == lane;
             // (local staging [parity][side][z][y]: the next launch's senders may still copy this epoch's
             // deferred chunks while its own tiles stage theirs)
-            double *xloc = R.xloc + ((long long)(F.epoch & 1) * 2 + xrs) * sy * F.s[2];
+            E *xloc = reinterpret_cast<E *>(R.xloc) + ((long long)(F.epoch & 1) * 2 + xrs) * sy * F.s[2];
             // the x halo column beside the send layer: the neighbour's previous-epoch values, staged in my
             // receive rows by its senders (first step of a run: T holds it)
             const int hside = xrs == 0 ? 1 : 0, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
-            const double *hrow = (F.wait_prev && R.halo[0][hside].active && rowv)
-                                     ? R.xrem + ((long long)((F.epoch - 1) & 1) * 2 + hside) * sy * F.s[2] + y
-                                     : nullptr;   // (cell z of the row at hrow[z sy])
+            const E *hrow = (F.wait_prev && R.halo[0][hside].active && rowv)
+                                ? reinterpret_cast<const E *>(R.xrem) +
+                                      ((long long)((F.epoch - 1) & 1) * 2 + hside) * sy * F.s[2] + y
+                                : nullptr;   // (cell z of the row at hrow[z sy])
             const bool hpatch = hrow && (xh >> 1) == lane;
-            double h0 = 0.0;
+            E h0 = E(0);
             if (hrow) {   // (warp-uniform) this chunk's staged halo values of the row, into the first group
-                for (int z = zs + lane; z < ze; z += 32) cp_async8f(&sHx[warp][z - zs], hrow + (long long)z * sy);
+                for (int z = zs + lane; z < ze; z += 32) cp_elem<E>(&sHx[warp][z - zs], hrow + (long long)z * sy);
                 if (hpatch) h0 = __ldcg(hrow + (long long)zs * sy);
             }
-#define XSWEEP(YFv, UPv, YD) fused_sweep<YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, YD, \
+#define XSWEEP(YFv, UPv, YD) fused_sweep<E, YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, YD, \
                                                           sX[warp], slane, hpatch, h0, sHx[warp])
             if (xrs == 0) {   // upper: send layer s-2
                 if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
@@ -407,11 +446,11 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                 if (r < nr) xloc[(long long)z * sy + ty0 + r] = sX[r][z - zs];
             }
         } else if (did & 12u) {
-            fused_sweep<true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, ydst, nullptr,
-                                            false, false, 0.0, nullptr);
+            fused_sweep<E, true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, ydst, nullptr,
+                                               false, false, E(0), nullptr);
         } else {
-            fused_sweep<false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr, nullptr,
-                                             false, false, 0.0, nullptr);
+            fused_sweep<E, false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr,
+                                                nullptr, false, false, E(0), nullptr);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver
@@ -419,8 +458,9 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
         const FusedFace &fz = R.face[2][rs];
         if (rowv && p < sx) {
             const long long o = (long long)fz.layer * sxy + (long long)y * sx + p;
-            const double2 v = *reinterpret_cast<const double2 *>(R.T2 + o);
-            store_pair(fz.dst + o + (long long)((rs == 0 ? 0 : F.s[2] - 1) - fz.layer) * sxy, w0, w1, v.x, v.y);
+            const vec2<E> v = *reinterpret_cast<const vec2<E> *>(reinterpret_cast<const E *>(R.T2) + o);
+            store_pair(reinterpret_cast<E *>(fz.dst) + o + (long long)((rs == 0 ? 0 : F.s[2] - 1) - fz.layer) * sxy,
+                       w0, w1, v.x, v.y);
         }
     }
     TRACE_AT(1);
@@ -452,6 +492,7 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
 }
 
 // forward my fresh halo line (axis b, side) x (face a, rs) over the third axis range [lo, hi)
+template <typename E>
 __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRank &R, int b, int side, int a, int rs,
                                              int lo, int hi, int part, int nparts) {
     const FusedFace &fc = R.face[a][rs];
@@ -464,13 +505,14 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
         c[a] = fc.layer;
         c[third] = t;
         if (forward_phase(F, R, a, c) != b || later_halo(F, R, a, c)) continue;
-        double v;
+        E v;
         if (b == 0 && c[1] >= 1 && c[1] < F.s[1] - 1 && c[2] >= 1 && c[2] < F.s[2] - 1)   // staged, not in T2
-            v = __ldcg(R.xrem + ((long long)(F.epoch & 1) * 2 + side) * F.s[1] * F.s[2] + (long long)c[2] * F.s[1] + c[1]);
+            v = __ldcg(reinterpret_cast<const E *>(R.xrem) + ((long long)(F.epoch & 1) * 2 + side) * F.s[1] * F.s[2] +
+                       (long long)c[2] * F.s[1] + c[1]);
         else
-            v = __ldcg(R.T2 + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
+            v = __ldcg(reinterpret_cast<const E *>(R.T2) + ((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]);
         c[a] = rs == 0 ? 0 : F.s[a] - 1;
-        fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v;
+        reinterpret_cast<E *>(fc.dst)[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = v;
         any = true;
     }
     return any;
@@ -489,15 +531,22 @@ __device__ __forceinline__ bool forward_line(const FusedParams &F, const FusedRa
 // several SMs (one SM drains NVLink stores at only ~6 GB/s: a 64-plane chunk took 45 us in one block)
 // while each sender's pieces lie in different chunks.  (All senders copying a slice of every chunk
 // measured slower: each pays a system fence per chunk in sequence.)
-__device__ __forceinline__ void x_piece_copy(const double *loc, double *dst, int za, int zb, int sy) {
-    const long long a0 = (long long)za * sy, a1 = (long long)zb * sy;
+template <typename E>
+__device__ __forceinline__ void x_piece_copy(const E *loc, E *dst, int za, int zb, int sy) {
+    constexpr int W = 16 / sizeof(E);   // elements per 16-B word
+    long long a0 = (long long)za * sy;
+    const long long a1 = (long long)zb * sy;
     constexpr int U = 4;
-    if (a0 < a1 && !(a0 & 1)) {
-        const double2 *s2 = reinterpret_cast<const double2 *>(loc + a0);
-        double2 *d2 = reinterpret_cast<double2 *>(dst + a0);
-        const long long n2 = (a1 - a0) >> 1;
+    // (head up to a 16-B boundary; the local and the receiver's staging blocks have the same offsets from
+    // 16-B aligned allocations, so both are aligned from there on)
+    for (; a0 < a1 && (reinterpret_cast<uintptr_t>(loc + a0) % 16); ++a0)
+        if (threadIdx.x == 0) dst[a0] = __ldcg(loc + a0);
+    if (a0 < a1) {
+        const uint4 *s2 = reinterpret_cast<const uint4 *>(loc + a0);
+        uint4 *d2 = reinterpret_cast<uint4 *>(dst + a0);
+        const long long n2 = (a1 - a0) / W;
         for (long long t0 = threadIdx.x; t0 < n2; t0 += (long long)blockDim.x * U) {
-            double2 v[U];
+            uint4 v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const long long t = t0 + (long long)u * blockDim.x;
@@ -509,12 +558,11 @@ __device__ __forceinline__ void x_piece_copy(const double *loc, double *dst, int
                 if (t < n2) d2[t] = v[u];
             }
         }
-        if (((a1 - a0) & 1) && threadIdx.x == 0) dst[a1 - 1] = __ldcg(loc + a1 - 1);
-    } else {
-        for (long long t = a0 + threadIdx.x; t < a1; t += blockDim.x) dst[t] = __ldcg(loc + t);
+        for (long long t = a0 + n2 * W + threadIdx.x; t < a1; t += blockDim.x) dst[t] = __ldcg(loc + t);   // tail
     }
 }
 
+template <typename E>
 __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &R, int b) {
     if (b < F.nrim) {
         const int per = F.nrim / 6;
@@ -540,9 +588,9 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
                 c[b1] = u;
                 c[b2] = v;
                 if (forward_phase(F, R, a, c) >= 0 || later_halo(F, R, a, c)) continue;
-                const double val = R.T2[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]];
+                const E val = reinterpret_cast<const E *>(R.T2)[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]];
                 c[a] = rs == 0 ? 0 : F.s[a] - 1;
-                fc.dst[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = val;
+                reinterpret_cast<E *>(fc.dst)[((long long)c[2] * F.s[1] + c[1]) * F.s[0] + c[0]] = val;
             }
             fence_acq_rel_sys();
         }
@@ -572,9 +620,9 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
             const unsigned long long ep = pass ? F.epoch : F.epoch - 1;
             const int c0 = pass ? 0 : F.undefer_from, c1 = pass ? F.defer_from : F.nchunks;
             const unsigned target = pass ? F.xtarget : F.xtarget_prev;
-            const double *loc = R.xloc + ((long long)(ep & 1) * 2 + rs) * sy * sz;
+            const E *loc = reinterpret_cast<const E *>(R.xloc) + ((long long)(ep & 1) * 2 + rs) * sy * sz;
             // the receiver's staging of its halo side rs ([z][y]), the epoch's parity
-            double *dst = R.xrem_peer[rs] + ((long long)(ep & 1) * 2 + rs) * sy * sz;
+            E *dst = reinterpret_cast<E *>(R.xrem_peer[rs]) + ((long long)(ep & 1) * 2 + rs) * sy * sz;
             int u = 0;   // piece index, in chunk order
             for (int pos = 0; pos < c1; ++pos) {
               const int2 zr = F.zr[pos];
@@ -620,9 +668,9 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
             bool fwd = false;
             for (int side = 0; side < 2; ++side)
                 for (int rs = 0; rs < 2; ++rs) {
-                    if (hb == 0) fwd |= forward_line(F, R, 0, side, 1, rs, zr.x, zr.y, q, F.nfwd);
+                    if (hb == 0) fwd |= forward_line<E>(F, R, 0, side, 1, rs, zr.x, zr.y, q, F.nfwd);
                     if (R.face[2][rs].layer >= zr.x && R.face[2][rs].layer < zr.y)
-                        fwd |= forward_line(F, R, hb, side, 2, rs, 0, F.s[hb == 0 ? 1 : 0], q, F.nfwd);
+                        fwd |= forward_line<E>(F, R, hb, side, 2, rs, 0, F.s[hb == 0 ? 1 : 0], q, F.nfwd);
                 }
             if (__syncthreads_or(fwd)) fence_acq_rel_sys();
             __syncthreads();
@@ -643,6 +691,7 @@ __device__ __noinline__ void fused_extra(const FusedParams &F, const FusedRank &
 // arrived -- the step is complete for any later work on the stream -- and the last epoch's staged x halo
 // columns (inner rows and planes) are copied into T2.  blockIdx.y = hosted rank.  (Waits only for flags
 // of the launch before it on the stream.)
+template <typename E>
 __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
     const FusedRank &R = F.r[blockIdx.y];
     for (int f = threadIdx.x; f < 6 * F.nchunks; f += blockDim.x) {
@@ -658,11 +707,11 @@ __global__ void fused_drain_kernel(const __grid_constant__ FusedParams F) {
     for (int side = 0; side < 2; ++side) {
         if (!R.halo[0][side].active) continue;
         const int hx = side == 0 ? 0 : sx - 1;
-        const double *stg = R.xrem + ((long long)(F.epoch & 1) * 2 + side) * sy * sz;
+        const E *stg = reinterpret_cast<const E *>(R.xrem) + ((long long)(F.epoch & 1) * 2 + side) * sy * sz;
         for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < ncell;
              t += (long long)gridDim.x * blockDim.x) {
             const int y = 1 + (int)(t % (sy - 2)), z = 1 + (int)(t / (sy - 2));
-            R.T2[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(stg + (long long)z * sy + y);
+            reinterpret_cast<E *>(R.T2)[(long long)z * sxy + (long long)y * sx + hx] = __ldcg(stg + (long long)z * sy + y);
         }
     }
 }
@@ -694,7 +743,7 @@ static void build_layout(igg_grid *g, const bool act[3][2], bool zex) {
     const int ytiles = (n1 - 2 + kFTY - 1) / kFTY;
     const int wz = n2 - 2;
     if (g_fused_occ < 0) {
-        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false>, 32 * kFTY, 0));
+        IGG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_fused_occ, heat_fused_kernel<false, double>, 32 * kFTY, 0));
         IGG_CUDA(cudaDeviceGetAttribute(&g_fused_nsm, cudaDevAttrMultiProcessorCount, g->device));
     }
     const int kc1 = kFKC, kc2 = g->fused_kc2 > 0 ? g->fused_kc2 : 8;
@@ -888,11 +937,13 @@ IGG_API igg_status igg_debug_fused_trace(unsigned long long *host, int nblocks) 
 
 namespace igg {
 
-// One step of every hosted rank: T2[lr] = step!(T[lr]) plus the faces into the receivers.
-// wait_prev: the previous step of the same run was fused (its faces are awaited tile by tile);
-// drain: the step completes the run (rim, forwarders, drain: complete on the stream afterwards).
-void fused_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, const HeatCoef &k,
-                cudaStream_t s, bool wait_prev, bool drain) {
+// One step of every hosted rank: T2[lr] = step!(T[lr]) plus the faces into the receivers; element type E
+// (binary64, or binary32 with kf).  wait_prev: the previous step of the same run was fused (its faces are
+// awaited tile by tile); drain: the step completes the run (rim, forwarders, drain: complete on the
+// stream afterwards).
+template <typename E>
+static void fused_step_t(igg_grid *g, E *const *T2, const E *const *T, const E *const *Ci, const HeatCoef &k,
+                         const HeatCoefF &kf, cudaStream_t s, bool wait_prev, bool drain) {
     const int L = g->nlocal;
     // [data ctr | rim/forward ctr] x 6 x kMaxChunks, ticket (8), x-piece ctr [parity][2] x kMaxChunks
     const size_t ctr_words = 16 * kMaxChunks + 8;
@@ -919,6 +970,7 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     F.timeout_cycles = (long long)(g->spin_timeout_ms * g->clock_khz);
     F.err = g->d_err;
     F.k = k;
+    F.kf = kf;
     F.nranks = L;
     bool act[3][2] = {{false, false}, {false, false}, {false, false}};
     bool zex = false;
@@ -926,9 +978,9 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     // * kMaxChunks (a remote process hosts one rank: its offsets with lr = 0, L = 1)
     for (int lr = 0; lr < L; ++lr) {
         FusedRank &R = F.r[lr];
-        R.T = T[lr];
-        R.Ci = Ci[lr];
-        R.T2 = T2[lr];
+        R.T = reinterpret_cast<const double *>(T[lr]);
+        R.Ci = reinterpret_cast<const double *>(Ci[lr]);
+        R.T2 = reinterpret_cast<double *>(T2[lr]);
         R.ctr = g->fused_ctr + lr * ctr_words;
         R.ctr_x = R.ctr + 6 * kMaxChunks;
         R.rim_ticket = R.ctr + 12 * kMaxChunks;
@@ -949,13 +1001,13 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
                     zex = zex || a == 2;
                     const int li = local_index(g, nb);
                     if (li >= 0) {   // a rank on this GPU: its arrays directly
-                        f.dst = T2[li];
+                        f.dst = reinterpret_cast<double *>(T2[li]);
                         f.flag = g->flags + (li * 6 + a * 2 + rs) * kMaxChunks;
                         f.xflag = g->flags + (L * 6 + li * 6 + a * 2 + rs) * kMaxChunks;
                         if (a == 0) R.xrem_peer[rs] = g->fused_xrem + li * 2 * stg_words;
                     } else {         // another process (one rank each): its arrays mapped over NVLink
                         const int pp = proc_of(g, nb);
-                        f.dst = peer_arrays(g, T2[lr])[pp];
+                        f.dst = peer_arrays(g, reinterpret_cast<double *>(T2[lr]))[pp];
                         f.flag = g->peer_flags[pp] + (a * 2 + rs) * kMaxChunks;
                         f.xflag = g->peer_flags[pp] + (6 + a * 2 + rs) * kMaxChunks;
                         if (a == 0) R.xrem_peer[rs] = peer_arrays(g, g->fused_xrem)[pp];
@@ -1018,17 +1070,26 @@ void fused_step(igg_grid *g, double *const *T2, const double *const *T, const do
     const long long blocks = (long long)F.per_rank * L;
     prof_begin(g, s);
     if (L > 1)
-        heat_fused_kernel<true><<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
+        heat_fused_kernel<true, E><<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
     else
-        heat_fused_kernel<false><<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
+        heat_fused_kernel<false, E><<<(unsigned)blocks, 32 * kFTY, 0, s>>>(F);
     IGG_CUDA(cudaGetLastError());
     g->launches++;
     prof_end(g, s, (long long)(g->n[0] - 2) * (g->n[1] - 2) * (g->n[2] - 2) * L);
     if (drain && comm) {
-        fused_drain_kernel<<<dim3(xex ? 2 * g->sm_count / L + 1 : 1, L), 128, 0, s>>>(F);
+        fused_drain_kernel<E><<<dim3(xex ? 2 * g->sm_count / L + 1 : 1, L), 128, 0, s>>>(F);
         IGG_CUDA(cudaGetLastError());
         g->launches++;
     }
+}
+
+void fused_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, const HeatCoef &k,
+                cudaStream_t s, bool wait_prev, bool drain) {
+    fused_step_t<double>(g, T2, T, Ci, k, HeatCoefF{}, s, wait_prev, drain);
+}
+void fused_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci,
+                    const HeatCoefF &kf, cudaStream_t s, bool wait_prev, bool drain) {
+    fused_step_t<float>(g, T2, T, Ci, HeatCoef{}, kf, s, wait_prev, drain);
 }
 
 }  // namespace igg

@@ -936,21 +936,38 @@ IGG_API igg_status igg_acoustic_run(igg_grid *g, double **F, int nt, double dt, 
     IGG_CATCH
 }
 
-IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci,
-                                     float lam, float dt, float dx, float dy, float dz, const int bw[3],
-                                     igg_stream_t stream) {
-    IGG_TRY
-    igg::check_live(g, "igg_heat_step_f32");
+namespace igg {
+// one binary32 step (igg_heat_step_f32); wait_prev / drain as heat_step (pipelining inside
+// igg_heat_run_f32 on the fused path)
+static void heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci, float lam,
+                          float dt, float dx, float dy, float dz, const int bw[3], cudaStream_t s, bool wait_prev,
+                          bool drain) {
     if (!T2 || !T || !Ci) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field list");
     for (int a = 0; a < 3; ++a)
         if (g->n[a] == 2) fail(IGG_E_ARG, "igg_heat_step_f32: an axis needs 1 or at least 3 cells");
-    cudaStream_t s = (cudaStream_t)stream;
     std::vector<igg_field> f(g->nlocal);
+    bool aligned = true;
     for (int lr = 0; lr < g->nlocal; ++lr) {
         if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field pointer");
         f[lr] = igg_field{reinterpret_cast<double *>(T2[lr]), {g->n[0], g->n[1], g->n[2]}, 4};
+        aligned = aligned && ((reinterpret_cast<uintptr_t>(T2[lr]) | reinterpret_cast<uintptr_t>(T[lr]) |
+                               reinterpret_cast<uintptr_t>(Ci[lr])) % 8 == 0);
     }
-    const igg::HeatCoefF k = igg::heat_coef_f32(lam, dt, dx, dy, dz);
+    const HeatCoefF k = heat_coef_f32(lam, dt, dx, dy, dz);
+    // the fused stencil + exchange kernel in binary32 (float2 lanes), as the binary64 step: P2P path, a 3-D
+    // grid with an exchanged axis, a hide_communication schedule requested with widths covering the overlap
+    const bool seq = !bw || (bw[0] == 0 && bw[1] == 0 && bw[2] == 0);
+    if (g->fused_f32 && !seq && g->stencil_kernel == 0 && aligned && fused_eligible(g)) {
+        for (int a = 0; a < 3; ++a) {
+            bool ex = false;
+            for (int lr = 0; lr < g->nlocal; ++lr) ex = ex || g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0;
+            if (ex && bw[a] < g->o[a])
+                fail(IGG_E_WIDTH, "heat_step: boundary width " + std::to_string(bw[a]) + " on axis " +
+                                      std::to_string(a) + " is below the field overlap " + std::to_string(g->o[a]));
+        }
+        fused_step_f32(g, T2, T, Ci, k, s, wait_prev, drain);
+        return;
+    }
     // @hide_communication bw: boundary slabs, then update_halo!(T2) on the comm stream
     // behind them, the inner box concurrently; bw = 0 (or NULL) is the sequential schedule.  With an
     // exchanged x axis the x slabs cut every row into 15 + inner + 15 cells, which costs more than the
@@ -977,6 +994,29 @@ IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float 
         // slower on a 2x1x1 split (0.313 vs 0.306 ms/step, profiles/r01_f32_scaling.txt); fused_mode
         // bit 8192 restores it for the ablation
         (g->fused_mode & 8192) ? 128 : 1);
+}
+}  // namespace igg
+
+IGG_API igg_status igg_heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci,
+                                     float lam, float dt, float dx, float dy, float dz, const int bw[3],
+                                     igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_heat_step_f32");
+    igg::heat_step_f32(g, T2, T, Ci, lam, dt, dx, dy, dz, bw, (cudaStream_t)stream, false, true);
+    IGG_CATCH
+}
+
+IGG_API igg_status igg_heat_run_f32(igg_grid *g, float **T, float **T2, const float *const *Ci, float lam, float dt,
+                                    float dx, float dy, float dz, int nt, const int bw[3], igg_stream_t stream) {
+    IGG_TRY
+    igg::check_live(g, "igg_heat_run_f32");
+    if (!T || !T2 || !Ci || nt < 0) fail(IGG_E_ARG, "igg_heat_run_f32: bad argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    igg::validate_peer_maps(g);   // collective: every cached peer mapping still names a live allocation
+    for (int it = 0; it < nt; ++it) {
+        igg::heat_step_f32(g, T2, T, Ci, lam, dt, dx, dy, dz, bw, s, it > 0, it == nt - 1);
+        for (int lr = 0; lr < g->nlocal; ++lr) std::swap(T[lr], T2[lr]);
+    }
     IGG_CATCH
 }
 
@@ -1227,6 +1267,7 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
         case IGG_OPT_LOCAL_P2P: g->local_p2p = value != 0; break;
         case IGG_OPT_HALO26: g->halo26 = value != 0 ? 1 : 0; break;
+        case IGG_OPT_FUSED_F32: g->fused_f32 = value != 0 ? 1 : 0; break;
         case IGG_OPT_FUSED_COMM_CTAS:
             if (value < 1 || value > 128) fail(IGG_E_ARG, "igg_set_option: FUSED_COMM_CTAS must be in [1, 128]");
             g->fused_ncomm = (int)value;

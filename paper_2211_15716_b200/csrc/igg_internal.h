@@ -115,6 +115,10 @@ constexpr int kMaxRegions = 16;
 struct HeatCoef {
     double lam, dt, rdx2, rdy2, rdz2;
 };
+// binary32 coefficients (rounded to float by the caller)
+struct HeatCoefF {
+    float lam, dt, rdx2, rdy2, rdz2;
+};
 struct HeatRegionList {
     HeatRegion r[kMaxRegions];
     int n;
@@ -186,6 +190,7 @@ struct FusedParams {
     long long timeout_cycles;
     int *err;
     HeatCoef k;
+    HeatCoefF kf;                    // (binary32 launches)
     FusedRank r[kMaxFusedRanks];
 };
 
@@ -202,9 +207,6 @@ void launch_heat_slabs(HeatRegionList &L, cudaStream_t s);
 // (all local ranks' inner boxes, or the boundary slabs), one launch
 void launch_heat_box_list(HeatRegionList &L, cudaStream_t s, int variant);
 // binary32 heat step on the box [lo, hi) (size-1 axes allowed); coefficients rounded to float by the caller
-struct HeatCoefF {
-    float lam, dt, rdx2, rdy2, rdz2;
-};
 HeatCoefF heat_coef_f32(float lam, float dt, float dx, float dy, float dz);
 void launch_heat_f32(float *T2, const float *T, const float *Ci, const int n[3], const int lo[3], const int hi[3],
                      const HeatCoefF &k, cudaStream_t s, int variant);
@@ -337,6 +339,7 @@ struct igg_grid : igg::Geom {
     bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
     bool local_p2p = false;                              // IGG_OPT_LOCAL_P2P
     int halo26 = 1;                                      // IGG_OPT_HALO26: P2P update_halo as one 26-neighbour kernel
+    int fused_f32 = 0;                                   // IGG_OPT_FUSED_F32: binary32 steps through the fused kernel
     unsigned int *h26_ctr = nullptr;                     // [claim, stores done]
     struct H26Cache {
         std::vector<long long> key;                      // field pointers, sizes, element sizes, arena
@@ -400,6 +403,9 @@ void check_device_error(igg_grid *g, const char *who);
 // step that does not drain leaves its last x chunks to the next launch's senders)
 void fused_step(igg_grid *g, double *const *T2, const double *const *T, const double *const *Ci, const HeatCoef &k,
                 cudaStream_t s, bool wait_prev = false, bool drain = true);
+// the same for binary32 fields
+void fused_step_f32(igg_grid *g, float *const *T2, const float *const *T, const float *const *Ci,
+                    const HeatCoefF &kf, cudaStream_t s, bool wait_prev = false, bool drain = true);
 void prof_begin(igg_grid *g, cudaStream_t s);
 void prof_end(igg_grid *g, cudaStream_t s, long long cells);
 void tl_mark(igg_grid *g, cudaStream_t s, int k);   // k = 0..4 of the current step

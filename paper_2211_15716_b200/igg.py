@@ -36,6 +36,7 @@ OPT_FUSED_COMM_CTAS = 10
 OPT_HALO_STREAM = 12
 OPT_LOCAL_P2P = 13
 OPT_HALO26 = 14
+OPT_FUSED_F32 = 15
 
 STATUS = {0: "IGG_OK", 1: "IGG_E_ARG", 2: "IGG_E_STATE", 3: "IGG_E_STAGGER", 4: "IGG_E_WIDTH",
           5: "IGG_E_CUDA", 6: "IGG_E_NCCL", 7: "IGG_E_TIMEOUT", 8: "IGG_E_UNSUPPORTED", 9: "IGG_E_BOOTSTRAP"}
@@ -260,12 +261,18 @@ class Grid:
         (T, T2) after the swaps (T = the state after nt steps)."""
         n = self.local_ranks
         t, t2, c = (_as_list(x, n) for x in (T, T2, Ci))
+        import torch
+        f32 = t[0].dtype == torch.float32   # the binary32 variant (igg_heat_run_f32)
         for x in t2 + t + c:
-            if tuple(x.shape) != (self.n[2], self.n[1], self.n[0]):
-                raise ValueError("heat_run fields must have the canonical local shape (nz, ny, nx)")
-        pt, pt2 = _ptr_array(t), _ptr_array(t2)
-        _ok(L.lib().igg_heat_run(self._handle(), pt, pt2, _ptr_array(c), lam, dt, dx, dy, dz, int(nt), _i3(bw),
-                                 _stream(stream)))
+            if tuple(x.shape) != (self.n[2], self.n[1], self.n[0]) or (f32 and x.dtype != torch.float32):
+                raise ValueError("heat_run fields must have the canonical local shape (nz, ny, nx) and one dtype")
+        if f32:
+            arr = lambda ts: (ctypes.c_void_p * len(ts))(*[_dev_ptr(q, allow_f32=True) for q in ts])
+            _ok(L.lib().igg_heat_run_f32(self._handle(), arr(t), arr(t2), arr(c), lam, dt, dx, dy, dz, int(nt),
+                                         _i3(bw), _stream(stream)))
+        else:
+            _ok(L.lib().igg_heat_run(self._handle(), _ptr_array(t), _ptr_array(t2), _ptr_array(c), lam, dt, dx,
+                                     dy, dz, int(nt), _i3(bw), _stream(stream)))
         swapped = nt % 2 == 1
         return (list(t2), list(t)) if swapped else (list(t), list(t2))
 

@@ -166,3 +166,49 @@ def test_update_halo_p2p_protocol_staggered(dims, per):
                 assert np.array_equal(dev[f][r].cpu().numpy(), ref[r][f]), (dims, per, r, f)
     finally:
         g.finalize()
+
+
+def _run_f32(n, dims, per, nt, per_step=False):
+    import torch
+    R = dims[0] * dims[1] * dims[2]
+    g = P.init_global_grid(*n, dims=dims, periods=per, local_ranks=R, device=0, path="p2p")
+    try:
+        g.set_option(P.OPT_FUSED_F32, 1)
+        T, T2, Ci = app.alloc_fields(g, dtype=torch.float32)
+        app.init_random(g, T, T2, Ci)
+        from oracle import heat3d as OH
+        N = _N(n, dims, per)
+        T0g, Cig = SI.global_heat_fields(*N)
+        d = [OH.spacing(1.0, N[i], bool(per[i])) for i in range(3)]
+        dt = OH.stable_dt(*d, 1.0, Cig)
+        l0 = g.kernel_launches()
+        T, T2 = app.run(g, T, T2, Ci, nt, dt, d, per_step=per_step)
+        torch.cuda.synchronize()
+        g.check()
+        ref = OH.heat_run_f32(T0g, Cig, nt, per, 1.0, dt, *d)
+        return [t.cpu().numpy() for t in T], ref, g.kernel_launches() - l0
+    finally:
+        g.finalize()
+
+
+@pytest.mark.parametrize("n,dims,per", [CASES[0], CASES[1], CASES[4], CASES[5], CASES[7], CASES[9]])
+@pytest.mark.parametrize("per_step", [False, True])
+def test_fused_binary32_virtual_ranks_bit_exact(n, dims, per, per_step):
+    """The binary32 variant through the same fused kernel (float2 lanes): one launch per
+    step over all ranks, pipelined (igg_heat_run_f32) and per step, bit-exact vs the binary32 oracle
+    (reading 24) on the global grid."""
+    nt = 5
+    out, ref, launches = _run_f32(n, dims, per, nt, per_step=per_step)
+    for r, got in enumerate(out):
+        W = OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)
+        assert got.dtype == np.float32 and np.array_equal(got, W), (n, dims, per, r)
+    assert launches == (2 * nt if per_step else nt + 1), launches
+
+
+def test_fused_binary32_full_size_512():
+    """Two binary32 ranks of 512^3 (2x1x1) in the fused kernel, 3 pipelined steps, every cell bit-exact."""
+    n, dims, per, nt = (512, 512, 512), (2, 1, 1), (0, 0, 0), 3
+    out, ref, launches = _run_f32(n, dims, per, nt)
+    assert launches == nt + 1
+    for r, got in enumerate(out):
+        assert np.array_equal(got, OG.window(ref, OG.coords_of_rank(r, dims), dims, n, (2, 2, 2), per, n)), r
