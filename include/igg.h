@@ -356,9 +356,9 @@ enum {
                                     the receiver (26-neighbour single phase, bit-identical to the
                                     dimension-sequential result); 0: the per-axis pack/flag/unpack kernels */
     IGG_OPT_FUSED_F32 = 15       /* 1: binary32 steps on the P2P path use the fused stencil + exchange kernel
-                                    (float2 lanes of the binary64 kernel; bit-exact); 0 (default): the split
-                                    schedule -- the float2 sweep measured 0.347 ms per 512^3 step against
-                                    0.252 ms for the float4 box kernel */
+                                    (float4 lanes, 128-cell tile rows; bit-exact; needs nx % 4 == 0, nx >= 130);
+                                    0 (default): the split schedule -- the fused binary32 sweep is 4.8 % slower
+                                    than the float4 box kernel, a tie for x splits */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

@@ -58,24 +58,28 @@ __device__ __forceinline__ void cp_async8f(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-// element type E of the sweep: binary64 (the paper's Float64) or binary32; a lane holds
-// a pair of x-adjacent cells (vec2<E>: 16 or 8 bytes) in both
-template <typename E> struct V2;
-template <> struct V2<double> { using t = double2; };
-template <> struct V2<float> { using t = float2; };
-template <typename E> using vec2 = typename V2<E>::t;
+// element type E of the sweep: binary64 (the paper's Float64) or binary32.  A lane holds
+// kV<E> x-adjacent cells, one 16-B vector (double2 / float4): a tile row is 32 kV<E> cells
+template <typename E> struct VT;
+template <> struct VT<double> { using t = double2; };
+template <> struct VT<float> { using t = float4; };
+template <typename E> using vec = typename VT<E>::t;
+template <typename E> constexpr int kV = 16 / (int)sizeof(E);
+template <typename E> constexpr int kTW = 32 * kV<E>;   // tile width in cells
 template <typename E>
-__device__ __forceinline__ vec2<E> ldg2(const E *p) { return __ldg(reinterpret_cast<const vec2<E> *>(p)); }
-template <typename E>
-__device__ __forceinline__ vec2<E> mk2(E a, E b) {
-    vec2<E> r;
-    r.x = a;
-    r.y = b;
-    return r;
+__device__ __forceinline__ vec<E> ldgv(const E *p) { return __ldg(reinterpret_cast<const vec<E> *>(p)); }
+__device__ __forceinline__ double vget(const double2 &v, int k) { return k == 0 ? v.x : v.y; }
+__device__ __forceinline__ float vget(const float4 &v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+__device__ __forceinline__ void vset(double2 &v, int k, double a) { if (k == 0) v.x = a; else v.y = a; }
+__device__ __forceinline__ void vset(float4 &v, int k, float a) {
+    if (k == 0) v.x = a; else if (k == 1) v.y = a; else if (k == 2) v.z = a; else v.w = a;
 }
 template <typename E>
-__device__ __forceinline__ void cp_pair(void *smem, const void *gmem) {   // one pair, L1-bypassing if 16 B
-    if constexpr (sizeof(E) == 8) cp_async16f(smem, gmem); else cp_async8f(smem, gmem);
+__device__ __forceinline__ vec<E> vzero() {
+    vec<E> r;
+#pragma unroll
+    for (int k = 0; k < kV<E>; ++k) vset(r, k, E(0));
+    return r;
 }
 template <typename E>
 __device__ __forceinline__ void cp_elem(void *smem, const void *gmem) {   // one element
@@ -205,76 +209,79 @@ constexpr int kFKC = 64;   // longest z-chunk
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
+// the lane's kV cells at d, cell k only where bit k of wm is set (a 16-B store when all are)
 template <typename E>
-__device__ __forceinline__ void store_pair(E *d, bool w0, bool w1, E r0, E r1) {
-    if (w0 && w1) {
-        *reinterpret_cast<vec2<E> *>(d) = mk2<E>(r0, r1);
+__device__ __forceinline__ void store_vec(E *d, unsigned wm, const vec<E> &r) {
+    if (wm == (1u << kV<E>) - 1) {
+        *reinterpret_cast<vec<E> *>(d) = r;
     } else {
-        if (w0) d[0] = r0;
-        if (w1) d[1] = r1;
+#pragma unroll
+        for (int k = 0; k < kV<E>; ++k)
+            if (wm >> k & 1) d[k] = vget(r, k);
     }
 }
 
-// UP (XS only): the tile holds the upper x send layer s-2 -- element .x of its lane's pair -- else the
-// lower one, layer 1 -- element .y of lane 0 (s even: pairs never straddle)
+// UP (XS only): the tile holds the upper x send layer s-2 and the halo s-1 -- elements V-2 and V-1 of their
+// lanes' vectors (s is a multiple of V) -- else the lower send layer 1 and the halo 0: elements 1 and 0
+// (compile-time element choice: a run-time index measured 8 us slower per step at 2x1x1)
 template <typename E, bool YF, bool XS, bool UP>
-__device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, vec2<E> (*sT)[32 * kFTY],
-                                            vec2<E> (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
-                                            long long i, bool pair_in, bool w0, bool w1, E *ydst,
-                                            E *sx_row, bool slane, bool hpatch, E h0,
-                                            const E *hx_row) {
+__device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, vec<E> (*sT)[32 * kFTY],
+                                            vec<E> (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
+                                            long long i, bool row_in, unsigned wm, E *ydst, E *sx_row, bool slane,
+                                            bool hpatch, E h0, const E *hx_row) {
+    constexpr int V = kV<E>;
+    constexpr int es = UP ? V - 2 : 1, eh = UP ? V - 1 : 0;
     const E *__restrict__ T = reinterpret_cast<const E *>(R.T);
     const E *__restrict__ Ci = reinterpret_cast<const E *>(R.Ci);
     E *__restrict__ T2 = reinterpret_cast<E *>(R.T2);
     const int tid = threadIdx.x, lane = tid & 31;
 #pragma unroll
     for (int q = 0; q < kFD; ++q) {
-        if (pair_in && zs + q < ze) {
-            cp_pair<E>(&sT[q][tid], T + i + (q + 1) * sxy);
-            cp_pair<E>(&sC[q][tid], Ci + i + q * sxy);
+        if (row_in && zs + q < ze) {
+            cp_async16f(&sT[q][tid], T + i + (q + 1) * sxy);
+            cp_async16f(&sC[q][tid], Ci + i + q * sxy);
         }
         cp_commit();
     }
-    const vec2<E> zero2 = mk2<E>(E(0), E(0));
-    vec2<E> zm = pair_in ? ldg2(T + i - sxy) : zero2;
-    vec2<E> c = pair_in ? ldg2(T + i) : zero2;
-    if (XS && hpatch) {   // (one lane) substitutes the staged x halo values for T's, plane zs first
-        if (UP) c.y = h0; else c.x = h0;
-    }
-    const bool lo_edge = lane == 0 && w0, hi_edge = lane == 31 && w1;
+    const vec<E> zero = vzero<E>();
+    vec<E> zm = row_in ? ldgv(T + i - sxy) : zero;
+    vec<E> c = row_in ? ldgv(T + i) : zero;
+    if (XS && hpatch) vset(c, eh, h0);   // (one lane) the staged x halo value instead of T's, plane zs first
+    const bool lo_edge = lane == 0 && (wm & 1u), hi_edge = lane == 31 && (wm >> (V - 1) & 1u);
+    const bool full = wm == (1u << V) - 1;
     int slot = 0;
 #pragma unroll 2
     for (int z = zs; z < ze; ++z, i += sxy) {
         cp_wait<kFD - 1>();
         if (XS) __syncwarp();   // (the halo row in hx_row, fetched by the whole warp in group 0)
-        vec2<E> ym = zero2, yp = zero2;
-        if (pair_in) {
-            ym = ldg2(T + i - sx);
-            yp = ldg2(T + i + sx);
+        vec<E> ym = zero, yp = zero;
+        if (row_in) {
+            ym = ldgv(T + i - sx);
+            yp = ldgv(T + i + sx);
         }
-        const vec2<E> zp = sT[slot][tid];
-        const vec2<E> ci = sC[slot][tid];
-        E xm = __shfl_up_sync(0xffffffffu, c.y, 1);
-        E xp = __shfl_down_sync(0xffffffffu, c.x, 1);
+        const vec<E> zp = sT[slot][tid];
+        const vec<E> ci = sC[slot][tid];
+        E xm = __shfl_up_sync(0xffffffffu, vget(c, V - 1), 1);
+        E xp = __shfl_down_sync(0xffffffffu, vget(c, 0), 1);
         if (lo_edge) xm = __ldg(T + i - 1);
-        if (hi_edge) xp = __ldg(T + i + 2);
-        const E r0 = cell(c.x, xm, c.y, ym.x, yp.x, zm.x, zp.x, ci.x, coef_of(F, E()));
-        const E r1 = cell(c.y, c.x, xp, ym.y, yp.y, zm.y, zp.y, ci.y, coef_of(F, E()));
-        if (FUSED_STCS && w0 && w1)   // T2 is not re-read in this step (evict-first keeps L2 for T)
-            __stcs(reinterpret_cast<vec2<E> *>(T2 + i), mk2<E>(r0, r1));
+        if (hi_edge) xp = __ldg(T + i + V);
+        vec<E> r;
+#pragma unroll
+        for (int k = 0; k < V; ++k)
+            vset(r, k, cell(vget(c, k), k == 0 ? xm : vget(c, k - 1), k == V - 1 ? xp : vget(c, k + 1), vget(ym, k),
+                            vget(yp, k), vget(zm, k), vget(zp, k), vget(ci, k), coef_of(F, E())));
+        if (FUSED_STCS && full)   // T2 is not re-read in this step (evict-first keeps L2 for T)
+            __stcs(reinterpret_cast<vec<E> *>(T2 + i), r);
         else
-            store_pair(T2 + i, w0, w1, r0, r1);
-        if (YF && ydst) store_pair(ydst + i, w0, w1, r0, r1);   // (warp-uniform) y face row: ydst + i
-        if (XS && slane) sx_row[z - zs] = UP ? r0 : r1;          // (one lane) the x send cell, plane by plane
+            store_vec(T2 + i, wm, r);
+        if (YF && ydst) store_vec(ydst + i, wm, r);   // (warp-uniform) y face row: ydst + i
+        if (XS && slane) sx_row[z - zs] = vget(r, es);   // (one lane) the x send cell, plane by plane
         zm = c;
         c = zp;
-        if (XS && hpatch && z + 1 < ze) {   // plane z+1's x halo cell: the neighbour's staged value
-            const E h = hx_row[z + 1 - zs];
-            if (UP) c.y = h; else c.x = h;
-        }
-        if (pair_in && z + kFD < ze) {
-            cp_pair<E>(&sT[slot][tid], T + i + (kFD + 1) * sxy);
-            cp_pair<E>(&sC[slot][tid], Ci + i + kFD * sxy);
+        if (XS && hpatch && z + 1 < ze) vset(c, eh, hx_row[z + 1 - zs]);   // plane z+1's staged x halo cell
+        if (row_in && z + kFD < ze) {
+            cp_async16f(&sT[slot][tid], T + i + (kFD + 1) * sxy);
+            cp_async16f(&sC[slot][tid], Ci + i + kFD * sxy);
         }
         cp_commit();
         slot = slot + 1 == kFD ? 0 : slot + 1;
@@ -308,8 +315,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <bool MR, typename E>
 __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_constant__ FusedParams F) {
     TRACE_AT(0);
-    __shared__ vec2<E> sT[kFD][32 * kFTY];
-    __shared__ vec2<E> sC[kFD][32 * kFTY];
+    __shared__ vec<E> sT[kFD][32 * kFTY];
+    __shared__ vec<E> sC[kFD][32 * kFTY];
     __shared__ E sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
     __shared__ E sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
@@ -363,13 +370,16 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     const int sx = F.s[0], sy = F.s[1];
     const int ty0 = 1 + ty * kFTY;
     const int y = ty0 + warp;
-    const int p = tx * 64 + 2 * lane;
+    constexpr int V = kV<E>, TW = kTW<E>;
+    const int p = tx * TW + V * lane;   // my first cell
     const bool rowv = y < sy - 1;
-    const bool pair_in = rowv && p < sx;
-    const bool w0 = pair_in && p >= 1 && p < sx - 1;
-    const bool w1 = pair_in && p + 1 >= 1 && p + 1 < sx - 1;
+    const bool row_in = rowv && p < sx;   // (sx is a multiple of V: a lane's cells are all in or all out)
+    unsigned wm = 0u;                     // the cells of my vector that this step writes
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+        if (row_in && p + k >= 1 && p + k < sx - 1) wm |= 1u << k;
     const long long sxy = (long long)sx * sy;
-    const int xlo = max(tx * 64, 1), xhi = min(tx * 64 + 64, sx - 1);   // inner x of this tile
+    const int xlo = max(tx * TW, 1), xhi = min(tx * TW + TW, sx - 1);   // inner x of this tile
     const int yhi = min(ty0 + kFTY, sy - 1);
 
     // faces this tile holds (bit f = 2a + rs; rs 0: my upper send layer -> the upper neighbour's halo 0,
@@ -412,26 +422,26 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                 ydst = reinterpret_cast<E *>(R.face[1][rs].dst) + (long long)((rs == 0 ? 0 : sy - 1) - y) * sx;
         }
         if (xrs >= 0) {
-            const int xf = R.face[0][xrs].layer - tx * 64;
-            const bool slane = rowv && (xf >> 1) == lane;
+            const int xf = R.face[0][xrs].layer - tx * TW;
+            const bool slane = rowv && xf / V == lane;
             // (local staging [parity][side][z][y]: the next launch's senders may still copy this epoch's
             // deferred chunks while its own tiles stage theirs)
             E *xloc = reinterpret_cast<E *>(R.xloc) + ((long long)(F.epoch & 1) * 2 + xrs) * sy * F.s[2];
             // the x halo column beside the send layer: the neighbour's previous-epoch values, staged in my
             // receive rows by its senders (first step of a run: T holds it)
-            const int hside = xrs == 0 ? 1 : 0, xh = (hside == 0 ? 0 : sx - 1) - tx * 64;
+            const int hside = xrs == 0 ? 1 : 0, xh = (hside == 0 ? 0 : sx - 1) - tx * TW;
             const E *hrow = (F.wait_prev && R.halo[0][hside].active && rowv)
                                 ? reinterpret_cast<const E *>(R.xrem) +
                                       ((long long)((F.epoch - 1) & 1) * 2 + hside) * sy * F.s[2] + y
                                 : nullptr;   // (cell z of the row at hrow[z sy])
-            const bool hpatch = hrow && (xh >> 1) == lane;
+            const bool hpatch = hrow && xh / V == lane;
             E h0 = E(0);
             if (hrow) {   // (warp-uniform) this chunk's staged halo values of the row, into the first group
                 for (int z = zs + lane; z < ze; z += 32) cp_elem<E>(&sHx[warp][z - zs], hrow + (long long)z * sy);
                 if (hpatch) h0 = __ldcg(hrow + (long long)zs * sy);
             }
-#define XSWEEP(YFv, UPv, YD) fused_sweep<E, YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, YD, \
-                                                          sX[warp], slane, hpatch, h0, sHx[warp])
+#define XSWEEP(YFv, UPv, YD) fused_sweep<E, YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, YD, \
+                                                             sX[warp], slane, hpatch, h0, sHx[warp])
             if (xrs == 0) {   // upper: send layer s-2
                 if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
             } else {          // lower: send layer 1
@@ -446,21 +456,21 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                 if (r < nr) xloc[(long long)z * sy + ty0 + r] = sX[r][z - zs];
             }
         } else if (did & 12u) {
-            fused_sweep<E, true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, ydst, nullptr,
-                                               false, false, E(0), nullptr);
+            fused_sweep<E, true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, ydst, nullptr, false,
+                                               false, E(0), nullptr);
         } else {
-            fused_sweep<E, false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, pair_in, w0, w1, nullptr,
-                                                nullptr, false, false, E(0), nullptr);
+            fused_sweep<E, false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, nullptr, nullptr, false,
+                                                false, E(0), nullptr);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver
         const int rs = (did & 16u) ? 0 : 1;
         const FusedFace &fz = R.face[2][rs];
-        if (rowv && p < sx) {
+        if (row_in) {
             const long long o = (long long)fz.layer * sxy + (long long)y * sx + p;
-            const vec2<E> v = *reinterpret_cast<const vec2<E> *>(reinterpret_cast<const E *>(R.T2) + o);
-            store_pair(reinterpret_cast<E *>(fz.dst) + o + (long long)((rs == 0 ? 0 : F.s[2] - 1) - fz.layer) * sxy,
-                       w0, w1, v.x, v.y);
+            const vec<E> v = *reinterpret_cast<const vec<E> *>(reinterpret_cast<const E *>(R.T2) + o);
+            store_vec(reinterpret_cast<E *>(fz.dst) + o + (long long)((rs == 0 ? 0 : F.s[2] - 1) - fz.layer) * sxy,
+                      wm, v);
         }
     }
     TRACE_AT(1);
@@ -737,9 +747,9 @@ static int g_fused_occ = -1, g_fused_nsm = 0;
 // ones).  The end chunks hold the z send/halo layers (planes 1, 2 .. s-3, s-2), so a step's z halo
 // reads come last and wait for nothing in the steady state, and the short chunks shorten the tail.
 // Depends on the geometry only: every rank numbers chunks identically (flags are per chunk position).
-static void build_layout(igg_grid *g, const bool act[3][2], bool zex) {
+static void build_layout(igg_grid *g, const bool act[3][2], bool zex, int tw) {
     const int n0 = g->n[0], n1 = g->n[1], n2 = g->n[2];
-    const int xtiles = (n0 - 1 + 63) / 64;
+    const int xtiles = (n0 - 1 + tw - 1) / tw;   // (tw: tile width in cells, 32 lanes x one 16-B vector)
     const int ytiles = (n1 - 2 + kFTY - 1) / kFTY;
     const int wz = n2 - 2;
     if (g_fused_occ < 0) {
@@ -1020,12 +1030,12 @@ static void fused_step_t(igg_grid *g, E *const *T2, const E *const *T, const E *
                 h.xflag = g->flags + (L * 6 + lr * 6 + a * 2 + rs) * kMaxChunks;
             }
     }
-    int key = 0;
+    int key = sizeof(E) == 4 ? 64 : 0;   // (the layout depends on the tile width)
     for (int a = 0; a < 3; ++a)
         for (int rs = 0; rs < 2; ++rs) key |= (act[a][rs] ? 1 : 0) << (a * 2 + rs);
     if (g->fused_key != key) {
         if (g->fused_deferred >= 0) fail(IGG_E_STATE, "fused step: topology changed inside a run");
-        build_layout(g, act, zex);
+        build_layout(g, act, zex, kTW<E>);
         g->fused_key = key;
         if (g->fused_xcnt) {   // the x senders' cumulative counters restart with the layout
             IGG_CUDA(cudaMemset(g->fused_xcnt, 0, sizeof(unsigned) * 2 * kMaxChunks * L));

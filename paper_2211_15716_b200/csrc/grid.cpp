@@ -951,13 +951,15 @@ static void heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, 
         if (!T2[lr] || !T[lr] || !Ci[lr]) fail(IGG_E_ARG, "igg_heat_step_f32: NULL field pointer");
         f[lr] = igg_field{reinterpret_cast<double *>(T2[lr]), {g->n[0], g->n[1], g->n[2]}, 4};
         aligned = aligned && ((reinterpret_cast<uintptr_t>(T2[lr]) | reinterpret_cast<uintptr_t>(T[lr]) |
-                               reinterpret_cast<uintptr_t>(Ci[lr])) % 8 == 0);
+                               reinterpret_cast<uintptr_t>(Ci[lr])) % 16 == 0);
     }
     const HeatCoefF k = heat_coef_f32(lam, dt, dx, dy, dz);
-    // the fused stencil + exchange kernel in binary32 (float2 lanes), as the binary64 step: P2P path, a 3-D
-    // grid with an exchanged axis, a hide_communication schedule requested with widths covering the overlap
+    // the fused stencil + exchange kernel in binary32 (float4 lanes: 128-cell tile rows), as the binary64
+    // step: P2P path, a 3-D grid with an exchanged axis, a hide_communication schedule requested with widths
+    // covering the overlap; rows of whole 16-B vectors and two x tiles at least (the x faces in different tiles)
     const bool seq = !bw || (bw[0] == 0 && bw[1] == 0 && bw[2] == 0);
-    if (g->fused_f32 && !seq && g->stencil_kernel == 0 && aligned && fused_eligible(g)) {
+    if (g->fused_f32 && !seq && g->stencil_kernel == 0 && aligned && g->n[0] % 4 == 0 && g->n[0] >= 130 &&
+        fused_eligible(g)) {
         for (int a = 0; a < 3; ++a) {
             bool ex = false;
             for (int lr = 0; lr < g->nlocal; ++lr) ex = ex || g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0;

@@ -95,8 +95,8 @@ def test_split_schedule_guards(n, dims, per, opts):
 def test_binary32_guards(fused):
     import torch
     o = {P.OPT_FUSED_F32: fused}
-    a = _heat((132, 20, 18), (2, 1, 1), (0, 1, 0), 3, dtype=torch.float32, options=o)
-    b = _heat((132, 20, 18), (2, 1, 1), (0, 1, 0), 3, dtype=torch.float32, options=o)
+    a = _heat((260, 20, 18), (2, 1, 1), (0, 1, 0), 3, dtype=torch.float32, options=o)
+    b = _heat((260, 20, 18), (2, 1, 1), (0, 1, 0), 3, dtype=torch.float32, options=o)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
 

@@ -191,10 +191,20 @@ def _run_f32(n, dims, per, nt, per_step=False):
         g.finalize()
 
 
-@pytest.mark.parametrize("n,dims,per", [CASES[0], CASES[1], CASES[4], CASES[5], CASES[7], CASES[9]])
+F32_CASES = [   # (binary32 tiles are 128 cells wide: rows of whole float4 vectors, two x tiles at least)
+    ((132, 36, 34), (2, 1, 1), (0, 0, 0)),
+    ((132, 36, 34), (2, 1, 1), (1, 1, 1)),
+    ((132, 36, 34), (2, 2, 1), (0, 0, 0)),
+    ((132, 20, 22), (2, 2, 2), (1, 0, 1)),
+    ((136, 18, 20), (4, 1, 1), (1, 0, 0)),
+    ((260, 20, 22), (1, 2, 2), (0, 1, 1)),   # three x tiles
+]
+
+
+@pytest.mark.parametrize("n,dims,per", F32_CASES)
 @pytest.mark.parametrize("per_step", [False, True])
 def test_fused_binary32_virtual_ranks_bit_exact(n, dims, per, per_step):
-    """The binary32 variant through the same fused kernel (float2 lanes): one launch per
+    """The binary32 variant through the same fused kernel (float4 lanes): one launch per
     step over all ranks, pipelined (igg_heat_run_f32) and per step, bit-exact vs the binary32 oracle
     (reading 24) on the global grid."""
     nt = 5
