@@ -957,8 +957,13 @@ static void heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, 
     // the fused stencil + exchange kernel in binary32 (float4 lanes: 128-cell tile rows), as the binary64
     // step: P2P path, a 3-D grid with an exchanged axis, a hide_communication schedule requested with widths
     // covering the overlap; rows of whole 16-B vectors and two x tiles at least (the x faces in different tiles)
+    // (auto: when the x axis is exchanged -- 2 GPUs, 2x1x1 at 512^3: 0.280 ms fused vs 0.287 ms split; for a
+    // y or z split the float4 box kernel's split schedule is faster)
     const bool seq = !bw || (bw[0] == 0 && bw[1] == 0 && bw[2] == 0);
-    if (g->fused_f32 && !seq && g->stencil_kernel == 0 && aligned && g->n[0] % 4 == 0 && g->n[0] >= 130 &&
+    bool xex = false;
+    for (int lr = 0; lr < g->nlocal; ++lr) xex = xex || g->nbr[lr][0][0] >= 0 || g->nbr[lr][0][1] >= 0;
+    const bool want = g->fused_f32 > 0 || (g->fused_f32 < 0 && xex);
+    if (want && !seq && g->stencil_kernel == 0 && aligned && g->n[0] % 4 == 0 && g->n[0] >= 130 &&
         fused_eligible(g)) {
         for (int a = 0; a < 3; ++a) {
             bool ex = false;
@@ -975,8 +980,6 @@ static void heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, 
     // exchanged x axis the x slabs cut every row into 15 + inner + 15 cells, which costs more than the
     // exposed exchange (2x1x1 at 512^3: 0.306 ms hidden vs 0.287 ms sequential), so the
     // step runs sequentially there (same cells, same result); fused_mode bit 16384 keeps the slabs.
-    bool xex = false;
-    for (int lr = 0; lr < g->nlocal; ++lr) xex = xex || g->nbr[lr][0][0] >= 0 || g->nbr[lr][0][1] >= 0;
     const int zero[3] = {0, 0, 0};
     const int *bw_eff = (xex && !(g->fused_mode & 16384)) ? zero : bw;
     igg::hide_comm(
@@ -1269,7 +1272,7 @@ IGG_API igg_status igg_set_option(igg_grid *g, int key, long long value) {
         case IGG_OPT_HALO_STREAM: g->halo_on_caller = value != 0; break;
         case IGG_OPT_LOCAL_P2P: g->local_p2p = value != 0; break;
         case IGG_OPT_HALO26: g->halo26 = value != 0 ? 1 : 0; break;
-        case IGG_OPT_FUSED_F32: g->fused_f32 = value != 0 ? 1 : 0; break;
+        case IGG_OPT_FUSED_F32: g->fused_f32 = value < 0 ? -1 : value != 0 ? 1 : 0; break;
         case IGG_OPT_FUSED_COMM_CTAS:
             if (value < 1 || value > 128) fail(IGG_E_ARG, "igg_set_option: FUSED_COMM_CTAS must be in [1, 128]");
             g->fused_ncomm = (int)value;

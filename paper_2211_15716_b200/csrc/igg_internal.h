@@ -339,7 +339,8 @@ struct igg_grid : igg::Geom {
     bool halo_on_caller = false;                         // IGG_OPT_HALO_STREAM
     bool local_p2p = false;                              // IGG_OPT_LOCAL_P2P
     int halo26 = 1;                                      // IGG_OPT_HALO26: P2P update_halo as one 26-neighbour kernel
-    int fused_f32 = 0;                                   // IGG_OPT_FUSED_F32: binary32 steps through the fused kernel
+    int fused_f32 = -1;                                  // IGG_OPT_FUSED_F32: binary32 steps through the fused kernel
+                                                         // (-1: when the x axis is exchanged)
     unsigned int *h26_ctr = nullptr;                     // [claim, stores done]
     struct H26Cache {
         std::vector<long long> key;                      // field pointers, sizes, element sizes, arena
