@@ -7,6 +7,9 @@ for d in 2,1,1 1,2,1 1,1,2; do
   timeout 600 $TR bench.py --gpus 2 --dims $d --no-e2e > gpurun_out/${T}_n2_${d//,/}.json 2> gpurun_out/${T}_n2_${d//,/}.err
 done
 timeout 600 $TR bench.py --gpus 2 > gpurun_out/${T}_n2.json 2> gpurun_out/${T}_n2.err
+timeout 600 $TR bench.py --gpus 2 --dims 2,1,1 --dtype f32 --no-e2e > gpurun_out/${T}_f32_n2_211.json 2> gpurun_out/${T}_f32_n2_211.err
+timeout 600 $TR bench.py --gpus 2 --dims 2,1,1 --dtype f32 --fused-f32 --no-e2e > gpurun_out/${T}_f32f_n2_211.json 2> gpurun_out/${T}_f32f_n2_211.err
+timeout 600 $TR bench.py --gpus 2 --workload acoustic --no-e2e > gpurun_out/${T}_ac_n2.json 2> gpurun_out/${T}_ac_n2.err
 HALO_SIZES=${HALO_SIZES:-64,128,256,512,768} timeout 900 $TR scripts/halo_sweep.py > gpurun_out/${T}_halo.txt 2>&1
 timeout 900 $TR scripts/b10_staggered.py > gpurun_out/${T}_b10.txt 2>&1
 echo done
