@@ -227,7 +227,7 @@ __device__ __forceinline__ void store_vec(E *d, unsigned wm, const vec<E> &r) {
 template <typename E, bool YF, bool XS, bool UP>
 __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRank &R, vec<E> (*sT)[32 * kFTY],
                                             vec<E> (*sC)[32 * kFTY], int sx, long long sxy, int zs, int ze,
-                                            long long i, bool row_in, unsigned wm, E *ydst, E *sx_row, bool slane,
+                                            long long i, bool row_in, unsigned wm, E *ydst, E *xdst, int xs, bool slane,
                                             bool hpatch, E h0, const E *hx_row) {
     constexpr int V = kV<E>;
     constexpr int es = UP ? V - 2 : 1, eh = UP ? V - 1 : 0;
@@ -275,7 +275,7 @@ __device__ __forceinline__ void fused_sweep(const FusedParams &F, const FusedRan
         else
             store_vec(T2 + i, wm, r);
         if (YF && ydst) store_vec(ydst + i, wm, r);   // (warp-uniform) y face row: ydst + i
-        if (XS && slane) sx_row[z - zs] = vget(r, es);   // (one lane) the x send cell, plane by plane
+        if (XS && slane) xdst[(long long)z * xs] = vget(r, es);   // (one lane) the x send cell -> local staging
         zm = c;
         c = zp;
         if (XS && hpatch && z + 1 < ze) vset(c, eh, hx_row[z + 1 - zs]);   // plane z+1's staged x halo cell
@@ -317,7 +317,6 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
     TRACE_AT(0);
     __shared__ vec<E> sT[kFD][32 * kFTY];
     __shared__ vec<E> sC[kFD][32 * kFTY];
-    __shared__ E sX[kFTY][kFKC];   // the x send cells of each row, plane by plane
     __shared__ E sHx[kFTY][kFKC];  // the staged x halo cells of each row, plane by plane
     // (the rank index stays a run-time value even for one rank: the parameters are then read through
     // uniform registers instead of being re-materialised from the constant bank in the sweep)
@@ -441,26 +440,19 @@ __global__ void __launch_bounds__(32 * kFTY, 10) heat_fused_kernel(const __grid_
                 if (hpatch) h0 = __ldcg(hrow + (long long)zs * sy);
             }
 #define XSWEEP(YFv, UPv, YD) fused_sweep<E, YFv, true, UPv>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, YD, \
-                                                             sX[warp], slane, hpatch, h0, sHx[warp])
+                                                             xloc + y, sy, slane, hpatch, h0, sHx[warp])
             if (xrs == 0) {   // upper: send layer s-2
                 if (did & 12u) XSWEEP(true, true, ydst); else XSWEEP(false, true, nullptr);
             } else {          // lower: send layer 1
                 if (did & 12u) XSWEEP(true, false, ydst); else XSWEEP(false, false, nullptr);
             }
 #undef XSWEEP
-            // the tile's send cells into the local staging, plane by plane (the kFTY rows of a plane adjacent)
-            __syncthreads();
-            const int nr = min(kFTY, sy - 1 - ty0);
-            for (int t = tid; t < (ze - zs) * kFTY; t += blockDim.x) {
-                const int r = t % kFTY, z = zs + t / kFTY;
-                if (r < nr) xloc[(long long)z * sy + ty0 + r] = sX[r][z - zs];
-            }
         } else if (did & 12u) {
-            fused_sweep<E, true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, ydst, nullptr, false,
+            fused_sweep<E, true, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, ydst, nullptr, 0, false,
                                                false, E(0), nullptr);
         } else {
-            fused_sweep<E, false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, nullptr, nullptr, false,
-                                                false, E(0), nullptr);
+            fused_sweep<E, false, false, false>(F, R, sT, sC, sx, sxy, zs, ze, i0, row_in, wm, nullptr, nullptr, 0,
+                                                false, false, E(0), nullptr);
         }
     }
     if (did & 48u) {   // z face: my row of the layer plane (written by this thread just now) -> the receiver

@@ -129,9 +129,18 @@ struct HeatRegionList {
 // ---------------------------------------------------------------- fused stencil + exchange (fused.cu)
 constexpr int kMaxChunks = 128;      // z-chunks per step (flags / counters per face and chunk)
 constexpr int kMaxFusedRanks = 8;    // ranks hosted on one GPU that one fused launch covers
-constexpr int kFusedDefer = 3;       // x chunks a pipelined step leaves to the next launch's senders
-constexpr int kFusedXSenders = 16;   // x sender blocks per x face and rank
-constexpr int kFusedXPiece = 8;      // planes per x sender work piece
+#ifndef FUSED_DEFER   // (ablation builds sweep these three)
+#define FUSED_DEFER 3
+#endif
+#ifndef FUSED_XSENDERS
+#define FUSED_XSENDERS 16
+#endif
+#ifndef FUSED_XPIECE
+#define FUSED_XPIECE 8
+#endif
+constexpr int kFusedDefer = FUSED_DEFER;         // x chunks a pipelined step leaves to the next launch's senders
+constexpr int kFusedXSenders = FUSED_XSENDERS;   // x sender blocks per x face and rank
+constexpr int kFusedXPiece = FUSED_XPIECE;       // planes per x sender work piece
 struct FusedFace {                   // one face I send, indexed by the RECEIVER's halo side
     double *dst;                     // the receiver's T2 (a sibling's, or peer-mapped); lands in its halo layer
     unsigned long long *flag;        // receiver's data flags of (axis, side): [kMaxChunks] (z faces: [0])
