@@ -14,10 +14,14 @@
 // Pipelined schedule (igg_heat_run): step t's tiles that read halo cells wait, before their sweep, for
 // step t-1's flags of exactly those cells; the z chunks holding the z send/halo layers are visited LAST
 // in every step, so in the steady state no tile waits (the awaited faces were published a whole step
-// earlier).  y and z faces land in the receiver's T2 halo rows/planes; x faces (one value per row and
-// plane: a T2 column) are captured in shared memory during the sweep and stored, z-contiguous, into the
-// receiver's staging buffer, from which the receiver's halo tiles read them into shared memory (never
-// written into the T array being swept).  Face cells the stencil does not compute (global boundary,
+// earlier).  y and z faces land in the receiver's T2 halo rows/planes.  x faces (one value per row and
+// plane: a T2 column) go through staging buffers laid out [parity][side][z][y] (a run of planes is one
+// contiguous block): the send lanes store them into the LOCAL staging from the sweep, the tile counts
+// itself after a GPU-scope release, and x sender blocks move 8-plane pieces into the receiver's staging
+// under one system-scope release per piece (the last chunks of a step that does not complete its run are
+// moved by the next launch's senders: no tail); the receiver's halo tiles read them into shared memory
+// with their first cp.async group (never written into the T array being swept).  Face cells the stencil
+// does not compute (global boundary,
 // edges/corners of the dimension-sequential update_halo) are sent by rim blocks and
 // forwarded by forwarder blocks of the LAST step of a run, which also drains (awaits every incoming
 // face and copies the staged x columns into T2).  Hazard argument and forward progress: DESIGN.md §6.
@@ -201,11 +205,12 @@ constexpr int kFKC = 64;   // longest z-chunk
 //  * YF (CTA-uniform): the warp whose row is a y send layer stores its results also into the receiver's
 //    halo row (ydst + i) -- the same 16-B stores as T2's (the z send layer, the first or last plane of an
 //    end chunk, is copied after the sweep: one row per warp, just written);
-//  * XS (CTA-uniform: the tile holds an x send layer): the lane holding the send cell keeps its value of
-//    every plane in shared memory, and after the sweep the warp stores the row z-contiguously into this
-//    rank's LOCAL x staging buffer, from which the x sender blocks move it into the receiver's T2 column
-//    (one system-scope release per chunk and sender instead of one per face tile).  The receiver needs
-//    nothing: its next step reads the x halo from T like any other cell.
+//  * XS (CTA-uniform: the tile holds an x send layer): the lane holding the send cell stores its value of
+//    every plane into this rank's LOCAL x staging ([z][y]), from which the x sender blocks move it into
+//    the receiver's staging (one system-scope release per piece instead of one per face tile); the lane
+//    holding the x halo cell substitutes the neighbour's staged value (sHx, fetched in the first cp.async
+//    group) for T's, plane by plane.
+// The element type E is binary64 or binary32; a lane holds one 16-B vector of kV<E> cells.
 #ifndef FUSED_STCS
 #define FUSED_STCS 1
 #endif
