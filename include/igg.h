@@ -358,8 +358,8 @@ enum {
     IGG_OPT_FUSED_F32 = 15       /* binary32 steps on the P2P path through the fused stencil + exchange kernel
                                     (float4 lanes, 128-cell tile rows; bit-exact; needs nx % 4 == 0, nx >= 130):
                                     1 = always, 0 = never (the split schedule), -1 (default) = when the x axis is
-                                    exchanged (the fused binary32 sweep is 4.8 % slower than the float4 box kernel,
-                                    faster than the sequential x-split schedule) */
+                                    the only exchanged one (the fused binary32 sweep is 4.8 % slower than the float4
+                                    box kernel, faster than the sequential x-split schedule) */
 };
 igg_status igg_set_option(igg_grid *grid, int key, long long value);
 

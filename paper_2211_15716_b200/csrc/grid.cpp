@@ -957,12 +957,15 @@ static void heat_step_f32(igg_grid *g, float *const *T2, const float *const *T, 
     // the fused stencil + exchange kernel in binary32 (float4 lanes: 128-cell tile rows), as the binary64
     // step: P2P path, a 3-D grid with an exchanged axis, a hide_communication schedule requested with widths
     // covering the overlap; rows of whole 16-B vectors and two x tiles at least (the x faces in different tiles)
-    // (auto: when the x axis is exchanged -- 2 GPUs, 2x1x1 at 512^3: 0.280 ms fused vs 0.287 ms split; for a
-    // y or z split the float4 box kernel's split schedule is faster)
+    // (auto: when only the x axis is exchanged -- 2 GPUs, 2x1x1 at 512^3: 0.280 ms fused vs 0.287 ms split;
+    // with y or z exchanged too the float4 box kernel's split schedule is faster: 2x2x1 0.2875 vs 0.2917 ms)
     const bool seq = !bw || (bw[0] == 0 && bw[1] == 0 && bw[2] == 0);
-    bool xex = false;
-    for (int lr = 0; lr < g->nlocal; ++lr) xex = xex || g->nbr[lr][0][0] >= 0 || g->nbr[lr][0][1] >= 0;
-    const bool want = g->fused_f32 > 0 || (g->fused_f32 < 0 && xex);
+    bool xex = false, yzex = false;
+    for (int lr = 0; lr < g->nlocal; ++lr) {
+        xex = xex || g->nbr[lr][0][0] >= 0 || g->nbr[lr][0][1] >= 0;
+        for (int a = 1; a < 3; ++a) yzex = yzex || g->nbr[lr][a][0] >= 0 || g->nbr[lr][a][1] >= 0;
+    }
+    const bool want = g->fused_f32 > 0 || (g->fused_f32 < 0 && xex && !yzex);
     if (want && !seq && g->stencil_kernel == 0 && aligned && g->n[0] % 4 == 0 && g->n[0] >= 130 &&
         fused_eligible(g)) {
         for (int a = 0; a < 3; ++a) {
