@@ -76,6 +76,11 @@ __device__ __forceinline__ unsigned long long ld_acq_sys(const unsigned long lon
 // protocol needs; __threadfence_system would be the heavier sequentially consistent fence.sc
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned ld_acq_gpu_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void spin(const unsigned long long *f, unsigned long long v, long long timeout, int *err) {
     const long long t0 = clock64();
     while (ld_acq_sys(f) < v) {
@@ -232,6 +237,19 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
         const unsigned long long *const *we = reinterpret_cast<const unsigned long long *const *>(base + P.o_wait_end);
         for (int q = threadIdx.x; q < P.nwait_end; q += blockDim.x) spin(we[q], epoch, timeout, err);
         if (threadIdx.x == 0) {
+            // every block has claimed for the last time, but some may still be counting their store chunks
+            // (the incoming faces can be complete before this launch's own stores are): the counters are
+            // reset only after the last count -- else a late count lands in the next launch's counter and
+            // this launch's data flags are never published (seen as a flag timeout with the exchange
+            // running beside a long inner-box kernel)
+            const long long t0 = clock64();
+            while (ld_acq_gpu_u32(ctr + 1) < (unsigned)P.nstore_chunks) {
+                if (clock64() - t0 > timeout) {
+                    atomicExch(err, 1);
+                    break;
+                }
+                __nanosleep(64);
+            }
             ctr[0] = 0u;
             ctr[1] = 0u;
         }
