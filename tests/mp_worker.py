@@ -298,6 +298,11 @@ def main():
         acoustic_case(path, n, dims, (0, 0, 0), 1, (16, 4, 4))
         heat_f32_case(path, n, dims, (1, 0, 1))
         heat_f32_case(path, (520, 20, 34), dims, (0, 0, 0), bw=(16, 2, 2))   # hide_communication, float4 kernel
+        if path == "p2p" and world == 2:
+            # y / z splits: the 26-neighbour exchange beside a long inner-box kernel (the counter-reset
+            # race of the exchange's last block showed up exactly here as flag timeouts)
+            for d2 in ((1, 1, 2), (1, 2, 1)):
+                heat_f32_case(path, (256, 256, 256), d2, (0, 0, 0), bw=(16, 2, 2), nt=12)
         heat_f32_case(path, (264, 36, 34), dims, (1, 1, 0), bw=(0, 0, 0))
         acoustic_case(path, n, dims, (1, 0, 1), 1, (4, 4, 4))
         halo_case(path, n, dims, (1, 1, 1), 1, sizes, seed=2)
