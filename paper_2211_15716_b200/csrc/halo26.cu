@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
                 fence_acq_rel_sys();
                 unsigned long long *const *sig = reinterpret_cast<unsigned long long *const *>(base + P.o_signal);
                 for (int q = 0; q < P.nsignal; ++q) st_relaxed_sys(sig[q], epoch);
+                atomicExch(ctr + 1, 0u);   // (the last count of this launch: the counter restarts)
             }
         }
         mydone = 0;
@@ -236,23 +237,11 @@ __global__ void __launch_bounds__(kH26Threads) halo26_kernel(const char *__restr
     if (bt == nbatch + gridDim.x - 1) {   // the last block to leave: every incoming face, then reset
         const unsigned long long *const *we = reinterpret_cast<const unsigned long long *const *>(base + P.o_wait_end);
         for (int q = threadIdx.x; q < P.nwait_end; q += blockDim.x) spin(we[q], epoch, timeout, err);
-        if (threadIdx.x == 0) {
-            // every block has claimed for the last time, but some may still be counting their store chunks
-            // (the incoming faces can be complete before this launch's own stores are): the counters are
-            // reset only after the last count -- else a late count lands in the next launch's counter and
-            // this launch's data flags are never published (seen as a flag timeout with the exchange
-            // running beside a long inner-box kernel)
-            const long long t0 = clock64();
-            while (ld_acq_gpu_u32(ctr + 1) < (unsigned)P.nstore_chunks) {
-                if (clock64() - t0 > timeout) {
-                    atomicExch(err, 1);
-                    break;
-                }
-                __nanosleep(64);
-            }
-            ctr[0] = 0u;
-            ctr[1] = 0u;
-        }
+        // (every block has claimed for the last time: the claim counter restarts for the next launch; the
+        // store counter is reset by the block whose count completes it -- some blocks may still be counting
+        // here, since the incoming faces can be complete before this launch's own stores are; resetting it
+        // here let a late count land in the next launch, whose data flags were then never published)
+        if (threadIdx.x == 0) ctr[0] = 0u;
     }
     H26_AT(4);
     H26_VAL(7, (unsigned long long)P.nchunks | ((unsigned long long)P.nstore_chunks << 20) |
